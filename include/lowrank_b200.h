@@ -1,0 +1,192 @@
+/*
+ * lowrank_b200.h -- C ABI of the B200-native ID / CUR hot path.
+ *
+ * Drop-in boundary for the reference library `lowrank` (header-only C++ on
+ * Eigen, /root/reference/proj/include/lowrank).  Each entry point replaces
+ * the reference template cited next to it; include/lowrank/lowrank_b200.hpp
+ * re-declares the reference's C++ names (namespace lowrank) on top of this
+ * ABI, and INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - matrices are column-major double with an explicit leading dimension;
+ *     pivots are 0-based int64 (core.hpp:12-20);
+ *   - outputs are caller-allocated;
+ *   - plain names take HOST pointers (inputs copied to the GPU, outputs copied
+ *     back, the call returns when results are on the host); the `_d`
+ *     variants take DEVICE pointers and are stream-ordered on the context's
+ *     stream (they still synchronise where the reference would throw, i.e.
+ *     after validation reductions);
+ *   - every call returns an LR_* status; the message of the last failure on
+ *     the calling thread is lr_last_error(), mirroring the exception classes
+ *     of core.hpp:22-42 (invalid_argument, SingularityError{index},
+ *     ConvergenceError, runtime_error).
+ *   - there is no CPU fallback: without a usable sm_100 device every call
+ *     returns LR_ECUDA.
+ */
+#ifndef LOWRANK_B200_H
+#define LOWRANK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define LR_OK 0
+#define LR_EINVAL 1      /* std::invalid_argument                          */
+#define LR_ESINGULAR 2   /* lowrank::SingularityError (lr_last_singular_index) */
+#define LR_ECONVERGE 3   /* lowrank::ConvergenceError                      */
+#define LR_ERUNTIME 4    /* std::runtime_error                             */
+#define LR_ECUDA 5       /* device / driver failure                        */
+#define LR_EUNSUPPORTED 6 /* reference feature not on the B200 path yet    */
+
+/* SolveKind, solve.hpp:9 */
+#define LR_SOLVE_BACKSUB 0
+#define LR_SOLVE_PINV 1
+#define LR_SOLVE_TIKHONOV 2
+
+/* SketchKind, sketch.hpp:19 */
+#define LR_SKETCH_GAUSSIAN 0
+#define LR_SKETCH_SRFT 1
+
+/* CUR middle factor */
+#define LR_U_VT_RPINV 0       /* cur.hpp:30: u = col_basis()^T pinv(r)        */
+#define LR_U_CPINV_A_RPINV 1  /* lowrank_main.cpp:215: u = pinv(c) a pinv(r)  */
+
+/* SolveStrategy, solve.hpp:16-32 (defaults: BACKSUB, 1e-12, 0, escalate=1) */
+typedef struct {
+  int kind;
+  double threshold;
+  double ridge;
+  int escalate;
+} lr_solve_strategy;
+
+/* SketchConfig, sketch.hpp:21-33 (defaults: GAUSSIAN, p=10, 0, q=0, 1, seed 0) */
+typedef struct {
+  int kind;
+  int oversample;
+  int64_t srft_samples;
+  int power;
+  int reorthonormalize;
+  uint64_t seed;
+} lr_sketch_config;
+
+typedef struct lr_ctx lr_ctx;
+
+typedef struct {
+  long long cpqr_steps;      /* Householder steps run by the last call           */
+  long long norm_recomputes; /* exact norm recomputations (cpqr.hpp:80-83)       */
+  int solve_escalated;       /* 1 if the last coefficient solve took the pinv path */
+  int pinv_fast_path;        /* 1 if the last CUR U used the CholeskyQR2 route    */
+} lr_stats;
+
+lr_solve_strategy lr_solve_strategy_default(void);
+lr_sketch_config lr_sketch_config_default(void);
+
+const char* lr_last_error(void);
+int64_t lr_last_singular_index(void);
+
+int lr_ctx_create(lr_ctx** out, int device);
+int lr_ctx_destroy(lr_ctx* ctx);
+/* run subsequent _d calls on this cudaStream_t (NULL = the context's own stream) */
+int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
+int lr_ctx_get_stats(lr_ctx* ctx, lr_stats* out);
+int lr_ctx_synchronize(lr_ctx* ctx);
+
+/* rng.hpp:74-94 gaussian_matrix<double>(rows, cols, seed): out rows x cols (ld rows) */
+int lr_gaussian_matrix(lr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);
+int lr_gaussian_matrix_d(lr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ldo);
+
+/* sketch.hpp:67-78 sketch_gaussian(a, ell, seed).y: y ell x n (ld ell) */
+int lr_sketch_gaussian(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
+                       uint64_t seed, double* y);
+int lr_sketch_gaussian_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
+                         uint64_t seed, double* y, int64_t ldy);
+
+/* cpqr.hpp:32-114 cpqr_partial(a, k): q m x k (may be NULL), s k x n, pivots n */
+int lr_cpqr_partial(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q,
+                    double* s, int64_t* pivots);
+int lr_cpqr_partial_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q,
+                      double* s, int64_t* pivots);
+/* cpqr.hpp:118-122 cpqr_full(a): k = min(m, n) */
+int lr_cpqr_full(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double* q, double* s,
+                 int64_t* pivots);
+
+/* solve.hpp:104-145 stabilized_coeff_solve(s11, s12, strategy): t k x nc */
+int lr_stabilized_coeff_solve(lr_ctx* ctx, int64_t k, int64_t nc, const double* s11, int64_t ld11,
+                              const double* s12, int64_t ld12, lr_solve_strategy strategy, double* t);
+
+/* svd.hpp:132-183 svd(a): r = min(m,n); u m x r, sigma r, v n x r */
+int lr_svd(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double* u, double* sigma, double* v);
+/* svd.hpp:193-207 pinv(a, threshold): out n x m */
+int lr_pinv(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double threshold, double* out);
+
+/* id.hpp:91-105 id_column(a, k, strategy): pivots n, coeff k x (n-k) */
+int lr_id_column(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                 lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+/* id.hpp:108-119 id_row(a, k, strategy): pivots m, coeff k x (m-k) */
+int lr_id_row(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+              lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+
+/* sketch.hpp:200-223 randomized_id(a, k, cfg, strategy): pivots n, coeff k x (n-k) */
+int lr_randomized_id(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                     lr_sketch_config cfg, lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+int lr_randomized_id_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       lr_sketch_config cfg, lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+
+/* id.hpp:124-134 tsid_from_column_id(a, col_id, strategy): row pivots m,
+   row coeff k x (m-k), skeleton k x k.  (col coeff is carried by the caller) */
+int lr_tsid_from_column_id(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                           const int64_t* col_pivots, lr_solve_strategy strategy, int64_t* row_pivots,
+                           double* row_coeff, double* skeleton);
+
+/* cur.hpp:23-34 cur_from_two_sided(a, tsid, thr) (u_mode LR_U_VT_RPINV) or the
+   lowrank_main.cpp:215 middle factor (LR_U_CPINV_A_RPINV): c m x k, u k x k, r k x n */
+int lr_cur_from_two_sided(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                          const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots,
+                          double pinv_threshold, int u_mode, double* c, double* u, double* r);
+
+/* sketch.hpp:227-234 randomized_cur(a, k, cfg, strategy, thr) (+ u_mode).
+   Optional outputs (may be NULL): col_coeff k x (n-k), row_coeff k x (m-k), skeleton k x k */
+int lr_randomized_cur(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                      lr_sketch_config cfg, lr_solve_strategy strategy, double pinv_threshold, int u_mode,
+                      int64_t* col_pivots, int64_t* row_pivots, double* c, double* u, double* r,
+                      double* col_coeff, double* row_coeff, double* skeleton);
+int lr_randomized_cur_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                        lr_sketch_config cfg, lr_solve_strategy strategy, double pinv_threshold, int u_mode,
+                        int64_t* col_pivots, int64_t* row_pivots, double* c, double* u, double* r,
+                        double* col_coeff, double* row_coeff, double* skeleton);
+
+/* cur.hpp:37-42 cur_id(a, k, strategy, thr) (+ u_mode), deterministic */
+int lr_cur_id(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+              lr_solve_strategy strategy, double pinv_threshold, int u_mode, int64_t* col_pivots,
+              int64_t* row_pivots, double* c, double* u, double* r, double* col_coeff, double* row_coeff,
+              double* skeleton);
+int lr_cur_id_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                lr_solve_strategy strategy, double pinv_threshold, int u_mode, int64_t* col_pivots,
+                int64_t* row_pivots, double* c, double* u, double* r, double* col_coeff, double* row_coeff,
+                double* skeleton);
+
+/* ||A - C U R||_F and ||A||_F (core.hpp:64-67 on cur.hpp:77-80): out[0], out[1] */
+int lr_cur_error_fro(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                     const double* c, const double* u, const double* r, double* out);
+int lr_cur_error_fro_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       const double* c, const double* u, const double* r, double* out);
+
+/* Y (M x N) = P^T Q on the DMMA GEMM (benchmark / test access to the contraction kernel) */
+int lr_gemm_tn_d(lr_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
+                 int64_t ldq, double* out, int64_t ldo);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

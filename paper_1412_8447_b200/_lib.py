@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in include/lowrank_b200.h.
+
+The shared library ``liblowrank_b200.so`` is built in-tree by
+``__graft_entry__.build()`` (``make -C paper_1412_8447_b200/csrc``).  There is
+no CPU fallback: if the library or a B200 is missing, creating a context
+raises ``LowrankCudaError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblowrank_b200.so")
+
+LR_OK, LR_EINVAL, LR_ESINGULAR, LR_ECONVERGE, LR_ERUNTIME, LR_ECUDA, LR_EUNSUPPORTED = range(7)
+LR_SOLVE_BACKSUB, LR_SOLVE_PINV, LR_SOLVE_TIKHONOV = range(3)
+LR_SKETCH_GAUSSIAN, LR_SKETCH_SRFT = range(2)
+LR_U_VT_RPINV, LR_U_CPINV_A_RPINV = range(2)
+
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_dp = ctypes.c_void_p  # double* (host or device address)
+c_ip = ctypes.c_void_p  # int64_t*
+
+
+class lr_solve_strategy(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("threshold", ctypes.c_double), ("ridge", ctypes.c_double),
+                ("escalate", ctypes.c_int)]
+
+
+class lr_sketch_config(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("oversample", ctypes.c_int), ("srft_samples", c_i64),
+                ("power", ctypes.c_int), ("reorthonormalize", ctypes.c_int), ("seed", c_u64)]
+
+
+class lr_stats(ctypes.Structure):
+    _fields_ = [("cpqr_steps", ctypes.c_longlong), ("norm_recomputes", ctypes.c_longlong),
+                ("solve_escalated", ctypes.c_int), ("pinv_fast_path", ctypes.c_int)]
+
+
+# every exported symbol of include/lowrank_b200.h with its argument types
+SIGNATURES = {
+    "lr_last_error": ([], ctypes.c_char_p),
+    "lr_last_singular_index": ([], c_i64),
+    "lr_solve_strategy_default": ([], lr_solve_strategy),
+    "lr_sketch_config_default": ([], lr_sketch_config),
+    "lr_ctx_create": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int], ctypes.c_int),
+    "lr_ctx_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_set_stream": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_get_stats": ([ctypes.c_void_p, ctypes.POINTER(lr_stats)], ctypes.c_int),
+    "lr_ctx_synchronize": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_gaussian_matrix": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
+    "lr_gaussian_matrix_d": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp, c_i64], ctypes.c_int),
+    "lr_sketch_gaussian": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
+    "lr_sketch_gaussian_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_u64, c_dp, c_i64],
+                             ctypes.c_int),
+    "lr_cpqr_partial": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_ip], ctypes.c_int),
+    "lr_cpqr_partial_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_ip], ctypes.c_int),
+    "lr_cpqr_full": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp, c_ip], ctypes.c_int),
+    "lr_stabilized_coeff_solve": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, lr_solve_strategy,
+                                   c_dp], ctypes.c_int),
+    "lr_svd": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp, c_dp], ctypes.c_int),
+    "lr_pinv": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, ctypes.c_double, c_dp], ctypes.c_int),
+    "lr_id_column": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
+                     ctypes.c_int),
+    "lr_id_row": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
+                  ctypes.c_int),
+    "lr_randomized_id": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config,
+                          lr_solve_strategy, c_ip, c_dp], ctypes.c_int),
+    "lr_randomized_id_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config,
+                            lr_solve_strategy, c_ip, c_dp], ctypes.c_int),
+    "lr_tsid_from_column_id": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, lr_solve_strategy,
+                                c_ip, c_dp, c_dp], ctypes.c_int),
+    "lr_cur_from_two_sided": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp, c_ip,
+                               ctypes.c_double, ctypes.c_int, c_dp, c_dp, c_dp], ctypes.c_int),
+    "lr_randomized_cur": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config,
+                           lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip, c_dp, c_dp, c_dp, c_dp,
+                           c_dp, c_dp], ctypes.c_int),
+    "lr_randomized_cur_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config,
+                             lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip, c_dp, c_dp, c_dp, c_dp,
+                             c_dp, c_dp], ctypes.c_int),
+    "lr_cur_id": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, ctypes.c_double,
+                   ctypes.c_int, c_ip, c_ip, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),
+    "lr_cur_id_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, ctypes.c_double,
+                     ctypes.c_int, c_ip, c_ip, c_dp, c_dp, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),
+    "lr_cur_error_fro": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp],
+                         ctypes.c_int),
+    "lr_cur_error_fro_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp],
+                           ctypes.c_int),
+    "lr_gemm_tn_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64],
+                     ctypes.c_int),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class LowrankCudaError(RuntimeError):
+    """The B200 library or device is unavailable (no CPU fallback exists)."""
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load liblowrank_b200.so and bind every C-ABI symbol (fails loudly)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise LowrankCudaError(
+                f"{path} is missing: build it with __graft_entry__.build() (there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib

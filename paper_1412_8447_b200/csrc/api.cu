@@ -1,0 +1,1025 @@
+// api.cu -- the C ABI (include/lowrank_b200.h) and the host orchestration of
+// the ID / CUR pipeline over the sm_100a kernels.  Every entry point mirrors
+// one template of the reference library (cited per function) in argument
+// meaning, validation order and error class; the arithmetic runs on the GPU
+// only (no CPU fallback: a missing device is LR_ECUDA).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lowrank_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace lrb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_sing = -1;
+
+struct LrError {
+  int code;
+  std::string msg;
+  int64_t index;
+};
+[[noreturn]] void fail(int code, const std::string& msg, int64_t index = -1) { throw LrError{code, msg, index}; }
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return LR_OK;
+  } catch (const LrError& e) {
+    g_err = e.msg;
+    if (e.code == LR_ESINGULAR) g_sing = e.index;
+    return e.code;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return LR_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return LR_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LR_ERUNTIME;
+  }
+}
+
+inline int64_t even(int64_t x) { return x + (x & 1); }
+
+// stream-ordered device buffer from the (caching) default memory pool
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  cudaStream_t st = nullptr;
+  DBuf() = default;
+  DBuf(size_t n, cudaStream_t s) : st(s) {
+    LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(n, 1), s));
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    reset();
+    p = o.p;
+    st = o.st;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  operator T*() const { return p; }
+};
+
+}  // namespace
+
+struct lr_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t st = nullptr;
+  Workspace ws;
+  int* h_flags = nullptr;  // pinned
+  double* h_scal = nullptr;
+  long long* h_ll = nullptr;
+  lr_stats stats{};
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+void sync(lr_ctx* c) { LRB_CUDA(cudaStreamSynchronize(c->st)); }
+
+void require_nonempty(int64_t m, int64_t n, const char* who) {
+  if (m < 1 || n < 1) fail(LR_EINVAL, std::string(who) + ": matrix must be nonempty");
+}
+void require_rank_in_range(int64_t k, int64_t rows, int64_t cols, const char* who) {
+  if (k < 1 || k > std::min(rows, cols))
+    fail(LR_EINVAL, std::string(who) + ": rank " + std::to_string(k) + " out of range for " + std::to_string(rows) +
+                        "x" + std::to_string(cols) + " matrix");
+}
+void require_sample_count(int64_t ell, int64_t rows, const char* who) {
+  if (ell < 1 || ell > rows)
+    fail(LR_EINVAL, std::string(who) + ": sample count " + std::to_string(ell) + " out of range for " +
+                        std::to_string(rows) + " rows");
+}
+void require_ld(int64_t rows, int64_t ld, const char* who) {
+  if (ld < std::max<int64_t>(rows, 1)) fail(LR_EINVAL, std::string(who) + ": leading dimension smaller than rows");
+}
+
+bool device_all_finite(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda) {
+  DBuf<int> f(1, c->st);
+  LRB_CUDA(cudaMemsetAsync(f.p, 0, sizeof(int), c->st));
+  check_finite(m, n, a, lda, f, c->st);
+  LRB_CUDA(cudaMemcpyAsync(c->h_flags, f.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return c->h_flags[0] == 0;
+}
+
+// GEMM wrapper: pads misaligned operands (TMA needs 16B-aligned base and ld)
+void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
+          double* out, int64_t ldo, double alpha = 1.0, double beta = 0.0, int splits = -1) {
+  auto ok = [](const double* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0); };
+  DBuf<double> pp, qq;
+  if (!ok(P, ldp)) {
+    const int64_t l = even(K);
+    pp = DBuf<double>((size_t)l * M, c->st);
+    copy_matrix(K, M, P, ldp, pp, l, c->st);
+    P = pp;
+    ldp = l;
+  }
+  if (!ok(Q, ldq)) {
+    const int64_t l = even(K);
+    qq = DBuf<double>((size_t)l * N, c->st);
+    copy_matrix(K, N, Q, ldq, qq, l, c->st);
+    Q = qq;
+    ldq = l;
+  }
+  gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st);
+}
+
+// ---------------------------------------------------------------- CPQR
+// In-place CPQR of a working matrix W (ld even, 16B aligned).  Throws the
+// reference's non-finite error for `who`.
+void cpqr_core(lr_ctx* c, int64_t m, int64_t n, double* W, int64_t ldw, int64_t k, int64_t* piv, double* tau,
+               const char* who) {
+  DBuf<int> flags(1, c->st);
+  DBuf<long long> rec(1, c->st);
+  LRB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), c->st));
+  LRB_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(long long), c->st));
+  cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, c->st);
+  LRB_CUDA(cudaMemcpyAsync(c->h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  LRB_CUDA(cudaMemcpyAsync(c->h_ll, rec.p, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (c->h_flags[0]) fail(LR_EINVAL, std::string(who) + ": matrix has non-finite entries");
+  c->stats.cpqr_steps += k;
+  c->stats.norm_recomputes += c->h_ll[0];
+}
+
+// ---------------------------------------------------------------- triangular solve
+void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out, int64_t ldo);
+
+// solve.hpp:104-145 on device.  s11 upper part (+ diagonal) is used; when
+// `check_inputs` the reference's validation (finite, strictly-lower zero) runs.
+void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld11, const double* s12, int64_t ld12,
+                const lr_solve_strategy& strat, double* t, int64_t ldt, bool check_inputs) {
+  if (check_inputs) {
+    DBuf<int> fl(2, c->st);
+    LRB_CUDA(cudaMemsetAsync(fl.p, 0, 2 * sizeof(int), c->st));
+    check_upper_triangular(k, s11, ld11, fl, c->st);
+    check_finite(k, nc, s12, ld12, fl.p + 1, c->st);
+    LRB_CUDA(cudaMemcpyAsync(c->h_flags, fl.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (c->h_flags[1]) fail(LR_EINVAL, "stabilized_coeff_solve: non-finite entries");
+    if (c->h_flags[0]) fail(LR_EINVAL, "stabilized_coeff_solve: block is not upper triangular");
+  }
+  c->stats.solve_escalated = 0;
+  if (nc == 0) return;
+  int kind = strat.kind;
+  if (kind == LR_SOLVE_BACKSUB && strat.escalate) {
+    DBuf<double> mm(2, c->st);
+    diag_absminmax(k, s11, ld11, mm, c->st);
+    LRB_CUDA(cudaMemcpyAsync(c->h_scal, mm.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const double dmax = c->h_scal[0], dmin = c->h_scal[1];
+    if (dmax == 0.0 || dmin == 0.0 || dmax / dmin > 1e10) kind = LR_SOLVE_PINV;
+  }
+  if (kind == LR_SOLVE_BACKSUB) {
+    DBuf<double> Mt((size_t)k * k, c->st);
+    DBuf<int> zr(k, c->st);
+    backsub_operator_t(k, s11, ld11, strat.threshold, Mt, zr, c->st);
+    gemm(c, k, nc, k, Mt, k, s12, ld12, t, ldt);
+    if (!strat.escalate) {  // allow_singularity_error (solve.hpp:75-83)
+      std::vector<int> hz(k);
+      LRB_CUDA(cudaMemcpyAsync(hz.data(), zr.p, sizeof(int) * k, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      bool any = false;
+      for (int z : hz) any |= z != 0;
+      if (any) {
+        DBuf<double> res(k, c->st), part(4 * num_sms() + 4, c->st), smax(1, c->st);
+        max_abs(k, nc, s12, ld12, part, smax, c->st);
+        backsub_residual_rows(k, nc, s11, ld11, s12, ld12, t, ldt, hz.data(), res, c->st);
+        std::vector<double> hres(k);
+        double rhs_scale = 0.0;
+        LRB_CUDA(cudaMemcpyAsync(hres.data(), res.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
+        LRB_CUDA(cudaMemcpyAsync(&rhs_scale, smax.p, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        for (int64_t i = k - 1; i >= 0; --i)
+          if (hz[i] && hres[i] > strat.threshold * rhs_scale)
+            fail(LR_ESINGULAR,
+                 "stabilized_coeff_solve: zero diagonal with inconsistent right-hand side at index " +
+                     std::to_string(i),
+                 i);
+      }
+    }
+    return;
+  }
+  if (kind == LR_SOLVE_PINV) {
+    c->stats.solve_escalated = 1;
+    // clean upper-triangular copy (the working matrix carries reflectors below the diagonal)
+    DBuf<double> s((size_t)k * k, c->st), sp((size_t)k * k, c->st), spt((size_t)k * k, c->st);
+    copy_upper(k, s11, ld11, s, k, c->st);
+    pinv_core(c, k, k, s, k, strat.threshold, sp, k);
+    transpose_matrix(k, k, sp, k, spt, k, c->st);
+    gemm(c, k, nc, k, spt, k, s12, ld12, t, ldt);
+    return;
+  }
+  // Tikhonov (solve.hpp:133-142): (S11^T S11 + ridge^2 I) T = S11^T S12, solved
+  // by Cholesky on the GPU (the reference runs CG to 1e-28 relative residual).
+  DBuf<double> s((size_t)k * k, c->st), rhs((size_t)k * nc, c->st);
+  copy_upper(k, s11, ld11, s, k, c->st);
+  DBuf<double> eye((size_t)k * k, c->st);
+  {
+    std::vector<double> he((size_t)k * k, 0.0);
+    for (int64_t i = 0; i < k; ++i) he[i + i * k] = strat.ridge * strat.ridge;
+    LRB_CUDA(cudaMemcpyAsync(eye.p, he.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, c->st));
+    sync(c);
+  }
+  gemm(c, k, k, k, s, k, s, k, eye, k, 1.0, 1.0);  // eye = S^T S + ridge^2 I
+  gemm(c, k, nc, k, s, k, s12, ld12, rhs, k);      // rhs = S^T S12
+  DBuf<int> info(1, c->st);
+  cholesky_upper(k, eye, k, info, c->st);
+  DBuf<double> ri((size_t)k * k, c->st), rit((size_t)k * k, c->st), y((size_t)k * nc, c->st);
+  tri_upper_inverse(k, eye, k, ri, k, c->st);
+  transpose_matrix(k, k, ri, k, rit, k, c->st);
+  gemm(c, k, nc, k, ri, k, rhs, k, y, k);     // y = R^-T rhs
+  gemm(c, k, nc, k, rit, k, y, k, t, ldt);    // t = R^-1 y
+}
+
+// ---------------------------------------------------------------- SVD / pinv
+void svd_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* u, double* sigma, double* v) {
+  const bool transposed = m < n;
+  if (!transposed) {
+    if (!jacobi_svd(c->ws, m, n, a, lda, u, sigma, v, c->st))
+      fail(LR_ECONVERGE, "svd: one-sided Jacobi did not converge within 60 sweeps for " + std::to_string(m) + "x" +
+                             std::to_string(n) + " input");
+    return;
+  }
+  DBuf<double> at((size_t)n * m, c->st);
+  transpose_matrix(m, n, a, lda, at, n, c->st);
+  // svd of a^T (n x m): ub (n x m), vb (m x m); swap (svd.hpp:181)
+  if (!jacobi_svd(c->ws, n, m, at, n, v, sigma, u, c->st))
+    fail(LR_ECONVERGE, "svd: one-sided Jacobi did not converge within 60 sweeps for " + std::to_string(m) + "x" +
+                           std::to_string(n) + " input");
+}
+
+// out (n x m) = V_r diag(1/s) U_r^T with rank r = #{s >= thr * s_1}
+void pinv_svd_path(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out,
+                   int64_t ldo) {
+  const int64_t r = std::min(m, n);
+  DBuf<double> u((size_t)m * r, c->st), s(r, c->st), v((size_t)n * r, c->st);
+  svd_core(c, m, n, a, lda, u, s, v);
+  std::vector<double> hs(r);
+  LRB_CUDA(cudaMemcpyAsync(hs.data(), s.p, sizeof(double) * r, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  int64_t rank = 0;
+  if (hs[0] != 0.0)
+    while (rank < r && hs[rank] >= thr * hs[0]) ++rank;
+  if (rank == 0) {
+    for (int64_t j = 0; j < m; ++j) LRB_CUDA(cudaMemsetAsync(out + j * ldo, 0, sizeof(double) * n, c->st));
+    return;
+  }
+  // P = (V_r D)^T (rank x n), Q = U_r^T (rank x m); out = P^T Q
+  std::vector<double> inv(rank);
+  for (int64_t l = 0; l < rank; ++l) inv[l] = 1.0 / hs[l];
+  DBuf<double> vd((size_t)n * rank, c->st), P((size_t)even(rank) * n, c->st), Q((size_t)even(rank) * m, c->st);
+  copy_matrix(n, rank, v, n, vd, n, c->st);
+  for (int64_t l = 0; l < rank; ++l) scale_matrix((int)n, 1, vd.p + l * n, n, inv[l], c->st);
+  transpose_matrix(n, rank, vd, n, P, even(rank), c->st);
+  transpose_matrix(m, rank, u, m, Q, even(rank), c->st);
+  gemm(c, n, m, rank, P, even(rank), Q, even(rank), out, ldo);
+}
+
+// CholeskyQR2 of a tall X (rows x k, ld) given also X^T (k x rows, ldt):
+// R (k x k upper) with X = Q R, Rinv = R^-1.  Returns false when the Gram
+// factorisation breaks down or cond bound ||R||_F ||R^-1||_F > 1e7.
+bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, const double* Xt, int64_t ldxt,
+             double* R, double* Rinv) {
+  DBuf<double> G((size_t)k * k, c->st), R1inv((size_t)k * k, c->st), Q1((size_t)even(rows) * k, c->st);
+  DBuf<int> info(2, c->st);
+  gemm(c, k, k, rows, X, ldx, X, ldx, G, k);  // G1 = X^T X
+  cholesky_upper(k, G, k, info, c->st);        // G <- R1
+  LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (c->h_flags[0] != 0) return false;
+  tri_upper_inverse(k, G, k, R1inv, k, c->st);
+  gemm(c, rows, k, k, Xt, ldxt, R1inv, k, Q1, even(rows));  // Q1 = X R1^-1
+  DBuf<double> G2((size_t)k * k, c->st), R2t((size_t)k * k, c->st);
+  gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k);  // G2 = Q1^T Q1
+  cholesky_upper(k, G2, k, info.p + 1, c->st);
+  LRB_CUDA(cudaMemcpyAsync(c->h_flags + 1, info.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (c->h_flags[1] != 0) return false;
+  // R = R2 R1: R(i,j) = sum_l R2(i,l) R1(l,j) -> P = R2^T
+  transpose_matrix(k, k, G2, k, R2t, k, c->st);
+  gemm(c, k, k, k, R2t, k, G, k, R, k);
+  tri_upper_inverse(k, R, k, Rinv, k, c->st);
+  DBuf<double> part(4 * num_sms() + 4, c->st), f(2, c->st);
+  frob2(k, k, R, k, part, f, c->st);
+  frob2(k, k, Rinv, k, part, f.p + 1, c->st);
+  LRB_CUDA(cudaMemcpyAsync(c->h_scal, f.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  const double cond_bound = std::sqrt(c->h_scal[0]) * std::sqrt(c->h_scal[1]);
+  return std::isfinite(cond_bound) && cond_bound < 1e7;
+}
+
+void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out, int64_t ldo) {
+  if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+  require_nonempty(m, n, "svd");
+  if (!device_all_finite(c, m, n, a, lda)) fail(LR_EINVAL, "svd: matrix has non-finite entries");
+  // fast path on the tall orientation when provably no singular value is truncated
+  const bool tall = m >= n;
+  const int64_t rows = tall ? m : n, k = tall ? n : m;
+  if (rows >= 2 * k && k >= 8) {
+    DBuf<double> X((size_t)even(rows) * k, c->st), Xt((size_t)even(k) * rows, c->st);
+    if (tall) {
+      copy_matrix(m, n, a, lda, X, even(rows), c->st);
+      transpose_matrix(m, n, a, lda, Xt, even(k), c->st);
+    } else {
+      transpose_matrix(m, n, a, lda, X, even(rows), c->st);
+      copy_matrix(m, n, a, lda, Xt, even(k), c->st);
+    }
+    DBuf<double> R((size_t)k * k, c->st), Ri((size_t)k * k, c->st);
+    if (cholqr2(c, rows, k, X, even(rows), Xt, even(k), R, Ri)) {
+      // X^+ = R^-1 R^-T X^T (k x rows).  Qt = R^-T X^T: Qt(l,j) = sum_t Ri(t,l) Xt(t,j)
+      DBuf<double> Qt((size_t)even(k) * rows, c->st), Rit((size_t)k * k, c->st);
+      gemm(c, k, rows, k, Ri, k, Xt, even(k), Qt, even(k));
+      transpose_matrix(k, k, Ri, k, Rit, k, c->st);
+      if (tall) {
+        gemm(c, k, rows, k, Rit, k, Qt, even(k), out, ldo);  // out (n x m) = R^-1 Qt
+      } else {
+        DBuf<double> xp((size_t)k * rows, c->st);
+        gemm(c, k, rows, k, Rit, k, Qt, even(k), xp, k);  // pinv(a^T) (m x n)
+        transpose_matrix(k, rows, xp, k, out, ldo, c->st);
+      }
+      c->stats.pinv_fast_path = 1;
+      return;
+    }
+  }
+  c->stats.pinv_fast_path = 0;
+  pinv_svd_path(c, m, n, a, lda, thr, out, ldo);
+}
+
+// ---------------------------------------------------------------- pipelines
+struct ColumnIdDev {
+  DBuf<double> W;  // working matrix after CPQR (k rows of s in its top)
+  int64_t ldw = 0;
+};
+
+// id.hpp:91-105 on a working copy; pivots/coeff device pointers
+void id_column_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                    const lr_solve_strategy& strat, int64_t* piv, double* coeff, int64_t ldc) {
+  require_rank_in_range(k, m, n, "id_column");
+  require_nonempty(m, n, "cpqr_partial");
+  const int64_t ldw = even(m);
+  DBuf<double> W((size_t)ldw * n, c->st), tau(k, c->st);
+  copy_matrix(m, n, a, lda, W, ldw, c->st);
+  cpqr_core(c, m, n, W, ldw, k, piv, tau, "cpqr_partial");
+  solve_core(c, k, n - k, W, ldw, W.p + k * ldw, ldw, strat, coeff, ldc, false);
+}
+
+// sketch.hpp:67-78 into y (ell x n, ldy); a must be validated by the caller
+void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
+                 double* y, int64_t ldy) {
+  DBuf<double> omt((size_t)m * even(ell), c->st);
+  // Omega^T (m x ell): element (i,j) of Omega stored at omt[j + i*m]
+  gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  gemm(c, ell, n, m, omt, m, a, lda, y, ldy);
+}
+
+// sketch.hpp:200-223
+void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                        const lr_sketch_config& cfg, const lr_solve_strategy& strat, int64_t* piv, double* coeff,
+                        int64_t ldc) {
+  require_rank_in_range(k, m, n, "randomized_id");
+  if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
+    fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch with power 0 runs on the B200 path");
+  const int64_t ell = k + cfg.oversample;
+  if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
+  require_nonempty(m, n, "sketch_gaussian");
+  require_sample_count(ell, m, "sketch_gaussian");
+  const int64_t ldy = even(ell);
+  DBuf<double> Y((size_t)ldy * n, c->st);
+  sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
+  const int64_t steps = std::min(ell, n);  // cpqr_full
+  if (steps < k) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
+  DBuf<double> tau(steps, c->st);
+  try {
+    cpqr_core(c, ell, n, Y, ldy, steps, piv, tau, "cpqr_partial");
+  } catch (const LrError& e) {
+    // Y is non-finite: distinguish a non-finite A (sketch_gaussian's check) from overflow in Y
+    if (e.code == LR_EINVAL && !device_all_finite(c, m, n, a, lda))
+      fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+    throw;
+  }
+  solve_core(c, k, n - k, Y, ldy, Y.p + k * ldy, ldy, strat, coeff, ldc, false);
+}
+
+// id.hpp:124-134: row ID of C = A(:, J) (full rank) + skeleton
+void tsid_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
+               const lr_solve_strategy& strat, int64_t* row_piv, double* row_coeff, int64_t ldrc, double* skeleton,
+               double* C_out /* m x k or null */, double* Ct_keep /* k x m (ld even(k)) or null */) {
+  (void)n;
+  DBuf<double> Cb;
+  double* C = C_out;
+  if (!C) {
+    Cb = DBuf<double>((size_t)m * k, c->st);
+    C = Cb;
+  }
+  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
+  const int64_t ldct = even(k);
+  DBuf<double> Ct((size_t)ldct * m, c->st);
+  transpose_matrix(m, k, C, m, Ct, ldct, c->st);
+  if (Ct_keep) copy_matrix(k, m, Ct, ldct, Ct_keep, ldct, c->st);
+  // id_row(c, k) = id_column(c^T, k) (id.hpp:109-119)
+  require_rank_in_range(k, k, m, "id_column");
+  DBuf<double> tau(k, c->st);
+  cpqr_core(c, k, m, Ct, ldct, k, row_piv, tau, "cpqr_partial");
+  solve_core(c, k, m - k, Ct, ldct, Ct.p + k * ldct, ldct, strat, row_coeff, ldrc, false);
+  if (skeleton) gather_rows(k, k, C, m, row_piv, skeleton, k, c->st);
+}
+
+// cur.hpp:23-34 / lowrank_main.cpp:215 given skeleton index sets
+void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
+              const double* col_coeff, int64_t ldcc, const int64_t* row_piv, double thr, int u_mode, double* C,
+              double* U, double* R, const double* Ct_in /* k x m ld even(k), may be null */) {
+  if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
+  gather_rows(k, n, a, lda, row_piv, R, k, c->st);
+  const int64_t ldk = even(k);
+  DBuf<double> Ctb;
+  const double* Ct = Ct_in;
+  if (!Ct) {
+    Ctb = DBuf<double>((size_t)ldk * m, c->st);
+    transpose_matrix(m, k, C, m, Ctb, ldk, c->st);
+    Ct = Ctb;
+  }
+  DBuf<double> Rt((size_t)even(n) * k, c->st), Rk((size_t)ldk * n, c->st);
+  transpose_matrix(k, n, R, k, Rt, even(n), c->st);
+  copy_matrix(k, n, R, k, Rk, ldk, c->st);  // R with an even leading dimension for TMA
+  DBuf<double> Sr((size_t)k * k, c->st), Sri((size_t)k * k, c->st);
+  const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
+  c->stats.pinv_fast_path = 0;
+  if (u_mode == LR_U_CPINV_A_RPINV) {
+    DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st);
+    DBuf<double> Cm((size_t)even(m) * k, c->st);
+    copy_matrix(m, k, C, m, Cm, even(m), c->st);
+    const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci);
+    if (c_ok && r_ok) {
+      c->stats.pinv_fast_path = 1;
+      // U = Rc^-1 Rc^-T (C^T A R^T) Sr^-1 Sr^-T
+      DBuf<double> Xt((size_t)even(n) * k, c->st), W((size_t)k * k, c->st);
+      gemm(c, n, k, m, a, lda, Cm, even(m), Xt, even(n));        // X^T = A^T C  (n x k)
+      gemm(c, k, k, n, Xt, even(n), Rt, even(n), W, k);          // W = X R^T = C^T A R^T
+      DBuf<double> t1((size_t)k * k, c->st), t2((size_t)k * k, c->st), tt((size_t)k * k, c->st);
+      gemm(c, k, k, k, Rci, k, W, k, t1, k);                     // t1 = Rc^-T W
+      transpose_matrix(k, k, Rci, k, tt, k, c->st);
+      gemm(c, k, k, k, tt, k, t1, k, t2, k);                     // t2 = Rc^-1 t1
+      transpose_matrix(k, k, t2, k, tt, k, c->st);
+      gemm(c, k, k, k, tt, k, Sri, k, t1, k);                    // t1 = t2 Sr^-1
+      transpose_matrix(k, k, t1, k, tt, k, c->st);
+      transpose_matrix(k, k, Sri, k, t2, k, c->st);
+      gemm(c, k, k, k, tt, k, t2, k, U, k);                      // U = t1 Sr^-T
+      return;
+    }
+    // general path: explicit truncated pseudoinverses (SVD route when ill-conditioned)
+    DBuf<double> Cp((size_t)k * m, c->st), Rp((size_t)n * k, c->st);
+    pinv_core(c, m, k, C, m, thr, Cp, k);
+    pinv_core(c, k, n, R, k, thr, Rp, n);
+    // (Cp A) Rp: X^T = A^T Cp^T (n x k) then U = X Rp
+    DBuf<double> Cpt((size_t)even(m) * k, c->st), Xt((size_t)even(n) * k, c->st);
+    transpose_matrix(k, m, Cp, k, Cpt, even(m), c->st);
+    gemm(c, n, k, m, a, lda, Cpt, even(m), Xt, even(n));
+    DBuf<double> Rpe((size_t)even(n) * k, c->st);
+    copy_matrix(n, k, Rp, n, Rpe, even(n), c->st);
+    gemm(c, k, k, n, Xt, even(n), Rpe, even(n), U, k);
+    return;
+  }
+  // u = basis()^T pinv(r) (cur.hpp:30) = R+^T(:, J_skel)^T + coeff R+(J_res, :)
+  DBuf<double> Rpt((size_t)ldk * n, c->st);  // R+^T (k x n)
+  if (r_ok) {
+    c->stats.pinv_fast_path = 1;
+    DBuf<double> Qrt((size_t)ldk * n, c->st), Srit((size_t)k * k, c->st);
+    gemm(c, k, n, k, Sri, k, Rk, ldk, Qrt, ldk);  // Qr^T = Sr^-T R
+    transpose_matrix(k, k, Sri, k, Srit, k, c->st);
+    gemm(c, k, n, k, Srit, k, Qrt, ldk, Rpt, ldk);  // R+^T = Sr^-1 Qr^T
+  } else {
+    DBuf<double> Rp((size_t)n * k, c->st);
+    pinv_core(c, k, n, R, k, thr, Rp, n);
+    transpose_matrix(n, k, Rp, n, Rpt, ldk, c->st);
+  }
+  // G = R+^T(:, J): columns permuted by the column pivots
+  DBuf<double> G((size_t)ldk * n, c->st);
+  DBuf<int64_t> pv(n, c->st);
+  // col_piv holds the full permutation (n entries)
+  gather_columns(k, n, Rpt, ldk, col_piv, G, ldk, c->st);
+  // U^T = G_skel + G_res coeff^T -> U^T(b,a) = sum_l G_res^T(l,b) coeff^T(l,a)
+  const int64_t nr = n - k;
+  DBuf<double> Ut((size_t)k * k, c->st);
+  copy_matrix(k, k, G, ldk, Ut, k, c->st);
+  if (nr > 0) {
+    DBuf<double> Grt((size_t)even(nr) * k, c->st), cft((size_t)even(nr) * k, c->st);
+    transpose_matrix(k, nr, G.p + k * ldk, ldk, Grt, even(nr), c->st);
+    transpose_matrix(k, nr, col_coeff, ldcc, cft, even(nr), c->st);
+    gemm(c, k, k, nr, Grt, even(nr), cft, even(nr), Ut, k, 1.0, 1.0);
+  }
+  transpose_matrix(k, k, Ut, k, U, k, c->st);
+}
+
+void error_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* C,
+                const double* U, const double* R, double* out_host) {
+  const int64_t ldk = even(k);
+  DBuf<double> Ut((size_t)ldk * k, c->st), Rk((size_t)ldk * n, c->st), UR((size_t)ldk * n, c->st),
+      Ct((size_t)ldk * m, c->st);
+  transpose_matrix(k, k, U, k, Ut, ldk, c->st);
+  copy_matrix(k, n, R, k, Rk, ldk, c->st);
+  gemm(c, k, n, k, Ut, ldk, Rk, ldk, UR, ldk);  // UR = U R
+  transpose_matrix(m, k, C, m, Ct, ldk, c->st);
+  const int tiles = gemm_tn_grid_ctas((int)m, (int)n);
+  DBuf<double> part(std::max(tiles, 4 * num_sms()) + 4, c->st), res(2, c->st);
+  int np = 0;
+  const double* A = a;
+  DBuf<double> Apad;
+  gemm_tn_resid_sq(c->ws, (int)m, (int)n, (int)k, Ct, ldk, UR, ldk, A, lda, part, &np, c->st);
+  sum_partials(part, np, res, c->st);
+  frob2(m, n, a, lda, part, res.p + 1, c->st);
+  LRB_CUDA(cudaMemcpyAsync(out_host, res.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  out_host[0] = std::sqrt(out_host[0]);
+  out_host[1] = std::sqrt(out_host[1]);
+}
+
+// host <-> device staging helpers for the plain (host-pointer) entry points
+DBuf<double> to_dev(lr_ctx* c, int64_t m, int64_t n, const double* h, int64_t ld, int64_t* ld_out) {
+  const int64_t l = even(m);
+  DBuf<double> d((size_t)l * n, c->st);
+  LRB_CUDA(cudaMemcpy2DAsync(d.p, l * sizeof(double), h, ld * sizeof(double), m * sizeof(double), n,
+                             cudaMemcpyHostToDevice, c->st));
+  *ld_out = l;
+  return d;
+}
+void to_host(lr_ctx* c, int64_t m, int64_t n, const double* d, int64_t ldd, double* h, int64_t ldh) {
+  if (!h || m <= 0 || n <= 0) return;
+  LRB_CUDA(cudaMemcpy2DAsync(h, ldh * sizeof(double), d, ldd * sizeof(double), m * sizeof(double), n,
+                             cudaMemcpyDeviceToHost, c->st));
+}
+void idx_to_host(lr_ctx* c, int64_t n, const int64_t* d, int64_t* h) {
+  if (h && n > 0) LRB_CUDA(cudaMemcpyAsync(h, d, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+}
+
+lr_ctx* checked(lr_ctx* c) {
+  if (!c) fail(LR_EINVAL, "null lr_ctx");
+  LRB_CUDA(cudaSetDevice(c->device));
+  return c;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* lr_last_error(void) { return g_err.c_str(); }
+int64_t lr_last_singular_index(void) { return g_sing; }
+
+lr_solve_strategy lr_solve_strategy_default(void) { return {LR_SOLVE_BACKSUB, 1e-12, 0.0, 1}; }
+lr_sketch_config lr_sketch_config_default(void) { return {LR_SKETCH_GAUSSIAN, 10, 0, 0, 1, 0}; }
+
+int lr_ctx_create(lr_ctx** out, int device) {
+  return guard([&] {
+    if (!out) fail(LR_EINVAL, "lr_ctx_create: null output");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+      throw CudaError("lr_ctx_create: no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop;
+    LRB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError("lr_ctx_create: sm_100 (B200) device required");
+    LRB_CUDA(cudaSetDevice(device));
+    auto* c = new lr_ctx();
+    c->device = device;
+    LRB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->st = c->own;
+    LRB_CUDA(cudaMallocHost(&c->h_flags, 64));
+    LRB_CUDA(cudaMallocHost(&c->h_scal, 64));
+    LRB_CUDA(cudaMallocHost(&c->h_ll, 64));
+    cudaMemPool_t pool;
+    LRB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    LRB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = c;
+  });
+}
+
+int lr_ctx_destroy(lr_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    c->ws.release_all();
+    cudaFreeHost(c->h_flags);
+    cudaFreeHost(c->h_scal);
+    cudaFreeHost(c->h_ll);
+    cudaStreamDestroy(c->own);
+    delete c;
+  });
+}
+
+int lr_ctx_set_stream(lr_ctx* c, void* s) {
+  return guard([&] { checked(c)->st = s ? static_cast<cudaStream_t>(s) : c->own; });
+}
+int lr_ctx_get_stats(lr_ctx* c, lr_stats* out) {
+  return guard([&] { *out = checked(c)->stats; });
+}
+int lr_ctx_synchronize(lr_ctx* c) {
+  return guard([&] { sync(checked(c)); });
+}
+
+// rng.hpp:74-94
+int lr_gaussian_matrix_d(lr_ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ldo) {
+  return guard([&] {
+    checked(c);
+    if (rows < 1 || cols < 1) fail(LR_EINVAL, "gaussian_matrix: dimensions must be positive");
+    gaussian_matrix(rows, cols, seed, out, ldo, false, c->st);
+  });
+}
+int lr_gaussian_matrix(lr_ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+  return guard([&] {
+    checked(c);
+    if (rows < 1 || cols < 1) fail(LR_EINVAL, "gaussian_matrix: dimensions must be positive");
+    DBuf<double> d((size_t)rows * cols, c->st);
+    gaussian_matrix(rows, cols, seed, d, rows, false, c->st);
+    to_host(c, rows, cols, d, rows, out, rows);
+    sync(c);
+  });
+}
+
+// sketch.hpp:67-78
+int lr_sketch_gaussian_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
+                         double* y, int64_t ldy) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "sketch_gaussian");
+    require_ld(m, lda, "sketch_gaussian");
+    if (!device_all_finite(c, m, n, a, lda)) fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+    require_sample_count(ell, m, "sketch_gaussian");
+    sketch_core(c, m, n, a, lda, ell, seed, y, ldy);
+  });
+}
+int lr_sketch_gaussian(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
+                       double* y) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "sketch_gaussian");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    if (!device_all_finite(c, m, n, d, l)) fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+    require_sample_count(ell, m, "sketch_gaussian");
+    DBuf<double> yd((size_t)ell * n, c->st);
+    sketch_core(c, m, n, d, l, ell, seed, yd, ell);
+    to_host(c, ell, n, yd, ell, y, ell);
+    sync(c);
+  });
+}
+
+// cpqr.hpp:32-114
+int lr_cpqr_partial_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q, double* s,
+                      int64_t* pivots) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "cpqr_partial");
+    if (!device_all_finite(c, m, n, a, lda)) fail(LR_EINVAL, "cpqr_partial: matrix has non-finite entries");
+    require_rank_in_range(k, m, n, "cpqr_partial");
+    const int64_t ldw = even(m);
+    DBuf<double> W((size_t)ldw * n, c->st), tau(k, c->st);
+    copy_matrix(m, n, a, lda, W, ldw, c->st);
+    cpqr_core(c, m, n, W, ldw, k, pivots, tau, "cpqr_partial");
+    cpqr_extract_s(m, n, W, ldw, k, s, k, c->st);
+    if (q) cpqr_form_q(m, n, W, ldw, k, tau, q, m, c->st);
+  });
+}
+int lr_cpqr_partial(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q, double* s,
+                    int64_t* pivots) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "cpqr_partial");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    if (!device_all_finite(c, m, n, d, l)) fail(LR_EINVAL, "cpqr_partial: matrix has non-finite entries");
+    require_rank_in_range(k, m, n, "cpqr_partial");
+    DBuf<double> tau(k, c->st), sd((size_t)k * n, c->st), qd(q ? (size_t)m * k : 1, c->st);
+    DBuf<int64_t> pd(n, c->st);
+    cpqr_core(c, m, n, d, l, k, pd, tau, "cpqr_partial");
+    cpqr_extract_s(m, n, d, l, k, sd, k, c->st);
+    if (q) cpqr_form_q(m, n, d, l, k, tau, qd, m, c->st);
+    to_host(c, k, n, sd, k, s, k);
+    if (q) to_host(c, m, k, qd, m, q, m);
+    idx_to_host(c, n, pd, pivots);
+    sync(c);
+  });
+}
+int lr_cpqr_full(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* q, double* s,
+                 int64_t* pivots) {
+  if (m < 1 || n < 1) {
+    g_err = "cpqr_full: matrix must be nonempty";
+    return LR_EINVAL;
+  }
+  return lr_cpqr_partial(c, m, n, a, lda, std::min(m, n), q, s, pivots);
+}
+
+// solve.hpp:104-145
+int lr_stabilized_coeff_solve(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld11, const double* s12,
+                              int64_t ld12, lr_solve_strategy strat, double* t) {
+  return guard([&] {
+    checked(c);
+    if (k < 0 || nc < 0) fail(LR_EINVAL, "stabilized_coeff_solve: row count mismatch");
+    if (k == 0) return;
+    int64_t l11, l12 = even(k);
+    DBuf<double> d11 = to_dev(c, k, k, s11, ld11, &l11);
+    DBuf<double> d12 = nc > 0 ? to_dev(c, k, nc, s12, ld12, &l12) : DBuf<double>(1, c->st);
+    DBuf<double> td((size_t)k * std::max<int64_t>(nc, 1), c->st);
+    solve_core(c, k, nc, d11, l11, d12, l12, strat, td, k, true);
+    to_host(c, k, nc, td, k, t, k);
+    sync(c);
+  });
+}
+
+// svd.hpp:132-183 / 193-207
+int lr_svd(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* u, double* sigma, double* v) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "svd");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    if (!device_all_finite(c, m, n, d, l)) fail(LR_EINVAL, "svd: matrix has non-finite entries");
+    const int64_t r = std::min(m, n);
+    DBuf<double> ud((size_t)m * r, c->st), sd(r, c->st), vd((size_t)n * r, c->st);
+    svd_core(c, m, n, d, l, ud, sd, vd);
+    to_host(c, m, r, ud, m, u, m);
+    to_host(c, r, 1, sd, r, sigma, r);
+    to_host(c, n, r, vd, n, v, n);
+    sync(c);
+  });
+}
+int lr_pinv(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out) {
+  return guard([&] {
+    checked(c);
+    if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+    require_nonempty(m, n, "svd");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<double> od((size_t)n * m, c->st);
+    pinv_core(c, m, n, d, l, thr, od, n);
+    to_host(c, n, m, od, n, out, n);
+    sync(c);
+  });
+}
+
+// id.hpp:91-119
+int lr_id_column(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_solve_strategy strat,
+                 int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, m, n, "id_column");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> pd(n, c->st);
+    DBuf<double> cd((size_t)k * std::max<int64_t>(n - k, 1), c->st);
+    id_column_core(c, m, n, d, l, k, strat, pd, cd, k);
+    idx_to_host(c, n, pd, pivots);
+    to_host(c, k, n - k, cd, k, coeff, k);
+    sync(c);
+  });
+}
+int lr_id_row(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_solve_strategy strat,
+              int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, n, m, "id_column");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    const int64_t lt = even(n);
+    DBuf<double> dt((size_t)lt * m, c->st);
+    transpose_matrix(m, n, d, l, dt, lt, c->st);
+    DBuf<int64_t> pd(m, c->st);
+    DBuf<double> cd((size_t)k * std::max<int64_t>(m - k, 1), c->st);
+    id_column_core(c, n, m, dt, lt, k, strat, pd, cd, k);
+    idx_to_host(c, m, pd, pivots);
+    to_host(c, k, m - k, cd, k, coeff, k);
+    sync(c);
+  });
+}
+
+// sketch.hpp:200-223
+int lr_randomized_id_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       lr_sketch_config cfg, lr_solve_strategy strat, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "randomized_id");
+    randomized_id_core(c, m, n, a, lda, k, cfg, strat, pivots, coeff, k);
+  });
+}
+int lr_randomized_id(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_sketch_config cfg,
+                     lr_solve_strategy strat, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, m, n, "randomized_id");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> pd(n, c->st);
+    DBuf<double> cd((size_t)k * std::max<int64_t>(n - k, 1), c->st);
+    randomized_id_core(c, m, n, d, l, k, cfg, strat, pd, cd, k);
+    idx_to_host(c, n, pd, pivots);
+    to_host(c, k, n - k, cd, k, coeff, k);
+    sync(c);
+  });
+}
+
+// id.hpp:124-134
+int lr_tsid_from_column_id(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                           const int64_t* col_pivots, lr_solve_strategy strat, int64_t* row_pivots, double* row_coeff,
+                           double* skeleton) {
+  return guard([&] {
+    checked(c);
+    if (k < 1 || k > std::min(m, n)) require_rank_in_range(k, k, m, "id_column");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> cp(n, c->st), rp(m, c->st);
+    LRB_CUDA(cudaMemcpyAsync(cp.p, col_pivots, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+    DBuf<double> rc((size_t)k * std::max<int64_t>(m - k, 1), c->st), sk((size_t)k * k, c->st);
+    tsid_core(c, m, n, d, l, k, cp, strat, rp, rc, k, sk, nullptr, nullptr);
+    idx_to_host(c, m, rp, row_pivots);
+    to_host(c, k, m - k, rc, k, row_coeff, k);
+    to_host(c, k, k, sk, k, skeleton, k);
+    sync(c);
+  });
+}
+
+// cur.hpp:23-34, lowrank_main.cpp:210-215
+int lr_cur_from_two_sided(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                          const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots, double thr,
+                          int u_mode, double* C, double* U, double* R) {
+  return guard([&] {
+    checked(c);
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> cp(n, c->st), rp(m, c->st);
+    LRB_CUDA(cudaMemcpyAsync(cp.p, col_pivots, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+    LRB_CUDA(cudaMemcpyAsync(rp.p, row_pivots, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->st));
+    int64_t lcc = k;
+    DBuf<double> cc = n > k ? to_dev(c, k, n - k, col_coeff, k, &lcc) : DBuf<double>(1, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n, c->st);
+    cur_core(c, m, n, d, l, k, cp, cc, lcc, rp, thr, u_mode, Cd, Ud, Rd, nullptr);
+    to_host(c, m, k, Cd, m, C, m);
+    to_host(c, k, k, Ud, k, U, k);
+    to_host(c, k, n, Rd, k, R, k);
+    sync(c);
+  });
+}
+
+// sketch.hpp:227-234 (+ lowrank_main.cpp:215 when u_mode == LR_U_CPINV_A_RPINV)
+int lr_randomized_cur_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                        lr_sketch_config cfg, lr_solve_strategy strat, double thr, int u_mode, int64_t* col_pivots,
+                        int64_t* row_pivots, double* C, double* U, double* R, double* col_coeff, double* row_coeff,
+                        double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "randomized_cur");
+    DBuf<double> cc, rc;
+    if (!col_coeff) {
+      cc = DBuf<double>((size_t)k * std::max<int64_t>(n - k, 1), c->st);
+      col_coeff = cc;
+    }
+    if (!row_coeff) {
+      rc = DBuf<double>((size_t)k * std::max<int64_t>(m - k, 1), c->st);
+      row_coeff = rc;
+    }
+    randomized_id_core(c, m, n, a, lda, k, cfg, strat, col_pivots, col_coeff, k);
+    DBuf<double> Ct((size_t)even(k) * m, c->st);
+    tsid_core(c, m, n, a, lda, k, col_pivots, strat, row_pivots, row_coeff, k, skeleton, C, Ct);
+    cur_core(c, m, n, a, lda, k, col_pivots, col_coeff, k, row_pivots, thr, u_mode, C, U, R, Ct);
+  });
+}
+int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_sketch_config cfg,
+                      lr_solve_strategy strat, double thr, int u_mode, int64_t* col_pivots, int64_t* row_pivots,
+                      double* C, double* U, double* R, double* col_coeff, double* row_coeff, double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, m, n, "randomized_id");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> cp(n, c->st), rp(m, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n, c->st),
+        ccd((size_t)k * std::max<int64_t>(n - k, 1), c->st), rcd((size_t)k * std::max<int64_t>(m - k, 1), c->st),
+        skd((size_t)k * k, c->st);
+    randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k);
+    DBuf<double> Ct((size_t)even(k) * m, c->st);
+    tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
+    cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+    idx_to_host(c, n, cp, col_pivots);
+    idx_to_host(c, m, rp, row_pivots);
+    to_host(c, m, k, Cd, m, C, m);
+    to_host(c, k, k, Ud, k, U, k);
+    to_host(c, k, n, Rd, k, R, k);
+    to_host(c, k, n - k, ccd, k, col_coeff, k);
+    to_host(c, k, m - k, rcd, k, row_coeff, k);
+    to_host(c, k, k, skd, k, skeleton, k);
+    sync(c);
+  });
+}
+
+// cur.hpp:37-42 cur_id(a, k): id_two_sided -> cur_from_two_sided
+int lr_cur_id_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_solve_strategy strat,
+                double thr, int u_mode, int64_t* col_pivots, int64_t* row_pivots, double* C, double* U, double* R,
+                double* col_coeff, double* row_coeff, double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "cur_id");
+    DBuf<double> cc, rc;
+    if (!col_coeff) {
+      cc = DBuf<double>((size_t)k * std::max<int64_t>(n - k, 1), c->st);
+      col_coeff = cc;
+    }
+    if (!row_coeff) {
+      rc = DBuf<double>((size_t)k * std::max<int64_t>(m - k, 1), c->st);
+      row_coeff = rc;
+    }
+    id_column_core(c, m, n, a, lda, k, strat, col_pivots, col_coeff, k);
+    DBuf<double> Ct((size_t)even(k) * m, c->st);
+    tsid_core(c, m, n, a, lda, k, col_pivots, strat, row_pivots, row_coeff, k, skeleton, C, Ct);
+    cur_core(c, m, n, a, lda, k, col_pivots, col_coeff, k, row_pivots, thr, u_mode, C, U, R, Ct);
+  });
+}
+int lr_cur_id(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_solve_strategy strat,
+              double thr, int u_mode, int64_t* col_pivots, int64_t* row_pivots, double* C, double* U, double* R,
+              double* col_coeff, double* row_coeff, double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, m, n, "id_column");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<int64_t> cp(n, c->st), rp(m, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n, c->st),
+        ccd((size_t)k * std::max<int64_t>(n - k, 1), c->st), rcd((size_t)k * std::max<int64_t>(m - k, 1), c->st),
+        skd((size_t)k * k, c->st);
+    id_column_core(c, m, n, d, l, k, strat, cp, ccd, k);
+    DBuf<double> Ct((size_t)even(k) * m, c->st);
+    tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
+    cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+    idx_to_host(c, n, cp, col_pivots);
+    idx_to_host(c, m, rp, row_pivots);
+    to_host(c, m, k, Cd, m, C, m);
+    to_host(c, k, k, Ud, k, U, k);
+    to_host(c, k, n, Rd, k, R, k);
+    to_host(c, k, n - k, ccd, k, col_coeff, k);
+    to_host(c, k, m - k, rcd, k, row_coeff, k);
+    to_host(c, k, k, skd, k, skeleton, k);
+    sync(c);
+  });
+}
+
+int lr_cur_error_fro_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* C,
+                       const double* U, const double* R, double* out) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "cur_error_fro");
+    if (lda % 2 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0) {
+      const int64_t l = even(m);
+      DBuf<double> ap((size_t)l * n, c->st);
+      copy_matrix(m, n, a, lda, ap, l, c->st);
+      error_core(c, m, n, ap, l, k, C, U, R, out);
+      return;
+    }
+    error_core(c, m, n, a, lda, k, C, U, R, out);
+  });
+}
+int lr_cur_error_fro(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* C,
+                     const double* U, const double* R, double* out) {
+  return guard([&] {
+    checked(c);
+    int64_t l, lc, lu, lr;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    DBuf<double> Cd = to_dev(c, m, k, C, m, &lc);
+    DBuf<double> Ud = to_dev(c, k, k, U, k, &lu);
+    DBuf<double> Rd = to_dev(c, k, n, R, k, &lr);
+    // error_core expects C (ld m), U (ld k), R (ld k)
+    DBuf<double> Cc((size_t)m * k, c->st), Uc((size_t)k * k, c->st), Rc((size_t)k * n, c->st);
+    copy_matrix(m, k, Cd, lc, Cc, m, c->st);
+    copy_matrix(k, k, Ud, lu, Uc, k, c->st);
+    copy_matrix(k, n, Rd, lr, Rc, k, c->st);
+    error_core(c, m, n, d, l, k, Cc, Uc, Rc, out);
+  });
+}
+
+int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
+                 int64_t ldq, double* out, int64_t ldo) {
+  return guard([&] {
+    checked(c);
+    gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,468 @@
+// cpqr.cu -- truncated column-pivoted Householder QR on B200.
+//
+// Restates cpqr.hpp:32-114 exactly in its observable pivot semantics:
+//   * pivot = first maximum of the running squared norms over positions
+//     [step, n) (strict >, cpqr.hpp:49-51): ties go to the lowest position;
+//   * full-column swap of data, norm2, norm2_exact and pivot (cpqr.hpp:52-57);
+//   * reflector beta = -sign(alpha)|x|, tau = (beta-alpha)/beta, v = x/(alpha-beta)
+//     (cpqr.hpp:59-66), applied as W -= (tau v)(v^T W) (cpqr.hpp:68-75);
+//   * downdate norm2 -= W(step,j)^2 and exact recompute below 1e-6 of the last
+//     exact value (cpqr.hpp:78-84).
+//
+// B200 design: ONE persistent cooperative kernel runs all k steps.  Columns
+// are statically partitioned over CTAs (and round-robin over warps); a warp
+// owns a whole column and keeps up to 64*CH rows in registers (the sketch Y
+// and C^T have <= 512 rows, so one 16-byte load per lane per 64 rows moves the
+// column in and out exactly once per step).  Each step is one fused HBM pass
+//   dot(v, col) -> rank-1 update -> row-s downdate -> (rare) exact recompute
+//   -> per-warp / per-CTA argmax on (norm2 desc, position asc)
+// followed by a single grid barrier.  The winning CTA's best column is staged
+// in a double-buffered candidate slot, so every CTA rebuilds the next
+// reflector redundantly (identical inputs, fixed reduction tree => identical
+// bits) without a second barrier.  Rows > 64*CH (tall deterministic IDs)
+// stream through L2 in two passes.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace lrb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxSmemRows = 6144;  // v and tau*v kept in shared memory up to this height
+
+struct CpqrArgs {
+  double* W;
+  int64_t m, n, ld, k;
+  int64_t* piv;
+  double* nrm;
+  double* nrmx;
+  double* tau;
+  double* pval;      // [2][G]
+  long long* ppos;   // [2][G]
+  double* cand;      // [2][G][m]
+  double* scratch;   // [G][3*m]: old-s column, pivot R rows, (v,tv if not in smem)
+  int* flags;
+  unsigned long long* recomputes;
+};
+
+struct Best {
+  double v;
+  long long p;
+};
+__device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
+  return v1 > v2 || (v1 == v2 && p1 < p2);
+}
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
+    const long long op = __shfl_xor_sync(0xffffffffu, b.p, o);
+    if (better(ov, op, b.v, b.p)) { b.v = ov; b.p = op; }
+  }
+  return b;
+}
+
+// fixed-order CTA sum (all threads receive the result)
+__device__ double cta_sum(double x, double* sh) {
+  x = warp_sum(x);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[w] = x;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) t += sh[i];
+  return t;
+}
+
+template <int CH>
+__global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dyn[];
+  __shared__ double sh_red[kWarps];
+  __shared__ double sh_bv[kWarps];
+  __shared__ long long sh_bp[kWarps];
+  __shared__ double sh_scal[4];  // alpha, beta, tau, colnorm
+  __shared__ long long sh_piv[2];  // p, winner cta
+  __shared__ long long sh_state[3];  // piv[p], piv[s] (bits), unused
+  __shared__ double sh_nst[4];     // nrm[p], nrmx[p], nrm[s], nrmx[s]
+
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = a.m, n = a.n, ld = a.ld, k = a.k;
+  const int64_t c0 = n * cta / G, c1 = n * (cta + 1) / G;
+  double* scr = a.scratch + (int64_t)cta * 3 * m;
+  double* olds = scr;          // old column at position s (when swapped into p)
+  double* pivr = scr + m;      // pivot column rows < s
+  const bool vs = m <= kMaxSmemRows;
+  double* vv = vs ? dyn : scr + 2 * m;           // v[i] for i >= s (v[s] = 1)
+  double* tv = vs ? dyn + m : nullptr;  // tau*v; recomputed on the fly when v is not in smem
+  const int nchunks = (int)((m + 63) / 64);
+  unsigned long long my_recomputes = 0;
+
+  // ------------------------------------------------------------ init
+  {
+    Best b{-INFINITY, (long long)INT64_MAX};
+    int bad = 0;
+    for (int64_t j = c0 + warp; j < c1; j += kWarps) {
+      const double* col = a.W + j * ld;
+      double acc = 0.0;
+      for (int t = 0; t < nchunks; ++t) {
+        const int64_t i = 64 * t + 2 * lane;
+        if (i + 1 < m) {
+          const double2 x = *reinterpret_cast<const double2*>(col + i);
+          bad |= !isfinite(x.x) | !isfinite(x.y);
+          acc = fma(x.x, x.x, acc);
+          acc = fma(x.y, x.y, acc);
+        } else if (i < m) {
+          const double x = col[i];
+          bad |= !isfinite(x);
+          acc = fma(x, x, acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        a.nrm[j] = acc;
+        a.nrmx[j] = acc;
+        a.piv[j] = j;
+      }
+      if (better(acc, j, b.v, b.p)) { b.v = acc; b.p = j; }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags, 1);
+    if (lane == 0) { sh_bv[warp] = b.v; sh_bp[warp] = b.p; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Best cb{sh_bv[0], sh_bp[0]};
+      for (int w = 1; w < kWarps; ++w)
+        if (better(sh_bv[w], sh_bp[w], cb.v, cb.p)) { cb.v = sh_bv[w]; cb.p = sh_bp[w]; }
+      a.pval[cta] = cb.v;
+      a.ppos[cta] = cb.p;
+      sh_piv[0] = cb.p;
+    }
+    __syncthreads();
+    const long long bp = sh_piv[0];
+    if (bp < n)
+      for (int64_t i = threadIdx.x; i < m; i += kThreads) a.cand[(int64_t)cta * m + i] = a.W[bp * ld + i];
+  }
+  grid.sync();
+  if (__ldcg(a.flags) != 0) return;
+
+  // ------------------------------------------------------------ steps
+  for (int64_t s = 0; s < k; ++s) {
+    const int par = (int)(s & 1), nxt = par ^ 1;
+    // (1) global argmax over the per-CTA partials, fixed order
+    if (warp == 0) {
+      Best b{-INFINITY, (long long)INT64_MAX};
+      long long bc = -1;
+      for (int c = lane; c < G; c += 32) {
+        const double v = __ldcg(a.pval + (int64_t)par * G + c);
+        const long long p = __ldcg(a.ppos + (int64_t)par * G + c);
+        if (better(v, p, b.v, b.p)) { b.v = v; b.p = p; bc = c; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
+        const long long op = __shfl_xor_sync(0xffffffffu, b.p, o);
+        const long long oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(ov, op, b.v, b.p)) { b.v = ov; b.p = op; bc = oc; }
+      }
+      if (lane == 0) { sh_piv[0] = b.p; sh_piv[1] = bc; }
+    }
+    __syncthreads();
+    const int64_t p = sh_piv[0];
+    const int wc = (int)sh_piv[1];
+    const double* x = a.cand + ((int64_t)par * G + wc) * m;  // pivot column, rows >= s valid
+
+    // (2) reflector, redundantly per CTA (cpqr.hpp:59-66)
+    double part = 0.0;
+    for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
+      const double xi = __ldcg(x + i);
+      part = fma(xi, xi, part);
+    }
+    const double cn2 = cta_sum(part, sh_red);
+    const double colnorm = sqrt(cn2);
+    const double alpha = __ldcg(x + s);
+    double beta = alpha, tau = 0.0, scale = 1.0;
+    const bool apply = colnorm > 0.0;
+    if (apply) {
+      beta = alpha >= 0.0 ? -colnorm : colnorm;
+      tau = (beta - alpha) / beta;
+      scale = alpha - beta;
+    }
+    if (vs) {
+      for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
+        const double vi = (i == s) ? 1.0 : (apply ? __ldcg(x + i) / scale : 0.0);
+        vv[i] = vi;
+        tv[i] = tau * vi;
+      }
+    } else {
+      for (int64_t i = s + threadIdx.x; i < m; i += kThreads)
+        vv[i] = (i == s) ? 1.0 : (apply ? __ldcg(x + i) / scale : 0.0);
+    }
+    if (cta == 0 && threadIdx.x == 0) a.tau[s] = tau;
+
+    // (3) swap bookkeeping by the owner of position p
+    const bool owner = (p >= c0 && p < c1);
+    const bool swapped = owner && p != s;
+    if (swapped) {
+      for (int64_t i = threadIdx.x; i < m; i += kThreads) olds[i] = __ldcg(a.W + s * ld + i);
+      for (int64_t i = threadIdx.x; i < s; i += kThreads) pivr[i] = a.W[p * ld + i];
+      if (threadIdx.x == 0) {
+        sh_state[0] = a.piv[p];
+        sh_state[1] = __ldcg(a.piv + s);
+        sh_nst[0] = a.nrm[p];
+        sh_nst[1] = a.nrmx[p];
+        sh_nst[2] = __ldcg(a.nrm + s);
+        sh_nst[3] = __ldcg(a.nrmx + s);
+      }
+    }
+    __syncthreads();
+
+    // (4) fused trailing pass over owned positions j in (s, n)
+    Best b{-INFINITY, (long long)INT64_MAX};
+    const int64_t jstart = c0 + warp;
+    for (int64_t j = jstart; j < c1; j += kWarps) {
+      if (j <= s) continue;
+      const bool from_s = swapped && j == p;
+      const double* src = from_s ? olds : a.W + j * ld;
+      double* dst = a.W + j * ld;
+      double cache[CH][2];
+      double dot = 0.0;
+      // pass A: load active rows (>= s) and dot with v
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        const int64_t i = 64 * t + 2 * lane;
+        cache[t][0] = cache[t][1] = 0.0;
+        if (64 * (t + 1) > s && i < m) {
+          if (i + 1 < m) {
+            const double2 xx = from_s ? make_double2(__ldcg(src + i), __ldcg(src + i + 1))
+                                      : *reinterpret_cast<const double2*>(src + i);
+            cache[t][0] = xx.x;
+            cache[t][1] = xx.y;
+          } else {
+            cache[t][0] = from_s ? __ldcg(src + i) : src[i];
+          }
+          if (i >= s) dot = fma(cache[t][0], vv[i], dot);
+          if (i + 1 >= s && i + 1 < m) dot = fma(cache[t][1], vv[i + 1], dot);
+        }
+      }
+      for (int t = CH; t < nchunks; ++t) {  // streamed rows
+        const int64_t i = 64 * t + 2 * lane;
+        if (i < m && i >= s) dot = fma(from_s ? __ldcg(src + i) : src[i], vv[i], dot);
+        if (i + 1 < m && i + 1 >= s) dot = fma(from_s ? __ldcg(src + i + 1) : src[i + 1], vv[i + 1], dot);
+      }
+      dot = warp_sum(dot);
+      // pass B: update (W -= (tau v) w), collect row s and the tail square sum
+      double xs = 0.0, tail2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        const int64_t i = 64 * t + 2 * lane;
+        if (64 * (t + 1) > s && i < m) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t r = i + e;
+            if (r >= s && r < m) {
+              double c = cache[t][e];
+              if (apply) c = fma(-(vs ? tv[r] : tau * vv[r]), dot, c);
+              cache[t][e] = c;
+              if (r == s) xs = c;
+              else tail2 = fma(c, c, tail2);
+            }
+          }
+          if (i + 1 < m) {
+            *reinterpret_cast<double2*>(dst + i) = make_double2(cache[t][0], cache[t][1]);
+          } else {
+            dst[i] = cache[t][0];
+          }
+        }
+      }
+      for (int t = CH; t < nchunks; ++t) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = 64 * t + 2 * lane + e;
+          if (r < m) {
+            double c = from_s ? __ldcg(src + r) : src[r];
+            if (r >= s) {
+              if (apply) c = fma(-(vs ? tv[r] : tau * vv[r]), dot, c);
+              if (r == s) xs = c;
+              else tail2 = fma(c, c, tail2);
+            }
+            dst[r] = c;  // rows < s copied through unchanged (needed when from_s)
+          }
+        }
+      }
+      if (from_s) {
+        // rows < s of the swapped-in column, and rows in cached chunks wholly below s
+        for (int64_t r = lane; r < m && r < s; r += 32)
+          if (r < 64 * (int64_t)CH) dst[r] = __ldcg(olds + r);
+      }
+      // row s lives in lane (s%64)/2 of chunk s/64 (or the streamed part)
+      xs = __shfl_sync(0xffffffffu, xs, (int)((s % 64) / 2));
+      double nr = from_s ? sh_nst[2] : a.nrm[j];
+      double nx = from_s ? sh_nst[3] : a.nrmx[j];
+      nr -= xs * xs;
+      if (nr < 1e-6 * nx) {
+        nr = warp_sum(tail2);
+        nx = nr;
+        ++my_recomputes;
+      }
+      if (lane == 0) {
+        a.nrm[j] = nr;
+        a.nrmx[j] = nx;
+        if (from_s) a.piv[j] = sh_state[1];
+      }
+      if (better(nr, j, b.v, b.p)) { b.v = nr; b.p = j; }
+    }
+
+    // (5) CTA argmax, pivot column write-back, candidate staging
+    if (lane == 0) { sh_bv[warp] = b.v; sh_bp[warp] = b.p; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Best cb{sh_bv[0], sh_bp[0]};
+      for (int w = 1; w < kWarps; ++w)
+        if (better(sh_bv[w], sh_bp[w], cb.v, cb.p)) { cb.v = sh_bv[w]; cb.p = sh_bp[w]; }
+      a.pval[(int64_t)nxt * G + cta] = cb.v;
+      a.ppos[(int64_t)nxt * G + cta] = cb.p;
+      sh_piv[0] = cb.p;
+    }
+    if (owner) {
+      double* ps = a.W + s * ld;
+      if (swapped) {
+        for (int64_t i = threadIdx.x; i < s; i += kThreads) ps[i] = pivr[i];
+        if (threadIdx.x == 0) {
+          a.piv[s] = sh_state[0];
+          a.nrm[s] = sh_nst[0];
+          a.nrmx[s] = sh_nst[1];
+        }
+      }
+      for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
+        double val;
+        if (!apply) val = __ldcg(x + i);
+        else val = (i == s) ? beta : vv[i];
+        ps[i] = val;
+      }
+    }
+    __syncthreads();
+    const long long bp = sh_piv[0];
+    if (bp < n) {
+      double* cd = a.cand + ((int64_t)nxt * G + cta) * m;
+      for (int64_t i = s + 1 + threadIdx.x; i < m; i += kThreads) cd[i] = a.W[bp * ld + i];
+    }
+    grid.sync();
+  }
+  if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
+}
+
+// s (k x n) = top k rows, strict lower zeroed, rows with negative diagonal negated
+__global__ void extract_s_kernel(int64_t m, int64_t n, const double* __restrict__ W, int64_t ld, int64_t k,
+                                 double* __restrict__ s, int64_t lds) {
+  const int64_t total = k * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % k, j = t / k;
+    double v = (i > j) ? 0.0 : W[i + j * ld];
+    if (W[i + i * ld] < 0.0) v = -v;
+    s[i + j * lds] = v;
+  }
+}
+
+// q(:, c) = H_0 ... H_{k-1} e_c, then the sign fix; one warp per column
+__global__ void form_q_kernel(int64_t m, const double* __restrict__ W, int64_t ld, int64_t k,
+                              const double* __restrict__ tau, double* __restrict__ q, int64_t ldq) {
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= k) return;
+  double* qc = q + c * ldq;
+  for (int64_t i = lane; i < m; i += 32) qc[i] = (i == c) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int64_t st = k - 1; st >= 0; --st) {
+    const double t = tau[st];
+    if (t == 0.0) continue;
+    const double* v = W + st * ld;  // v(st) = 1, v(i>st) = W(i, st)
+    double d = 0.0;
+    for (int64_t i = st + lane; i < m; i += 32) d = fma(qc[i], i == st ? 1.0 : v[i], d);
+    d = warp_sum(d);
+    for (int64_t i = st + lane; i < m; i += 32) qc[i] = fma(-(t * (i == st ? 1.0 : v[i])), d, qc[i]);
+    __syncwarp();
+  }
+  if (W[c + c * ld] < 0.0)
+    for (int64_t i = lane; i < m; i += 32) qc[i] = -qc[i];
+}
+
+template <int CH>
+void launch_cpqr(CpqrArgs& args, size_t smem, cudaStream_t st) {
+  auto kern = cpqr_kernel<CH>;
+  if (smem > 48 * 1024) LRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  per_sm = std::max(1, std::min(per_sm, 4));
+  int G = per_sm * num_sms();
+  // no more CTAs than columns / warps worth of work
+  const int64_t max_g = std::max<int64_t>(1, (args.n + kWarps - 1) / kWarps);
+  if (G > max_g) G = (int)max_g;
+  (void)G;
+  void* params[] = {&args};
+  LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kThreads), params, smem, st));
+}
+
+int cpqr_grid(int64_t n, int64_t m) {
+  (void)m;
+  const int64_t max_g = std::max<int64_t>(1, (n + kWarps - 1) / kWarps);
+  return (int)std::min<int64_t>(4 * num_sms(), max_g);
+}
+
+}  // namespace
+
+void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
+                  double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
+  const int Gmax = cpqr_grid(n, m);
+  // state: nrm, nrmx (n each), pval (2G), ppos (2G), cand (2 G m), scratch (G 3m)
+  const size_t bytes = sizeof(double) * (2 * (size_t)n + 2 * (size_t)Gmax + 2 * (size_t)Gmax * m +
+                                         3 * (size_t)Gmax * m) +
+                       sizeof(long long) * 2 * (size_t)Gmax + 256;
+  uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
+  CpqrArgs a{};
+  a.W = W;
+  a.m = m;
+  a.n = n;
+  a.ld = ld;
+  a.k = k;
+  a.piv = pivots;
+  a.tau = tau;
+  double* d = reinterpret_cast<double*>(base);
+  a.nrm = d;
+  a.nrmx = d + n;
+  a.pval = d + 2 * n;
+  a.cand = a.pval + 2 * Gmax;
+  a.scratch = a.cand + 2 * (size_t)Gmax * m;
+  a.ppos = reinterpret_cast<long long*>(a.scratch + 3 * (size_t)Gmax * m);
+  a.flags = d_flags;
+  a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
+  const size_t smem = m <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)m : 0;
+  if (m <= 512) launch_cpqr<8>(a, smem, st);
+  else launch_cpqr<16>(a, smem, st);
+}
+
+void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,
+                    cudaStream_t st) {
+  (void)m;
+  const int64_t total = k * n;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * num_sms()));
+  extract_s_kernel<<<g, 256, 0, st>>>(m, n, W, ld, k, s, lds);
+  LRB_CHECK_LAUNCH();
+}
+
+void cpqr_form_q(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, const double* tau, double* q,
+                 int64_t ldq, cudaStream_t st) {
+  (void)n;
+  const int wpb = 8;
+  form_q_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(m, W, ld, k, tau, q, ldq);
+  LRB_CHECK_LAUNCH();
+}
+
+}  // namespace lrb

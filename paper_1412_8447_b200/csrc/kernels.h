@@ -1,0 +1,135 @@
+// kernels.h -- host-side entry points of the device kernels (internal to the
+// library; the public boundary is include/lowrank_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstddef>
+#include <vector>
+
+namespace lrb {
+
+enum { kEpiStore = 0, kEpiSplitK = 1, kEpiResid = 2 };
+
+// Named, grow-only device scratch buffers owned by a context.
+enum class WsSlot : int {
+  kSplitK = 0,
+  kOmega,
+  kSample,
+  kWork,
+  kCpqrState,
+  kCand,
+  kTri,
+  kTri2,
+  kTmp0,
+  kTmp1,
+  kTmp2,
+  kTmp3,
+  kTmp4,
+  kTmp5,
+  kTmp6,
+  kTmp7,
+  kPartials,
+  kHostCopyA,
+  kHostCopyB,
+  kCount
+};
+
+class Workspace {
+ public:
+  Workspace() : ptr_((size_t)WsSlot::kCount, nullptr), cap_((size_t)WsSlot::kCount, 0) {}
+  ~Workspace();
+  void* get(WsSlot s, size_t bytes);
+  double* get_doubles(WsSlot s, size_t n) { return static_cast<double*>(get(s, n * sizeof(double))); }
+  void release_all();
+
+ private:
+  std::vector<void*> ptr_;
+  std::vector<size_t> cap_;
+};
+
+// ---------------------------------------------------------------- GEMM
+int gemm_tn_grid_ctas(int M, int N);
+// out(MxN) = alpha P^T Q + beta out; P: KxM (ldp), Q: KxN (ldq), K-contiguous.
+// splits <= 0 chooses a deterministic split-K factor from the shape.
+void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
+             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st);
+// per-CTA partial sums of (R - P^T Q)^2 written to partials_out[0..*num_partials)
+void gemm_tn_resid_sq(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q,
+                      int64_t ldq, const double* R, int64_t ldr, double* partials_out, int* num_partials,
+                      cudaStream_t st);
+
+// ---------------------------------------------------------------- rng
+// rows x cols Gaussian matrix with the reference stream semantics.  If
+// transposed, writes out^T (cols x rows, ld = ldo) instead.
+void gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ldo, bool transposed,
+                     cudaStream_t st);
+
+// ---------------------------------------------------------------- elementwise / data movement
+void scale_matrix(int M, int N, double* a, int64_t lda, double beta, cudaStream_t st);
+void copy_matrix(int64_t m, int64_t n, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t st);
+// dst (k x k) = upper triangle of src, strict lower part zero
+void copy_upper(int64_t k, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t st);
+void transpose_matrix(int64_t m, int64_t n, const double* src, int64_t lds, double* dst, int64_t ldd,
+                      cudaStream_t st);
+void gather_columns(int64_t m, int64_t k, const double* a, int64_t lda, const int64_t* idx, double* out,
+                    int64_t ldo, cudaStream_t st);
+// out(i, j) = a(idx[i], j): k x n (ldo)
+void gather_rows(int64_t k, int64_t n, const double* a, int64_t lda, const int64_t* idx, double* out,
+                 int64_t ldo, cudaStream_t st);
+// out(j, i) = a(idx[i], j): n x k (ldo), i.e. the transpose of gather_rows
+void gather_rows_t(int64_t k, int64_t n, const double* a, int64_t lda, const int64_t* idx, double* out,
+                   int64_t ldo, cudaStream_t st);
+// flag[0] |= 1 if any entry non-finite
+void check_finite(int64_t m, int64_t n, const double* a, int64_t lda, int* flag, cudaStream_t st);
+// deterministic sum of n doubles into out[0] (single block, fixed order)
+void sum_partials(const double* p, int n, double* out, cudaStream_t st);
+// per-column squared norms summed: partial sums of squares of a (m x n) -> out[0]
+void frob2(int64_t m, int64_t n, const double* a, int64_t lda, double* partials, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- CPQR
+struct CpqrStats {
+  long long recomputes;
+};
+// Truncated column-pivoted Householder QR (cpqr.hpp:32-114) of W (m x n,
+// ld), in place: after return the upper part holds s (unsigned), the strict
+// lower part the reflectors, pivots the permutation and tau the k scalars.
+// Device pointers; pivots (n int64), tau (k), flags (1 int: nonfinite input).
+void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
+                  double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st);
+// s (k x n, lds) = top k rows of W with strict lower part zeroed and the sign fix
+void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,
+                    cudaStream_t st);
+// q (m x k) = H_0 .. H_{k-1} [I; 0] with the sign fix of cpqr.hpp:105-112
+void cpqr_form_q(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, const double* tau, double* q,
+                 int64_t ldq, cudaStream_t st);
+
+// ---------------------------------------------------------------- triangular / small dense
+// Mt (k x k) = transpose of the back-substitution operator of solve.hpp:62-89
+// applied to the identity: rows with |d_i| <= thr*max|d| are zero.  s11 may
+// carry row sign flips (ignored: they cancel).  zero_rows (k ints) marks them.
+void backsub_operator_t(int64_t k, const double* s11, int64_t ld11, double threshold, double* Mt, int* zero_rows,
+                        cudaStream_t st);
+// diag stats of an upper-triangular block: out[0]=max|d|, out[1]=min|d|
+void diag_absminmax(int64_t k, const double* s11, int64_t ld11, double* out, cudaStream_t st);
+// strict-lower part nonzero / nonfinite flags for a k x k block (flags[0]: lower nonzero, flags[1]: nonfinite)
+void check_upper_triangular(int64_t k, const double* s11, int64_t ld11, int* flags, cudaStream_t st);
+// max |x| over an m x n block -> out[0]
+void max_abs(int64_t m, int64_t n, const double* a, int64_t lda, double* partials, double* out, cudaStream_t st);
+// residual check rows for the singularity test: res[i] = max_c |S12(i,c) - sum_{j>i} S11(i,j) T(j,c)|
+void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld11, const double* s12,
+                           int64_t ld12, const double* t, int64_t ldt, const int* zero_rows, double* res,
+                           cudaStream_t st);
+// Cholesky G = R^T R (upper R, k x k, in place on a copy); info[0] = first failing column+1 or 0
+void cholesky_upper(int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st);
+// inverse of an upper-triangular R (k x k) -> Rinv (upper)
+void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
+
+// ---------------------------------------------------------------- Jacobi SVD (svd.hpp:39-183 semantics)
+// thin SVD of a (m x n, m >= n assumed by caller after transposition):
+// u (m x n), sigma (n), v (n x n); returns false if not converged in 60 sweeps
+bool jacobi_svd(Workspace& ws, int64_t m, int64_t n, const double* a, int64_t lda, double* u, double* sigma,
+                double* v, cudaStream_t st);
+
+}  // namespace lrb

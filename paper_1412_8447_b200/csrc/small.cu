@@ -1,0 +1,221 @@
+// small.cu -- k x k triangular and small dense kernels that sit between the
+// big contractions: the back-substitution operator of solve.hpp:62-89,
+// escalation statistics (solve.hpp:119-126), the singularity residual test
+// (solve.hpp:75-83), Cholesky for CholeskyQR2 and triangular inverses.
+// These are latency-bound (k <= a few thousand); each uses one warp per
+// column with a fixed reduction order so results are reproducible.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lrb {
+
+namespace {
+
+__device__ double block_max_abs_diag(int64_t k, const double* s11, int64_t ld11, double* sh) {
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) mx = fmax(mx, fabs(s11[i + i * ld11]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, sh[w]);
+  __syncthreads();
+  return t;
+}
+
+// One warp per column c of the operator M = backsub(S11, I) (col-major k x k):
+//   for i = c..0: rhs = delta(i,c) - sum_{j>i} S11(i,j) M(j,c)  (j ascending)
+//                 M(i,c) = |d_i| <= tol ? 0 : rhs / d_i
+__global__ void backsub_operator_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11, double threshold,
+                                        double* __restrict__ M, int* __restrict__ zero_rows) {
+  __shared__ double sh[32];
+  const double tol = threshold * block_max_abs_diag(k, s11, ld11, sh);
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  if (blockIdx.x == 0)
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) zero_rows[i] = fabs(s11[i + i * ld11]) <= tol;
+  if (c >= k) return;
+  double* mc = M + c * k;
+  for (int64_t i = c + 1 + lane; i < k; i += 32) mc[i] = 0.0;
+  for (int64_t i = c; i >= 0; --i) {
+    double acc = 0.0;
+    for (int64_t j = i + 1 + lane; j <= c; j += 32) acc = fma(s11[i + j * ld11], mc[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double d = s11[i + i * ld11];
+      const double rhs = (i == c ? 1.0 : 0.0) - acc;
+      mc[i] = fabs(d) <= tol ? 0.0 : rhs / d;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void diag_minmax_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11, double* out) {
+  __shared__ double smx[32], smn[32];
+  double mx = 0.0, mn = INFINITY;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+    const double d = fabs(s11[i + i * ld11]);
+    mx = fmax(mx, d);
+    mn = fmin(mn, d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) { smx[threadIdx.x >> 5] = mx; smn[threadIdx.x >> 5] = mn; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a = fmax(a, smx[w]); b = fmin(b, smn[w]); }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+__global__ void check_upper_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11, int* flags) {
+  int lower = 0, bad = 0;
+  const int64_t total = k * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % k, j = t / k;
+    const double x = s11[i + j * ld11];
+    bad |= !isfinite(x);
+    lower |= (i > j) && (x != 0.0);
+  }
+  if (__syncthreads_or(lower) && threadIdx.x == 0) atomicOr(flags + 0, 1);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags + 1, 1);
+}
+
+// res[i] (only for zero rows) = max_c |S12(i,c) - sum_{j>i} S11(i,j) T(j,c)|, as per-block partial maxima
+__global__ void backsub_residual_kernel(int64_t k, int64_t nc, const double* __restrict__ s11, int64_t ld11,
+                                        const double* __restrict__ s12, int64_t ld12, const double* __restrict__ t,
+                                        int64_t ldt, int64_t row, double* __restrict__ partial) {
+  double mx = 0.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    double rhs = s12[row + c * ld12];
+    for (int64_t j = row + 1; j < k; ++j) rhs -= s11[row + j * ld11] * t[j + c * ldt];
+    mx = fmax(mx, fabs(rhs));
+  }
+  __shared__ double sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = fmax(a, sh[w]);
+    partial[blockIdx.x] = a;
+  }
+}
+
+__global__ void max_reduce_kernel(const double* __restrict__ p, int n, double* out) {
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < n; ++i) a = fmax(a, p[i]);
+    out[0] = a;
+  }
+}
+
+// Right-looking Cholesky G = R^T R on the upper triangle, one CTA.
+__global__ void cholesky_upper_kernel(int64_t k, double* __restrict__ g, int64_t ldg, int* info) {
+  __shared__ double sdiag;
+  __shared__ int sfail;
+  if (threadIdx.x == 0) sfail = 0;
+  __syncthreads();
+  for (int64_t j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = g[j + j * ldg];
+      if (!(d > 0.0) || !isfinite(d)) {
+        sfail = 1;
+        info[0] = (int)(j + 1);
+      } else {
+        sdiag = sqrt(d);
+        g[j + j * ldg] = sdiag;
+      }
+    }
+    __syncthreads();
+    if (sfail) return;
+    const double rd = sdiag;
+    for (int64_t c = j + 1 + threadIdx.x; c < k; c += blockDim.x) g[j + c * ldg] /= rd;
+    __syncthreads();
+    // trailing update of the upper triangle: G(a,b) -= R(j,a) R(j,b), j < a <= b
+    const int64_t nt = k - j - 1;
+    const int64_t tot = nt * nt;
+    for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+      const int64_t a = j + 1 + t % nt, b = j + 1 + t / nt;
+      if (a <= b) g[a + b * ldg] = fma(-g[j + a * ldg], g[j + b * ldg], g[a + b * ldg]);
+    }
+    __syncthreads();
+  }
+  // zero the strict lower part so R is a clean upper-triangular factor
+  for (int64_t t = threadIdx.x; t < k * k; t += blockDim.x) {
+    const int64_t a = t % k, b = t / k;
+    if (a > b) g[a + b * ldg] = 0.0;
+  }
+  if (threadIdx.x == 0) info[0] = 0;
+}
+
+}  // namespace
+
+void backsub_operator_t(int64_t k, const double* s11, int64_t ld11, double threshold, double* Mt, int* zero_rows,
+                        cudaStream_t st) {
+  // M is written col-major into Mt's storage first, then transposed in place via a temp
+  double* tmp = nullptr;
+  LRB_CUDA(cudaMallocAsync(&tmp, sizeof(double) * k * k, st));
+  const int wpb = 8;
+  backsub_operator_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(k, s11, ld11, threshold, tmp,
+                                                                                zero_rows);
+  LRB_CHECK_LAUNCH();
+  transpose_matrix(k, k, tmp, k, Mt, k, st);
+  LRB_CUDA(cudaFreeAsync(tmp, st));
+}
+
+void diag_absminmax(int64_t k, const double* s11, int64_t ld11, double* out, cudaStream_t st) {
+  diag_minmax_kernel<<<1, 256, 0, st>>>(k, s11, ld11, out);
+  LRB_CHECK_LAUNCH();
+}
+
+void check_upper_triangular(int64_t k, const double* s11, int64_t ld11, int* flags, cudaStream_t st) {
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((k * k + 255) / 256, 4 * num_sms()));
+  check_upper_kernel<<<g, 256, 0, st>>>(k, s11, ld11, flags);
+  LRB_CHECK_LAUNCH();
+}
+
+void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld11, const double* s12, int64_t ld12,
+                           const double* t, int64_t ldt, const int* zero_rows_host, double* res, cudaStream_t st) {
+  // zero_rows_host: host array; res: device array of k (only zero rows written)
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nc + 255) / 256, 2 * num_sms()));
+  double* partial = nullptr;
+  LRB_CUDA(cudaMallocAsync(&partial, sizeof(double) * g, st));
+  for (int64_t i = k - 1; i >= 0; --i) {
+    if (!zero_rows_host[i]) continue;
+    backsub_residual_kernel<<<g, 256, 0, st>>>(k, nc, s11, ld11, s12, ld12, t, ldt, i, partial);
+    LRB_CHECK_LAUNCH();
+    max_reduce_kernel<<<1, 32, 0, st>>>(partial, g, res + i);
+    LRB_CHECK_LAUNCH();
+  }
+  LRB_CUDA(cudaFreeAsync(partial, st));
+}
+
+void cholesky_upper(int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st) {
+  cholesky_upper_kernel<<<1, 1024, 0, st>>>(k, g, ldg, info);
+  LRB_CHECK_LAUNCH();
+}
+
+void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st) {
+  int* zr = nullptr;
+  LRB_CUDA(cudaMallocAsync(&zr, sizeof(int) * k, st));
+  double* tmp = nullptr;
+  LRB_CUDA(cudaMallocAsync(&tmp, sizeof(double) * k * k, st));
+  const int wpb = 8;
+  // threshold 0: only exactly-zero diagonals are treated as singular (rows zeroed)
+  backsub_operator_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(k, r, ldr, 0.0, tmp, zr);
+  LRB_CHECK_LAUNCH();
+  copy_matrix(k, k, tmp, k, rinv, ldi, st);
+  LRB_CUDA(cudaFreeAsync(tmp, st));
+  LRB_CUDA(cudaFreeAsync(zr, st));
+}
+
+}  // namespace lrb

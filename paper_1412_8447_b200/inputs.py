@@ -1,0 +1,139 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+Not part of the hot path: these build A = U diag(s) V^T with Haar-orthonormal
+factors (thin QR of seeded Gaussians) and the BASELINE spectra.  The seeds
+follow matgen.hpp:45-46 (U <- derive_seed(g, 1), V <- derive_seed(g, 2));
+the Gaussian entries follow rng.hpp:74-94.  The QR rounding differs from the
+reference's Eigen HouseholderQR, so the input BYTES are defined by this
+module (hashes recorded by the tests) and every comparison hands the same
+bytes to both sides.
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+M1 = np.uint64(0xBF58476D1CE4E5B9)
+M2 = np.uint64(0x94D049BB133111EB)
+
+
+def mix64(z: np.ndarray) -> np.ndarray:
+    z = (z ^ (z >> np.uint64(30))) * M1
+    z = (z ^ (z >> np.uint64(27))) * M2
+    return z ^ (z >> np.uint64(31))
+
+
+def stream_value(seed: int, index) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        idx = np.asarray(index, dtype=np.uint64)
+        return mix64(np.uint64(seed) + (idx + np.uint64(1)) * GOLDEN)
+
+
+def derive_seed(seed: int, tag: int) -> int:
+    """rng.hpp:32-34."""
+    with np.errstate(over="ignore"):
+        return int(stream_value(seed, np.uint64(tag) ^ np.uint64(0xD1B54A32D192ED03)))
+
+
+def gaussian_np(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Vectorised rng.hpp:74-94 for INPUT generation (numpy's log/sin/cos may
+    differ from glibc by an ulp; the oracle's gaussian_matrix is the checker)."""
+    total = rows * cols
+    pairs = np.arange(0, total, 2, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u1 = ((stream_value(seed, pairs) >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+        u2 = (stream_value(seed, pairs + np.uint64(1)) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    r = np.sqrt(-2.0 * np.log(u1))
+    ang = 2.0 * math.pi * u2
+    flat = np.empty(total + (total & 1))
+    flat[0::2] = r * np.cos(ang)
+    flat[1::2] = r * np.sin(ang)
+    return np.asfortranarray(flat[:total].reshape(rows, cols))
+
+
+def haar_np(rows: int, cols: int, seed: int) -> np.ndarray:
+    q, r = np.linalg.qr(gaussian_np(rows, cols, seed))
+    return np.asfortranarray(q * np.sign(np.diag(r)))
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    m: int
+    n: int
+    width: int
+    spectrum: Callable[[np.ndarray], np.ndarray]
+    k: int
+    oversample: int
+    pipeline: str
+    seed: int = 1412
+    sketch_seed: int = 1
+
+    def singular_values(self) -> np.ndarray:
+        return self.spectrum(np.arange(self.width, dtype=np.float64))
+
+
+# BASELINE.json configs[0..3] (configs[4], sparse, is not on this round's path)
+CONFIGS = {
+    "c1": Config("c1", 1000, 800, 800, lambda j: np.exp(-j / 20.0), 50, 0, "id_column"),
+    "c2": Config("c2", 4000, 3000, 3000, lambda j: (j + 1.0) ** -2, 100, 0, "cur_id"),
+    "c3": Config("c3", 20000, 20000, 2000, lambda j: np.exp(-j / 40.0), 200, 10, "randomized_id"),
+    "c4": Config("c4", 65536, 65536, 1024, lambda j: (1.0 + j / 50.0) ** -3, 500, 10, "randomized_cur"),
+}
+
+
+def scaled(cfg: Config, m: int, n: int, width: int | None = None, k: int | None = None) -> Config:
+    """Same spectrum shape on a smaller instance (parity cases, CPU samples)."""
+    return Config(cfg.name + f"_{m}x{n}", m, n, width or min(cfg.width, m, n), cfg.spectrum, k or cfg.k,
+                  cfg.oversample, cfg.pipeline, cfg.seed, cfg.sketch_seed)
+
+
+def synthetic_np(cfg: Config) -> np.ndarray:
+    """A = U diag(s) V^T on the host (configs small enough for host RAM)."""
+    u = haar_np(cfg.m, cfg.width, derive_seed(cfg.seed, 1))
+    v = haar_np(cfg.n, cfg.width, derive_seed(cfg.seed, 2))
+    return np.asfortranarray((u * cfg.singular_values()) @ v.T)
+
+
+def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None):
+    """A = U diag(s) V^T generated on the GPU, column-major (input plumbing:
+    torch QR / matmul build the input, the product path never uses them)."""
+    import torch
+
+    from .lowrank import default_context, empty_colmajor
+
+    ctx = default_context()
+    lib = ctx.lib
+
+    def gauss(rows, cols, seed):
+        g = empty_colmajor(rows, cols, device)
+        rc = lib.lr_gaussian_matrix_d(ctx.h, rows, cols, seed, g.data_ptr(), rows)
+        if rc != 0:
+            raise RuntimeError(lib.lr_last_error().decode())
+        ctx.synchronize()
+        return g
+
+    def haar(rows, cols, seed):
+        q, r = torch.linalg.qr(gauss(rows, cols, seed))
+        return q * torch.sign(torch.diagonal(r))
+
+    u = haar(cfg.m, cfg.width, derive_seed(cfg.seed, 1))
+    v = haar(cfg.n, cfg.width, derive_seed(cfg.seed, 2))
+    us = u * torch.as_tensor(cfg.singular_values(), device=device)
+    del u
+    a = empty_colmajor(cfg.m, cfg.n, device)
+    step = col_block or cfg.n
+    for j0 in range(0, cfg.n, step):
+        j1 = min(cfg.n, j0 + step)
+        a[:, j0:j1] = us @ v[j0:j1].T
+    torch.cuda.synchronize()
+    return a
+
+
+def sha256(a: np.ndarray) -> str:
+    return hashlib.sha256(np.asfortranarray(a).tobytes(order="F")).hexdigest()

@@ -1,0 +1,260 @@
+"""GPU parity: the B200 path (through the C ABI) against the CPU oracle and the
+golden fixtures produced by the reference's own code.
+
+Tolerances (north_star): identical index sets; C, R, skeleton bit-exact;
+ID/CUR factors and the relative Frobenius error within 1e-10 relative.
+Gaussian entries: the integer stream is exact, CUDA's log/sincos give a
+few-ulp difference from glibc (hard part 4).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import rel
+from paper_1412_8447_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "golden_small.npz")
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def ulp_close(a, b, ulps=8):
+    scale = np.maximum(np.abs(a), np.abs(b))
+    return np.all(np.abs(a - b) <= ulps * np.spacing(np.maximum(scale, 1e-300)))
+
+
+# ------------------------------------------------------------------ rng / sketch
+def test_gaussian_matrix_stream(lr, oracle):
+    for rows, cols, seed in [(7, 5, 123), (5, 12, 3), (1, 1, 0), (33, 17, 2**63 + 11)]:
+        g = lr.gaussian_matrix(rows, cols, seed)
+        o = oracle.gaussian_matrix(rows, cols, seed)
+        assert ulp_close(g, o, 8)
+        assert np.array_equal(g, lr.gaussian_matrix(rows, cols, seed))
+
+
+def test_sketch_of_identity_is_the_operator(lr):  # test_sketch.cpp:27-31
+    y = lr.sketch_gaussian(np.eye(12), 5, 3).y
+    assert np.array_equal(y, lr.gaussian_matrix(5, 12, 3))
+
+
+def test_sketch_of_zero_is_zero(lr):  # test_sketch.cpp:33-36
+    assert np.all(lr.sketch_gaussian(np.zeros((10, 6)), 4, 1).y == 0.0)
+
+
+@pytest.mark.parametrize("shape,ell", [((300, 200), 37), ((1000, 129), 130), ((257, 1031), 64)])
+def test_sketch_matches_oracle(lr, oracle, shape, ell):
+    a = oracle.gaussian_matrix(*shape, 5)
+    y = lr.sketch_gaussian(a, ell, 9).y
+    assert rel(y, oracle.sketch_gaussian(a, ell, 9)) <= 1e-13
+
+
+def test_sketch_validation(lr):  # test_sketch.cpp:50-54
+    a = np.ones((6, 9))
+    with pytest.raises(ValueError):
+        lr.sketch_gaussian(a, 7, 1)
+    bad = a.copy()
+    bad[1, 1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        lr.sketch_gaussian(bad, 3, 1)
+
+
+def test_gemm_kernel_vs_numpy(lr):
+    import torch
+    for (M, N, K) in [(510, 1000, 777), (128, 128, 16), (5, 7, 3), (300, 260, 4100)]:
+        P = torch.randn(K, M, dtype=torch.float64, device="cuda")
+        Q = torch.randn(K, N, dtype=torch.float64, device="cuda")
+        Pc = P.T.contiguous().T if K > 1 else P  # column-major K x M
+        Pc = lr.empty_colmajor(K, M, "cuda"); Pc.copy_(P)
+        Qc = lr.empty_colmajor(K, N, "cuda"); Qc.copy_(Q)
+        out = lr.empty_colmajor(M, N, "cuda")
+        ctx = lr.default_context()
+        rc = ctx.lib.lr_gemm_tn_d(ctx.h, M, N, K, Pc.data_ptr(), Pc.stride(1), Qc.data_ptr(), Qc.stride(1),
+                                  out.data_ptr(), out.stride(1))
+        assert rc == 0, ctx.lib.lr_last_error()
+        ctx.synchronize()
+        ref = (P.T @ Q).cpu().numpy()
+        assert rel(out.cpu().numpy(), ref) <= 1e-14
+
+
+# ------------------------------------------------------------------ CPQR
+def test_cpqr_golden(lr, gold):
+    q = lr.cpqr_partial(gold["cpqr_a"], int(gold["cpqr_k"]))
+    assert np.array_equal(q.pivots, gold["cpqr_piv"])
+    assert rel(q.s, gold["cpqr_s"]) <= 1e-12 and rel(q.q, gold["cpqr_q"]) <= 1e-12
+    f = lr.cpqr_full(gold["cpqrf_a"])
+    assert np.array_equal(f.pivots, gold["cpqrf_piv"])
+    assert rel(f.s, gold["cpqrf_s"]) <= 1e-12 and rel(f.q, gold["cpqrf_q"]) <= 1e-12
+
+
+def test_cpqr_known_answers(lr):
+    q = lr.cpqr_partial(np.eye(3), 2)  # test_cpqr.cpp:29-38
+    assert list(q.pivots) == [0, 1, 2] and np.array_equal(q.s, [[1, 0, 0], [0, 1, 0]])
+    a = np.zeros((2, 2)); a[0, 0], a[1, 1] = 1.0, 2.0  # :40-49
+    q = lr.cpqr_partial(a, 2)
+    assert list(q.pivots) == [1, 0] and abs(q.s[0, 0]) == pytest.approx(2.0)
+    q = lr.cpqr_full(np.array([[5.0]]))  # :64-71
+    assert q.q[0, 0] == pytest.approx(1.0) and q.s[0, 0] == pytest.approx(5.0)
+    a = np.zeros((3, 4)); a[0, 1] = a[1, 2] = a[2, 3] = 2.0; a[0, 0] = 1.0  # ties -> lowest position
+    assert list(lr.cpqr_partial(a, 3).pivots[:3]) == [1, 2, 3]
+
+
+def test_cpqr_rank_deficient_and_det(lr, oracle):
+    g = oracle.gaussian_matrix(6, 3, 11)
+    dup = np.column_stack([g[:, 0], g[:, 1], g[:, 0], g[:, 2]])
+    q = lr.cpqr_full(dup)
+    assert abs(q.s[3, 3]) <= 1e-12 * abs(q.s[0, 0])
+    assert np.linalg.norm(dup[:, q.pivots] - q.q @ q.s) <= 1e-12 * np.linalg.norm(dup)
+    a = oracle.gaussian_matrix(12, 12, 3)
+    q = lr.cpqr_full(a)
+    assert np.prod(np.abs(np.diag(q.s))) == pytest.approx(abs(np.linalg.det(a)), rel=1e-8)
+
+
+@pytest.mark.parametrize("shape,k", [((510, 3000), 510), ((500, 4096), 500), ((1000, 800), 50),
+                                     ((4000, 300), 100), ((64, 64), 64), ((3, 1000), 3), ((777, 5), 5)])
+def test_cpqr_matches_oracle(lr, oracle, shape, k):
+    a = inputs.synthetic_np(inputs.scaled(inputs.CONFIGS["c4"], shape[0], shape[1], width=min(shape), k=k))
+    g = lr.cpqr_partial(a, k)
+    o = oracle.cpqr(a, k)
+    assert np.array_equal(g.pivots, o["pivots"])
+    assert rel(g.s, o["s"]) <= TOL and rel(g.q, o["q"]) <= TOL
+    st = lr.default_context().stats()
+    assert st["cpqr_steps"] >= k
+
+
+def test_cpqr_validation(lr, oracle):
+    a = oracle.gaussian_matrix(4, 4, 1)
+    for k in (0, 5):
+        with pytest.raises(ValueError, match="out of range"):
+            lr.cpqr_partial(a, k)
+    bad = a.copy(); bad[2, 2] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        lr.cpqr_partial(bad, 2)
+
+
+# ------------------------------------------------------------------ coefficient solve
+@pytest.mark.parametrize("kind,esc,ridge", [(0, 1, 0.0), (0, 0, 0.0), (1, 0, 0.0), (2, 0, 0.3)])
+def test_coeff_solve_strategies(lr, oracle, kind, esc, ridge):
+    s11 = np.triu(oracle.gaussian_matrix(40, 40, 23) + 6.0 * np.eye(40))
+    s12 = oracle.gaussian_matrix(40, 333, 24)
+    strat = lr.SolveStrategy(kind, 1e-12, ridge, bool(esc))
+    t = lr.stabilized_coeff_solve(s11, s12, strat)
+    assert rel(t, oracle.coeff_solve(s11, s12, kind, 1e-12, ridge, esc)) <= 1e-10
+
+
+def test_coeff_solve_edge_cases(lr, oracle):
+    s11 = np.zeros((2, 2)); s11[0, 0] = 1.0  # test_solve.cpp:29-38
+    t = lr.stabilized_coeff_solve(s11, np.array([[1.0], [0.0]]), lr.SolveStrategy.back_substitution())
+    assert t[0, 0] == pytest.approx(1.0) and t[1, 0] == 0.0
+    with pytest.raises(lr.SingularityError) as e:  # :40-51
+        lr.stabilized_coeff_solve(s11, np.array([[1.0], [0.5]]), lr.SolveStrategy.back_substitution())
+    assert e.value.index() == 1
+    s11 = np.array([[1.0, 0.5], [0.0, 1e-12]])  # :68-78 escalation == pinv path
+    s12 = oracle.gaussian_matrix(2, 2, 8)
+    a = lr.stabilized_coeff_solve(s11, s12)
+    b = lr.stabilized_coeff_solve(s11, s12, lr.SolveStrategy.truncated_pinv())
+    assert np.array_equal(a, b)
+    assert lr.default_context().stats()["solve_escalated"] == 1
+    t = lr.stabilized_coeff_solve(np.eye(3), np.zeros((3, 0)))  # :112-118
+    assert t.shape == (3, 0)
+    with pytest.raises(ValueError, match="upper triangular"):
+        lr.stabilized_coeff_solve(oracle.gaussian_matrix(3, 3, 2), np.eye(3))
+    with pytest.raises(ValueError):
+        lr.stabilized_coeff_solve(oracle.gaussian_matrix(3, 2, 1), np.eye(3))
+
+
+# ------------------------------------------------------------------ SVD / pinv
+@pytest.mark.parametrize("shape", [(9, 6), (5, 12), (8, 8), (300, 40), (40, 300)])
+def test_svd_pinv_match_oracle(lr, oracle, shape):
+    a = oracle.gaussian_matrix(*shape, 11)
+    s = lr.svd(a)
+    _, so, _ = oracle.svd(a)
+    assert rel(s.sigma, so) <= 1e-12
+    r = min(shape)
+    assert np.linalg.norm(s.u.T @ s.u - np.eye(r)) <= 1e-12 * r
+    assert np.linalg.norm(a - (s.u * s.sigma) @ s.v.T) <= 1e-12 * np.linalg.norm(a)
+    assert rel(lr.pinv(a), oracle.pinv(a)) <= TOL
+
+
+def test_pinv_truncation_and_validation(lr):
+    a = np.zeros((2, 2)); a[0, 0] = 2.0  # test_svd.cpp:85-91
+    p = lr.pinv(a)
+    assert p[0, 0] == pytest.approx(0.5) and abs(p[0, 1]) + abs(p[1, 0]) + abs(p[1, 1]) <= 1e-14
+    for thr in (0.0, 1.5):
+        with pytest.raises(ValueError, match="threshold"):
+            lr.pinv(np.eye(3), thr)
+
+
+# ------------------------------------------------------------------ ID / CUR against the reference fixtures
+def test_id_column_golden(lr, gold):
+    cid = lr.id_column(gold["id_a"], int(gold["id_k"]))
+    assert np.array_equal(cid.pivots, gold["id_piv"])
+    assert rel(cid.coeff, gold["id_coeff"]) <= TOL
+
+
+def test_randomized_id_golden(lr, gold):
+    cfg = lr.SketchConfig(oversample=int(gold["rid_p"]), seed=int(gold["rid_seed"]))
+    cid = lr.randomized_id(gold["rid_a"], int(gold["rid_k"]), cfg)
+    assert np.array_equal(cid.pivots, gold["rid_piv"])
+    assert rel(cid.coeff, gold["rid_coeff"]) <= TOL
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_randomized_cur_golden(lr, gold, mode):
+    a = gold["rcur_a"]
+    cfg = lr.SketchConfig(oversample=int(gold["rcur_p"]), seed=int(gold["rcur_seed"]))
+    cur, ts = lr.randomized_cur(a, int(gold["rcur_k"]), cfg, u_mode=mode, return_tsid=True)
+    assert np.array_equal(cur.col_pivots, gold[f"rcur{mode}_col_pivots"])
+    assert np.array_equal(cur.row_pivots, gold[f"rcur{mode}_row_pivots"])
+    assert np.array_equal(cur.c, gold[f"rcur{mode}_c"]) and np.array_equal(cur.r, gold[f"rcur{mode}_r"])
+    assert np.array_equal(ts.skeleton, gold["rcur_skeleton"])
+    assert rel(cur.u, gold[f"rcur{mode}_u"]) <= TOL
+    assert rel(ts.col_id.coeff, gold["rcur_col_coeff"]) <= TOL
+    assert rel(ts.row_id.coeff, gold["rcur_row_coeff"]) <= TOL
+
+
+def test_cur_id_golden(lr, gold):
+    cur = lr.cur_id(gold["cur_a"], int(gold["cur_k"]), u_mode=lr.U_CPINV_A_RPINV)
+    assert np.array_equal(cur.col_pivots, gold["cur_col_pivots"])
+    assert np.array_equal(cur.row_pivots, gold["cur_row_pivots"])
+    assert rel(cur.u, gold["cur_u"]) <= TOL
+
+
+def test_randomized_cur_is_bitwise_repeatable(lr, oracle):  # test_sketch.cpp:170-183
+    a = inputs.synthetic_np(inputs.scaled(inputs.CONFIGS["c4"], 600, 700, width=300, k=60))
+    cfg = lr.SketchConfig(seed=17)
+    c1 = lr.randomized_cur(a, 60, cfg, u_mode=1)
+    c2 = lr.randomized_cur(a, 60, cfg, u_mode=1)
+    for f in ("c", "u", "r", "col_pivots", "row_pivots"):
+        assert np.array_equal(getattr(c1, f), getattr(c2, f))
+
+
+def test_exact_rank_recovery(lr, oracle):  # test_sketch.cpp:139-146, test_cur.cpp:19-23
+    a = oracle.gaussian_matrix(50, 5, 91) @ oracle.gaussian_matrix(5, 35, 1091)
+    cid = lr.randomized_id(a, 5, lr.SketchConfig(seed=7))
+    assert np.linalg.norm(a - lr.reconstruct(a, cid)) <= 1e-8 * np.linalg.norm(a)
+    cur = lr.randomized_cur(a, 5, lr.SketchConfig(seed=7))
+    assert np.linalg.norm(a - lr.reconstruct(cur)) <= 1e-8 * np.linalg.norm(a)
+
+
+def test_error_kernel_matches_oracle(lr, oracle, gold):
+    a = gold["rcur_a"]
+    cur = lr.randomized_cur(a, 40, lr.SketchConfig(seed=7), u_mode=1)
+    e = lr.cur_error_fro(a, cur)
+    o = oracle.cur_error_fro(a, cur.c, cur.u, cur.r)
+    assert e[0] == pytest.approx(o[0], rel=1e-10) and e[1] == pytest.approx(o[1], rel=1e-13)
+
+
+def test_validation_messages(lr, oracle):
+    a = oracle.gaussian_matrix(6, 9, 2)
+    with pytest.raises(ValueError, match="randomized_id: rank"):
+        lr.randomized_id(a, 0)
+    with pytest.raises(ValueError, match="sample count"):
+        lr.randomized_id(a, 5, lr.SketchConfig(oversample=10))
+    with pytest.raises(NotImplementedError):
+        lr.randomized_id(a, 2, lr.SketchConfig(power=1))
