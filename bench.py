@@ -1,0 +1,401 @@
+#!/usr/bin/env python3
+"""Benchmark: time-to-CUR for randomized CUR, BASELINE.json configs[3]
+(A 65536 x 65536 fp64 = U diag(s) V^T, width 1024, s_j = (1+j/50)^-3,
+k = 500, p = 10, U = C^+ A R^+).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one full randomized CUR (sketch -> CPQR(Y) -> T solve -> row ID
+on C -> U = C^+ A R^+ and the tsID skeleton) with A resident in HBM
+(`value`), and again through the host C ABI with A in pinned host memory and
+the factors copied back (`e2e`).  A is 34.4 GB, larger than the 126 MB L2, so
+no flush is needed between steps.  Device time = CUDA events on the stream
+the library launches on, max over ranks.
+
+N > 1 (torchrun): replicas -- every rank factors its own copy of A (weak
+scaling); the column-sharded path is not in this round.
+
+--impl reference: the reference's CPU algorithm (the C restatement in
+oracle/, see DESIGN.md for why not oracle/_ref) on this host's cores, on a
+bounded C4-shaped sample, extrapolated stage by stage to 65536^2.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = 65536
+K_RANK = 500
+OVERSAMPLE = 10
+ELL = K_RANK + OVERSAMPLE
+FP64_PEAK_TFLOPS = 37.1  # profiles/r01_fp64_peak.jsonl: DMMA m8n8k4 microbenchmark, this pool's B200
+FP64_PEAK_SOURCE = "profiles/r01_fp64_peak.jsonl (tools/microbench/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 entry)"
+
+
+def flops_model(m, n, k, ell):
+    """Algorithmic FP64 flop counts."""
+    cpqr_y = sum(4.0 * (ell - s) * (n - s - 1) for s in range(min(ell, n)))
+    cpqr_ct = sum(4.0 * (k - s) * (m - s - 1) for s in range(k))
+    return {
+        "sketch": 2.0 * ell * m * n,
+        "cpqr_y": cpqr_y,
+        "t_col": float(k) * k * (n - k),
+        "cpqr_ct": cpqr_ct,
+        "t_row": float(k) * k * (m - k),
+        "qr_c_rt": 2 * 2.0 * k * k * (m + n),
+        "cta": 2.0 * k * m * n,
+        "ctar": 2.0 * k * k * n,
+    }
+
+
+def cpqr_bytes(rows, cols, steps):
+    """Algorithmic HBM bytes of the fused CPQR pass: trailing block read+write
+    plus 32 B/column of norm state, per step."""
+    return sum(16.0 * (rows - s) * (cols - s) + 32.0 * (cols - s) for s in range(steps))
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def cpu_reference_estimate(sample=2048, threads=0, repeats=1):
+    """The reference algorithm on the host (oracle port), stage by stage, on a
+    C4-shaped sample (sample x sample, width 1024 -> min(sample,1024), k=500,
+    p=10) and extrapolated to 65536^2 by each stage's exact size scaling:
+    GEMM-like stages by (M/m)(N/n), n-linear stages by N/n, m-linear by M/m.
+    Returns (estimated seconds, details)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+    from paper_1412_8447_b200 import inputs
+    o = Oracle()
+    o.set_threads(threads)
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], sample, sample, width=min(1024, sample), k=K_RANK)
+    a = inputs.synthetic_np(cfg)
+    m = n = sample
+    k, ell = K_RANK, ELL
+    t = {}
+
+    def timed(name, fn):
+        t0 = time.perf_counter()
+        r = fn()
+        t[name] = time.perf_counter() - t0
+        return r
+
+    for _ in range(repeats):
+        y = timed("sketch", lambda: o.sketch_gaussian(a, ell, 1))
+        q = timed("cpqr_y", lambda: o.cpqr(y, ell, want_q=True))  # cpqr_full computes q (cpqr.hpp:91-103)
+        piv = q["pivots"]
+        s1 = q["s"][:k]
+        coeff = timed("t_col", lambda: o.coeff_solve(s1[:, :k], s1[:, k:]))
+        c = np.asfortranarray(a[:, piv[:k]])
+        rp, rc, sk = timed("tsid", lambda: o.tsid(a, k, piv))
+        r = np.asfortranarray(a[rp[:k], :])
+        rpinv = timed("pinv_r", lambda: o.pinv(r))
+        cpinv = timed("pinv_c", lambda: o.pinv(c))
+        x = np.empty((k, n), order="F")
+        timed("cpinv_a", lambda: o.L.lro_gemm_nn(k, n, m, cpinv.ctypes.data, k, a.ctypes.data, m, x.ctypes.data, k))
+        u = np.empty((k, k), order="F")
+        timed("x_rpinv", lambda: o.L.lro_gemm_nn(k, k, n, x.ctypes.data, k, rpinv.ctypes.data, n, u.ctypes.data, k))
+    fm, fn_ = M / m, N / n
+    scale = {"sketch": fm * fn_, "cpqr_y": fn_, "t_col": fn_, "tsid": fm, "pinv_r": fn_, "pinv_c": fm,
+             "cpinv_a": fm * fn_, "x_rpinv": fn_}
+    # the reference's cur-pinv path computes pinv(r) twice: once inside
+    # cur_from_two_sided (cur.hpp:30) and again in lowrank_main.cpp:215
+    mult = {"pinv_r": 2.0}
+    est = sum(t[s] * scale[s] * mult.get(s, 1.0) for s in t)
+    sample_secs = sum(t.values()) + t["pinv_r"]
+    return est, {"stage_seconds_sample": {s: round(v, 4) for s, v in t.items()}, "sample_seconds": sample_secs,
+                 "scale": scale, "sample": f"{m}x{n} C4-shaped (width {cfg.width}), k={k}, p={OVERSAMPLE}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_estimate(args.cpu_sample, threads)
+    vals = []
+    det = None
+    for _ in range(args.steps):
+        v, det = cpu_reference_estimate(args.cpu_sample, threads)
+        vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "metric": "time-to-CUR (s), randomized CUR 65536^2 k=500",
+        "impl": "reference",
+        "value": value,
+        "unit": "s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": value * 1e3,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded U diag(s) V^T, C4 spectrum)",
+        "config": {"workload": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, "
+                               "U = C^+ A R^+)", "m": M, "n": N, "k": K_RANK, "oversample": OVERSAMPLE,
+                   "u_mode": "cpinv_a_rpinv"},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
+                         "sample": det["sample"] + "; stage times extrapolated to 65536^2 "
+                                                   "(GEMM stages x(M/m)(N/n), n-linear x N/n, m-linear x M/m)"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "details": det,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_1412_8447_b200 as lr
+    from paper_1412_8447_b200 import inputs
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = inputs.CONFIGS["c4"]
+    cfg = inputs.Config(cfg.name, args.m, args.n, min(cfg.width, args.m, args.n), cfg.spectrum, args.k,
+                        OVERSAMPLE, cfg.pipeline, cfg.seed + rank, cfg.sketch_seed)
+    ctx = lr.Context(local_rank)
+    lr.lowrank._default = ctx
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    t0 = time.time()
+    a = inputs.synthetic_torch(cfg, device=dev, col_block=8192)
+    gen_s = time.time() - t0
+    sk = lr.SketchConfig(oversample=OVERSAMPLE, seed=cfg.sketch_seed)
+    out = None
+    for _ in range(args.warmup):
+        out = lr.randomized_cur_device(a, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=out)
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    ctx.enable_timing(True)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    launches0 = ctx.kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            out = lr.randomized_cur_device(a, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=out)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stages = ctx.stage_report()
+    ctx.enable_timing(False)
+    stats = ctx.stats()
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # accuracy (outside the timed region): ||A - CUR||_F / ||A||_F
+    err, na = lr.cur_error_fro_device(a, out, ctx=ctx)
+
+    # e2e through the host C ABI: pinned host A, factors copied back
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((cfg.n, cfg.m), dtype=torch.float64, pin_memory=True).T
+        host.copy_(a)
+        del a
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        ha = host.numpy()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx)  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        k = cfg.k
+        d2h = 8 * (cfg.n + cfg.m) + 8 * (cfg.m * k + k * k + k * cfg.n + k * (cfg.n - k) + k * (cfg.m - k) + k * k)
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * cfg.m * cfg.n, "d2h_bytes_per_step": d2h,
+               "steps": e2e_steps, "host_buffer": "pinned"}
+
+    if rank != 0:
+        return
+    fm = flops_model(cfg.m, cfg.n, cfg.k, cfg.k + OVERSAMPLE)
+    total_flops = sum(fm.values())
+    st = {k: v["ms"] / max(1, v["count"]) for k, v in stages.items()}
+    sketch_ms = st.get("sketch_gemm")
+    peaks = read_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6548.5)
+    roof = None
+    if sketch_ms:
+        ach = fm["sketch"] / (sketch_ms * 1e-3) / 1e12
+        roof = {"kernel": "gemm_tn_kernel (sketch Y = Omega A)", "bound": "tensor", "achieved": round(ach, 3),
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+                "traffic": None, "peak_source": FP64_PEAK_SOURCE,
+                "algorithmic": f"2*l*m*n = {fm['sketch']:.4e} flop per launch"}
+    secondary = {}
+    if st.get("ctA_gemm"):
+        ach = fm["cta"] / (st["ctA_gemm"] * 1e-3) / 1e12
+        secondary["ctA_gemm"] = {"bound": "tensor", "achieved": round(ach, 3), "unit": "TFLOP/s",
+                                 "frac": round(ach / FP64_PEAK_TFLOPS, 4)}
+    if st.get("cpqr_sample"):
+        b = cpqr_bytes(cfg.k + OVERSAMPLE, cfg.n, cfg.k + OVERSAMPLE)
+        ach = b / (st["cpqr_sample"] * 1e-3) / 1e9
+        secondary["cpqr_sample"] = {"bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                                    "frac": round(ach / hbm_peak, 4), "peak": hbm_peak,
+                                    "algorithmic_bytes": b}
+    if st.get("cpqr_ct"):
+        b = cpqr_bytes(cfg.k, cfg.m, cfg.k)
+        ach = b / (st["cpqr_ct"] * 1e-3) / 1e9
+        secondary["cpqr_ct"] = {"bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                                "frac": round(ach / hbm_peak, 4), "peak": hbm_peak, "algorithmic_bytes": b}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        est, det = cpu_reference_estimate(args.cpu_sample, os.cpu_count() or 1)
+        cpu = {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+               "sample": det["sample"] + "; stage times extrapolated to 65536^2", "details": det}
+    line = {
+        "metric": "time-to-CUR (s), randomized CUR 65536^2 k=500",
+        "value": ms / 1e3,
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded U diag(s) V^T, C4 spectrum, generated on device)",
+        "config": {"workload": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, "
+                               "U = C^+ A R^+)", "m": cfg.m, "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE,
+                   "u_mode": "cpinv_a_rpinv", "l2": "A (34.4 GB) exceeds L2; no flush needed",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "fp64_tflops": round(total_flops / (ms * 1e-3) / 1e12, 3),
+        "algorithmic_flops": total_flops,
+        "rel_error_fro": err / na,
+        "roofline": roof,
+        "roofline_secondary": secondary,
+        "stages_ms": {k: round(v, 3) for k, v in st.items()},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+        "lib_stats": stats,
+        "input_gen_s": round(gen_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--m", type=int, default=M)
+    p.add_argument("--n", type=int, default=N)
+    p.add_argument("--k", type=int, default=K_RANK)
+    p.add_argument("--cpu-sample", type=int, default=2048)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -96,6 +96,14 @@ int lr_ctx_destroy(lr_ctx* ctx);
 int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
 int lr_ctx_get_stats(lr_ctx* ctx, lr_stats* out);
 int lr_ctx_synchronize(lr_ctx* ctx);
+/* per-stage device time with CUDA events on the context stream (tracing):
+   enable, then read a JSON object {stage: {ms, count}} accumulated since the
+   last reset (the report synchronises the stream) */
+int lr_ctx_enable_timing(lr_ctx* ctx, int on);
+int lr_ctx_stage_report(lr_ctx* ctx, char* buf, int64_t buflen);
+int lr_ctx_reset_stats(lr_ctx* ctx);
+/* number of kernels this library has launched in the process */
+long long lr_kernel_launches(void);
 
 /* rng.hpp:74-94 gaussian_matrix<double>(rows, cols, seed): out rows x cols (ld rows) */
 int lr_gaussian_matrix(lr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);

@@ -51,6 +51,10 @@ SIGNATURES = {
     "lr_ctx_set_stream": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_get_stats": ([ctypes.c_void_p, ctypes.POINTER(lr_stats)], ctypes.c_int),
     "lr_ctx_synchronize": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_enable_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "lr_ctx_stage_report": ([ctypes.c_void_p, ctypes.c_char_p, c_i64], ctypes.c_int),
+    "lr_ctx_reset_stats": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_kernel_launches": ([], ctypes.c_longlong),
     "lr_gaussian_matrix": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
     "lr_gaussian_matrix_d": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp, c_i64], ctypes.c_int),
     "lr_sketch_gaussian": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),

@@ -88,9 +88,47 @@ struct lr_ctx {
   double* h_scal = nullptr;
   long long* h_ll = nullptr;
   lr_stats stats{};
+  // stage timing with CUDA events on the context stream (lr_ctx_enable_timing)
+  bool timing = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  std::vector<std::pair<std::string, double>> stage_ms;
+  std::vector<std::pair<std::string, long long>> stage_count;
 };
 
 namespace {
+
+// Close the interval since the previous mark and label it `stage`.
+void mark(lr_ctx* c, const char* stage) {
+  if (!c->timing) return;
+  cudaEvent_t e;
+  LRB_CUDA(cudaEventCreate(&e));
+  LRB_CUDA(cudaEventRecord(e, c->st));
+  c->marks.emplace_back(stage, e);
+}
+
+void flush_marks(lr_ctx* c) {
+  if (c->marks.empty()) return;
+  LRB_CUDA(cudaStreamSynchronize(c->st));
+  for (size_t i = 1; i < c->marks.size(); ++i) {
+    const std::string& name = c->marks[i].first;
+    if (name == "begin") continue;
+    float ms = 0.f;
+    LRB_CUDA(cudaEventElapsedTime(&ms, c->marks[i - 1].second, c->marks[i].second));
+    bool found = false;
+    for (size_t j = 0; j < c->stage_ms.size(); ++j)
+      if (c->stage_ms[j].first == name) {
+        c->stage_ms[j].second += ms;
+        c->stage_count[j].second += 1;
+        found = true;
+      }
+    if (!found) {
+      c->stage_ms.emplace_back(name, ms);
+      c->stage_count.emplace_back(name, 1);
+    }
+  }
+  for (auto& m : c->marks) cudaEventDestroy(m.second);
+  c->marks.clear();
+}
 
 // ---------------------------------------------------------------- helpers
 void sync(lr_ctx* c) { LRB_CUDA(cudaStreamSynchronize(c->st)); }
@@ -389,7 +427,9 @@ void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, 
   DBuf<double> omt((size_t)m * even(ell), c->st);
   // Omega^T (m x ell): element (i,j) of Omega stored at omt[j + i*m]
   gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  mark(c, "omega");
   gemm(c, ell, n, m, omt, m, a, lda, y, ldy);
+  mark(c, "sketch_gemm");
 }
 
 // sketch.hpp:200-223
@@ -417,7 +457,9 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
       fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
     throw;
   }
+  mark(c, "cpqr_sample");
   solve_core(c, k, n - k, Y, ldy, Y.p + k * ldy, ldy, strat, coeff, ldc, false);
+  mark(c, "coeff_solve_col");
 }
 
 // id.hpp:124-134: row ID of C = A(:, J) (full rank) + skeleton
@@ -439,9 +481,12 @@ void tsid_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, in
   // id_row(c, k) = id_column(c^T, k) (id.hpp:109-119)
   require_rank_in_range(k, k, m, "id_column");
   DBuf<double> tau(k, c->st);
+  mark(c, "gather_c");
   cpqr_core(c, k, m, Ct, ldct, k, row_piv, tau, "cpqr_partial");
+  mark(c, "cpqr_ct");
   solve_core(c, k, m - k, Ct, ldct, Ct.p + k * ldct, ldct, strat, row_coeff, ldrc, false);
   if (skeleton) gather_rows(k, k, C, m, row_piv, skeleton, k, c->st);
+  mark(c, "coeff_solve_row");
 }
 
 // cur.hpp:23-34 / lowrank_main.cpp:215 given skeleton index sets
@@ -463,28 +508,36 @@ void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int
   transpose_matrix(k, n, R, k, Rt, even(n), c->st);
   copy_matrix(k, n, R, k, Rk, ldk, c->st);  // R with an even leading dimension for TMA
   DBuf<double> Sr((size_t)k * k, c->st), Sri((size_t)k * k, c->st);
+  mark(c, "gather_r");
   const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
+  mark(c, "cholqr2_r");
   c->stats.pinv_fast_path = 0;
   if (u_mode == LR_U_CPINV_A_RPINV) {
     DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st);
     DBuf<double> Cm((size_t)even(m) * k, c->st);
     copy_matrix(m, k, C, m, Cm, even(m), c->st);
     const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci);
+    mark(c, "cholqr2_c");
     if (c_ok && r_ok) {
       c->stats.pinv_fast_path = 1;
-      // U = Rc^-1 Rc^-T (C^T A R^T) Sr^-1 Sr^-T
+      // C = Qc Rc, R^T = Qr Sr  =>  U = C^+ A R^+ = Rc^-1 (Qc^T A Qr) Sr^-T.
+      // The big contraction uses the orthonormal Qc (not C): applying Rc^-1
+      // to C^T A would square cond(C) in the least-squares error.
+      DBuf<double> Qc((size_t)even(m) * k, c->st), Qr((size_t)even(n) * k, c->st);
+      gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m));            // Qc = C Rc^-1  (m x k)
+      gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n));            // Qr = R^T Sr^-1 (n x k)
       DBuf<double> Xt((size_t)even(n) * k, c->st), W((size_t)k * k, c->st);
-      gemm(c, n, k, m, a, lda, Cm, even(m), Xt, even(n));        // X^T = A^T C  (n x k)
-      gemm(c, k, k, n, Xt, even(n), Rt, even(n), W, k);          // W = X R^T = C^T A R^T
-      DBuf<double> t1((size_t)k * k, c->st), t2((size_t)k * k, c->st), tt((size_t)k * k, c->st);
-      gemm(c, k, k, k, Rci, k, W, k, t1, k);                     // t1 = Rc^-T W
+      mark(c, "form_q");
+      gemm(c, n, k, m, a, lda, Qc, even(m), Xt, even(n));        // X^T = A^T Qc  (n x k)
+      mark(c, "ctA_gemm");
+      gemm(c, k, k, n, Xt, even(n), Qr, even(n), W, k);          // W = Qc^T A Qr
+      DBuf<double> t1((size_t)k * k, c->st), tt((size_t)k * k, c->st), st((size_t)k * k, c->st);
       transpose_matrix(k, k, Rci, k, tt, k, c->st);
-      gemm(c, k, k, k, tt, k, t1, k, t2, k);                     // t2 = Rc^-1 t1
-      transpose_matrix(k, k, t2, k, tt, k, c->st);
-      gemm(c, k, k, k, tt, k, Sri, k, t1, k);                    // t1 = t2 Sr^-1
+      gemm(c, k, k, k, tt, k, W, k, t1, k);                      // t1 = Rc^-1 W
       transpose_matrix(k, k, t1, k, tt, k, c->st);
-      transpose_matrix(k, k, Sri, k, t2, k, c->st);
-      gemm(c, k, k, k, tt, k, t2, k, U, k);                      // U = t1 Sr^-T
+      transpose_matrix(k, k, Sri, k, st, k, c->st);
+      gemm(c, k, k, k, tt, k, st, k, U, k);                      // U = t1 Sr^-T
+      mark(c, "u_small");
       return;
     }
     // general path: explicit truncated pseudoinverses (SVD route when ill-conditioned)
@@ -897,6 +950,7 @@ int lr_randomized_cur_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
       rc = DBuf<double>((size_t)k * std::max<int64_t>(m - k, 1), c->st);
       row_coeff = rc;
     }
+    mark(c, "begin");
     randomized_id_core(c, m, n, a, lda, k, cfg, strat, col_pivots, col_coeff, k);
     DBuf<double> Ct((size_t)even(k) * m, c->st);
     tsid_core(c, m, n, a, lda, k, col_pivots, strat, row_pivots, row_coeff, k, skeleton, C, Ct);
@@ -1013,6 +1067,46 @@ int lr_cur_error_fro(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t l
     error_core(c, m, n, d, l, k, Cc, Uc, Rc, out);
   });
 }
+
+int lr_ctx_enable_timing(lr_ctx* c, int on) {
+  return guard([&] {
+    checked(c);
+    flush_marks(c);
+    c->timing = on != 0;
+  });
+}
+
+int lr_ctx_stage_report(lr_ctx* c, char* buf, int64_t buflen) {
+  return guard([&] {
+    checked(c);
+    flush_marks(c);
+    std::string s = "{";
+    for (size_t i = 0; i < c->stage_ms.size(); ++i) {
+      if (i) s += ", ";
+      char tmp[160];
+      snprintf(tmp, sizeof tmp, "\"%s\": {\"ms\": %.6f, \"count\": %lld}", c->stage_ms[i].first.c_str(),
+               c->stage_ms[i].second, c->stage_count[i].second);
+      s += tmp;
+    }
+    s += "}";
+    if (buf && buflen > 0) {
+      strncpy(buf, s.c_str(), (size_t)buflen - 1);
+      buf[buflen - 1] = 0;
+    }
+  });
+}
+
+int lr_ctx_reset_stats(lr_ctx* c) {
+  return guard([&] {
+    checked(c);
+    flush_marks(c);
+    c->stage_ms.clear();
+    c->stage_count.clear();
+    c->stats = lr_stats{};
+  });
+}
+
+long long lr_kernel_launches(void) { return (long long)lrb::g_kernel_launches; }
 
 int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo) {

@@ -26,7 +26,13 @@ struct CudaError : std::runtime_error {
                              __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
 
-#define LRB_CHECK_LAUNCH() LRB_CUDA(cudaGetLastError())
+// every kernel launch site calls this: error check + launch accounting
+extern unsigned long long g_kernel_launches;
+#define LRB_CHECK_LAUNCH()                     \
+  do {                                         \
+    ++::lrb::g_kernel_launches;                \
+    LRB_CUDA(cudaGetLastError());              \
+  } while (0)
 
 constexpr int kNumSMsB200 = 148;
 

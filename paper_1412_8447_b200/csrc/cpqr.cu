@@ -408,6 +408,7 @@ void launch_cpqr(CpqrArgs& args, size_t smem, cudaStream_t st) {
   (void)G;
   void* params[] = {&args};
   LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kThreads), params, smem, st));
+  LRB_CHECK_LAUNCH();
 }
 
 int cpqr_grid(int64_t n, int64_t m) {

@@ -9,6 +9,8 @@
 
 namespace lrb {
 
+unsigned long long g_kernel_launches = 0;
+
 // ---------------------------------------------------------------- workspace
 Workspace::~Workspace() { release_all(); }
 

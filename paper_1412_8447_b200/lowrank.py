@@ -25,7 +25,7 @@ __all__ = [
     "stabilized_coeff_solve", "svd", "pinv", "id_column", "id_row", "tsid_from_column_id", "id_two_sided",
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
-    "randomized_cur_device", "cur_error_fro_device", "U_VT_RPINV", "U_CPINV_A_RPINV",
+    "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
 ]
 
 LowrankCudaError = L.LowrankCudaError
@@ -250,6 +250,21 @@ class Context:
 
     def synchronize(self) -> None:
         _raise(self.lib.lr_ctx_synchronize(self.h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        _raise(self.lib.lr_ctx_enable_timing(self.h, int(on)))
+
+    def stage_report(self) -> dict:
+        import json
+        buf = ctypes.create_string_buffer(1 << 16)
+        _raise(self.lib.lr_ctx_stage_report(self.h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def reset_stats(self) -> None:
+        _raise(self.lib.lr_ctx_reset_stats(self.h))
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.lr_kernel_launches())
 
 
 _default: Optional[Context] = None

@@ -69,7 +69,6 @@ def test_gemm_kernel_vs_numpy(lr):
     for (M, N, K) in [(510, 1000, 777), (128, 128, 16), (5, 7, 3), (300, 260, 4100)]:
         P = torch.randn(K, M, dtype=torch.float64, device="cuda")
         Q = torch.randn(K, N, dtype=torch.float64, device="cuda")
-        Pc = P.T.contiguous().T if K > 1 else P  # column-major K x M
         Pc = lr.empty_colmajor(K, M, "cuda"); Pc.copy_(P)
         Qc = lr.empty_colmajor(K, N, "cuda"); Qc.copy_(Q)
         out = lr.empty_colmajor(M, N, "cuda")
