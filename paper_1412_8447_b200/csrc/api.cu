@@ -281,7 +281,7 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
   gemm(c, k, k, k, s, k, s, k, eye, k, 1.0, 1.0);  // eye = S^T S + ridge^2 I
   gemm(c, k, nc, k, s, k, s12, ld12, rhs, k);      // rhs = S^T S12
   DBuf<int> info(1, c->st);
-  cholesky_upper(k, eye, k, info, c->st);
+  cholesky_upper(c->ws, k, eye, k, info, c->st);
   DBuf<double> ri((size_t)k * k, c->st), rit((size_t)k * k, c->st), y((size_t)k * nc, c->st);
   tri_upper_inverse(k, eye, k, ri, k, c->st);
   transpose_matrix(k, k, ri, k, rit, k, c->st);
@@ -341,7 +341,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   DBuf<double> G((size_t)k * k, c->st), R1inv((size_t)k * k, c->st), Q1((size_t)even(rows) * k, c->st);
   DBuf<int> info(2, c->st);
   gemm(c, k, k, rows, X, ldx, X, ldx, G, k);  // G1 = X^T X
-  cholesky_upper(k, G, k, info, c->st);        // G <- R1
+  cholesky_upper(c->ws, k, G, k, info, c->st);  // G <- R1
   LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   sync(c);
   if (c->h_flags[0] != 0) return false;
@@ -349,7 +349,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   gemm(c, rows, k, k, Xt, ldxt, R1inv, k, Q1, even(rows));  // Q1 = X R1^-1
   DBuf<double> G2((size_t)k * k, c->st), R2t((size_t)k * k, c->st);
   gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k);  // G2 = Q1^T Q1
-  cholesky_upper(k, G2, k, info.p + 1, c->st);
+  cholesky_upper(c->ws, k, G2, k, info.p + 1, c->st);
   LRB_CUDA(cudaMemcpyAsync(c->h_flags + 1, info.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   sync(c);
   if (c->h_flags[1] != 0) return false;

@@ -12,15 +12,19 @@
 // B200 design: ONE persistent cooperative kernel runs all k steps.  Columns
 // are statically partitioned over CTAs (and round-robin over warps); a warp
 // owns a whole column and keeps up to 64*CH rows in registers (the sketch Y
-// and C^T have <= 512 rows, so one 16-byte load per lane per 64 rows moves the
-// column in and out exactly once per step).  Each step is one fused HBM pass
+// and C^T have <= 512 rows: one 16-byte load per lane per 64 rows moves a
+// column in and out exactly once per step), with the next column's loads
+// issued before the current one is reduced (register double buffering).
+// Each step is one fused HBM pass
 //   dot(v, col) -> rank-1 update -> row-s downdate -> (rare) exact recompute
 //   -> per-warp / per-CTA argmax on (norm2 desc, position asc)
-// followed by a single grid barrier.  The winning CTA's best column is staged
-// in a double-buffered candidate slot, so every CTA rebuilds the next
-// reflector redundantly (identical inputs, fixed reduction tree => identical
-// bits) without a second barrier.  Rows > 64*CH (tall deterministic IDs)
-// stream through L2 in two passes.
+// followed by a single grid barrier.  At the end of a step every CTA builds
+// the Householder reflector of ITS best column (fresh norm, beta, tau, v) and
+// stages it in a double-buffered candidate slot; the next step only reads the
+// winner's slot, so the serial part of a step is one batched L2 round trip.
+// Sweep direction alternates per step so the columns written last are read
+// first while still in L2.  Rows > 64*CH (tall deterministic IDs) stream
+// through L2 in two passes.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -35,6 +39,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSmemRows = 6144;  // v and tau*v kept in shared memory up to this height
+constexpr int kMaxG = 512;          // partial slots read by one warp (16 per lane)
+constexpr int kHdr = 4;             // candidate header: alpha, beta, tau, apply
 
 struct CpqrArgs {
   double* W;
@@ -45,27 +51,14 @@ struct CpqrArgs {
   double* tau;
   double* pval;      // [2][G]
   long long* ppos;   // [2][G]
-  double* cand;      // [2][G][m]
-  double* scratch;   // [G][3*m]: old-s column, pivot R rows, (v,tv if not in smem)
+  double* cand;      // [2][G][kHdr + m]: reflector of each CTA's best column
+  double* scratch;   // [G][4*m]: old-s column, pivot R rows, (v, tau*v if not in smem)
   int* flags;
   unsigned long long* recomputes;
 };
 
-struct Best {
-  double v;
-  long long p;
-};
 __device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
-}
-__device__ __forceinline__ Best warp_best(Best b) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
-    const long long op = __shfl_xor_sync(0xffffffffu, b.p, o);
-    if (better(ov, op, b.v, b.p)) { b.v = ov; b.p = op; }
-  }
-  return b;
 }
 
 // fixed-order CTA sum (all threads receive the result)
@@ -81,34 +74,95 @@ __device__ double cta_sum(double x, double* sh) {
   return t;
 }
 
+// Reflector of column jb (rows s0..m-1, cpqr.hpp:59-66) into candidate slot cd.
+// When colnorm == 0 the slot carries x itself (the column is left untouched).
+__device__ void stage_candidate(const CpqrArgs& a, double* cd, int64_t s0, long long jb, double* sh) {
+  const int64_t m = a.m;
+  if (jb >= a.n || s0 >= m) {
+    __syncthreads();
+    return;
+  }
+  const double* x = a.W + jb * a.ld;
+  double part = 0.0;
+  for (int64_t i = s0 + threadIdx.x; i < m; i += kThreads) part = fma(x[i], x[i], part);
+  const double cn2 = cta_sum(part, sh);
+  const double colnorm = sqrt(cn2);
+  const double alpha = x[s0];
+  const bool apply = colnorm > 0.0;
+  double beta = alpha, tau = 0.0, scale = 1.0;
+  if (apply) {
+    beta = alpha >= 0.0 ? -colnorm : colnorm;
+    tau = (beta - alpha) / beta;
+    scale = alpha - beta;
+  }
+  for (int64_t i = s0 + threadIdx.x; i < m; i += kThreads)
+    cd[kHdr + i] = apply ? ((i == s0) ? 1.0 : x[i] / scale) : x[i];
+  if (threadIdx.x == 0) {
+    cd[0] = alpha;
+    cd[1] = beta;
+    cd[2] = tau;
+    cd[3] = apply ? 1.0 : 0.0;
+  }
+}
+
+// per-warp column state
 template <int CH>
-__global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
+struct Col {
+  double c[CH][2];
+  double nr, nx;
+};
+
+template <int CH>
+__device__ __forceinline__ void load_col(Col<CH>& col, const double* src, bool cross_cta, int64_t s, int64_t m,
+                                         int lane) {
+#pragma unroll
+  for (int t = 0; t < CH; ++t) {
+    const int64_t i = 64 * t + 2 * lane;
+    col.c[t][0] = col.c[t][1] = 0.0;
+    if (64 * (t + 1) > s && i < m) {
+      if (i + 1 < m) {
+        const double2 xx = cross_cta ? __ldcg(reinterpret_cast<const double2*>(src + i))
+                                     : *reinterpret_cast<const double2*>(src + i);
+        col.c[t][0] = xx.x;
+        col.c[t][1] = xx.y;
+      } else {
+        col.c[t][0] = cross_cta ? __ldcg(src + i) : src[i];
+      }
+    }
+  }
+}
+
+template <int CH, bool PF>
+__global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dyn[];
   __shared__ double sh_red[kWarps];
   __shared__ double sh_bv[kWarps];
   __shared__ long long sh_bp[kWarps];
-  __shared__ double sh_scal[4];  // alpha, beta, tau, colnorm
-  __shared__ long long sh_piv[2];  // p, winner cta
-  __shared__ long long sh_state[3];  // piv[p], piv[s] (bits), unused
-  __shared__ double sh_nst[4];     // nrm[p], nrmx[p], nrm[s], nrmx[s]
+  __shared__ double sh_hdr[kHdr];
+  __shared__ long long sh_piv[2];    // p, winner cta
+  __shared__ long long sh_state[2];  // piv[p], piv[s]
+  __shared__ double sh_nst[4];       // nrm[p], nrmx[p], nrm[s], nrmx[s]
 
   const int G = gridDim.x, cta = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = a.m, n = a.n, ld = a.ld, k = a.k;
   const int64_t c0 = n * cta / G, c1 = n * (cta + 1) / G;
-  double* scr = a.scratch + (int64_t)cta * 3 * m;
-  double* olds = scr;          // old column at position s (when swapped into p)
-  double* pivr = scr + m;      // pivot column rows < s
+  const int64_t cand_sz = kHdr + m;
+  double* scr = a.scratch + (int64_t)cta * 4 * m;
+  double* olds = scr;      // old column at position s (when swapped into p)
+  double* pivr = scr + m;  // pivot column rows < s
   const bool vs = m <= kMaxSmemRows;
-  double* vv = vs ? dyn : scr + 2 * m;           // v[i] for i >= s (v[s] = 1)
-  double* tv = vs ? dyn + m : nullptr;  // tau*v; recomputed on the fly when v is not in smem
+  double* vv = vs ? dyn : scr + 2 * m;      // v[i] for i >= s (v[s] = 1)
+  double* tv = vs ? dyn + m : scr + 3 * m;  // tau * v
   const int nchunks = (int)((m + 63) / 64);
+  const int64_t cnt = (c1 - c0 - warp + kWarps - 1) / kWarps;  // columns of this warp
   unsigned long long my_recomputes = 0;
 
   // ------------------------------------------------------------ init
   {
-    Best b{-INFINITY, (long long)INT64_MAX};
+    double bv = -INFINITY;
+    long long bp = INT64_MAX;
     int bad = 0;
     for (int64_t j = c0 + warp; j < c1; j += kWarps) {
       const double* col = a.W + j * ld;
@@ -132,23 +186,22 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
         a.nrmx[j] = acc;
         a.piv[j] = j;
       }
-      if (better(acc, j, b.v, b.p)) { b.v = acc; b.p = j; }
+      if (better(acc, j, bv, bp)) { bv = acc; bp = j; }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags, 1);
-    if (lane == 0) { sh_bv[warp] = b.v; sh_bp[warp] = b.p; }
+    if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
     __syncthreads();
     if (threadIdx.x == 0) {
-      Best cb{sh_bv[0], sh_bp[0]};
+      double cv = sh_bv[0];
+      long long cp = sh_bp[0];
       for (int w = 1; w < kWarps; ++w)
-        if (better(sh_bv[w], sh_bp[w], cb.v, cb.p)) { cb.v = sh_bv[w]; cb.p = sh_bp[w]; }
-      a.pval[cta] = cb.v;
-      a.ppos[cta] = cb.p;
-      sh_piv[0] = cb.p;
+        if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      a.pval[cta] = cv;
+      a.ppos[cta] = cp;
+      sh_piv[0] = cp;
     }
     __syncthreads();
-    const long long bp = sh_piv[0];
-    if (bp < n)
-      for (int64_t i = threadIdx.x; i < m; i += kThreads) a.cand[(int64_t)cta * m + i] = a.W[bp * ld + i];
+    stage_candidate(a, a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0], sh_red);
   }
   grid.sync();
   if (__ldcg(a.flags) != 0) return;
@@ -156,57 +209,46 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
   // ------------------------------------------------------------ steps
   for (int64_t s = 0; s < k; ++s) {
     const int par = (int)(s & 1), nxt = par ^ 1;
-    // (1) global argmax over the per-CTA partials, fixed order
+    // (1) global argmax over the per-CTA partials: one batched load per lane
     if (warp == 0) {
-      Best b{-INFINITY, (long long)INT64_MAX};
-      long long bc = -1;
-      for (int c = lane; c < G; c += 32) {
-        const double v = __ldcg(a.pval + (int64_t)par * G + c);
-        const long long p = __ldcg(a.ppos + (int64_t)par * G + c);
-        if (better(v, p, b.v, b.p)) { b.v = v; b.p = p; bc = c; }
+      double pv[kMaxG / 32];
+      long long pp[kMaxG / 32];
+#pragma unroll
+      for (int r = 0; r < kMaxG / 32; ++r) {
+        const int c = lane + 32 * r;
+        pv[r] = c < G ? __ldcg(a.pval + (int64_t)par * G + c) : -INFINITY;
+        pp[r] = c < G ? __ldcg(a.ppos + (int64_t)par * G + c) : INT64_MAX;
       }
+      double bv = pv[0];
+      long long bp = pp[0];
+      int bc = lane;
+#pragma unroll
+      for (int r = 1; r < kMaxG / 32; ++r)
+        if (better(pv[r], pp[r], bv, bp)) { bv = pv[r]; bp = pp[r]; bc = lane + 32 * r; }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
-        const long long op = __shfl_xor_sync(0xffffffffu, b.p, o);
-        const long long oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (better(ov, op, b.v, b.p)) { b.v = ov; b.p = op; bc = oc; }
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const long long op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(ov, op, bv, bp)) { bv = ov; bp = op; bc = oc; }
       }
-      if (lane == 0) { sh_piv[0] = b.p; sh_piv[1] = bc; }
+      if (lane == 0) { sh_piv[0] = bp; sh_piv[1] = bc; }
     }
     __syncthreads();
     const int64_t p = sh_piv[0];
-    const int wc = (int)sh_piv[1];
-    const double* x = a.cand + ((int64_t)par * G + wc) * m;  // pivot column, rows >= s valid
+    const double* cd = a.cand + ((int64_t)par * G + sh_piv[1]) * cand_sz;
 
-    // (2) reflector, redundantly per CTA (cpqr.hpp:59-66)
-    double part = 0.0;
-    for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
-      const double xi = __ldcg(x + i);
-      part = fma(xi, xi, part);
-    }
-    const double cn2 = cta_sum(part, sh_red);
-    const double colnorm = sqrt(cn2);
-    const double alpha = __ldcg(x + s);
-    double beta = alpha, tau = 0.0, scale = 1.0;
-    const bool apply = colnorm > 0.0;
-    if (apply) {
-      beta = alpha >= 0.0 ? -colnorm : colnorm;
-      tau = (beta - alpha) / beta;
-      scale = alpha - beta;
-    }
-    if (vs) {
+    // (2) the winner's reflector -> v, tau*v (one batched L2 round trip)
+    {
+      const double tau_b = __ldcg(cd + 2);
+      const bool apply_b = __ldcg(cd + 3) != 0.0;
       for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
-        const double vi = (i == s) ? 1.0 : (apply ? __ldcg(x + i) / scale : 0.0);
+        const double vi = __ldcg(cd + kHdr + i);
         vv[i] = vi;
-        tv[i] = tau * vi;
+        tv[i] = apply_b ? tau_b * vi : 0.0;
       }
-    } else {
-      for (int64_t i = s + threadIdx.x; i < m; i += kThreads)
-        vv[i] = (i == s) ? 1.0 : (apply ? __ldcg(x + i) / scale : 0.0);
+      if (threadIdx.x < kHdr) sh_hdr[threadIdx.x] = __ldcg(cd + threadIdx.x);
     }
-    if (cta == 0 && threadIdx.x == 0) a.tau[s] = tau;
-
     // (3) swap bookkeeping by the owner of position p
     const bool owner = (p >= c0 && p < c1);
     const bool swapped = owner && p != s;
@@ -223,42 +265,43 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
       }
     }
     __syncthreads();
+    const double tau = sh_hdr[2];
+    const bool apply = sh_hdr[3] != 0.0;
+    if (cta == 0 && threadIdx.x == 0) a.tau[s] = tau;
 
     // (4) fused trailing pass over owned positions j in (s, n)
-    Best b{-INFINITY, (long long)INT64_MAX};
-    const int64_t jstart = c0 + warp;
-    for (int64_t j = jstart; j < c1; j += kWarps) {
-      if (j <= s) continue;
+    double bv = -INFINITY;
+    long long bp = INT64_MAX;
+    auto col_of = [&](int64_t it) { return c0 + warp + kWarps * ((s & 1) ? (cnt - 1 - it) : it); };
+    auto next_valid = [&](int64_t it) {
+      while (it < cnt && col_of(it) <= s) ++it;
+      return it;
+    };
+    auto fetch = [&](Col<CH>& cb, int64_t j) {
+      const bool from_s = swapped && j == p;
+      load_col<CH>(cb, from_s ? olds : a.W + j * ld, false, s, m, lane);
+      cb.nr = from_s ? sh_nst[2] : a.nrm[j];
+      cb.nx = from_s ? sh_nst[3] : a.nrmx[j];
+    };
+    auto process = [&](Col<CH>& cb, int64_t j) {
       const bool from_s = swapped && j == p;
       const double* src = from_s ? olds : a.W + j * ld;
       double* dst = a.W + j * ld;
-      double cache[CH][2];
       double dot = 0.0;
-      // pass A: load active rows (>= s) and dot with v
 #pragma unroll
       for (int t = 0; t < CH; ++t) {
         const int64_t i = 64 * t + 2 * lane;
-        cache[t][0] = cache[t][1] = 0.0;
         if (64 * (t + 1) > s && i < m) {
-          if (i + 1 < m) {
-            const double2 xx = from_s ? make_double2(__ldcg(src + i), __ldcg(src + i + 1))
-                                      : *reinterpret_cast<const double2*>(src + i);
-            cache[t][0] = xx.x;
-            cache[t][1] = xx.y;
-          } else {
-            cache[t][0] = from_s ? __ldcg(src + i) : src[i];
-          }
-          if (i >= s) dot = fma(cache[t][0], vv[i], dot);
-          if (i + 1 >= s && i + 1 < m) dot = fma(cache[t][1], vv[i + 1], dot);
+          if (i >= s) dot = fma(cb.c[t][0], vv[i], dot);
+          if (i + 1 >= s && i + 1 < m) dot = fma(cb.c[t][1], vv[i + 1], dot);
         }
       }
-      for (int t = CH; t < nchunks; ++t) {  // streamed rows
+      for (int t = CH; t < nchunks; ++t) {  // streamed rows (tall matrices)
         const int64_t i = 64 * t + 2 * lane;
-        if (i < m && i >= s) dot = fma(from_s ? __ldcg(src + i) : src[i], vv[i], dot);
-        if (i + 1 < m && i + 1 >= s) dot = fma(from_s ? __ldcg(src + i + 1) : src[i + 1], vv[i + 1], dot);
+        if (i < m && i >= s) dot = fma(src[i], vv[i], dot);
+        if (i + 1 < m && i + 1 >= s) dot = fma(src[i + 1], vv[i + 1], dot);
       }
       dot = warp_sum(dot);
-      // pass B: update (W -= (tau v) w), collect row s and the tail square sum
       double xs = 0.0, tail2 = 0.0;
 #pragma unroll
       for (int t = 0; t < CH; ++t) {
@@ -268,18 +311,15 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
           for (int e = 0; e < 2; ++e) {
             const int64_t r = i + e;
             if (r >= s && r < m) {
-              double c = cache[t][e];
-              if (apply) c = fma(-(vs ? tv[r] : tau * vv[r]), dot, c);
-              cache[t][e] = c;
+              double c = cb.c[t][e];
+              if (apply) c = fma(-tv[r], dot, c);
+              cb.c[t][e] = c;
               if (r == s) xs = c;
               else tail2 = fma(c, c, tail2);
             }
           }
-          if (i + 1 < m) {
-            *reinterpret_cast<double2*>(dst + i) = make_double2(cache[t][0], cache[t][1]);
-          } else {
-            dst[i] = cache[t][0];
-          }
+          if (i + 1 < m) *reinterpret_cast<double2*>(dst + i) = make_double2(cb.c[t][0], cb.c[t][1]);
+          else dst[i] = cb.c[t][0];
         }
       }
       for (int t = CH; t < nchunks; ++t) {
@@ -287,9 +327,9 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
         for (int e = 0; e < 2; ++e) {
           const int64_t r = 64 * t + 2 * lane + e;
           if (r < m) {
-            double c = from_s ? __ldcg(src + r) : src[r];
+            double c = src[r];
             if (r >= s) {
-              if (apply) c = fma(-(vs ? tv[r] : tau * vv[r]), dot, c);
+              if (apply) c = fma(-tv[r], dot, c);
               if (r == s) xs = c;
               else tail2 = fma(c, c, tail2);
             }
@@ -297,16 +337,11 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
           }
         }
       }
-      if (from_s) {
-        // rows < s of the swapped-in column, and rows in cached chunks wholly below s
-        for (int64_t r = lane; r < m && r < s; r += 32)
-          if (r < 64 * (int64_t)CH) dst[r] = __ldcg(olds + r);
-      }
-      // row s lives in lane (s%64)/2 of chunk s/64 (or the streamed part)
+      if (from_s)  // rows < s of the swapped-in column that sit in skipped cached chunks
+        for (int64_t r = lane; r < s && r < 64 * (int64_t)CH; r += 32) dst[r] = olds[r];
       xs = __shfl_sync(0xffffffffu, xs, (int)((s % 64) / 2));
-      double nr = from_s ? sh_nst[2] : a.nrm[j];
-      double nx = from_s ? sh_nst[3] : a.nrmx[j];
-      nr -= xs * xs;
+      double nr = cb.nr - xs * xs;
+      double nx = cb.nx;
       if (nr < 1e-6 * nx) {
         nr = warp_sum(tail2);
         nx = nr;
@@ -317,19 +352,41 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
         a.nrmx[j] = nx;
         if (from_s) a.piv[j] = sh_state[1];
       }
-      if (better(nr, j, b.v, b.p)) { b.v = nr; b.p = j; }
+      if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
+    };
+    if constexpr (!PF) {
+      Col<CH> A;
+      for (int64_t it = next_valid(0); it < cnt; it = next_valid(it + 1)) {
+        fetch(A, col_of(it));
+        process(A, col_of(it));
+      }
+    } else {
+      Col<CH> A, B;
+      int64_t it = next_valid(0);
+      if (it < cnt) fetch(A, col_of(it));
+      while (it < cnt) {
+        const int64_t it2 = next_valid(it + 1);
+        if (it2 < cnt) fetch(B, col_of(it2));
+        process(A, col_of(it));
+        if (it2 >= cnt) break;
+        const int64_t it3 = next_valid(it2 + 1);
+        if (it3 < cnt) fetch(A, col_of(it3));
+        process(B, col_of(it2));
+        it = it3;
+      }
     }
 
     // (5) CTA argmax, pivot column write-back, candidate staging
-    if (lane == 0) { sh_bv[warp] = b.v; sh_bp[warp] = b.p; }
+    if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
     __syncthreads();
     if (threadIdx.x == 0) {
-      Best cb{sh_bv[0], sh_bp[0]};
+      double cv = sh_bv[0];
+      long long cp = sh_bp[0];
       for (int w = 1; w < kWarps; ++w)
-        if (better(sh_bv[w], sh_bp[w], cb.v, cb.p)) { cb.v = sh_bv[w]; cb.p = sh_bp[w]; }
-      a.pval[(int64_t)nxt * G + cta] = cb.v;
-      a.ppos[(int64_t)nxt * G + cta] = cb.p;
-      sh_piv[0] = cb.p;
+        if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      a.pval[(int64_t)nxt * G + cta] = cv;
+      a.ppos[(int64_t)nxt * G + cta] = cp;
+      sh_piv[0] = cp;
     }
     if (owner) {
       double* ps = a.W + s * ld;
@@ -341,25 +398,16 @@ __global__ void __launch_bounds__(kThreads) cpqr_kernel(CpqrArgs a) {
           a.nrmx[s] = sh_nst[1];
         }
       }
-      for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
-        double val;
-        if (!apply) val = __ldcg(x + i);
-        else val = (i == s) ? beta : vv[i];
-        ps[i] = val;
-      }
+      const double beta = sh_hdr[1];
+      for (int64_t i = s + threadIdx.x; i < m; i += kThreads) ps[i] = (apply && i == s) ? beta : vv[i];
     }
     __syncthreads();
-    const long long bp = sh_piv[0];
-    if (bp < n) {
-      double* cd = a.cand + ((int64_t)nxt * G + cta) * m;
-      for (int64_t i = s + 1 + threadIdx.x; i < m; i += kThreads) cd[i] = a.W[bp * ld + i];
-    }
+    stage_candidate(a, a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0], sh_red);
     grid.sync();
   }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
 }
 
-// s (k x n) = top k rows, strict lower zeroed, rows with negative diagonal negated
 __global__ void extract_s_kernel(int64_t m, int64_t n, const double* __restrict__ W, int64_t ld, int64_t k,
                                  double* __restrict__ s, int64_t lds) {
   const int64_t total = k * n;
@@ -394,38 +442,35 @@ __global__ void form_q_kernel(int64_t m, const double* __restrict__ W, int64_t l
     for (int64_t i = lane; i < m; i += 32) qc[i] = -qc[i];
 }
 
-template <int CH>
-void launch_cpqr(CpqrArgs& args, size_t smem, cudaStream_t st) {
-  auto kern = cpqr_kernel<CH>;
+
+template <int CH, bool PF>
+int launch_cpqr(CpqrArgs& args, size_t smem, int Gmax, cudaStream_t st) {
+  auto kern = cpqr_kernel<CH, PF>;
   if (smem > 48 * 1024) LRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-  per_sm = std::max(1, std::min(per_sm, 4));
-  int G = per_sm * num_sms();
-  // no more CTAs than columns / warps worth of work
-  const int64_t max_g = std::max<int64_t>(1, (args.n + kWarps - 1) / kWarps);
-  if (G > max_g) G = (int)max_g;
-  (void)G;
+  per_sm = std::max(1, std::min(per_sm, 2));
+  int G = std::min(per_sm * num_sms(), Gmax);
   void* params[] = {&args};
   LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kThreads), params, smem, st));
   LRB_CHECK_LAUNCH();
+  return G;
 }
 
-int cpqr_grid(int64_t n, int64_t m) {
-  (void)m;
+int cpqr_grid(int64_t n) {
   const int64_t max_g = std::max<int64_t>(1, (n + kWarps - 1) / kWarps);
-  return (int)std::min<int64_t>(4 * num_sms(), max_g);
+  return (int)std::min<int64_t>(std::min(2 * num_sms(), kMaxG), max_g);
 }
 
 }  // namespace
 
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                   double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
-  const int Gmax = cpqr_grid(n, m);
-  // state: nrm, nrmx (n each), pval (2G), ppos (2G), cand (2 G m), scratch (G 3m)
-  const size_t bytes = sizeof(double) * (2 * (size_t)n + 2 * (size_t)Gmax + 2 * (size_t)Gmax * m +
-                                         3 * (size_t)Gmax * m) +
-                       sizeof(long long) * 2 * (size_t)Gmax + 256;
+  const int Gmax = cpqr_grid(n);
+  const size_t cand_sz = kHdr + (size_t)m;
+  // state: nrm, nrmx (n each), pval (2G), cand (2 G cand_sz), scratch (G 4m), ppos (2G)
+  const size_t nd = 2 * (size_t)n + 2 * (size_t)Gmax + 2 * (size_t)Gmax * cand_sz + 4 * (size_t)Gmax * m;
+  const size_t bytes = sizeof(double) * nd + sizeof(long long) * 2 * (size_t)Gmax + 256;
   uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
   CpqrArgs a{};
   a.W = W;
@@ -440,13 +485,13 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
   a.nrmx = d + n;
   a.pval = d + 2 * n;
   a.cand = a.pval + 2 * Gmax;
-  a.scratch = a.cand + 2 * (size_t)Gmax * m;
-  a.ppos = reinterpret_cast<long long*>(a.scratch + 3 * (size_t)Gmax * m);
+  a.scratch = a.cand + 2 * (size_t)Gmax * cand_sz;
+  a.ppos = reinterpret_cast<long long*>(a.scratch + 4 * (size_t)Gmax * m);
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
   const size_t smem = m <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)m : 0;
-  if (m <= 512) launch_cpqr<8>(a, smem, st);
-  else launch_cpqr<16>(a, smem, st);
+  if (m <= 512) launch_cpqr<8, true>(a, smem, Gmax, st);
+  else launch_cpqr<16, false>(a, smem, Gmax, st);
 }
 
 void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,

@@ -122,7 +122,7 @@ void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld1
                            int64_t ld12, const double* t, int64_t ldt, const int* zero_rows, double* res,
                            cudaStream_t st);
 // Cholesky G = R^T R (upper R, k x k, in place on a copy); info[0] = first failing column+1 or 0
-void cholesky_upper(int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st);
+void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st);
 // inverse of an upper-triangular R (k x k) -> Rinv (upper)
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
 

@@ -118,7 +118,82 @@ __global__ void max_reduce_kernel(const double* __restrict__ p, int n, double* o
   }
 }
 
-// Right-looking Cholesky G = R^T R on the upper triangle, one CTA.
+// ---- blocked Cholesky (G = R^T R, upper): diagonal block in shared memory,
+// panel by forward substitution, trailing SYRK on the DMMA GEMM.
+constexpr int kCholB = 64;
+
+__global__ void chol_diag_kernel(int64_t j0, int jb, double* __restrict__ g, int64_t ldg, int* info) {
+  __shared__ double a[kCholB][kCholB + 1];
+  __shared__ int fail;
+  if (info[0] != 0) return;
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
+    const int i = t % jb, j = t / jb;
+    a[i][j] = g[(j0 + i) + (j0 + j) * ldg];
+  }
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = a[j][j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        fail = j + 1;
+      } else {
+        a[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double rd = a[j][j];
+    for (int c = j + 1 + threadIdx.x; c < jb; c += blockDim.x) a[j][c] /= rd;
+    __syncthreads();
+    const int nt = jb - j - 1;
+    for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+      const int r = j + 1 + t % nt, c = j + 1 + t / nt;
+      if (r <= c) a[r][c] = fma(-a[j][r], a[j][c], a[r][c]);
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) info[0] = (int)(j0 + fail);
+    return;
+  }
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
+    const int i = t % jb, j = t / jb;
+    g[(j0 + i) + (j0 + j) * ldg] = i <= j ? a[i][j] : 0.0;
+  }
+}
+
+// X(:, c) = R_JJ^-T G(J, c) for the columns right of the diagonal block
+__global__ void chol_panel_kernel(int64_t k, int64_t j0, int jb, double* __restrict__ g, int64_t ldg,
+                                  const int* info) {
+  __shared__ double r[kCholB][kCholB + 1];
+  if (info[0] != 0) return;
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
+    const int i = t % jb, j = t / jb;
+    r[i][j] = g[(j0 + i) + (j0 + j) * ldg];
+  }
+  __syncthreads();
+  const int64_t c = j0 + jb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  double x[kCholB];
+  double* col = g + c * ldg + j0;
+#pragma unroll 8
+  for (int i = 0; i < jb; ++i) {
+    double v = col[i];
+    for (int l = 0; l < i; ++l) v = fma(-r[l][i], x[l], v);
+    x[i] = v / r[i][i];
+  }
+  for (int i = 0; i < jb; ++i) col[i] = x[i];
+}
+
+__global__ void zero_strict_lower_kernel(int64_t k, double* __restrict__ g, int64_t ldg) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k * k; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % k, j = t / k;
+    if (i > j) g[i + j * ldg] = 0.0;
+  }
+}
+
+// Right-looking Cholesky G = R^T R on the upper triangle, one CTA (small k).
 __global__ void cholesky_upper_kernel(int64_t k, double* __restrict__ g, int64_t ldg, int* info) {
   __shared__ double sdiag;
   __shared__ int sfail;
@@ -199,8 +274,27 @@ void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld1
   LRB_CUDA(cudaFreeAsync(partial, st));
 }
 
-void cholesky_upper(int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st) {
-  cholesky_upper_kernel<<<1, 1024, 0, st>>>(k, g, ldg, info);
+void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st) {
+  if (k <= 2 * kCholB || (ldg & 1) || (reinterpret_cast<uintptr_t>(g) & 15)) {
+    cholesky_upper_kernel<<<1, 1024, 0, st>>>(k, g, ldg, info);
+    LRB_CHECK_LAUNCH();
+    return;
+  }
+  LRB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  for (int64_t j0 = 0; j0 < k; j0 += kCholB) {
+    const int jb = (int)std::min<int64_t>(kCholB, k - j0);
+    chol_diag_kernel<<<1, 256, 0, st>>>(j0, jb, g, ldg, info);
+    LRB_CHECK_LAUNCH();
+    const int64_t nt = k - j0 - jb;
+    if (nt <= 0) break;
+    chol_panel_kernel<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(k, j0, jb, g, ldg, info);
+    LRB_CHECK_LAUNCH();
+    // G(J+, J+) -= X^T X with X = R(J, J+) (jb x nt): TN GEMM with K = jb
+    const double* X = g + j0 + (j0 + jb) * ldg;
+    double* T = g + (j0 + jb) + (j0 + jb) * ldg;
+    gemm_tn(ws, (int)nt, (int)nt, jb, X, ldg, X, ldg, T, ldg, -1.0, 1.0, 1, st);
+  }
+  zero_strict_lower_kernel<<<(unsigned)std::min<int64_t>((k * k + 255) / 256, 4096), 256, 0, st>>>(k, g, ldg);
   LRB_CHECK_LAUNCH();
 }
 
