@@ -1,0 +1,3 @@
+// Drop-in: the reference header lowrank/core.hpp resolved to the B200 implementation.
+#pragma once
+#include "lowrank_b200/lowrank.hpp"
