@@ -184,13 +184,22 @@ void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t l
 // ---------------------------------------------------------------- CPQR
 // In-place CPQR of a working matrix W (ld even, 16B aligned).  Throws the
 // reference's non-finite error for `who`.
+// Working-matrix leading dimension for CPQR: heights <= 512 are padded to a
+// multiple of 64 with zero rows (the predicate-free fast path of cpqr.cu).
+inline int64_t work_ld(int64_t m) { return m <= 512 ? ((m + 63) / 64) * 64 : even(m); }
+inline bool work_padded(int64_t m, int64_t ld) { return m <= 512 && ld == work_ld(m); }
+void zero_pad_rows(lr_ctx* c, double* W, int64_t m, int64_t ld, int64_t n) {
+  if (ld > m && n > 0)
+    LRB_CUDA(cudaMemset2DAsync(W + m, ld * sizeof(double), 0, (ld - m) * sizeof(double), n, c->st));
+}
+
 void cpqr_core(lr_ctx* c, int64_t m, int64_t n, double* W, int64_t ldw, int64_t k, int64_t* piv, double* tau,
-               const char* who) {
+               const char* who, bool padded = false) {
   DBuf<int> flags(1, c->st);
   DBuf<long long> rec(1, c->st);
   LRB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), c->st));
   LRB_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(long long), c->st));
-  cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, c->st);
+  cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, padded, c->st);
   LRB_CUDA(cudaMemcpyAsync(c->h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   LRB_CUDA(cudaMemcpyAsync(c->h_ll, rec.p, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -414,10 +423,11 @@ void id_column_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
                     const lr_solve_strategy& strat, int64_t* piv, double* coeff, int64_t ldc) {
   require_rank_in_range(k, m, n, "id_column");
   require_nonempty(m, n, "cpqr_partial");
-  const int64_t ldw = even(m);
+  const int64_t ldw = work_ld(m);
   DBuf<double> W((size_t)ldw * n, c->st), tau(k, c->st);
+  zero_pad_rows(c, W, m, ldw, n);
   copy_matrix(m, n, a, lda, W, ldw, c->st);
-  cpqr_core(c, m, n, W, ldw, k, piv, tau, "cpqr_partial");
+  cpqr_core(c, m, n, W, ldw, k, piv, tau, "cpqr_partial", work_padded(m, ldw));
   solve_core(c, k, n - k, W, ldw, W.p + k * ldw, ldw, strat, coeff, ldc, false);
 }
 
@@ -443,14 +453,15 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
   if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
   require_nonempty(m, n, "sketch_gaussian");
   require_sample_count(ell, m, "sketch_gaussian");
-  const int64_t ldy = even(ell);
+  const int64_t ldy = work_ld(ell);
   DBuf<double> Y((size_t)ldy * n, c->st);
+  zero_pad_rows(c, Y, ell, ldy, n);
   sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
   const int64_t steps = std::min(ell, n);  // cpqr_full
   if (steps < k) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
   DBuf<double> tau(steps, c->st);
   try {
-    cpqr_core(c, ell, n, Y, ldy, steps, piv, tau, "cpqr_partial");
+    cpqr_core(c, ell, n, Y, ldy, steps, piv, tau, "cpqr_partial", work_padded(ell, ldy));
   } catch (const LrError& e) {
     // Y is non-finite: distinguish a non-finite A (sketch_gaussian's check) from overflow in Y
     if (e.code == LR_EINVAL && !device_all_finite(c, m, n, a, lda))
@@ -474,15 +485,16 @@ void tsid_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, in
     C = Cb;
   }
   gather_columns(m, k, a, lda, col_piv, C, m, c->st);
-  const int64_t ldct = even(k);
+  const int64_t ldct = work_ld(k);
   DBuf<double> Ct((size_t)ldct * m, c->st);
+  zero_pad_rows(c, Ct, k, ldct, m);
   transpose_matrix(m, k, C, m, Ct, ldct, c->st);
-  if (Ct_keep) copy_matrix(k, m, Ct, ldct, Ct_keep, ldct, c->st);
+  if (Ct_keep) copy_matrix(k, m, Ct, ldct, Ct_keep, even(k), c->st);
   // id_row(c, k) = id_column(c^T, k) (id.hpp:109-119)
   require_rank_in_range(k, k, m, "id_column");
   DBuf<double> tau(k, c->st);
   mark(c, "gather_c");
-  cpqr_core(c, k, m, Ct, ldct, k, row_piv, tau, "cpqr_partial");
+  cpqr_core(c, k, m, Ct, ldct, k, row_piv, tau, "cpqr_partial", work_padded(k, ldct));
   mark(c, "cpqr_ct");
   solve_core(c, k, m - k, Ct, ldct, Ct.p + k * ldct, ldct, strat, row_coeff, ldrc, false);
   if (skeleton) gather_rows(k, k, C, m, row_piv, skeleton, k, c->st);
@@ -746,10 +758,11 @@ int lr_cpqr_partial_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
     require_nonempty(m, n, "cpqr_partial");
     if (!device_all_finite(c, m, n, a, lda)) fail(LR_EINVAL, "cpqr_partial: matrix has non-finite entries");
     require_rank_in_range(k, m, n, "cpqr_partial");
-    const int64_t ldw = even(m);
+    const int64_t ldw = work_ld(m);
     DBuf<double> W((size_t)ldw * n, c->st), tau(k, c->st);
+    zero_pad_rows(c, W, m, ldw, n);
     copy_matrix(m, n, a, lda, W, ldw, c->st);
-    cpqr_core(c, m, n, W, ldw, k, pivots, tau, "cpqr_partial");
+    cpqr_core(c, m, n, W, ldw, k, pivots, tau, "cpqr_partial", work_padded(m, ldw));
     cpqr_extract_s(m, n, W, ldw, k, s, k, c->st);
     if (q) cpqr_form_q(m, n, W, ldw, k, tau, q, m, c->st);
   });
@@ -765,9 +778,13 @@ int lr_cpqr_partial(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
     require_rank_in_range(k, m, n, "cpqr_partial");
     DBuf<double> tau(k, c->st), sd((size_t)k * n, c->st), qd(q ? (size_t)m * k : 1, c->st);
     DBuf<int64_t> pd(n, c->st);
-    cpqr_core(c, m, n, d, l, k, pd, tau, "cpqr_partial");
-    cpqr_extract_s(m, n, d, l, k, sd, k, c->st);
-    if (q) cpqr_form_q(m, n, d, l, k, tau, qd, m, c->st);
+    const int64_t lw = work_ld(m);
+    DBuf<double> W((size_t)lw * n, c->st);
+    zero_pad_rows(c, W, m, lw, n);
+    copy_matrix(m, n, d, l, W, lw, c->st);
+    cpqr_core(c, m, n, W, lw, k, pd, tau, "cpqr_partial", work_padded(m, lw));
+    cpqr_extract_s(m, n, W, lw, k, sd, k, c->st);
+    if (q) cpqr_form_q(m, n, W, lw, k, tau, qd, m, c->st);
     to_host(c, k, n, sd, k, s, k);
     if (q) to_host(c, m, k, qd, m, q, m);
     idx_to_host(c, n, pd, pivots);

@@ -132,7 +132,7 @@ __device__ __forceinline__ void load_col(Col<CH>& col, const double* src, bool c
   }
 }
 
-template <int CH, bool PF>
+template <int CH, bool PF, bool FAST>
 __global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dyn[];
@@ -149,12 +149,19 @@ __global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
   const int64_t m = a.m, n = a.n, ld = a.ld, k = a.k;
   const int64_t c0 = n * cta / G, c1 = n * (cta + 1) / G;
   const int64_t cand_sz = kHdr + m;
-  double* scr = a.scratch + (int64_t)cta * 4 * m;
-  double* olds = scr;      // old column at position s (when swapped into p)
-  double* pivr = scr + m;  // pivot column rows < s
-  const bool vs = m <= kMaxSmemRows;
-  double* vv = vs ? dyn : scr + 2 * m;      // v[i] for i >= s (v[s] = 1)
-  double* tv = vs ? dyn + m : scr + 3 * m;  // tau * v
+  double* scr = a.scratch + (int64_t)cta * 4 * ld;
+  double* olds = scr;       // old column at position s (when swapped into p)
+  double* pivr = scr + ld;  // pivot column rows < s
+  const bool vs = ld <= kMaxSmemRows;
+  double* vv = vs ? dyn : scr + 2 * ld;      // v[i] for i >= s (v[s] = 1)
+  double* tv = vs ? dyn + ld : scr + 3 * ld;  // tau * v
+  if (FAST) {
+    for (int64_t i = threadIdx.x; i < ld; i += kThreads) {
+      vv[i] = 0.0;
+      tv[i] = 0.0;
+      olds[i] = 0.0;
+    }
+  }
   const int nchunks = (int)((m + 63) / 64);
   const int64_t cnt = (c1 - c0 - warp + kWarps - 1) / kWarps;  // columns of this warp
   unsigned long long my_recomputes = 0;
@@ -242,6 +249,10 @@ __global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
     {
       const double tau_b = __ldcg(cd + 2);
       const bool apply_b = __ldcg(cd + 3) != 0.0;
+      if (FAST && s > 0 && threadIdx.x == 0) {  // keep v, tau*v zero above row s
+        vv[s - 1] = 0.0;
+        tv[s - 1] = 0.0;
+      }
       for (int64_t i = s + threadIdx.x; i < m; i += kThreads) {
         const double vi = __ldcg(cd + kHdr + i);
         vv[i] = vi;
@@ -354,7 +365,91 @@ __global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
       }
       if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
     };
-    if constexpr (!PF) {
+    // FAST path: ld % 64 == 0, ld <= 64*CH, rows [m, ld) are zero and
+    // vv/tv are zero outside [s, m): no per-element predicates at all.
+    const int t0 = (int)(s >> 6);
+    const int nld = (int)(ld >> 6);
+    auto fetch_fast = [&](Col<CH>& cb, int64_t j) {
+      const bool from_s = swapped && j == p;
+      const double* src = from_s ? olds : a.W + j * ld;
+      const int ts = from_s ? 0 : t0;
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        if (t >= ts && t < nld) {
+          const double2 xx = *reinterpret_cast<const double2*>(src + 64 * t + 2 * lane);
+          cb.c[t][0] = xx.x;
+          cb.c[t][1] = xx.y;
+        }
+      }
+      cb.nr = from_s ? sh_nst[2] : a.nrm[j];
+      cb.nx = from_s ? sh_nst[3] : a.nrmx[j];
+    };
+    auto process_fast = [&](Col<CH>& cb, int64_t j) {
+      const bool from_s = swapped && j == p;
+      const int ts = from_s ? 0 : t0;
+      double* dst = a.W + j * ld;
+      const double2* v2 = reinterpret_cast<const double2*>(vv);
+      const double2* tv2 = reinterpret_cast<const double2*>(tv);
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < CH; ++t)
+        if (t >= ts && t < nld) {
+          const double2 vx = v2[32 * t + lane];
+          d0 = fma(cb.c[t][0], vx.x, d0);
+          d1 = fma(cb.c[t][1], vx.y, d1);
+        }
+      const double dot = warp_sum(d0 + d1);
+      double xs = 0.0;
+#pragma unroll
+      for (int t = 0; t < CH; ++t)
+        if (t >= ts && t < nld) {
+          if (apply) {
+            const double2 tx = tv2[32 * t + lane];
+            cb.c[t][0] = fma(-tx.x, dot, cb.c[t][0]);
+            cb.c[t][1] = fma(-tx.y, dot, cb.c[t][1]);
+          }
+          if (t == t0) xs = (s & 1) ? cb.c[t][1] : cb.c[t][0];
+          *reinterpret_cast<double2*>(dst + 64 * t + 2 * lane) = make_double2(cb.c[t][0], cb.c[t][1]);
+        }
+      xs = __shfl_sync(0xffffffffu, xs, (int)((s & 63) >> 1));
+      double nr = cb.nr - xs * xs;
+      double nx = cb.nx;
+      if (nr < 1e-6 * nx) {  // rare: exact recompute from the registers (rows > s)
+        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < CH; ++t)
+          if (t >= t0 && t < nld) {
+            const int64_t r = 64 * t + 2 * lane;
+            if (r > s) q0 = fma(cb.c[t][0], cb.c[t][0], q0);
+            if (r + 1 > s) q1 = fma(cb.c[t][1], cb.c[t][1], q1);
+          }
+        nr = warp_sum(q0 + q1);
+        nx = nr;
+        ++my_recomputes;
+      }
+      if (lane == 0) {
+        a.nrm[j] = nr;
+        a.nrmx[j] = nx;
+        if (from_s) a.piv[j] = sh_state[1];
+      }
+      if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
+    };
+
+    if constexpr (FAST) {
+      Col<CH> A, B;
+      int64_t it = next_valid(0);
+      if (it < cnt) fetch_fast(A, col_of(it));
+      while (it < cnt) {
+        const int64_t it2 = next_valid(it + 1);
+        if (it2 < cnt) fetch_fast(B, col_of(it2));
+        process_fast(A, col_of(it));
+        if (it2 >= cnt) break;
+        const int64_t it3 = next_valid(it2 + 1);
+        if (it3 < cnt) fetch_fast(A, col_of(it3));
+        process_fast(B, col_of(it2));
+        it = it3;
+      }
+    } else if constexpr (!PF) {
       Col<CH> A;
       for (int64_t it = next_valid(0); it < cnt; it = next_valid(it + 1)) {
         fetch(A, col_of(it));
@@ -443,9 +538,9 @@ __global__ void form_q_kernel(int64_t m, const double* __restrict__ W, int64_t l
 }
 
 
-template <int CH, bool PF>
+template <int CH, bool PF, bool FAST>
 int launch_cpqr(CpqrArgs& args, size_t smem, int Gmax, cudaStream_t st) {
-  auto kern = cpqr_kernel<CH, PF>;
+  auto kern = cpqr_kernel<CH, PF, FAST>;
   if (smem > 48 * 1024) LRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
@@ -465,11 +560,11 @@ int cpqr_grid(int64_t n) {
 }  // namespace
 
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
-                  double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
+                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st) {
   const int Gmax = cpqr_grid(n);
   const size_t cand_sz = kHdr + (size_t)m;
   // state: nrm, nrmx (n each), pval (2G), cand (2 G cand_sz), scratch (G 4m), ppos (2G)
-  const size_t nd = 2 * (size_t)n + 2 * (size_t)Gmax + 2 * (size_t)Gmax * cand_sz + 4 * (size_t)Gmax * m;
+  const size_t nd = 2 * (size_t)n + 2 * (size_t)Gmax + 2 * (size_t)Gmax * cand_sz + 4 * (size_t)Gmax * ld;
   const size_t bytes = sizeof(double) * nd + sizeof(long long) * 2 * (size_t)Gmax + 256;
   uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
   CpqrArgs a{};
@@ -486,12 +581,14 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
   a.pval = d + 2 * n;
   a.cand = a.pval + 2 * Gmax;
   a.scratch = a.cand + 2 * (size_t)Gmax * cand_sz;
-  a.ppos = reinterpret_cast<long long*>(a.scratch + 4 * (size_t)Gmax * m);
+  a.ppos = reinterpret_cast<long long*>(a.scratch + 4 * (size_t)Gmax * ld);
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
-  const size_t smem = m <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)m : 0;
-  if (m <= 512) launch_cpqr<8, true>(a, smem, Gmax, st);
-  else launch_cpqr<16, false>(a, smem, Gmax, st);
+  const size_t smem = ld <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)ld : 0;
+  const bool fast = padded && ld % 64 == 0 && ld <= 512;
+  if (fast) launch_cpqr<8, true, true>(a, smem, Gmax, st);
+  else if (m <= 512) launch_cpqr<8, true, false>(a, smem, Gmax, st);
+  else launch_cpqr<16, false, false>(a, smem, Gmax, st);
 }
 
 void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,

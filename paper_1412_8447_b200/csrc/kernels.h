@@ -96,8 +96,9 @@ struct CpqrStats {
 // ld), in place: after return the upper part holds s (unsigned), the strict
 // lower part the reflectors, pivots the permutation and tau the k scalars.
 // Device pointers; pivots (n int64), tau (k), flags (1 int: nonfinite input).
+// `padded`: ld % 64 == 0 and rows [m, ld) of W are zero (enables the fast path).
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
-                  double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st);
+                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st);
 // s (k x n, lds) = top k rows of W with strict lower part zeroed and the sign fix
 void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,
                     cudaStream_t st);
