@@ -366,6 +366,74 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, local_rank):
+    """Column-sharded randomized CUR (paper_1412_8447_b200/distributed.py):
+    strong scaling, the whole 65536^2 problem split over the ranks."""
+    import torch
+
+    import paper_1412_8447_b200 as lr
+    from paper_1412_8447_b200 import distributed as D
+    from paper_1412_8447_b200 import inputs
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    base = inputs.CONFIGS["c4"]
+    cfg = inputs.Config(base.name, args.m, args.n, min(base.width, args.m, args.n), base.spectrum, args.k,
+                        OVERSAMPLE, base.pipeline, base.seed, base.sketch_seed)
+    ctx = lr.Context(local_rank)
+    lr.lowrank._default = ctx
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    off, n_g = D.shard_bounds(cfg.n, world, rank)
+    a = inputs.synthetic_torch(cfg, device=dev, col_block=8192, col_range=(off, n_g))
+    be = D.DeviceBackend(ctx, dev)
+    comm = D.TorchComm(lambda x: x, lambda t: t)
+    res = None
+    for _ in range(args.warmup):
+        res = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    launches0 = ctx.kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    if rank != 0:
+        return
+    fm = flops_model(cfg.m, cfg.n, cfg.k, cfg.k + OVERSAMPLE)
+    line = {
+        "metric": "time-to-CUR (s), randomized CUR 65536^2 k=500",
+        "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U diag(s) V^T, C4 spectrum, generated on device per column shard)",
+        "config": {"workload": "randomized CUR + tsID, BASELINE configs[3], column-sharded", "m": cfg.m,
+                   "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE, "u_mode": "cpinv_a_rpinv",
+                   "parallelism": f"column-sharded x{world}", "l2": "A shard exceeds L2; no flush needed"},
+        "fp64_tflops": round(sum(fm.values()) / (ms * 1e-3) / 1e12, 3),
+        "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": None, "cpu_baseline": None,
+        "roofline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -379,6 +447,8 @@ def main():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "sharded"],
+                   help="N>1: 'sharded' (column blocks of A, strong scaling) or 'replicas'")
     args = p.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -391,7 +461,11 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
-    run_ours(args, rank, world, local_rank)
+    mode = args.mode if args.mode != "auto" else ("sharded" if world > 1 else "single")
+    if mode == "sharded":
+        run_sharded(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -185,6 +185,26 @@ int lr_cur_error_fro(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t
 int lr_cur_error_fro_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                        const double* c, const double* u, const double* r, double* out);
 
+/* ---- shard-level primitives (device pointers) used by the column-sharded
+   multi-GPU orchestration (paper_1412_8447_b200/distributed.py) ---- */
+/* sketch.hpp:210-221: CPQR of a sample y (ell x n) then the coefficient solve */
+int lr_id_from_sample_d(lr_ctx* ctx, int64_t ell, int64_t n, const double* y, int64_t ldy, int64_t k,
+                        lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+/* id.hpp:124-134 given the column skeleton c = A(:, J) (m x k) */
+int lr_tsid_from_skeleton_columns_d(lr_ctx* ctx, int64_t m, int64_t k, const double* c, int64_t ldc,
+                                    lr_solve_strategy strategy, int64_t* row_pivots, double* row_coeff,
+                                    double* skeleton);
+/* core.hpp:70-85 gathers; a negative column index gathers a zero column */
+int lr_gather_columns_d(lr_ctx* ctx, int64_t m, int64_t k, const double* a, int64_t lda, const int64_t* idx,
+                        double* out, int64_t ldo);
+int lr_gather_rows_d(lr_ctx* ctx, int64_t k, int64_t n, const double* a, int64_t lda, const int64_t* idx,
+                     double* out, int64_t ldo);
+int lr_transpose_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double* out, int64_t ldo);
+int lr_cholesky_upper_d(lr_ctx* ctx, int64_t k, double* g, int64_t ldg);
+int lr_tri_upper_inverse_d(lr_ctx* ctx, int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi);
+int lr_cholqr2_d(lr_ctx* ctx, int64_t rows, int64_t k, const double* x, int64_t ldx, double* r, double* rinv,
+                 int* ok);
+
 /* Y (M x N) = P^T Q on the DMMA GEMM (benchmark / test access to the contraction kernel) */
 int lr_gemm_tn_d(lr_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo);

@@ -95,6 +95,17 @@ SIGNATURES = {
                            ctypes.c_int),
     "lr_gemm_tn_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64],
                      ctypes.c_int),
+    "lr_id_from_sample_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
+                            ctypes.c_int),
+    "lr_tsid_from_skeleton_columns_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, lr_solve_strategy, c_ip, c_dp,
+                                         c_dp], ctypes.c_int),
+    "lr_gather_columns_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_ip, c_dp, c_i64], ctypes.c_int),
+    "lr_gather_rows_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_ip, c_dp, c_i64], ctypes.c_int),
+    "lr_transpose_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
+    "lr_cholesky_upper_d": ([ctypes.c_void_p, c_i64, c_dp, c_i64], ctypes.c_int),
+    "lr_tri_upper_inverse_d": ([ctypes.c_void_p, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
+    "lr_cholqr2_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp, ctypes.POINTER(ctypes.c_int)],
+                     ctypes.c_int),
 }
 
 _lib = None

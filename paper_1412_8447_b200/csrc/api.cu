@@ -484,7 +484,7 @@ void tsid_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, in
     Cb = DBuf<double>((size_t)m * k, c->st);
     C = Cb;
   }
-  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
+  if (a) gather_columns(m, k, a, lda, col_piv, C, m, c->st);  // a == null: C_out already holds C
   const int64_t ldct = work_ld(k);
   DBuf<double> Ct((size_t)ldct * m, c->st);
   zero_pad_rows(c, Ct, k, ldct, m);
@@ -1124,6 +1124,80 @@ int lr_ctx_reset_stats(lr_ctx* c) {
 }
 
 long long lr_kernel_launches(void) { return (long long)lrb::g_kernel_launches; }
+
+// ---------------------------------------------------------------- shard primitives (distributed.py)
+// randomized_id's second half (sketch.hpp:210-221) on a sample y (ell x n).
+int lr_id_from_sample_d(lr_ctx* c, int64_t ell, int64_t n, const double* y, int64_t ldy, int64_t k,
+                        lr_solve_strategy strat, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(ell, n, "cpqr_partial");
+    const int64_t steps = std::min(ell, n);
+    if (k < 1 || steps < k) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
+    const int64_t lw = work_ld(ell);
+    DBuf<double> W((size_t)lw * n, c->st), tau(steps, c->st);
+    zero_pad_rows(c, W, ell, lw, n);
+    copy_matrix(ell, n, y, ldy, W, lw, c->st);
+    cpqr_core(c, ell, n, W, lw, steps, pivots, tau, "cpqr_partial", work_padded(ell, lw));
+    solve_core(c, k, n - k, W, lw, W.p + k * lw, lw, strat, coeff, k, false);
+  });
+}
+
+// id.hpp:124-134 given the column skeleton c = A(:, J) (m x k, ld ldc)
+int lr_tsid_from_skeleton_columns_d(lr_ctx* c, int64_t m, int64_t k, const double* cs, int64_t ldc,
+                                    lr_solve_strategy strat, int64_t* row_pivots, double* row_coeff,
+                                    double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, k, m, "id_column");
+    DBuf<double> C((size_t)m * k, c->st);
+    copy_matrix(m, k, cs, ldc, C, m, c->st);
+    tsid_core(c, m, k, nullptr, m, k, nullptr, strat, row_pivots, row_coeff, k, skeleton, C, nullptr);
+  });
+}
+
+// core.hpp:70-76 (idx[j] < 0 gathers a zero column: masked gather for shard assembly)
+int lr_gather_columns_d(lr_ctx* c, int64_t m, int64_t k, const double* a, int64_t lda, const int64_t* idx, double* out,
+                        int64_t ldo) {
+  return guard([&] { gather_columns(m, k, a, lda, idx, out, ldo, checked(c)->st); });
+}
+// core.hpp:79-85
+int lr_gather_rows_d(lr_ctx* c, int64_t k, int64_t n, const double* a, int64_t lda, const int64_t* idx, double* out,
+                     int64_t ldo) {
+  return guard([&] { gather_rows(k, n, a, lda, idx, out, ldo, checked(c)->st); });
+}
+
+// G = R^T R in place (upper R); LR_ERUNTIME if G is not numerically SPD
+int lr_cholesky_upper_d(lr_ctx* c, int64_t k, double* g, int64_t ldg) {
+  return guard([&] {
+    checked(c);
+    DBuf<int> info(1, c->st);
+    cholesky_upper(c->ws, k, g, ldg, info, c->st);
+    LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (c->h_flags[0]) fail(LR_ERUNTIME, "cholesky: leading minor " + std::to_string(c->h_flags[0]) + " not positive");
+  });
+}
+
+int lr_transpose_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* out, int64_t ldo) {
+  return guard([&] { transpose_matrix(m, n, a, lda, out, ldo, checked(c)->st); });
+}
+
+int lr_tri_upper_inverse_d(lr_ctx* c, int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi) {
+  return guard([&] { tri_upper_inverse(k, r, ldr, rinv, ldi, checked(c)->st); });
+}
+
+// CholeskyQR2 of a tall x (rows x k): r (k x k upper), rinv; *ok = 0 when the
+// factorisation broke down or cond bound >= 1e7 (caller falls back to SVD).
+int lr_cholqr2_d(lr_ctx* c, int64_t rows, int64_t k, const double* x, int64_t ldx, double* r, double* rinv, int* ok) {
+  return guard([&] {
+    checked(c);
+    DBuf<double> X((size_t)even(rows) * k, c->st), Xt((size_t)even(k) * rows, c->st);
+    copy_matrix(rows, k, x, ldx, X, even(rows), c->st);
+    transpose_matrix(rows, k, x, ldx, Xt, even(k), c->st);
+    *ok = cholqr2(c, rows, k, X, even(rows), Xt, even(k), r, rinv) ? 1 : 0;
+  });
+}
 
 int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo) {

@@ -119,10 +119,11 @@ __global__ void transpose_kernel(int64_t m, int64_t n, const double* __restrict_
 __global__ void gather_columns_kernel(int64_t m, int64_t k, const double* __restrict__ a, int64_t lda,
                                       const int64_t* __restrict__ idx, double* __restrict__ out, int64_t ldo) {
   for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
-    const double* src = a + idx[j] * lda;
+    const int64_t col = idx[j];  // negative: a zero column (masked gather for sharded assembly)
+    const double* src = a + (col >= 0 ? col : 0) * lda;
     double* dst = out + j * ldo;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-      dst[i] = src[i];
+      dst[i] = col >= 0 ? src[i] : 0.0;
   }
 }
 

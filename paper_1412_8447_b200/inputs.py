@@ -100,9 +100,10 @@ def synthetic_np(cfg: Config) -> np.ndarray:
     return np.asfortranarray((u * cfg.singular_values()) @ v.T)
 
 
-def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None):
+def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None, col_range=None):
     """A = U diag(s) V^T generated on the GPU, column-major (input plumbing:
-    torch QR / matmul build the input, the product path never uses them)."""
+    torch QR / matmul build the input, the product path never uses them).
+    col_range=(lo, width) builds only the column block A(:, lo:lo+width)."""
     import torch
 
     from .lowrank import default_context, empty_colmajor
@@ -126,11 +127,12 @@ def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None):
     v = haar(cfg.n, cfg.width, derive_seed(cfg.seed, 2))
     us = u * torch.as_tensor(cfg.singular_values(), device=device)
     del u
-    a = empty_colmajor(cfg.m, cfg.n, device)
-    step = col_block or cfg.n
-    for j0 in range(0, cfg.n, step):
-        j1 = min(cfg.n, j0 + step)
-        a[:, j0:j1] = us @ v[j0:j1].T
+    lo, width = col_range if col_range is not None else (0, cfg.n)
+    a = empty_colmajor(cfg.m, width, device)
+    step = col_block or width
+    for j0 in range(0, width, step):
+        j1 = min(width, j0 + step)
+        a[:, j0:j1] = us @ v[lo + j0:lo + j1].T
     torch.cuda.synchronize()
     return a
 
