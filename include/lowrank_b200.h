@@ -92,8 +92,10 @@ int64_t lr_last_singular_index(void);
 
 int lr_ctx_create(lr_ctx** out, int device);
 int lr_ctx_destroy(lr_ctx* ctx);
-/* run subsequent _d calls on this cudaStream_t (NULL = the context's own stream) */
+/* run subsequent _d calls on this cudaStream_t (NULL = the legacy default stream) */
 int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
+/* back to the context's own (non-blocking) stream, the default after creation */
+int lr_ctx_use_own_stream(lr_ctx* ctx);
 int lr_ctx_get_stats(lr_ctx* ctx, lr_stats* out);
 int lr_ctx_synchronize(lr_ctx* ctx);
 /* per-stage device time with CUDA events on the context stream (tracing):

@@ -694,7 +694,11 @@ int lr_ctx_destroy(lr_ctx* c) {
 }
 
 int lr_ctx_set_stream(lr_ctx* c, void* s) {
-  return guard([&] { checked(c)->st = s ? static_cast<cudaStream_t>(s) : c->own; });
+  // NULL is the CUDA legacy default stream (what torch reports for its default stream)
+  return guard([&] { checked(c)->st = s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy; });
+}
+int lr_ctx_use_own_stream(lr_ctx* c) {
+  return guard([&] { checked(c)->st = c->own; });
 }
 int lr_ctx_get_stats(lr_ctx* c, lr_stats* out) {
   return guard([&] { *out = checked(c)->stats; });
