@@ -52,6 +52,42 @@ __global__ void backsub_operator_kernel(int64_t k, const double* __restrict__ s1
   }
 }
 
+// Same operator, column-oriented ("axpy") form with the right-hand side held in
+// shared memory: for i = c..0: M(i,c) = x_i / d_i (or 0 for a zeroed row), then
+// x_j -= S11(j,i) M(i,c) for j < i.  S11's column i is contiguous, so each
+// step is one coalesced read (prefetched a step ahead) instead of a strided
+// row walk.  One warp per column; x for up to kAxpyMaxK rows.
+constexpr int kAxpyMaxK = 2048;
+constexpr int kAxpyWarps = 4;
+
+__global__ void backsub_operator_axpy_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11,
+                                             double threshold, double* __restrict__ M, int* __restrict__ zero_rows) {
+  extern __shared__ double xs_all[];
+  __shared__ double sh[32];
+  const double tol = threshold * block_max_abs_diag(k, s11, ld11, sh);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * kAxpyWarps + w;
+  if (blockIdx.x == 0)
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) zero_rows[i] = fabs(s11[i + i * ld11]) <= tol;
+  if (c >= k) return;
+  double* x = xs_all + (int64_t)w * k;
+  for (int64_t i = lane; i <= c; i += 32) x[i] = (i == c) ? 1.0 : 0.0;
+  double* mc = M + c * k;
+  for (int64_t i = c + 1 + lane; i < k; i += 32) mc[i] = 0.0;
+  __syncwarp();
+  // prefetch column c of S11 (rows < c) in 32-row chunks held per lane
+  for (int64_t i = c; i >= 0; --i) {
+    const double d = s11[i + i * ld11];
+    const double mi = fabs(d) <= tol ? 0.0 : x[i] / d;
+    if (lane == 0) mc[i] = mi;
+    if (mi != 0.0) {
+      const double* col = s11 + i * ld11;
+      for (int64_t j = lane; j < i; j += 32) x[j] = fma(-col[j], mi, x[j]);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void diag_minmax_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11, double* out) {
   __shared__ double smx[32], smn[32];
   double mx = 0.0, mn = INFINITY;
@@ -186,6 +222,37 @@ __global__ void chol_panel_kernel(int64_t k, int64_t j0, int jb, double* __restr
   for (int i = 0; i < jb; ++i) col[i] = x[i];
 }
 
+// Panel by forward substitution, one warp per column (axpy form, two rows per
+// lane in registers): X(i) = G(i) / R(i,i), then G(l) -= R(i,l) X(i) for l > i.
+__global__ void chol_panel_warp_kernel(int64_t k, int64_t j0, int jb, double* __restrict__ g, int64_t ldg,
+                                       const int* info) {
+  __shared__ double r[kCholB][kCholB + 1];
+  if (info[0] != 0) return;
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
+    const int i = t % jb, j = t / jb;
+    r[i][j] = g[(j0 + i) + (j0 + j) * ldg];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t c = j0 + jb + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= k) return;
+  double* col = g + c * ldg + j0;
+  double x0 = lane < jb ? col[lane] : 0.0;
+  double x1 = lane + 32 < jb ? col[lane + 32] : 0.0;
+  for (int i = 0; i < jb; ++i) {
+    const double raw = __shfl_sync(0xffffffffu, i < 32 ? x0 : x1, i & 31);
+    const double xi = raw / r[i][i];
+    if (lane == (i & 31)) {
+      if (i < 32) x0 = xi;
+      else x1 = xi;
+    }
+    if (lane > i && lane < jb) x0 = fma(-r[i][lane], xi, x0);
+    if (lane + 32 > i && lane + 32 < jb) x1 = fma(-r[i][lane + 32], xi, x1);
+  }
+  if (lane < jb) col[lane] = x0;
+  if (lane + 32 < jb) col[lane + 32] = x1;
+}
+
 __global__ void zero_strict_lower_kernel(int64_t k, double* __restrict__ g, int64_t ldg) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k * k; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t % k, j = t / k;
@@ -232,6 +299,25 @@ __global__ void cholesky_upper_kernel(int64_t k, double* __restrict__ g, int64_t
   if (threadIdx.x == 0) info[0] = 0;
 }
 
+void launch_backsub_operator(int64_t k, const double* s11, int64_t ld11, double threshold, double* M, int* zr,
+                             cudaStream_t st) {
+  if (k <= kAxpyMaxK) {
+    const size_t smem = sizeof(double) * kAxpyWarps * (size_t)k;
+    static bool attr = false;
+    if (!attr) {
+      LRB_CUDA(cudaFuncSetAttribute(backsub_operator_axpy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * kAxpyWarps * kAxpyMaxK)));
+      attr = true;
+    }
+    backsub_operator_axpy_kernel<<<(unsigned)((k + kAxpyWarps - 1) / kAxpyWarps), kAxpyWarps * 32, smem, st>>>(
+        k, s11, ld11, threshold, M, zr);
+  } else {
+    const int wpb = 8;
+    backsub_operator_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(k, s11, ld11, threshold, M, zr);
+  }
+  LRB_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 void backsub_operator_t(int64_t k, const double* s11, int64_t ld11, double threshold, double* Mt, int* zero_rows,
@@ -239,10 +325,7 @@ void backsub_operator_t(int64_t k, const double* s11, int64_t ld11, double thres
   // M is written col-major into Mt's storage first, then transposed in place via a temp
   double* tmp = nullptr;
   LRB_CUDA(cudaMallocAsync(&tmp, sizeof(double) * k * k, st));
-  const int wpb = 8;
-  backsub_operator_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(k, s11, ld11, threshold, tmp,
-                                                                                zero_rows);
-  LRB_CHECK_LAUNCH();
+  launch_backsub_operator(k, s11, ld11, threshold, tmp, zero_rows, st);
   transpose_matrix(k, k, tmp, k, Mt, k, st);
   LRB_CUDA(cudaFreeAsync(tmp, st));
 }
@@ -287,7 +370,7 @@ void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info,
     LRB_CHECK_LAUNCH();
     const int64_t nt = k - j0 - jb;
     if (nt <= 0) break;
-    chol_panel_kernel<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(k, j0, jb, g, ldg, info);
+    chol_panel_warp_kernel<<<(unsigned)((nt + 7) / 8), 256, 0, st>>>(k, j0, jb, g, ldg, info);
     LRB_CHECK_LAUNCH();
     // G(J+, J+) -= X^T X with X = R(J, J+) (jb x nt): TN GEMM with K = jb
     const double* X = g + j0 + (j0 + jb) * ldg;
@@ -303,10 +386,8 @@ void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, in
   LRB_CUDA(cudaMallocAsync(&zr, sizeof(int) * k, st));
   double* tmp = nullptr;
   LRB_CUDA(cudaMallocAsync(&tmp, sizeof(double) * k * k, st));
-  const int wpb = 8;
   // threshold 0: only exactly-zero diagonals are treated as singular (rows zeroed)
-  backsub_operator_kernel<<<(unsigned)((k + wpb - 1) / wpb), wpb * 32, 0, st>>>(k, r, ldr, 0.0, tmp, zr);
-  LRB_CHECK_LAUNCH();
+  launch_backsub_operator(k, r, ldr, 0.0, tmp, zr, st);
   copy_matrix(k, k, tmp, k, rinv, ldi, st);
   LRB_CUDA(cudaFreeAsync(tmp, st));
   LRB_CUDA(cudaFreeAsync(zr, st));
