@@ -36,8 +36,8 @@ namespace lrb {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kMaxWarps = 32;  // shared reductions sized for up to 1024 threads
+constexpr int kGridWarpsPerCta = 8;  // grid sizing estimate (columns per CTA)
 constexpr int kMaxSmemRows = 6144;  // v and tau*v kept in shared memory up to this height
 constexpr int kMaxG = 512;          // partial slots read by one warp (16 per lane)
 constexpr int kHdr = 4;             // candidate header: alpha, beta, tau, apply
@@ -69,8 +69,7 @@ __device__ double cta_sum(double x, double* sh) {
   if ((threadIdx.x & 31) == 0) sh[w] = x;
   __syncthreads();
   double t = 0.0;
-#pragma unroll
-  for (int i = 0; i < kWarps; ++i) t += sh[i];
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
   return t;
 }
 
@@ -84,7 +83,7 @@ __device__ void stage_candidate(const CpqrArgs& a, double* cd, int64_t s0, long 
   }
   const double* x = a.W + jb * a.ld;
   double part = 0.0;
-  for (int64_t i = s0 + threadIdx.x; i < m; i += kThreads) part = fma(x[i], x[i], part);
+  for (int64_t i = s0 + threadIdx.x; i < m; i += blockDim.x) part = fma(x[i], x[i], part);
   const double cn2 = cta_sum(part, sh);
   const double colnorm = sqrt(cn2);
   const double alpha = x[s0];
@@ -95,7 +94,7 @@ __device__ void stage_candidate(const CpqrArgs& a, double* cd, int64_t s0, long 
     tau = (beta - alpha) / beta;
     scale = alpha - beta;
   }
-  for (int64_t i = s0 + threadIdx.x; i < m; i += kThreads)
+  for (int64_t i = s0 + threadIdx.x; i < m; i += blockDim.x)
     cd[kHdr + i] = apply ? ((i == s0) ? 1.0 : x[i] / scale) : x[i];
   if (threadIdx.x == 0) {
     cd[0] = alpha;
@@ -132,13 +131,15 @@ __device__ __forceinline__ void load_col(Col<CH>& col, const double* src, bool c
   }
 }
 
-template <int CH, bool PF, bool FAST>
-__global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
+template <int CH, bool PF, bool FAST, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dyn[];
-  __shared__ double sh_red[kWarps];
-  __shared__ double sh_bv[kWarps];
-  __shared__ long long sh_bp[kWarps];
+  __shared__ double sh_red[kMaxWarps];
+  __shared__ double sh_bv[kMaxWarps];
+  __shared__ long long sh_bp[kMaxWarps];
+  constexpr int kWarps = NT / 32;
+  constexpr int kThreads = NT;
   __shared__ double sh_hdr[kHdr];
   __shared__ long long sh_piv[2];    // p, winner cta
   __shared__ long long sh_state[2];  // piv[p], piv[s]
@@ -435,7 +436,13 @@ __global__ void __launch_bounds__(kThreads, 2) cpqr_kernel(CpqrArgs a) {
       if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
     };
 
-    if constexpr (FAST) {
+    if constexpr (FAST && !PF) {
+      Col<CH> A;
+      for (int64_t it = next_valid(0); it < cnt; it = next_valid(it + 1)) {
+        fetch_fast(A, col_of(it));
+        process_fast(A, col_of(it));
+      }
+    } else if constexpr (FAST) {
       Col<CH> A, B;
       int64_t it = next_valid(0);
       if (it < cnt) fetch_fast(A, col_of(it));
@@ -538,23 +545,34 @@ __global__ void form_q_kernel(int64_t m, const double* __restrict__ W, int64_t l
 }
 
 
-template <int CH, bool PF, bool FAST>
+template <int CH, bool PF, bool FAST, int NT, int MINB>
 int launch_cpqr(CpqrArgs& args, size_t smem, int Gmax, cudaStream_t st) {
-  auto kern = cpqr_kernel<CH, PF, FAST>;
+  auto kern = cpqr_kernel<CH, PF, FAST, NT, MINB>;
   if (smem > 48 * 1024) LRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-  per_sm = std::max(1, std::min(per_sm, 2));
+  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  per_sm = std::max(1, std::min(per_sm, MINB));
   int G = std::min(per_sm * num_sms(), Gmax);
+  // never more CTAs than NT/32-warp groups of columns
+  G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (args.n + NT / 32 - 1) / (NT / 32)));
   void* params[] = {&args};
-  LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(kThreads), params, smem, st));
+  LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(NT), params, smem, st));
   LRB_CHECK_LAUNCH();
   return G;
 }
 
 int cpqr_grid(int64_t n) {
-  const int64_t max_g = std::max<int64_t>(1, (n + kWarps - 1) / kWarps);
-  return (int)std::min<int64_t>(std::min(2 * num_sms(), kMaxG), max_g);
+  const int64_t max_g = std::max<int64_t>(1, (n + kGridWarpsPerCta - 1) / kGridWarpsPerCta);
+  return (int)std::min<int64_t>(std::min(4 * num_sms(), kMaxG), max_g);
+}
+
+// CPQR kernel variant for the fast path (env LRB_CPQR_VARIANT selects for experiments)
+int cpqr_fast_variant() {
+  static int v = [] {
+    const char* e = getenv("LRB_CPQR_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -586,9 +604,20 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
   const size_t smem = ld <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)ld : 0;
   const bool fast = padded && ld % 64 == 0 && ld <= 512;
-  if (fast) launch_cpqr<8, true, true>(a, smem, Gmax, st);
-  else if (m <= 512) launch_cpqr<8, true, false>(a, smem, Gmax, st);
-  else launch_cpqr<16, false, false>(a, smem, Gmax, st);
+  if (fast) {
+    switch (cpqr_fast_variant()) {
+      // measured (tools/bench_cpqr.py, 510 x 65536): 1 CTA x 16 warps per SM with
+      // register double buffering is fastest (fewer CTAs -> cheaper grid barrier)
+      case 1: launch_cpqr<8, false, true, 512, 2>(a, smem, Gmax, st); break;   // 32 warps/SM, no prefetch
+      case 2: launch_cpqr<8, false, true, 256, 4>(a, smem, Gmax, st); break;   // 4 CTAs/SM, no prefetch
+      case 3: launch_cpqr<8, true, true, 256, 2>(a, smem, Gmax, st); break;    // 2 CTAs x 8 warps, prefetch
+      default: launch_cpqr<8, true, true, 512, 1>(a, smem, Gmax, st); break;   // 1 CTA x 16 warps, prefetch
+    }
+  } else if (m <= 512) {
+    launch_cpqr<8, true, false, 256, 2>(a, smem, Gmax, st);
+  } else {
+    launch_cpqr<16, false, false, 256, 2>(a, smem, Gmax, st);
+  }
 }
 
 void cpqr_extract_s(int64_t m, int64_t n, const double* W, int64_t ld, int64_t k, double* s, int64_t lds,
