@@ -187,6 +187,24 @@ int lr_cur_error_fro(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t
 int lr_cur_error_fro_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                        const double* c, const double* u, const double* r, double* out);
 
+/* ---- BASELINE config 5: randomized CUR of a CSR matrix (device pointers,
+   int64 indices).  The reference is dense-only (core.hpp:14-17); these apply
+   sketch.hpp:227-234 (+ lowrank_main.cpp:215 when u_mode says so) to the
+   densified matrix, with C = A(:, J) returned as a CSC extract and R = A(I, :)
+   as a CSR extract (index/value buffers need capacity nnz; the used length is
+   c_col_ptr[k] / r_row_ptr[k]).  col_coeff, row_coeff, skeleton may be NULL. */
+int lr_randomized_cur_csr_d(lr_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* val, int64_t k, lr_sketch_config cfg,
+                            lr_solve_strategy strategy, double pinv_threshold, int u_mode, int64_t* col_pivots,
+                            int64_t* row_pivots, double* u, int64_t* c_col_ptr, int64_t* c_row_idx, double* c_val,
+                            int64_t* r_row_ptr, int64_t* r_col_idx, double* r_val, double* col_coeff,
+                            double* row_coeff, double* skeleton);
+/* ||A - C U R||_F, ||A||_F for the sparse factors above: out[0], out[1] */
+int lr_cur_error_fro_csr_d(lr_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                           const int64_t* col_idx, const double* val, int64_t k, const int64_t* c_col_ptr,
+                           const int64_t* c_row_idx, const double* c_val, const double* u,
+                           const int64_t* r_row_ptr, const int64_t* r_col_idx, const double* r_val, double* out);
+
 /* ---- shard-level primitives (device pointers) used by the column-sharded
    multi-GPU orchestration (paper_1412_8447_b200/distributed.py) ---- */
 /* sketch.hpp:210-221: CPQR of a sample y (ell x n) then the coefficient solve */

@@ -96,6 +96,11 @@ SIGNATURES = {
                            ctypes.c_int),
     "lr_gemm_tn_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64],
                      ctypes.c_int),
+    "lr_randomized_cur_csr_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_ip, c_ip, c_dp, c_i64, lr_sketch_config,
+                                 lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip, c_dp, c_ip, c_ip, c_dp,
+                                 c_ip, c_ip, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),
+    "lr_cur_error_fro_csr_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_ip, c_ip, c_dp, c_i64, c_ip, c_ip, c_dp, c_dp,
+                                c_ip, c_ip, c_dp, c_dp], ctypes.c_int),
     "lr_id_from_sample_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
                             ctypes.c_int),
     "lr_tsid_from_skeleton_columns_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, lr_solve_strategy, c_ip, c_dp,

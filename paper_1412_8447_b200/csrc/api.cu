@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -502,12 +503,15 @@ void tsid_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, in
 }
 
 // cur.hpp:23-34 / lowrank_main.cpp:215 given skeleton index sets
-void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
-              const double* col_coeff, int64_t ldcc, const int64_t* row_piv, double thr, int u_mode, double* C,
-              double* U, double* R, const double* Ct_in /* k x m ld even(k), may be null */) {
+// Xt (n x k, ld ldxt) = A^T Q for Q (m x k, ld ldq): the one place U touches A
+using ApplyAt = std::function<void(const double* Q, int64_t ldq, double* Xt, int64_t ldxt)>;
+
+// U of the CUR from its skeletons C (m x k, ld m) and R (k x n, ld k):
+// cur.hpp:30 (u_mode LR_U_VT_RPINV) or lowrank_main.cpp:215 (LR_U_CPINV_A_RPINV)
+void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const double* R, const int64_t* col_piv,
+            const double* col_coeff, int64_t ldcc, double thr, int u_mode, double* U,
+            const double* Ct_in /* k x m ld even(k), may be null */, const ApplyAt& apply_at) {
   if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
-  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
-  gather_rows(k, n, a, lda, row_piv, R, k, c->st);
   const int64_t ldk = even(k);
   DBuf<double> Ctb;
   const double* Ct = Ct_in;
@@ -540,7 +544,7 @@ void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int
       gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n));            // Qr = R^T Sr^-1 (n x k)
       DBuf<double> Xt((size_t)even(n) * k, c->st), W((size_t)k * k, c->st);
       mark(c, "form_q");
-      gemm(c, n, k, m, a, lda, Qc, even(m), Xt, even(n));        // X^T = A^T Qc  (n x k)
+      apply_at(Qc, even(m), Xt, even(n));                        // X^T = A^T Qc  (n x k)
       mark(c, "ctA_gemm");
       gemm(c, k, k, n, Xt, even(n), Qr, even(n), W, k);          // W = Qc^T A Qr
       DBuf<double> t1((size_t)k * k, c->st), tt((size_t)k * k, c->st), st((size_t)k * k, c->st);
@@ -559,7 +563,7 @@ void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int
     // (Cp A) Rp: X^T = A^T Cp^T (n x k) then U = X Rp
     DBuf<double> Cpt((size_t)even(m) * k, c->st), Xt((size_t)even(n) * k, c->st);
     transpose_matrix(k, m, Cp, k, Cpt, even(m), c->st);
-    gemm(c, n, k, m, a, lda, Cpt, even(m), Xt, even(n));
+    apply_at(Cpt, even(m), Xt, even(n));
     DBuf<double> Rpe((size_t)even(n) * k, c->st);
     copy_matrix(n, k, Rp, n, Rpe, even(n), c->st);
     gemm(c, k, k, n, Xt, even(n), Rpe, even(n), U, k);
@@ -594,6 +598,17 @@ void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int
     gemm(c, k, k, nr, Grt, even(nr), cft, even(nr), Ut, k, 1.0, 1.0);
   }
   transpose_matrix(k, k, Ut, k, U, k, c->st);
+}
+
+// cur.hpp:23-34 / lowrank_main.cpp:215 on a dense A given the skeleton index sets
+void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
+              const double* col_coeff, int64_t ldcc, const int64_t* row_piv, double thr, int u_mode, double* C,
+              double* U, double* R, const double* Ct_in /* k x m ld even(k), may be null */) {
+  if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
+  gather_rows(k, n, a, lda, row_piv, R, k, c->st);
+  u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, u_mode, U, Ct_in,
+         [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) { gemm(c, n, k, m, a, lda, Q, ldq, Xt, ldxt); });
 }
 
 void error_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* C,
@@ -1128,6 +1143,120 @@ int lr_ctx_reset_stats(lr_ctx* c) {
 }
 
 long long lr_kernel_launches(void) { return (long long)lrb::g_kernel_launches; }
+
+// ---------------------------------------------------------------- sparse CUR (BASELINE config 5)
+// sketch.hpp:227-234 + lowrank_main.cpp:215 on a CSR matrix: the dense
+// contractions with A become SpMMs; C = A(:, J) and R = A(I, :) come back as
+// sparse extracts (CSC / CSR, capacity nnz each).  The reference has no sparse
+// path (core.hpp:14-17): semantics are those of the dense algorithm applied to
+// the densified matrix.
+int lr_randomized_cur_csr_d(lr_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* val, int64_t k, lr_sketch_config cfg,
+                            lr_solve_strategy strat, double thr, int u_mode, int64_t* col_pivots, int64_t* row_pivots,
+                            double* U, int64_t* c_col_ptr, int64_t* c_row_idx, double* c_val, int64_t* r_row_ptr,
+                            int64_t* r_col_idx, double* r_val, double* col_coeff, double* row_coeff,
+                            double* skeleton) {
+  return guard([&] {
+    checked(c);
+    require_rank_in_range(k, m, n, "randomized_id");
+    if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
+      fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch with power 0 runs on the B200 path");
+    const int64_t ell = k + cfg.oversample;
+    if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
+    if (nnz > 0 && !device_all_finite(c, nnz, 1, val, std::max<int64_t>(nnz, 1)))
+      fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+    require_sample_count(ell, m, "sketch_gaussian");
+    mark(c, "begin");
+    DBuf<int64_t> colp(n + 1, c->st), rowi(std::max<int64_t>(nnz, 1), c->st);
+    DBuf<double> cv(std::max<int64_t>(nnz, 1), c->st);
+    csr_to_csc(m, n, nnz, row_ptr, col_idx, val, colp, rowi, cv, c->st);
+    mark(c, "csr_to_csc");
+    // Y = Omega A (SpMM), Omega l x m column-major
+    DBuf<double> om((size_t)ell * m, c->st);
+    gaussian_matrix(ell, m, cfg.seed, om, ell, false, c->st);
+    const int64_t ldy = work_ld(ell);
+    DBuf<double> Y((size_t)ldy * n, c->st);
+    zero_pad_rows(c, Y, ell, ldy, n);
+    spmm_csc(ell, n, om, ell, colp, rowi, cv, Y, ldy, c->st);
+    mark(c, "sketch_spmm");
+    const int64_t steps = std::min(ell, n);
+    DBuf<double> tau(steps, c->st), cc, rc;
+    if (!col_coeff) {
+      cc = DBuf<double>((size_t)k * std::max<int64_t>(n - k, 1), c->st);
+      col_coeff = cc;
+    }
+    if (!row_coeff) {
+      rc = DBuf<double>((size_t)k * std::max<int64_t>(m - k, 1), c->st);
+      row_coeff = rc;
+    }
+    cpqr_core(c, ell, n, Y, ldy, steps, col_pivots, tau, "cpqr_partial", work_padded(ell, ldy));
+    mark(c, "cpqr_sample");
+    solve_core(c, k, n - k, Y, ldy, Y.p + k * ldy, ldy, strat, col_coeff, k, false);
+    mark(c, "coeff_solve_col");
+    // C = A(:, J) (CSC extract + dense copy), row ID of C
+    sparse_select(k, colp, rowi, cv, col_pivots, c_col_ptr, c_row_idx, c_val, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ct((size_t)even(k) * m, c->st);
+    sparse_scatter_cols(m, k, c_col_ptr, c_row_idx, c_val, Cd, m, c->st);
+    tsid_core(c, m, k, nullptr, m, k, nullptr, strat, row_pivots, row_coeff, k, skeleton, Cd, Ct);
+    // R = A(I, :) (CSR extract + dense copy)
+    sparse_select(k, row_ptr, col_idx, val, row_pivots, r_row_ptr, r_col_idx, r_val, c->st);
+    DBuf<double> Rd((size_t)k * n, c->st);
+    sparse_scatter_rows(k, n, r_row_ptr, r_col_idx, r_val, Rd, k, c->st);
+    u_core(c, m, n, k, Cd, Rd, col_pivots, col_coeff, k, thr, u_mode, U, Ct,
+           [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) {
+             // X^T = A^T Q  <=>  X = Q^T A (k x n): SpMM with Q^T as the dense operand
+             DBuf<double> Qt((size_t)k * m, c->st), X((size_t)k * n, c->st);
+             transpose_matrix(m, k, Q, ldq, Qt, k, c->st);
+             spmm_csc(k, n, Qt, k, colp, rowi, cv, X, k, c->st);
+             transpose_matrix(k, n, X, k, Xt, ldxt, c->st);
+           });
+    mark(c, "u_sparse");
+  });
+}
+
+// ||A - C U R||_F and ||A||_F for CSR A with C (CSC extract, m x k) and R (CSR
+// extract, k x n): ||A||^2 - 2 <A, CUR> + ||CUR||^2, where <A, CUR> only needs
+// CUR at A's nonzeros (an SpMM) and ||CUR||^2 = <(CU)^T CU, R R^T> (k x k).
+int lr_cur_error_fro_csr_d(lr_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                           const int64_t* col_idx, const double* val, int64_t k, const int64_t* c_col_ptr,
+                           const int64_t* c_row_idx, const double* c_val, const double* U, const int64_t* r_row_ptr,
+                           const int64_t* r_col_idx, const double* r_val, double* out) {
+  return guard([&] {
+    checked(c);
+    const int64_t ldk = even(k);
+    DBuf<int64_t> colp(n + 1, c->st), rowi(std::max<int64_t>(nnz, 1), c->st);
+    DBuf<double> cv(std::max<int64_t>(nnz, 1), c->st);
+    csr_to_csc(m, n, nnz, row_ptr, col_idx, val, colp, rowi, cv, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ct((size_t)ldk * m, c->st), Rd((size_t)ldk * n, c->st),
+        Rt((size_t)even(n) * k, c->st), CU((size_t)even(m) * k, c->st), CUt((size_t)k * m, c->st),
+        Z((size_t)k * n, c->st), G1((size_t)k * k, c->st), G2((size_t)k * k, c->st);
+    sparse_scatter_cols(m, k, c_col_ptr, c_row_idx, c_val, Cd, m, c->st);
+    sparse_scatter_rows(k, n, r_row_ptr, r_col_idx, r_val, Rd, ldk, c->st);
+    transpose_matrix(m, k, Cd, m, Ct, ldk, c->st);
+    gemm(c, m, k, k, Ct, ldk, U, k, CU, even(m));  // CU = C U
+    transpose_matrix(m, k, CU, even(m), CUt, k, c->st);
+    spmm_csc(k, n, CUt, k, colp, rowi, cv, Z, k, c->st);  // Z = (CU)^T A
+    transpose_matrix(k, n, Rd, ldk, Rt, even(n), c->st);
+    gemm(c, k, k, m, CU, even(m), CU, even(m), G1, k);    // (CU)^T CU
+    gemm(c, k, k, n, Rt, even(n), Rt, even(n), G2, k);    // R R^T
+    DBuf<double> part(4096 + 8, c->st), res(3, c->st);
+    int np = 0;
+    dot_sum(std::max<int64_t>(nnz, 1), 1, val, std::max<int64_t>(nnz, 1), val, std::max<int64_t>(nnz, 1), part, &np,
+            c->st);
+    sum_partials(part, np, res, c->st);
+    dot_sum(k, n, Z, k, Rd, ldk, part, &np, c->st);
+    sum_partials(part, np, res.p + 1, c->st);
+    dot_sum(k, k, G1, k, G2, k, part, &np, c->st);
+    sum_partials(part, np, res.p + 2, c->st);
+    double h[3];
+    LRB_CUDA(cudaMemcpyAsync(h, res.p, sizeof h, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const double a2 = nnz > 0 ? h[0] : 0.0;
+    const double e2 = a2 - 2.0 * h[1] + h[2];
+    out[0] = std::sqrt(std::max(e2, 0.0));
+    out[1] = std::sqrt(a2);
+  });
+}
 
 // ---------------------------------------------------------------- shard primitives (distributed.py)
 // randomized_id's second half (sketch.hpp:210-221) on a sample y (ell x n).

@@ -127,6 +127,24 @@ void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info,
 // inverse of an upper-triangular R (k x k) -> Rinv (upper)
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
 
+// ---------------------------------------------------------------- sparse (config 5)
+// CSR (m x n, int64 indices) -> CSC with rows ascending within each column
+void csr_to_csc(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int64_t* col_idx, const double* val,
+                int64_t* col_ptr, int64_t* row_idx, double* cval, cudaStream_t st);
+// out (p x n) = B (p x m) A for A in CSC (fixed per-column summation order)
+void spmm_csc(int64_t p, int64_t n, const double* B, int64_t ldb, const int64_t* col_ptr, const int64_t* row_idx,
+              const double* val, double* out, int64_t ldo, cudaStream_t st);
+// compressed segments sel[0..k) (columns of a CSC / rows of a CSR) -> new (k+1) ptr, idx, val
+void sparse_select(int64_t k, const int64_t* ptr, const int64_t* idx, const double* val, const int64_t* sel,
+                   int64_t* out_ptr, int64_t* out_idx, double* out_val, cudaStream_t st);
+void sparse_scatter_cols(int64_t rows, int64_t k, const int64_t* ptr, const int64_t* idx, const double* val,
+                         double* dense, int64_t ld, cudaStream_t st);
+void sparse_scatter_rows(int64_t k, int64_t cols, const int64_t* ptr, const int64_t* idx, const double* val,
+                         double* dense, int64_t ld, cudaStream_t st);
+// per-block partial sums of x .* y (m x n blocks)
+void dot_sum(int64_t m, int64_t n, const double* x, int64_t ldx, const double* y, int64_t ldy, double* partials,
+             int* num_partials, cudaStream_t st);
+
 // ---------------------------------------------------------------- Jacobi SVD (svd.hpp:39-183 semantics)
 // thin SVD of a (m x n, m >= n assumed by caller after transposition):
 // u (m x n), sigma (n), v (n x n); returns false if not converged in 60 sweeps

@@ -139,3 +139,33 @@ def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None, co
 
 def sha256(a: np.ndarray) -> str:
     return hashlib.sha256(np.asfortranarray(a).tobytes(order="F")).hexdigest()
+
+
+def synthetic_csr_torch(m: int, n: int, nnz_per_col: int, seed: int = 1412, device="cuda"):
+    """BASELINE config 5 input: m x n CSR (int64 indices) with nnz_per_col
+    nonzeros per column at seeded uniformly random distinct rows and values
+    N(0,1) * (i+1)^-0.5 * (j+1)^-1.  Input plumbing (torch RNG / sort)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    draw = nnz_per_col + max(8, nnz_per_col // 4)
+    r = torch.randint(0, m, (n, draw), generator=g, device=device, dtype=torch.int64)
+    r, _ = torch.sort(r, dim=1)
+    dup = torch.zeros_like(r, dtype=torch.bool)
+    dup[:, 1:] = r[:, 1:] == r[:, :-1]
+    r = torch.where(dup, torch.full_like(r, m), r)
+    r, _ = torch.sort(r, dim=1)
+    rows = r[:, :nnz_per_col]
+    if bool((rows >= m).any()):
+        raise RuntimeError("synthetic_csr_torch: not enough distinct rows drawn")
+    cols = torch.arange(n, device=device, dtype=torch.int64).repeat_interleave(nnz_per_col)
+    rows = rows.reshape(-1)
+    vals = torch.randn(rows.numel(), generator=g, device=device, dtype=torch.float64)
+    vals = vals * (rows.to(torch.float64) + 1.0).rsqrt() / (cols.to(torch.float64) + 1.0)
+    key = rows * n + cols
+    order = torch.argsort(key)
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    counts = torch.bincount(rows, minlength=m)
+    row_ptr = torch.zeros(m + 1, dtype=torch.int64, device=device)
+    row_ptr[1:] = torch.cumsum(counts, 0)
+    return row_ptr, cols.contiguous(), vals.contiguous()

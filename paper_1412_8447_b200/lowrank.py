@@ -610,3 +610,48 @@ def cur_error_fro_device(a, cur: dict, ctx: Optional[Context] = None):
     _raise(c.lib.lr_cur_error_fro_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(cur["c"]), _dptr(cur["u"]),
                                     _dptr(cur["r"]), _ptr(res)))
     return float(res[0]), float(res[1])
+
+
+# ------------------------------------------------------------------ sparse (BASELINE config 5)
+def randomized_cur_csr_device(row_ptr, col_idx, val, shape, k: int, cfg: Optional[SketchConfig] = None,
+                              strategy: Optional[SolveStrategy] = None, pinv_threshold: float = 1e-12,
+                              u_mode: int = U_CPINV_A_RPINV, ctx: Optional[Context] = None) -> dict:
+    """lr_randomized_cur_csr_d: randomized CUR of a CSR matrix on the GPU
+    (int64 row_ptr/col_idx, float64 values, all CUDA tensors).  C and R come
+    back as sparse extracts: (c_col_ptr, c_row_idx, c_val) CSC and
+    (r_row_ptr, r_col_idx, r_val) CSR."""
+    import torch
+    c = _ctx(ctx)
+    m, n = shape
+    nnz = int(val.numel())
+    dev = val.device
+    i64 = dict(dtype=torch.int64, device=dev)
+    out = {
+        "col_pivots": torch.empty(n, **i64), "row_pivots": torch.empty(m, **i64), "u": empty_colmajor(k, k, dev),
+        "c_col_ptr": torch.empty(k + 1, **i64), "c_row_idx": torch.empty(max(nnz, 1), **i64),
+        "c_val": torch.empty(max(nnz, 1), dtype=torch.float64, device=dev),
+        "r_row_ptr": torch.empty(k + 1, **i64), "r_col_idx": torch.empty(max(nnz, 1), **i64),
+        "r_val": torch.empty(max(nnz, 1), dtype=torch.float64, device=dev),
+        "col_coeff": empty_colmajor(k, max(n - k, 1), dev), "row_coeff": empty_colmajor(k, max(m - k, 1), dev),
+        "skeleton": empty_colmajor(k, k, dev),
+    }
+    _raise(c.lib.lr_randomized_cur_csr_d(
+        c.h, m, n, nnz, _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, (cfg or SketchConfig())._c(),
+        (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]),
+        _dptr(out["row_pivots"]), _dptr(out["u"]), _dptr(out["c_col_ptr"]), _dptr(out["c_row_idx"]),
+        _dptr(out["c_val"]), _dptr(out["r_row_ptr"]), _dptr(out["r_col_idx"]), _dptr(out["r_val"]),
+        _dptr(out["col_coeff"]), _dptr(out["row_coeff"]), _dptr(out["skeleton"])))
+    out["shape"] = (m, n)
+    return out
+
+
+def cur_error_fro_csr_device(row_ptr, col_idx, val, shape, cur: dict, ctx: Optional[Context] = None):
+    c = _ctx(ctx)
+    m, n = shape
+    k = cur["u"].shape[0]
+    res = np.empty(2)
+    _raise(c.lib.lr_cur_error_fro_csr_d(
+        c.h, m, n, int(val.numel()), _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, _dptr(cur["c_col_ptr"]),
+        _dptr(cur["c_row_idx"]), _dptr(cur["c_val"]), _dptr(cur["u"]), _dptr(cur["r_row_ptr"]),
+        _dptr(cur["r_col_idx"]), _dptr(cur["r_val"]), _ptr(res)))
+    return float(res[0]), float(res[1])
