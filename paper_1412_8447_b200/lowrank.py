@@ -26,6 +26,7 @@ __all__ = [
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
+    "randomized_cur_csr_device", "cur_error_fro_csr_device",
 ]
 
 LowrankCudaError = L.LowrankCudaError

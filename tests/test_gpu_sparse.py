@@ -71,7 +71,9 @@ def test_sparse_cur_full_size_properties(lr):
     cptr = res["c_col_ptr"].cpu().numpy()
     assert np.all(np.diff(cptr) == npc)
     res2 = lr.randomized_cur_csr_device(row_ptr, col_idx, val, (m, n), k, cfg)
-    for key in ("col_pivots", "row_pivots", "u", "c_val", "r_val"):
+    for key in ("col_pivots", "row_pivots", "u"):
         assert torch.equal(res[key], res2[key]), key
+    nc, nr = int(res["c_col_ptr"][-1]), int(res["r_row_ptr"][-1])
+    assert torch.equal(res["c_val"][:nc], res2["c_val"][:nc]) and torch.equal(res["r_val"][:nr], res2["r_val"][:nr])
     e, na = lr.cur_error_fro_csr_device(row_ptr, col_idx, val, (m, n), res)
     assert np.isfinite(e) and 0.0 < e / na <= 1.0
