@@ -1206,9 +1206,13 @@ int lr_randomized_cur_csr_d(lr_ctx* c, int64_t m, int64_t n, int64_t nnz, const 
            [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) {
              // X^T = A^T Q  <=>  X = Q^T A (k x n): SpMM with Q^T as the dense operand
              DBuf<double> Qt((size_t)k * m, c->st), X((size_t)k * n, c->st);
+             mark(c, "at_alloc");
              transpose_matrix(m, k, Q, ldq, Qt, k, c->st);
+             mark(c, "at_transpose_q");
              spmm_csc(k, n, Qt, k, colp, rowi, cv, X, k, c->st);
+             mark(c, "at_spmm");
              transpose_matrix(k, n, X, k, Xt, ldxt, c->st);
+             mark(c, "at_transpose_x");
            });
     mark(c, "u_sparse");
   });
