@@ -127,6 +127,23 @@ void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info,
 // inverse of an upper-triangular R (k x k) -> Rinv (upper)
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
 
+// ---------------------------------------------------------------- Ozaki-II FP64 emulation on INT8 tcgen05
+constexpr int kOzakiModuli = 16;
+// Scaled residue planes of a K x cols operand (K contiguous): planes[t] is an
+// int8 matrix (ld bytes per column) of x' mod m_t, x' = rint(x 2^shift[col]).
+struct OzakiOperand {
+  int8_t* planes = nullptr;
+  int* shift = nullptr;
+  int64_t K = 0, cols = 0, ld = 0, plane_stride = 0;
+  int beta = 0;
+};
+int ozaki_beta(int64_t K);
+size_t ozaki_plane_bytes(int64_t K, int64_t cols);
+void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta, OzakiOperand& op, cudaStream_t st);
+// out (M x N) = alpha P^T Q + beta out, reconstructed from 16 INT8 GEMMs
+void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, int64_t M, int64_t N, double* out,
+                   int64_t ldo, double alpha, double beta, cudaStream_t st);
+
 // ---------------------------------------------------------------- sparse (config 5)
 // CSR (m x n, int64 indices) -> CSC with rows ascending within each column
 void csr_to_csc(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int64_t* col_idx, const double* val,
