@@ -94,6 +94,15 @@ int lr_ctx_create(lr_ctx** out, int device);
 int lr_ctx_destroy(lr_ctx* ctx);
 /* run subsequent _d calls on this cudaStream_t (NULL = the legacy default stream) */
 int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
+/* engine for the two A-sized contractions (Y = Omega A, A^T Q):
+   LR_GEMM_DMMA (default): FP64 tensor-core GEMM (DMMA), FP64 rounding per FMA;
+   LR_GEMM_OZAKI_INT8: FP64 emulated on the INT8 tensor cores (Ozaki scheme II,
+   16 moduli): exact integer products of the inputs truncated to 54+ bits
+   relative to each column's largest entry (K <= 2^17; larger K uses DMMA) */
+#define LR_GEMM_DMMA 0
+#define LR_GEMM_OZAKI_INT8 1
+int lr_ctx_set_gemm_mode(lr_ctx* ctx, int mode);
+int lr_ctx_get_gemm_mode(lr_ctx* ctx);
 /* back to the context's own (non-blocking) stream, the default after creation */
 int lr_ctx_use_own_stream(lr_ctx* ctx);
 int lr_ctx_get_stats(lr_ctx* ctx, lr_stats* out);
@@ -225,7 +234,7 @@ int lr_tri_upper_inverse_d(lr_ctx* ctx, int64_t k, const double* r, int64_t ldr,
 int lr_cholqr2_d(lr_ctx* ctx, int64_t rows, int64_t k, const double* x, int64_t ldx, double* r, double* rinv,
                  int* ok);
 
-/* Y (M x N) = P^T Q on the DMMA GEMM (benchmark / test access to the contraction kernel) */
+/* Y (M x N) = P^T Q on the context's contraction engine (benchmark / test access) */
 int lr_gemm_tn_d(lr_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo);
 

@@ -50,6 +50,8 @@ SIGNATURES = {
     "lr_ctx_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_set_stream": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_use_own_stream": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_set_gemm_mode": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "lr_ctx_get_gemm_mode": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_get_stats": ([ctypes.c_void_p, ctypes.POINTER(lr_stats)], ctypes.c_int),
     "lr_ctx_synchronize": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_enable_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),

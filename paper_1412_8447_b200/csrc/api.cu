@@ -94,6 +94,16 @@ struct lr_ctx {
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
   std::vector<std::pair<std::string, double>> stage_ms;
   std::vector<std::pair<std::string, long long>> stage_count;
+  // contraction engine for the two A-sized GEMMs (lr_ctx_set_gemm_mode)
+  int gemm_mode = LR_GEMM_DMMA;
+  // Ozaki residue planes of A, kept for the duration of one CUR call so the
+  // sketch and the A^T Q contraction split A once (OzakiScope)
+  bool oz_cache_on = false;
+  const double* oz_src = nullptr;
+  int64_t oz_K = 0, oz_cols = 0, oz_ld = 0;
+  lrb::OzakiOperand oz_op;
+  DBuf<int8_t> oz_planes;
+  DBuf<int> oz_shift;
 };
 
 namespace {
@@ -181,6 +191,68 @@ void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t l
   }
   gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st);
 }
+
+// ---------------------------------------------------------------- A-sized contractions
+// Ozaki-II emulation applies while K fits exact int32 accumulation; beyond
+// that (and in the default mode) the DMMA GEMM runs.
+constexpr int64_t kOzakiMaxK = int64_t(1) << 17;
+
+struct OzakiTmp {
+  DBuf<int8_t> planes;
+  DBuf<int> shift;
+};
+
+// Residue planes of X (K x cols, K-contiguous).  `cacheable` operands (A of
+// the current CUR call) are split once and reused while an OzakiScope is open.
+const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
+                                  OzakiTmp& tmp, OzakiOperand& out) {
+  const int beta = ozaki_beta(K);
+  if (cacheable && c->oz_cache_on) {
+    if (c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx) return c->oz_op;
+    c->oz_planes = DBuf<int8_t>(ozaki_plane_bytes(K, cols), c->st);
+    c->oz_shift = DBuf<int>((size_t)cols, c->st);
+    c->oz_op.planes = c->oz_planes;
+    c->oz_op.shift = c->oz_shift;
+    ozaki_split(K, cols, X, ldx, beta, c->oz_op, c->st);
+    c->oz_src = X;
+    c->oz_K = K;
+    c->oz_cols = cols;
+    c->oz_ld = ldx;
+    return c->oz_op;
+  }
+  tmp.planes = DBuf<int8_t>(ozaki_plane_bytes(K, cols), c->st);
+  tmp.shift = DBuf<int>((size_t)cols, c->st);
+  out.planes = tmp.planes;
+  out.shift = tmp.shift;
+  ozaki_split(K, cols, X, ldx, beta, out, c->st);
+  return out;
+}
+
+// out (M x N) = P^T Q where P or Q is the input matrix A (`a_side` 0: P, 1: Q)
+void gemm_a(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
+            double* out, int64_t ldo, int a_side) {
+  if (c->gemm_mode != LR_GEMM_OZAKI_INT8 || K > kOzakiMaxK) {
+    gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
+    return;
+  }
+  OzakiTmp tp, tq;
+  OzakiOperand op, oq;
+  const OzakiOperand& Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, tp, op);
+  const OzakiOperand& Qo = ozaki_operand(c, K, N, Q, ldq, a_side == 1, tq, oq);
+  ozaki_gemm_tn(c->ws, Po, Qo, M, N, out, ldo, 1.0, 0.0, c->st);
+}
+
+// Scope of one CUR call: A's residue planes live until it closes.
+struct OzakiScope {
+  lr_ctx* c;
+  explicit OzakiScope(lr_ctx* cc) : c(cc) { c->oz_cache_on = true; }
+  ~OzakiScope() {
+    c->oz_cache_on = false;
+    c->oz_src = nullptr;
+    c->oz_planes.reset();
+    c->oz_shift.reset();
+  }
+};
 
 // ---------------------------------------------------------------- CPQR
 // In-place CPQR of a working matrix W (ld even, 16B aligned).  Throws the
@@ -439,7 +511,7 @@ void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, 
   // Omega^T (m x ell): element (i,j) of Omega stored at omt[j + i*m]
   gaussian_matrix(ell, m, seed, omt, m, true, c->st);
   mark(c, "omega");
-  gemm(c, ell, n, m, omt, m, a, lda, y, ldy);
+  gemm_a(c, ell, n, m, omt, m, a, lda, y, ldy, 1);
   mark(c, "sketch_gemm");
 }
 
@@ -608,7 +680,9 @@ void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int
   gather_columns(m, k, a, lda, col_piv, C, m, c->st);
   gather_rows(k, n, a, lda, row_piv, R, k, c->st);
   u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, u_mode, U, Ct_in,
-         [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) { gemm(c, n, k, m, a, lda, Q, ldq, Xt, ldxt); });
+         [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) {
+           gemm_a(c, n, k, m, a, lda, Q, ldq, Xt, ldxt, 0);
+         });
 }
 
 void error_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* C,
@@ -712,6 +786,14 @@ int lr_ctx_set_stream(lr_ctx* c, void* s) {
   // NULL is the CUDA legacy default stream (what torch reports for its default stream)
   return guard([&] { checked(c)->st = s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy; });
 }
+int lr_ctx_set_gemm_mode(lr_ctx* c, int mode) {
+  return guard([&] {
+    checked(c);
+    if (mode != LR_GEMM_DMMA && mode != LR_GEMM_OZAKI_INT8) fail(LR_EINVAL, "set_gemm_mode: unknown mode");
+    c->gemm_mode = mode;
+  });
+}
+int lr_ctx_get_gemm_mode(lr_ctx* c) { return c ? c->gemm_mode : -1; }
 int lr_ctx_use_own_stream(lr_ctx* c) {
   return guard([&] { checked(c)->st = c->own; });
 }
@@ -987,6 +1069,7 @@ int lr_randomized_cur_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
       row_coeff = rc;
     }
     mark(c, "begin");
+    OzakiScope scope(c);
     randomized_id_core(c, m, n, a, lda, k, cfg, strat, col_pivots, col_coeff, k);
     DBuf<double> Ct((size_t)even(k) * m, c->st);
     tsid_core(c, m, n, a, lda, k, col_pivots, strat, row_pivots, row_coeff, k, skeleton, C, Ct);
@@ -1005,10 +1088,13 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
     DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n, c->st),
         ccd((size_t)k * std::max<int64_t>(n - k, 1), c->st), rcd((size_t)k * std::max<int64_t>(m - k, 1), c->st),
         skd((size_t)k * k, c->st);
-    randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k);
-    DBuf<double> Ct((size_t)even(k) * m, c->st);
-    tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
-    cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+    {
+      OzakiScope scope(c);
+      randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k);
+      DBuf<double> Ct((size_t)even(k) * m, c->st);
+      tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
+      cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+    }
     idx_to_host(c, n, cp, col_pivots);
     idx_to_host(c, m, rp, row_pivots);
     to_host(c, m, k, Cd, m, C, m);
@@ -1340,7 +1426,9 @@ int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, in
                  int64_t ldq, double* out, int64_t ldo) {
   return guard([&] {
     checked(c);
-    gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
+    if (M < 1 || N < 1 || K < 1) fail(LR_EINVAL, "gemm_tn: dimensions must be positive");
+    // in the Ozaki mode both operands are split (no A cache outside a CUR call)
+    gemm_a(c, M, N, K, P, ldp, Q, ldq, out, ldo, -1);
   });
 }
 

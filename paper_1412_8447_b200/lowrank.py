@@ -244,6 +244,17 @@ class Context:
     def set_stream(self, stream_handle: int) -> None:
         _raise(self.lib.lr_ctx_set_stream(self.h, ctypes.c_void_p(stream_handle)))
 
+    GEMM_DMMA = 0
+    GEMM_OZAKI_INT8 = 1
+
+    def set_gemm_mode(self, mode: int) -> None:
+        """Engine of the A-sized contractions: GEMM_DMMA (FP64 tensor cores,
+        default) or GEMM_OZAKI_INT8 (FP64 emulated on the INT8 tensor cores)."""
+        _raise(self.lib.lr_ctx_set_gemm_mode(self.h, int(mode)))
+
+    def gemm_mode(self) -> int:
+        return int(self.lib.lr_ctx_get_gemm_mode(self.h))
+
     def stats(self) -> dict:
         st = L.lr_stats()
         _raise(self.lib.lr_ctx_get_stats(self.h, ctypes.byref(st)))

@@ -1,0 +1,152 @@
+"""The Ozaki-II contraction engine (LR_GEMM_OZAKI_INT8: FP64 emulated on the
+INT8 tcgen05 tensor cores) against exact and FP64 references, and the CUR
+pipeline run on it against the CPU oracle.
+
+Tolerances: the emulated product is exact for the inputs truncated to
+beta >= 54 bits relative to each column's largest entry, so per entry
+|C - C_exact| <= 2^-beta (max|P_i| sum|Q_j| + max|Q_j| sum|P_i|) (+ one final
+rounding); the pipeline keeps the north_star bar (identical index sets,
+1e-10 relative factors).
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import rel
+from paper_1412_8447_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture
+def ozaki(lr):
+    ctx = lr.default_context()
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+    try:
+        yield ctx
+    finally:
+        ctx.set_gemm_mode(ctx.GEMM_DMMA)
+
+
+def _gemm(lr, ctx, P, Q):
+    import torch
+    K, M = P.shape
+    N = Q.shape[1]
+    Pc = lr.empty_colmajor(K, M, "cuda"); Pc.copy_(torch.as_tensor(P, device="cuda"))
+    Qc = lr.empty_colmajor(K, N, "cuda"); Qc.copy_(torch.as_tensor(Q, device="cuda"))
+    out = lr.empty_colmajor(M, N, "cuda")
+    rc = ctx.lib.lr_gemm_tn_d(ctx.h, M, N, K, Pc.data_ptr(), Pc.stride(1), Qc.data_ptr(), Qc.stride(1),
+                              out.data_ptr(), out.stride(1))
+    assert rc == 0, ctx.lib.lr_last_error()
+    ctx.synchronize()
+    return out.cpu().numpy()
+
+
+def _exact(P, Q):
+    """P^T Q in extended precision (x87 long double, 64-bit significand)."""
+    return (P.astype(np.longdouble).T @ Q.astype(np.longdouble))
+
+
+def _bound(P, Q, beta):
+    aP, aQ = np.abs(P), np.abs(Q)
+    b = (aP.max(axis=0)[:, None] * aQ.sum(axis=0)[None, :] + aP.sum(axis=0)[:, None] * aQ.max(axis=0)[None, :])
+    return 2.0 ** -beta * b
+
+
+def _beta(K):
+    moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
+    log2m = sum(np.log2(moduli))
+    return min(int(np.floor((log2m - 1 - np.log2(max(K, 1))) / 2)), 62)
+
+
+def test_gemm_mode_switch(lr):
+    ctx = lr.default_context()
+    assert ctx.gemm_mode() == ctx.GEMM_DMMA
+    with pytest.raises(ValueError):
+        ctx.set_gemm_mode(7)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+    assert ctx.gemm_mode() == ctx.GEMM_OZAKI_INT8
+    ctx.set_gemm_mode(ctx.GEMM_DMMA)
+
+
+@pytest.mark.parametrize("M,N,K", [(510, 1000, 777), (128, 256, 128), (5, 7, 3), (300, 260, 4100),
+                                   (129, 257, 129), (1, 1, 1), (64, 300, 65536)])
+def test_ozaki_gemm_error_bound(lr, ozaki, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    P = rng.standard_normal((K, M))
+    Q = rng.standard_normal((K, N))
+    out = _gemm(lr, ozaki, P, Q)
+    ex = _exact(P, Q)
+    err = np.abs(out - ex).astype(np.float64)
+    bound = _bound(P, Q, _beta(K)) + np.abs(ex).astype(np.float64) * 2.0 ** -52
+    assert np.all(err <= bound)
+    # and at least as accurate as the FP64 GEMM overall
+    dm = (P.T @ Q)
+    assert np.linalg.norm(err) <= 2 * np.linalg.norm((dm - ex).astype(np.float64)) + 1e-300
+
+
+def test_ozaki_gemm_scaling_and_special_columns(lr, ozaki):
+    rng = np.random.default_rng(5)
+    K, M, N = 1000, 40, 70
+    P = rng.standard_normal((K, M))
+    Q = rng.standard_normal((K, N))
+    P[:, 3] = 0.0                       # zero column
+    Q[:, 5] = 0.0
+    P[:, 7] *= 2.0 ** 200               # per-column scales far apart
+    P[:, 8] *= 2.0 ** -300
+    Q[:, 9] *= 2.0 ** 150
+    Q[:, 10] *= 2.0 ** -250
+    P[::3, 11] *= 1e6                   # dynamic range inside a column
+    Q[:, 12] = np.round(Q[:, 12] * 8)   # small integers: exact
+    P[:, 13] = np.round(P[:, 13] * 8)
+    out = _gemm(lr, ozaki, P, Q)
+    ex = _exact(P, Q)
+    err = np.abs(out - ex).astype(np.float64)
+    bound = _bound(P, Q, _beta(K)) + np.abs(ex).astype(np.float64) * 2.0 ** -52
+    assert np.all(err <= bound)
+    assert np.all(out[3, :] == 0.0) and np.all(out[:, 5] == 0.0)
+    assert out[13, 12] == float(P[:, 13] @ Q[:, 12])  # integer data: exact
+
+
+def test_ozaki_gemm_deterministic(lr, ozaki):
+    rng = np.random.default_rng(9)
+    P = rng.standard_normal((3000, 300))
+    Q = rng.standard_normal((3000, 500))
+    assert np.array_equal(_gemm(lr, ozaki, P, Q), _gemm(lr, ozaki, P, Q))
+
+
+@pytest.mark.parametrize("shape,k,mode", [((2000, 1500), 50, 1), ((1200, 3000), 100, 0), ((4096, 4096), 500, 1)])
+def test_randomized_cur_on_ozaki_matches_oracle(lr, oracle, ozaki, shape, k, mode):
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], shape[0], shape[1], width=min(1024, min(shape)), k=k)
+    a = inputs.synthetic_np(cfg)
+    cur, ts = lr.randomized_cur(a, k, lr.SketchConfig(oversample=10, seed=1), u_mode=mode, return_tsid=True)
+    o = oracle.randomized_cur(a, k, 10, 1, u_mode=mode)
+    assert np.array_equal(cur.col_pivots, o["col_pivots"])
+    assert np.array_equal(cur.row_pivots, o["row_pivots"])
+    assert np.array_equal(cur.c, o["c"]) and np.array_equal(cur.r, o["r"])
+    assert rel(ts.col_id.coeff, o["col_coeff"]) <= TOL
+    assert rel(ts.row_id.coeff, o["row_coeff"]) <= TOL
+    assert rel(cur.u, o["u"]) <= TOL
+    e, na = lr.cur_error_fro(a, cur)
+    eo, nao = oracle.cur_error_fro(a, o["c"], o["u"], o["r"])
+    assert e / na == pytest.approx(eo / nao, rel=TOL)
+
+
+def test_device_cur_ozaki_equals_dmma_indices(lr):
+    """Same C4-shaped device problem on both engines: identical skeletons."""
+    import torch
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 8192, 8192, width=1024, k=500)
+    a = inputs.synthetic_torch(cfg)
+    sk = lr.SketchConfig(oversample=10, seed=1)
+    ctx = lr.default_context()
+    d = lr.randomized_cur_device(a, 500, sk, u_mode=lr.U_CPINV_A_RPINV)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+    try:
+        z = lr.randomized_cur_device(a, 500, sk, u_mode=lr.U_CPINV_A_RPINV)
+    finally:
+        ctx.set_gemm_mode(ctx.GEMM_DMMA)
+    torch.cuda.synchronize()
+    assert torch.equal(d["col_pivots"], z["col_pivots"]) and torch.equal(d["row_pivots"], z["row_pivots"])
+    assert torch.equal(d["c"], z["c"]) and torch.equal(d["r"], z["r"])
+    du, zu = d["u"].cpu().numpy(), z["u"].cpu().numpy()
+    assert rel(zu, du) <= TOL
