@@ -12,8 +12,12 @@ the factors copied back (`e2e`).  A is 34.4 GB, larger than the 126 MB L2, so
 no flush is needed between steps.  Device time = CUDA events on the stream
 the library launches on, max over ranks.
 
-N > 1 (torchrun): replicas -- every rank factors its own copy of A (weak
-scaling); the column-sharded path is not in this round.
+The two A-sized contractions run on the Ozaki-II engine by default
+(--engine ozaki: FP64 products emulated exactly on the INT8 tensor cores,
+DESIGN.md section 4); --engine dmma uses the FP64 DMMA GEMM.
+
+N > 1 (torchrun): the column-sharded path by default (--mode sharded, strong
+scaling, distributed.py); --mode replicas factors one copy of A per rank.
 
 --impl reference: the reference's CPU algorithm (the C restatement in
 oracle/, see DESIGN.md for why not oracle/_ref) on this host's cores, on a
@@ -60,6 +64,59 @@ def cpqr_bytes(rows, cols, steps):
     """Algorithmic HBM bytes of the fused CPQR pass: trailing block read+write
     plus 32 B/column of norm state, per step."""
     return sum(16.0 * (rows - s) * (cols - s) + 32.0 * (cols - s) for s in range(steps))
+
+
+def ozaki_split_bytes(rows, cols):
+    """colmax pass (read) + split pass (read 8 B, write 16 residue bytes) per element."""
+    return 32.0 * rows * cols
+
+
+def kernel_rooflines(cfg, st, stages, engine):
+    """Roofline entries of the step's big kernels from their CUDA-event stage
+    times (average per launch)."""
+    peaks = read_peaks()
+    hbm = peaks.get("hbm_gbs", 6548.5)
+    ell = cfg.k + OVERSAMPLE
+    out = {}
+    if engine == "ozaki":
+        # INT8 tensor peak: not in MEASURED_PEAKS.json; the B200 INT8/FP8 dense rate is
+        # 2x bf16, so 2 x the measured sustained cuBLAS bf16 figure (kernel timed in a long step)
+        i8 = 2.0 * peaks.get("bf16_tflops_sustained", 1393.6)
+        for name, cols, what in (("sketch_gemm", ell, "Y = Omega A"), ("ctA_gemm", cfg.k, "X^T = A^T Q_c")):
+            if st.get(name):
+                ops = 16 * 2.0 * cols * cfg.m * cfg.n
+                ach = ops / (st[name] * 1e-3) / 1e12
+                out[name] = {"kernel": f"imma_gemm_kernel + crt_kernel ({what}, 16 INT8 residue GEMMs)",
+                             "bound": "tensor", "achieved": round(ach, 1), "peak": round(i8, 1), "unit": "TOP/s",
+                             "frac": round(ach / i8, 4), "traffic": None,
+                             "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (INT8 = 2x bf16 rate)",
+                             "algorithmic": f"16 moduli x 2*{cols}*m*n = {ops:.4e} int8 op per launch"}
+        if st.get("ozaki_split"):
+            calls = stages["ozaki_split"]["count"]
+            b = (ozaki_split_bytes(cfg.m, cfg.n) + ozaki_split_bytes(cfg.m, ell) + ozaki_split_bytes(cfg.m, cfg.k))
+            ach = b / (stages["ozaki_split"]["ms"] / calls * 2 * 1e-3) / 1e9
+            out["ozaki_split"] = {"kernel": "colmax_kernel + split_kernel (A, Omega^T, Q_c residue planes)",
+                                  "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                                  "frac": round(ach / hbm, 4), "traffic": None,
+                                  "algorithmic": "32 B per element of each split operand (read 8 + 8, write 16)"}
+    else:
+        for name, key, what in (("sketch_gemm", "sketch", "Y = Omega A"), ("ctA_gemm", "cta", "X^T = A^T Q_c")):
+            if st.get(name):
+                fm = flops_model(cfg.m, cfg.n, cfg.k, ell)
+                ach = fm[key] / (st[name] * 1e-3) / 1e12
+                out[name] = {"kernel": f"gemm_tn_kernel ({what}, FP64 DMMA)", "bound": "tensor",
+                             "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                             "peak_source": FP64_PEAK_SOURCE, "algorithmic": f"{fm[key]:.4e} flop per launch"}
+    for name, rows, cols, steps in (("cpqr_sample", ell, cfg.n, ell), ("cpqr_ct", cfg.k, cfg.m, cfg.k)):
+        if st.get(name):
+            b = cpqr_bytes(rows, cols, steps)
+            ach = b / (st[name] * 1e-3) / 1e9
+            out[name] = {"kernel": "cpqr_kernel (persistent fused Householder step + norm downdate + argmax)",
+                         "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "traffic": None,
+                         "algorithmic": f"sum_s 16 (rows-s)(cols-s) + 32 (cols-s) = {b:.4e} B per launch"}
+    return out
 
 
 def read_peaks():
@@ -228,6 +285,7 @@ def run_ours(args, rank, world, local_rank):
     lr.lowrank._default = ctx
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8 if args.engine == "ozaki" else ctx.GEMM_DMMA)
 
     t0 = time.time()
     a = inputs.synthetic_torch(cfg, device=dev, col_block=8192)
@@ -301,32 +359,12 @@ def run_ours(args, rank, world, local_rank):
     fm = flops_model(cfg.m, cfg.n, cfg.k, cfg.k + OVERSAMPLE)
     total_flops = sum(fm.values())
     st = {k: v["ms"] / max(1, v["count"]) for k, v in stages.items()}
-    sketch_ms = st.get("sketch_gemm")
-    peaks = read_peaks()
-    hbm_peak = peaks.get("hbm_gbs", 6548.5)
-    roof = None
-    if sketch_ms:
-        ach = fm["sketch"] / (sketch_ms * 1e-3) / 1e12
-        roof = {"kernel": "gemm_tn_kernel (sketch Y = Omega A)", "bound": "tensor", "achieved": round(ach, 3),
-                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4),
-                "traffic": None, "peak_source": FP64_PEAK_SOURCE,
-                "algorithmic": f"2*l*m*n = {fm['sketch']:.4e} flop per launch"}
-    secondary = {}
-    if st.get("ctA_gemm"):
-        ach = fm["cta"] / (st["ctA_gemm"] * 1e-3) / 1e12
-        secondary["ctA_gemm"] = {"bound": "tensor", "achieved": round(ach, 3), "unit": "TFLOP/s",
-                                 "frac": round(ach / FP64_PEAK_TFLOPS, 4)}
-    if st.get("cpqr_sample"):
-        b = cpqr_bytes(cfg.k + OVERSAMPLE, cfg.n, cfg.k + OVERSAMPLE)
-        ach = b / (st["cpqr_sample"] * 1e-3) / 1e9
-        secondary["cpqr_sample"] = {"bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
-                                    "frac": round(ach / hbm_peak, 4), "peak": hbm_peak,
-                                    "algorithmic_bytes": b}
-    if st.get("cpqr_ct"):
-        b = cpqr_bytes(cfg.k, cfg.m, cfg.k)
-        ach = b / (st["cpqr_ct"] * 1e-3) / 1e9
-        secondary["cpqr_ct"] = {"bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
-                                "frac": round(ach / hbm_peak, 4), "peak": hbm_peak, "algorithmic_bytes": b}
+    per_step = {k: v["ms"] / args.steps for k, v in stages.items()}
+    kern = kernel_rooflines(cfg, st, stages, args.engine)
+    # the headline roofline is the kernel with the largest share of the step
+    dom = max(kern, key=lambda n: per_step.get(n, 0.0)) if kern else None
+    roof = dict(kern[dom], share_of_step=round(per_step[dom] / ms, 4)) if dom else None
+    secondary = {n: dict(v, share_of_step=round(per_step.get(n, 0.0) / ms, 4)) for n, v in kern.items() if n != dom}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         est, det = cpu_reference_estimate(args.cpu_sample, os.cpu_count() or 1)
@@ -348,6 +386,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, "
                                "U = C^+ A R^+)", "m": cfg.m, "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE,
                    "u_mode": "cpinv_a_rpinv", "l2": "A (34.4 GB) exceeds L2; no flush needed",
+                   "gemm_engine": {"ozaki": "ozaki_int8 (FP64 emulated on INT8 tcgen05, 16 moduli)",
+                                   "dmma": "fp64_dmma"}[args.engine],
                    "parallelism": "replicas" if world > 1 else "single"},
         "fp64_tflops": round(total_flops / (ms * 1e-3) / 1e12, 3),
         "algorithmic_flops": total_flops,
@@ -384,6 +424,7 @@ def run_sharded(args, rank, world, local_rank):
     lr.lowrank._default = ctx
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8 if args.engine == "ozaki" else ctx.GEMM_DMMA)
     off, n_g = D.shard_bounds(cfg.n, world, rank)
     a = inputs.synthetic_torch(cfg, device=dev, col_block=8192, col_range=(off, n_g))
     be = D.DeviceBackend(ctx, dev)
@@ -512,6 +553,8 @@ def main():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--workload", default="c4", choices=["c4", "c5"],
                    help="c4: dense randomized CUR 65536^2 (headline); c5: sparse CSR 200000x100000")
+    p.add_argument("--engine", default="ozaki", choices=["ozaki", "dmma"],
+                   help="contraction engine of the two A-sized GEMMs (lr_ctx_set_gemm_mode)")
     p.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "sharded"],
                    help="N>1: 'sharded' (column blocks of A, strong scaling) or 'replicas'")
     args = p.parse_args()

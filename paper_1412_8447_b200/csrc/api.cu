@@ -239,6 +239,7 @@ void gemm_a(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t
   OzakiOperand op, oq;
   const OzakiOperand& Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, tp, op);
   const OzakiOperand& Qo = ozaki_operand(c, K, N, Q, ldq, a_side == 1, tq, oq);
+  mark(c, "ozaki_split");
   ozaki_gemm_tn(c->ws, Po, Qo, M, N, out, ldo, 1.0, 0.0, c->st);
 }
 

@@ -26,6 +26,12 @@ namespace lrb {
 namespace {
 
 constexpr int kMod[kOzakiModuli] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+// the same list as a compile-time function usable in unrolled device loops
+__host__ __device__ constexpr int kmod(int t) {
+  return t == 0 ? 256 : t == 1 ? 255 : t == 2 ? 253 : t == 3 ? 251 : t == 4 ? 247 : t == 5 ? 241 : t == 6 ? 239
+       : t == 7 ? 233 : t == 8 ? 229 : t == 9 ? 227 : t == 10 ? 223 : t == 11 ? 217 : t == 12 ? 211
+       : t == 13 ? 199 : t == 14 ? 197 : 193;
+}
 __constant__ int c_mod[kOzakiModuli];
 __constant__ double c_inv_mod[kOzakiModuli];
 __constant__ unsigned long long c_Mt[kOzakiModuli][2];  // M / m_t (low, high limbs)
@@ -87,74 +93,133 @@ void upload_constants() {
 }
 
 // ------------------------------------------------------------ 1+2: scale and split
-// One block per column (grid-stride): pass 1 finds max|x| (HBM), pass 2 re-reads
-// the column (L2) and writes 16 residue bytes per 16-element K chunk.
-__global__ void __launch_bounds__(256) residue_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
-                                                      int64_t ldx, int beta, int8_t* __restrict__ planes,
-                                                      int64_t ldp, int64_t plane_stride, int* __restrict__ shift) {
+// Pass 1 (colmax_kernel): max|x| per column into an int64 bit pattern (non-
+// negative doubles order like their bit patterns) with atomicMax.
+// Pass 2 (split_kernel): x' = rint(x 2^s) once per element in FP64, then the
+// 16 residues without per-modulus FP64 work:
+//   * moduli in 8 pairs, P = m1 m2 < 2^16: r = x' - rint(x'/P) P (DFMA, exact
+//     integer, |r| < 2^17), moved into FP32 as the bit pattern 1.5*2^23 + r;
+//   * per modulus in FP32: q = rint(r/m) by the magic-add trick, then
+//     y = 1.5*2^23 + r - q m (FFMA, exact) whose low mantissa byte is the
+//     symmetric residue (|r/m - q| < 1/2 is never misrounded: the fp32
+//     reciprocal error |r| 2^-24/m < 2^-14 is below 1/(2m), the distance of
+//     r/m from a half-integer for odd m; 1/256 is exact);
+//   * bytes of 4 consecutive K entries are packed per plane (PRMT), one
+//     coalesced 4-byte store per plane.
+constexpr int kSplitRows = 4;  // K entries per thread per tile
+constexpr int kSplitThreads = 256;
+constexpr int kSplitTile = kSplitRows * kSplitThreads;
+
+__global__ void __launch_bounds__(256) colmax_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
+                                                     int64_t ldx, unsigned long long* __restrict__ cmax) {
   __shared__ double sh[8];
-  __shared__ int sh_shift;
-  for (int64_t j = blockIdx.x; j < cols; j += gridDim.x) {
+  const int64_t tiles_k = (K + kSplitTile - 1) / kSplitTile;
+  for (int64_t t = blockIdx.x; t < tiles_k * cols; t += gridDim.x) {
+    const int64_t j = t / tiles_k, i0 = (t % tiles_k) * kSplitTile;
     const double* x = X + j * ldx;
     double mx = 0.0;
-    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+    for (int e = 0; e < kSplitRows; ++e) {
+      const int64_t i = i0 + e * kSplitThreads + threadIdx.x;
+      if (i < K) mx = fmax(mx, fabs(x[i]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < 8; ++w) t = fmax(t, sh[w]);
-      int e = 0;
-      if (t > 0.0) {
-        frexp(t, &e);  // t < 2^e
-      }
-      const int s = t > 0.0 ? beta - e : 0;
-      sh_shift = s;
-      shift[j] = s;
-    }
-    __syncthreads();
-    const int s = sh_shift;
-    // 16 consecutive K entries per thread -> one 16-byte store per plane
-    for (int64_t i0 = 16 * (int64_t)threadIdx.x; i0 < K; i0 += 16 * (int64_t)blockDim.x) {
-      alignas(16) int8_t r[kOzakiModuli][16];
-#pragma unroll 4
-      for (int e = 0; e < 16; ++e) {
-        const int64_t i = i0 + e;
-        const double v = i < K ? rint(ldexp(x[i], s)) : 0.0;  // exact integer, |v| <= 2^beta
-#pragma unroll
-        for (int t = 0; t < kOzakiModuli; ++t) {
-          const double m = (double)c_mod[t];
-          double q = floor(v * c_inv_mod[t]);
-          double rr = fma(-q, m, v);  // exact: |rr| < 2m
-          if (rr < 0.0) rr += m;
-          if (rr >= m) rr -= m;
-          int ri = (int)rr;
-          if (ri > (c_mod[t] - 1) / 2) ri -= c_mod[t];  // symmetric: [-128, 127] (m = 256) / [-(m-1)/2, (m-1)/2]
-          r[t][e] = (int8_t)ri;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kOzakiModuli; ++t)
-        *reinterpret_cast<int4*>(planes + t * plane_stride + j * ldp + i0) = *reinterpret_cast<const int4*>(r[t]);
+      double m = sh[0];
+      for (int w = 1; w < kSplitThreads / 32; ++w) m = fmax(m, sh[w]);
+      if (m > 0.0) atomicMax(cmax + j, (unsigned long long)__double_as_longlong(m));
     }
     __syncthreads();
   }
 }
 
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+__global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
+                                                    int64_t ldx, bool vec2, int beta,
+                                                    const unsigned long long* __restrict__ cmax,
+                                                    int8_t* __restrict__ planes, int64_t ldp, int64_t plane_stride,
+                                                    int* __restrict__ shift) {
+  constexpr double M52 = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr float M23 = 12582912.0f;          // 1.5 * 2^23
+  const int64_t tiles_k = (K + kSplitTile - 1) / kSplitTile;
+  for (int64_t t = blockIdx.x; t < tiles_k * cols; t += gridDim.x) {
+    const int64_t j = t / tiles_k, tk = t % tiles_k;
+    const int64_t i0 = tk * kSplitTile + (int64_t)kSplitRows * threadIdx.x;
+    const double mx = __longlong_as_double((long long)cmax[j]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    const int sft = mx > 0.0 ? beta - e : 0;
+    if (tk == 0 && threadIdx.x == 0) shift[j] = sft;
+    if (i0 >= K) continue;
+    const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
+    const double* x = X + j * ldx + i0;
+    double v[kSplitRows];
+    if (vec2 && i0 + kSplitRows <= K) {
+      const double2 a = *reinterpret_cast<const double2*>(x);
+      const double2 b = *reinterpret_cast<const double2*>(x + 2);
+      v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q) v[q] = i0 + q < K ? x[q] : 0.0;
+    }
+    uint32_t byte[kOzakiModuli][kSplitRows];
+#pragma unroll
+    for (int q = 0; q < kSplitRows; ++q) {
+      const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
+#pragma unroll
+      for (int g = 0; g < kOzakiModuli / 2; ++g) {
+        const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
+        const double invP = 1.0 / P;
+        const double qg = fma(xp, invP, M52) - M52;
+        const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
+        const int lo = __double2loint(r + M52);
+        const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
+        const float rf = fb - M23;                           // r
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int tt = 2 * g + h;
+          const float m = (float)kmod(tt);
+          const float qq = fmaf(rf, 1.0f / m, M23) - M23;
+          const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
+          byte[tt][q] = (uint32_t)__float_as_int(y);
+        }
+      }
+    }
+    int8_t* out = planes + j * ldp + i0;
+#pragma unroll
+    for (int tt = 0; tt < kOzakiModuli; ++tt)
+      *reinterpret_cast<uint32_t*>(out + tt * plane_stride) = pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]);
+  }
+}
+
 // ------------------------------------------------------------ 3: tcgen05 INT8 GEMM
-constexpr int IBM = 128, IBN = 256, IBK = 128;  // tile (K in bytes = int8 elements)
-constexpr int ISTAGES = 4;
-constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK;
+// One CTA owns a 128 x 512 output tile of one plane (two 128x256 UMMAs into
+// all 512 TMEM columns).  Clusters of 4 CTAs stacked along M share the same
+// 512 Q columns: each CTA TMA-loads a 128-column slice of the Q stage and
+// multicasts it to the whole cluster, so a CTA pulls 8 KB (own P) + 8 KB (its
+// Q slice) from L2 per 64-byte K step for 128x512x64 MACs -- about 32 B per
+// 1024 MMA clocks, inside the per-SM share of L2 bandwidth.  Stage release is
+// cluster-wide: every CTA's MMA commit arrives on the stage's empty barrier
+// in all four CTAs (count 4).
+constexpr int IBM = 128, IBN = 512, IBK = 64;  // tile; K in bytes (= int8 elements) per stage
+constexpr int ICL = 4;                         // cluster size along M
+constexpr int ISTAGES = 5;
+constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, IB_SLICE = IB_BYTES / ICL;
 constexpr int ISTAGE_BYTES = IA_BYTES + IB_BYTES;
 constexpr int ITHREADS = 6 * 32;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2-5 epilogue
 constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = 512;
 
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
-  // K-major, SWIZZLE_128B: 8-row x 128 B atoms, SBO = 1024 B between atoms, LBO unused (1), version 1
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
+  // K-major, SWIZZLE_64B: 8-row x 64 B atoms, SBO = 512 B between atoms, LBO unused (1), version 1, layout 4
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -166,10 +231,28 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
-__global__ void __launch_bounds__(ITHREADS, 1)
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+__global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
     imma_gemm_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
-                     int K, int tiles_m, int tiles_n, int m_fast, int8_t* __restrict__ out, int64_t ldo,
-                     int64_t out_plane_stride) {
+                     int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ISTAGES * ISTAGE_BYTES);
@@ -179,20 +262,18 @@ __global__ void __launch_bounds__(ITHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int plane = blockIdx.z;
-  // rasterise along the smaller tile dimension so CTAs sharing an operand tile run together
-  const int tm = m_fast ? blockIdx.x % tiles_m : blockIdx.x / tiles_n;
-  const int tn = m_fast ? blockIdx.x / tiles_m : blockIdx.x % tiles_n;
-  const int m0 = tm * IBM, n0 = tn * IBN;
+  const uint32_t rank = cluster_rank();
+  const int m0 = blockIdx.x * IBM, n0 = blockIdx.y * IBN;
   const int nkb = (K + IBK - 1) / IBK;
 
   if (warp == 1) {
     if (lane == 0) {
       for (int s = 0; s < ISTAGES; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], ICL);
       }
       mbar_init(tmem_full, 1);
-      fence_barrier_init();
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_base_sh)),
@@ -200,7 +281,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  cluster_sync_all();  // barriers of every CTA initialised before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_base_sh;
 
@@ -211,17 +292,18 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ISTAGES;
         const uint32_t ph = (i / ISTAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], ph ^ 1);  // stage s free in all four CTAs
         uint8_t* sp = smem + s * ISTAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], ISTAGE_BYTES);
         tma_load_3d(sp, &tmp, &full[s], i * IBK, m0, plane);
-        tma_load_3d(sp + IA_BYTES, &tmq, &full[s], i * IBK, n0, plane);
+        tma_load_3d_mc(sp + IA_BYTES + rank * IB_SLICE, &tmq, &full[s], i * IBK, n0 + (int)rank * (IBN / ICL), plane,
+                       (uint16_t)((1u << ICL) - 1));
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // kind::i8: D s32, A/B signed int8, K-major, N = 256, M = 128
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(IBN >> 3) << 17) |
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                              ((uint32_t)(IBM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ISTAGES;
@@ -232,18 +314,23 @@ __global__ void __launch_bounds__(ITHREADS, 1)
         const uint32_t sb = sa + IA_BYTES;
 #pragma unroll
         for (int kk = 0; kk < IBK / 32; ++kk) {
-          const uint64_t da = smem_desc_sw128(sa + kk * 32);
-          const uint64_t db = smem_desc_sw128(sb + kk * 32);
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          const uint64_t da = smem_desc_sw64(sa + kk * 32);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t db = smem_desc_sw64(sb + h * 256 * IBK + kk * 32);
+            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + h * 256),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
         }
-        // frees the smem stage once these MMAs have read it
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         smem_u32(&empty[s]))
-                     : "memory");
+        // frees stage s in every CTA of the cluster once these MMAs have read it
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                smem_u32(&empty[s])),
+            "h"((uint16_t)((1u << ICL) - 1))
+            : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                        smem_u32(tmem_full))
@@ -257,8 +344,10 @@ __global__ void __launch_bounds__(ITHREADS, 1)
     const int q = warp & 3;
     const int row = m0 + 32 * q + lane;
     const int mod = c_mod[plane];
+    const double inv = c_inv_mod[plane];
     int8_t* o = out + (int64_t)plane * out_plane_stride;
-    for (int c0 = 0; c0 < IBN; c0 += 16) {
+    const int ncols = min(IBN, N - n0);
+    for (int c0 = 0; c0 < ncols; c0 += 16) {
       uint32_t v[16];
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
       asm volatile(
@@ -272,9 +361,8 @@ __global__ void __launch_bounds__(ITHREADS, 1)
         for (int e = 0; e < 16; ++e) {
           const int col = n0 + c0 + e;
           if (col < N) {
-            int r = (int)v[e] % mod;
-            if (r > (mod - 1) / 2) r -= mod;
-            else if (r < -(mod / 2)) r += mod;
+            const double x = (double)(int)v[e];
+            const int r = (int)fma(-rint(x * inv), (double)mod, x);  // |r| <= m/2 (+1 at an inexact tie)
             o[(int64_t)col * ldo + row] = (int8_t)r;
           }
         }
@@ -282,7 +370,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while cluster peers may still signal its barriers
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
@@ -336,10 +424,10 @@ CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int
   CUtensorMap map;
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)cols, (cuuint64_t)kOzakiModuli};
   cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)plane_stride};
-  cuuint32_t box[3] = {(cuuint32_t)IBK, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)IBK, (cuuint32_t)box_rows, 1};  // IBK bytes = the 64B swizzle span
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8 planes) failed: " + std::to_string((int)r));
   return map;
@@ -350,8 +438,8 @@ CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int
 int ozaki_beta(int64_t K) {
   // K 2^(2 beta) < M_crt / 2  (exact int32 partial sums need K <= 2^17)
   const double lm = crt_host().log2M - 1.0 - std::log2((double)std::max<int64_t>(K, 1));
-  int b = (int)std::floor(lm / 2.0) - 0;
-  return std::min(b, 62);
+  const int b = (int)std::floor(lm / 2.0);
+  return std::min(b, 60);  // |x'| <= 2^60 keeps the residue reduction exact
 }
 
 size_t ozaki_plane_bytes(int64_t K, int64_t cols) {
@@ -366,9 +454,19 @@ void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta
   op.ld = (K + 15) / 16 * 16;
   op.plane_stride = op.ld * cols;
   op.beta = beta;
-  const int g = (int)std::min<int64_t>(cols, 8 * num_sms());
-  residue_kernel<<<g, 256, 0, st>>>(K, cols, X, ldx, beta, op.planes, op.ld, op.plane_stride, op.shift);
+  if (K < 1 || cols < 1) return;
+  unsigned long long* cmax = nullptr;
+  LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cmax), sizeof(unsigned long long) * cols, st));
+  LRB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st));
+  const int64_t tiles = (K + kSplitTile - 1) / kSplitTile * cols;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 8 * num_sms()));
+  colmax_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, cmax);
   LRB_CHECK_LAUNCH();
+  const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
+  split_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, beta, cmax, op.planes, op.ld, op.plane_stride,
+                                            op.shift);
+  LRB_CHECK_LAUNCH();
+  LRB_CUDA(cudaFreeAsync(cmax, st));
 }
 
 void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, int64_t M, int64_t N, double* out,
@@ -382,13 +480,13 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
     attr = true;
   }
   const CUtensorMap tp = make_tmap_i8_planes(P.planes, P.K, P.cols, P.ld, P.plane_stride, IBM);
-  const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, IBN);
+  const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, IBN / ICL);
   const int64_t ldr = M;
   int8_t* res = static_cast<int8_t*>(ws.get(WsSlot::kTmp7, (size_t)M * N * kOzakiModuli));
   const int tiles_m = (int)((M + IBM - 1) / IBM), tiles_n = (int)((N + IBN - 1) / IBN);
-  dim3 grid(tiles_m * tiles_n, 1, kOzakiModuli);
-  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, tiles_m, tiles_n,
-                                                   tiles_m <= tiles_n ? 1 : 0, res, ldr, M * N);
+  // clusters of ICL CTAs along M: pad the M grid (extra CTAs compute zero rows and store nothing)
+  dim3 grid((tiles_m + ICL - 1) / ICL * ICL, tiles_n, kOzakiModuli);
+  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, M * N);
   LRB_CHECK_LAUNCH();
   const int64_t total = M * N;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * num_sms()));

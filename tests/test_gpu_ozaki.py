@@ -56,7 +56,7 @@ def _bound(P, Q, beta):
 def _beta(K):
     moduli = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
     log2m = sum(np.log2(moduli))
-    return min(int(np.floor((log2m - 1 - np.log2(max(K, 1))) / 2)), 62)
+    return min(int(np.floor((log2m - 1 - np.log2(max(K, 1))) / 2)), 60)
 
 
 def test_gemm_mode_switch(lr):

@@ -41,5 +41,5 @@ def run(M, N, K, mode, reps=3):
 if __name__ == "__main__":
     args = [int(x) for x in sys.argv[1:]] or [510, 65536, 65536, 65536, 500, 65536]
     for i in range(0, len(args), 3):
-        for mode in (0, 1):
+        for mode in [int(m) for m in os.environ.get("MODES", "0,1").split(",")]:
             print(json.dumps(run(*args[i:i + 3], mode)), flush=True)
