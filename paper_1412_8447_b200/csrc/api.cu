@@ -104,6 +104,9 @@ struct lr_ctx {
   lrb::OzakiOperand oz_op;
   DBuf<int8_t> oz_planes;
   DBuf<int> oz_shift;
+  // auxiliary streams of the host-pointer entry points: host->device upload
+  // of A (overlapped with the sketch) and device->host of finished factors
+  cudaStream_t up_st = nullptr, down_st = nullptr;
 };
 
 namespace {
@@ -516,10 +519,8 @@ void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, 
   mark(c, "sketch_gemm");
 }
 
-// sketch.hpp:200-223
-void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
-                        const lr_sketch_config& cfg, const lr_solve_strategy& strat, int64_t* piv, double* coeff,
-                        int64_t ldc) {
+// sketch.hpp:200-223 argument checks (before any work)
+int64_t check_randomized_id(int64_t m, int64_t n, int64_t k, const lr_sketch_config& cfg) {
   require_rank_in_range(k, m, n, "randomized_id");
   if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
     fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch with power 0 runs on the B200 path");
@@ -527,10 +528,24 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
   if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
   require_nonempty(m, n, "sketch_gaussian");
   require_sample_count(ell, m, "sketch_gaussian");
+  return ell;
+}
+
+// sketch.hpp:200-223.  Ypre: the sample Y (ell x n, ld work_ld(ell), zero
+// padded) already formed by the caller (the pipelined upload), else sketched here.
+void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                        const lr_sketch_config& cfg, const lr_solve_strategy& strat, int64_t* piv, double* coeff,
+                        int64_t ldc, double* Ypre = nullptr) {
+  const int64_t ell = check_randomized_id(m, n, k, cfg);
   const int64_t ldy = work_ld(ell);
-  DBuf<double> Y((size_t)ldy * n, c->st);
-  zero_pad_rows(c, Y, ell, ldy, n);
-  sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
+  DBuf<double> Yb;
+  double* Y = Ypre;
+  if (!Y) {
+    Yb = DBuf<double>((size_t)ldy * n, c->st);
+    Y = Yb;
+    zero_pad_rows(c, Y, ell, ldy, n);
+    sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
+  }
   const int64_t steps = std::min(ell, n);  // cpqr_full
   if (steps < k) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
   DBuf<double> tau(steps, c->st);
@@ -543,7 +558,7 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
     throw;
   }
   mark(c, "cpqr_sample");
-  solve_core(c, k, n - k, Y, ldy, Y.p + k * ldy, ldy, strat, coeff, ldc, false);
+  solve_core(c, k, n - k, Y, ldy, Y + k * ldy, ldy, strat, coeff, ldc, false);
   mark(c, "coeff_solve_col");
 }
 
@@ -727,6 +742,135 @@ void idx_to_host(lr_ctx* c, int64_t n, const int64_t* d, int64_t* h) {
   if (h && n > 0) LRB_CUDA(cudaMemcpyAsync(h, d, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
 }
 
+cudaStream_t aux_stream(cudaStream_t& s) {
+  if (!s) LRB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+bool is_pinned(const void* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Host -> device upload of A (m x n, lda) into d (ld l) in column chunks on
+// the upload stream, with the sketch Y = Omega A of each chunk issued on the
+// compute stream as soon as that chunk has landed: the PCIe transfer hides
+// the sketch (and, on the Ozaki engine, the residue split of A, which is kept
+// in the context's cache for the A^T Q contraction of the same call).
+void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* d, int64_t l, int64_t ell,
+                   uint64_t seed, double* Y, int64_t ldy) {
+  cudaStream_t up = aux_stream(c->up_st);
+  DBuf<double> omt((size_t)m * even(ell), c->st);
+  gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  const bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
+  OzakiTmp tp;
+  OzakiOperand om;
+  if (oz) {
+    ozaki_operand(c, m, ell, omt, m, false, tp, om);
+    // the cached operand of A, filled chunk by chunk
+    c->oz_planes = DBuf<int8_t>(ozaki_plane_bytes(m, n), c->st);
+    c->oz_shift = DBuf<int>((size_t)n, c->st);
+    c->oz_op.planes = c->oz_planes;
+    c->oz_op.shift = c->oz_shift;
+    c->oz_op.K = m;
+    c->oz_op.cols = n;
+    c->oz_op.ld = (m + 15) / 16 * 16;
+    c->oz_op.plane_stride = c->oz_op.ld * n;
+    c->oz_op.beta = ozaki_beta(m);
+    c->oz_src = d;
+    c->oz_K = m;
+    c->oz_cols = n;
+    c->oz_ld = l;
+  }
+  mark(c, "omega");
+  // ~8 chunks, whole 512-column tiles of the INT8 GEMM
+  const int64_t chunk = std::max<int64_t>(512, ((n + 7) / 8 + 511) / 512 * 512);
+  cudaEvent_t ready;
+  LRB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  cudaEvent_t start;
+  LRB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventRecord(start, c->st));  // d is allocated on the compute stream
+  LRB_CUDA(cudaStreamWaitEvent(up, start, 0));
+  for (int64_t off = 0; off < n; off += chunk) {
+    const int64_t nc = std::min(chunk, n - off);
+    LRB_CUDA(cudaMemcpy2DAsync(d + off * l, l * sizeof(double), a + off * lda, lda * sizeof(double),
+                               m * sizeof(double), nc, cudaMemcpyHostToDevice, up));
+    LRB_CUDA(cudaEventRecord(ready, up));
+    LRB_CUDA(cudaStreamWaitEvent(c->st, ready, 0));
+    if (oz) {
+      const OzakiOperand view = ozaki_cols(c->oz_op, off, nc);
+      ozaki_split_into(d + off * l, l, view, c->st);
+      ozaki_gemm_tn(c->ws, om, view, ell, nc, Y + off * ldy, ldy, 1.0, 0.0, c->st);
+    } else {
+      gemm(c, ell, nc, m, omt, m, d + off * l, l, Y + off * ldy, ldy);
+    }
+  }
+  cudaEventDestroy(ready);
+  cudaEventDestroy(start);
+  mark(c, "upload_sketch");
+}
+
+// Device -> host copies of finished factors.  Pinned destinations are copied
+// on the download stream as soon as their producer has run (overlapping the
+// rest of the pipeline); pageable ones are copied at the end on the compute
+// stream.  The destructor orders the compute stream after every download, so
+// the stream-ordered frees of the device buffers cannot overtake a copy.
+struct Downloads {
+  lr_ctx* c;
+  std::vector<std::function<void()>> deferred;
+  bool used = false;
+  explicit Downloads(lr_ctx* cc) : c(cc) {}
+  void mat(int64_t m, int64_t n, const double* dsrc, int64_t ldd, double* h, int64_t ldh) {
+    if (!h || m <= 0 || n <= 0) return;
+    if (is_pinned(h)) {
+      issue([=](cudaStream_t s) {
+        LRB_CUDA(cudaMemcpy2DAsync(h, ldh * sizeof(double), dsrc, ldd * sizeof(double), m * sizeof(double), n,
+                                   cudaMemcpyDeviceToHost, s));
+      });
+    } else {
+      deferred.push_back([=] { to_host(c, m, n, dsrc, ldd, h, ldh); });
+    }
+  }
+  void idx(int64_t n, const int64_t* dsrc, int64_t* h) {
+    if (!h || n <= 0) return;
+    if (is_pinned(h)) {
+      issue([=](cudaStream_t s) {
+        LRB_CUDA(cudaMemcpyAsync(h, dsrc, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+      });
+    } else {
+      deferred.push_back([=] { idx_to_host(c, n, dsrc, h); });
+    }
+  }
+  template <class F>
+  void issue(F f) {
+    cudaStream_t s = aux_stream(c->down_st);
+    cudaEvent_t e;
+    LRB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    LRB_CUDA(cudaEventRecord(e, c->st));
+    LRB_CUDA(cudaStreamWaitEvent(s, e, 0));
+    cudaEventDestroy(e);
+    f(s);
+    used = true;
+  }
+  void finish() {
+    for (auto& f : deferred) f();
+    deferred.clear();
+  }
+  ~Downloads() {
+    if (!used) return;
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(e, c->down_st);
+      cudaStreamWaitEvent(c->st, e, 0);
+      cudaEventDestroy(e);
+    }
+  }
+};
+
 lr_ctx* checked(lr_ctx* c) {
   if (!c) fail(LR_EINVAL, "null lr_ctx");
   LRB_CUDA(cudaSetDevice(c->device));
@@ -778,6 +922,8 @@ int lr_ctx_destroy(lr_ctx* c) {
     cudaFreeHost(c->h_flags);
     cudaFreeHost(c->h_scal);
     cudaFreeHost(c->h_ll);
+    if (c->up_st) cudaStreamDestroy(c->up_st);
+    if (c->down_st) cudaStreamDestroy(c->down_st);
     cudaStreamDestroy(c->own);
     delete c;
   });
@@ -1082,28 +1228,36 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
                       double* C, double* U, double* R, double* col_coeff, double* row_coeff, double* skeleton) {
   return guard([&] {
     checked(c);
-    require_rank_in_range(k, m, n, "randomized_id");
-    int64_t l;
-    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    require_ld(m, lda, "randomized_cur");
+    const int64_t ell = check_randomized_id(m, n, k, cfg);
+    const int64_t l = even(m);
+    DBuf<double> d((size_t)l * n, c->st);
     DBuf<int64_t> cp(n, c->st), rp(m, c->st);
     DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n, c->st),
         ccd((size_t)k * std::max<int64_t>(n - k, 1), c->st), rcd((size_t)k * std::max<int64_t>(m - k, 1), c->st),
         skd((size_t)k * k, c->st);
+    const int64_t ldy = work_ld(ell);
+    DBuf<double> Y((size_t)ldy * n, c->st);
+    zero_pad_rows(c, Y, ell, ldy, n);
     {
+      Downloads down(c);  // declared after the buffers it reads: drains first
       OzakiScope scope(c);
-      randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k);
+      mark(c, "begin");
+      upload_sketch(c, m, n, a, lda, d, l, ell, cfg.seed, Y, ldy);
+      randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k, Y);
+      down.idx(n, cp, col_pivots);
+      down.mat(k, n - k, ccd, k, col_coeff, k);
       DBuf<double> Ct((size_t)even(k) * m, c->st);
       tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
+      down.idx(m, rp, row_pivots);
+      down.mat(m, k, Cd, m, C, m);
+      down.mat(k, m - k, rcd, k, row_coeff, k);
+      down.mat(k, k, skd, k, skeleton, k);
       cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+      down.mat(k, k, Ud, k, U, k);
+      down.mat(k, n, Rd, k, R, k);
+      down.finish();
     }
-    idx_to_host(c, n, cp, col_pivots);
-    idx_to_host(c, m, rp, row_pivots);
-    to_host(c, m, k, Cd, m, C, m);
-    to_host(c, k, k, Ud, k, U, k);
-    to_host(c, k, n, Rd, k, R, k);
-    to_host(c, k, n - k, ccd, k, col_coeff, k);
-    to_host(c, k, m - k, rcd, k, row_coeff, k);
-    to_host(c, k, k, skd, k, skeleton, k);
     sync(c);
   });
 }

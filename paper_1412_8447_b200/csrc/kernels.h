@@ -140,6 +140,10 @@ struct OzakiOperand {
 int ozaki_beta(int64_t K);
 size_t ozaki_plane_bytes(int64_t K, int64_t cols);
 void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta, OzakiOperand& op, cudaStream_t st);
+// split X into an already laid-out operand (op.K, op.cols, op.ld, op.plane_stride, op.beta set)
+void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cudaStream_t st);
+// columns [off, off + cols) of an operand as an operand of its own (same planes)
+OzakiOperand ozaki_cols(const OzakiOperand& op, int64_t off, int64_t cols);
 // out (M x N) = alpha P^T Q + beta out, reconstructed from 16 INT8 GEMMs
 void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, int64_t M, int64_t N, double* out,
                    int64_t ldo, double alpha, double beta, cudaStream_t st);

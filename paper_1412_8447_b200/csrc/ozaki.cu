@@ -447,13 +447,9 @@ size_t ozaki_plane_bytes(int64_t K, int64_t cols) {
   return (size_t)ld * cols * kOzakiModuli;
 }
 
-void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta, OzakiOperand& op, cudaStream_t st) {
+void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cudaStream_t st) {
   upload_constants();
-  op.K = K;
-  op.cols = cols;
-  op.ld = (K + 15) / 16 * 16;
-  op.plane_stride = op.ld * cols;
-  op.beta = beta;
+  const int64_t K = op.K, cols = op.cols;
   if (K < 1 || cols < 1) return;
   unsigned long long* cmax = nullptr;
   LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cmax), sizeof(unsigned long long) * cols, st));
@@ -463,10 +459,27 @@ void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta
   colmax_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, cmax);
   LRB_CHECK_LAUNCH();
   const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
-  split_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, beta, cmax, op.planes, op.ld, op.plane_stride,
+  split_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, op.beta, cmax, op.planes, op.ld, op.plane_stride,
                                             op.shift);
   LRB_CHECK_LAUNCH();
   LRB_CUDA(cudaFreeAsync(cmax, st));
+}
+
+void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta, OzakiOperand& op, cudaStream_t st) {
+  op.K = K;
+  op.cols = cols;
+  op.ld = (K + 15) / 16 * 16;
+  op.plane_stride = op.ld * cols;
+  op.beta = beta;
+  ozaki_split_into(X, ldx, op, st);
+}
+
+OzakiOperand ozaki_cols(const OzakiOperand& op, int64_t off, int64_t cols) {
+  OzakiOperand v = op;
+  v.planes = op.planes + off * op.ld;
+  v.shift = op.shift + off;
+  v.cols = cols;
+  return v;
 }
 
 void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, int64_t M, int64_t N, double* out,

@@ -26,7 +26,7 @@ __all__ = [
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
-    "randomized_cur_csr_device", "cur_error_fro_csr_device",
+    "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
 ]
 
 LowrankCudaError = L.LowrankCudaError
@@ -467,10 +467,37 @@ def cur_from_two_sided(a, tsid: TwoSidedId, pinv_threshold: float = 1e-12, u_mod
     return CurDecomposition(C, U, R, cp.copy(), rp.copy())
 
 
-def _cur_outputs(m, n, k):
+CUR_OUTPUT_KEYS = ("col_pivots", "row_pivots", "c", "u", "r", "col_coeff", "row_coeff", "skeleton")
+
+
+def _cur_shapes(m, n, k):
+    return ((n,), (m,), (m, k), (k, k), (k, n), (k, max(n - k, 0)), (k, max(m - k, 0)), (k, k))
+
+
+def _cur_outputs(m, n, k, out=None):
+    if out is not None:
+        arrs = tuple(out[key] for key in CUR_OUTPUT_KEYS)
+        for key, arr, shp in zip(CUR_OUTPUT_KEYS, arrs, _cur_shapes(m, n, k)):
+            want = np.int64 if key.endswith("pivots") else np.float64
+            if arr.shape != shp or arr.dtype != want or not (arr.ndim == 1 or arr.flags.f_contiguous):
+                raise ValueError(f"out['{key}']: expected a {shp} column-major {np.dtype(want).name} array")
+        return arrs
     return (np.empty(n, dtype=np.int64), np.empty(m, dtype=np.int64), np.empty((m, k), order="F"),
             np.empty((k, k), order="F"), np.empty((k, n), order="F"), np.empty((k, max(n - k, 0)), order="F"),
             np.empty((k, max(m - k, 0)), order="F"), np.empty((k, k), order="F"))
+
+
+def pinned_cur_outputs(m: int, n: int, k: int) -> dict:
+    """Page-locked host buffers for randomized_cur(..., out=): the factors are
+    then copied back on a separate stream while the rest of the CUR runs."""
+    import torch
+    out = {}
+    for key, shp in zip(CUR_OUTPUT_KEYS, _cur_shapes(m, n, k)):
+        if key.endswith("pivots"):
+            out[key] = torch.empty(shp, dtype=torch.int64, pin_memory=True).numpy()
+        else:
+            out[key] = torch.empty(shp[::-1], dtype=torch.float64, pin_memory=True).numpy().T
+    return out
 
 
 def cur_id(a, k: int, strategy: Optional[SolveStrategy] = None, pinv_threshold: float = 1e-12,
@@ -506,13 +533,14 @@ def randomized_id(a, k: int, cfg: Optional[SketchConfig] = None, strategy: Optio
 
 def randomized_cur(a, k: int, cfg: Optional[SketchConfig] = None, strategy: Optional[SolveStrategy] = None,
                    pinv_threshold: float = 1e-12, u_mode: int = U_VT_RPINV, ctx: Optional[Context] = None,
-                   return_tsid: bool = False):
-    """sketch.hpp:227-234 (+ the lowrank_main.cpp:215 middle factor with U_CPINV_A_RPINV)."""
+                   return_tsid: bool = False, out: Optional[dict] = None):
+    """sketch.hpp:227-234 (+ the lowrank_main.cpp:215 middle factor with U_CPINV_A_RPINV).
+    `out`: preallocated outputs (e.g. pinned_cur_outputs) reused across calls."""
     c = _ctx(ctx)
     a = _f64(a)
     m, n = a.shape
     kk = max(int(k), 1)
-    cp, rp, C, U, R, cc, rc, sk = _cur_outputs(m, n, kk)
+    cp, rp, C, U, R, cc, rc, sk = _cur_outputs(m, n, kk, out if int(k) >= 1 else None)
     _raise(c.lib.lr_randomized_cur(c.h, m, n, _ptr(a), _ld(a), k, (cfg or SketchConfig())._c(),
                                    (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold), int(u_mode),
                                    _ptr(cp), _ptr(rp), _ptr(C), _ptr(U), _ptr(R), _ptr(cc), _ptr(rc), _ptr(sk)))

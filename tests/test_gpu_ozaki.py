@@ -150,3 +150,29 @@ def test_device_cur_ozaki_equals_dmma_indices(lr):
     assert torch.equal(d["c"], z["c"]) and torch.equal(d["r"], z["r"])
     du, zu = d["u"].cpu().numpy(), z["u"].cpu().numpy()
     assert rel(zu, du) <= TOL
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+def test_host_pipeline_pinned_outputs_match(lr, oracle, engine):
+    """The host entry point uploads A in column chunks overlapped with the
+    sketch and copies pinned outputs back on a second stream: same bits as the
+    plain (pageable) call, and the oracle's index sets."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 3000, 5000, width=1024, k=120)
+    a = inputs.synthetic_np(cfg)
+    ctx = lr.default_context()
+    ctx.set_gemm_mode(engine)
+    try:
+        sk = lr.SketchConfig(oversample=10, seed=3)
+        plain = lr.randomized_cur(a, 120, sk, u_mode=lr.U_CPINV_A_RPINV, return_tsid=True)
+        out = lr.pinned_cur_outputs(3000, 5000, 120)
+        piped = lr.randomized_cur(a, 120, sk, u_mode=lr.U_CPINV_A_RPINV, return_tsid=True, out=out)
+    finally:
+        ctx.set_gemm_mode(0)
+    (c1, t1), (c2, t2) = plain, piped
+    for x, y in [(c1.c, c2.c), (c1.u, c2.u), (c1.r, c2.r), (c1.col_pivots, c2.col_pivots),
+                 (c1.row_pivots, c2.row_pivots), (t1.col_id.coeff, t2.col_id.coeff),
+                 (t1.row_id.coeff, t2.row_id.coeff), (t1.skeleton, t2.skeleton)]:
+        assert np.array_equal(x, y)
+    o = oracle.randomized_cur(a, 120, 10, 3, u_mode=1)
+    assert np.array_equal(c2.col_pivots, o["col_pivots"]) and np.array_equal(c2.row_pivots, o["row_pivots"])
+    assert rel(c2.u, o["u"]) <= TOL
