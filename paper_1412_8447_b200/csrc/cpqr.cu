@@ -579,6 +579,10 @@ int cpqr_fast_variant() {
 
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                   double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st) {
+  if (cpqr_panel_supported(m, ld, padded)) {
+    cpqr_panel(ws, m, n, W, ld, k, pivots, tau, d_flags, d_recomputes, st);
+    return;
+  }
   const int Gmax = cpqr_grid(n);
   const size_t cand_sz = kHdr + (size_t)m;
   // state: nrm, nrmx (n each), pval (2G), cand (2 G cand_sz), scratch (G 4m), ppos (2G)

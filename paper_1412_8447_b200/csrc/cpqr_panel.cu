@@ -1,0 +1,612 @@
+// cpqr_panel.cu -- truncated column-pivoted Householder QR with delayed
+// (panel) trailing updates, for the short-wide working matrices of the path
+// (the sketch Y and C^T: m <= 512 rows, tens of thousands of columns).
+//
+// Same observable semantics as cpqr.hpp:32-114 (and as cpqr.cu): first
+// maximum of the running squared norms (ties -> lowest position), full column
+// swaps, reflector beta = -sign(alpha)|x|, tau = (beta-alpha)/beta,
+// v = x/(alpha-beta), downdate norm2 -= R(s,j)^2 and exact recompute below
+// 1e-6 of the last exact value.  Only the order of the floating-point work
+// differs (roundoff-level, like any reordering of the right-looking update).
+//
+// Why: the right-looking kernel streams the trailing matrix in AND out every
+// step.  Here the reflectors of a panel of NB steps are accumulated in the
+// compact form  A_cur = A_p - V F^T  (A_p: the matrix at panel start,
+// F = A_p^T V T built one column per step as in LAPACK's xLAQPS):
+//   per step, per trailing column j (one read of A_p(s:m, j), no write):
+//     F(j, c)   = tau (A_p(s:m, j)^T v - sum_{i<c} F(j, i) w_i),  w = V^T v
+//     R(s, j)   = A_p(s, j) - sum_{i<=c} V(s, i) F(j, i)          (row s only)
+//     norm2(j) -= R(s, j)^2  (exact recompute from A_p - V F^T when flagged)
+//   per panel: A_p(s1:m, s1:n) -= V(s1:m, :) F(s1:n, :)^T (panel_update_kernel).
+// HBM traffic per step is one read of the trailing block (half of the
+// right-looking pass) plus 256 B of F per column; the panel update is one
+// read+write every NB steps.
+//
+// Structure per panel: ONE persistent cooperative launch for the NB steps
+// (per step: batched argmax of per-CTA partials -> the winner's staged
+// reflector -> fused pass over owned columns -> per-CTA argmax + staging of
+// the CTA's best column's reflector for the next step -> one grid barrier),
+// then panel_update_kernel for the block update.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace lrb {
+
+namespace {
+
+constexpr int NB = 32;       // panel width (one F entry per lane)
+constexpr int CH = 8;        // 64-row chunks held in registers: ld <= 512
+constexpr int PT = 384;      // threads per CTA (12 warps, one CTA per SM; 170 registers)
+constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
+constexpr int PW = PT / 32;
+constexpr int kMaxG = 512;
+constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
+constexpr int kSmemMax = (NB + 3) * 64 * CH * (int)sizeof(double);
+
+struct PanelArgs {
+  double* W;
+  int64_t m, n, ld, k;
+  int64_t t0, t1;            // steps [t0, t1) of this launch (t1 - t0 <= NB)
+  int init;                  // first launch: norms, pivots, first candidate
+  int64_t* piv;
+  double* nrm;
+  double* nrmx;
+  double* tau;
+  double* pval;              // [2][G]
+  long long* ppos;           // [2][G]
+  double* cand;              // [2][G][kHdr + ld + NB]: reflector + w of each CTA's best column
+  double* F;                 // [n][NB] row-major
+  double* Vg;                // [ld][NB] row-major copy of the panel's V (GEMM operand)
+  int* flags;
+  unsigned long long* recomputes;
+};
+
+__device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
+  return v1 > v2 || (v1 == v2 && p1 < p2);
+}
+
+__device__ double cta_sum(double x, double* sh) {
+  x = warp_sum(x);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[w] = x;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < PW; ++i) t += sh[i];
+  return t;
+}
+
+struct Col {
+  double c[CH][2];
+  double f;   // F(j, lane) (lane < c), 0 otherwise
+  double nr, nx;
+};
+
+// state of one step's pass, shared by every column of a warp
+struct PassCtx {
+  const PanelArgs& a;
+  int64_t s;
+  int c;
+  int64_t p;
+  bool swapped, apply;
+  double tau, w_l, vr_l, vr_c;
+  int64_t c0, cnt;
+  int warp, lane;
+  const double* vv;
+  const double* Vs;
+  const double* olds;
+  const double* Fs;
+  const double* nst;     // nrm[p], nrmx[p], nrm[s], nrmx[s]
+  long long piv_s;
+  unsigned long long recomputes;
+};
+
+// exact squared norm of A_cur(s+1:m, j) = A_p - V(:, 0:c] F(j, 0:c]^T (the rare
+// recompute branch of cpqr.hpp:80-83); src = the column's A_p values
+__device__ __noinline__ double recompute_norm(const double* src, int64_t s, int64_t m, int64_t ld, int c,
+                                              const double* Vs, double f_lane, int lane) {
+  double f[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) f[i] = __shfl_sync(0xffffffffu, f_lane, i);
+  double q = 0.0;
+  for (int64_t r = s + 1 + lane; r < m; r += 32) {
+    double x = src[r];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (i <= c) x = fma(-Vs[i * ld + r], f[i], x);
+    q = fma(x, x, q);
+  }
+  return warp_sum(q);
+}
+
+// One step's pass over a warp's columns.  TC0 = first active 64-row chunk
+// (s / 64) and NLD = ld / 64 as compile-time constants: the chunk loop has no
+// per-column predicates (rows [m, ld) and v outside [s, m) are zero).
+// TC0 = -1: runtime chunk range.
+template <int TC0, int NLD>
+__device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp) {
+  const PanelArgs& a = x.a;
+  const int64_t s = x.s, ld = a.ld, m = a.m;
+  const int lane = x.lane, c = x.c;
+  const int tc0 = TC0 >= 0 ? TC0 : (int)(s >> 6);
+  const int nld = NLD >= 0 ? NLD : (int)(ld >> 6);
+  const int lsel = (int)((s & 63) >> 1);
+  auto col_of = [&](int64_t it) { return x.c0 + x.warp + PW * ((s & 1) ? (x.cnt - 1 - it) : it); };
+  auto next_valid = [&](int64_t it) {
+    while (it < x.cnt && col_of(it) <= s) ++it;
+    return it;
+  };
+  auto fetch = [&](Col& cb, int64_t j) {
+    const bool from_s = x.swapped && j == x.p;
+    const double* src = from_s ? x.olds : a.W + j * ld;
+#pragma unroll
+    for (int t = 0; t < CH; ++t)
+      if (t >= tc0 && t < nld) {
+        const double2* q = reinterpret_cast<const double2*>(src + 64 * t + 2 * lane);
+        const double2 xx = from_s ? *q : __ldcs(q);
+        cb.c[t][0] = xx.x;
+        cb.c[t][1] = xx.y;
+      }
+    cb.f = lane < c ? (from_s ? x.Fs[lane] : a.F[j * NB + lane]) : 0.0;
+    cb.nr = from_s ? x.nst[2] : a.nrm[j];
+    cb.nx = from_s ? x.nst[3] : a.nrmx[j];
+  };
+  auto process = [&](Col& cb, int64_t j) {
+    const bool from_s = x.swapped && j == x.p;
+    double* dst = a.W + j * ld;
+    const double2* v2 = reinterpret_cast<const double2*>(x.vv);
+    double d0 = 0.0, d1 = 0.0, xs = 0.0;
+#pragma unroll
+    for (int t = 0; t < CH; ++t)
+      if (t >= tc0 && t < nld) {
+        const double2 vx = v2[32 * t + lane];
+        d0 = fma(cb.c[t][0], vx.x, d0);
+        d1 = fma(cb.c[t][1], vx.y, d1);
+        if (t == tc0) xs = (s & 1) ? cb.c[t][1] : cb.c[t][0];
+      }
+    // dot - sum_i F(j,i) w_i   and   sum_{i<c} V(s,i) F(j,i): one pair of reductions
+    double e0 = d0 + d1 - cb.f * x.w_l;
+    double e1 = cb.f * x.vr_l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+    }
+    const double fnew = x.apply ? x.tau * e0 : 0.0;
+    // R(s, j) = A_p(s, j) - sum_{i<c} V(s,i) F(j,i) - V(s,c) F(j,c)
+    xs = __shfl_sync(0xffffffffu, xs, lsel);
+    xs = xs - e1 - x.vr_c * fnew;
+    if (lane == lsel) dst[s] = xs;
+    if (lane == c) cb.f = fnew;
+    if (lane == 0) a.F[j * NB + c] = fnew;
+    if (from_s) {
+      // position p receives the column of position s: every row, and its F row
+      for (int64_t r = lane; r < ld; r += 32)
+        if (r != s) dst[r] = x.olds[r];
+      if (lane < c) a.F[j * NB + lane] = cb.f;
+    }
+    double nr = cb.nr - xs * xs;
+    double nx = cb.nx;
+    if (nr < 1e-6 * nx) {
+      nr = recompute_norm(from_s ? x.olds : dst, s, m, ld, c, x.Vs, cb.f, lane);
+      nx = nr;
+      ++x.recomputes;
+    }
+    if (lane == 0) {
+      a.nrm[j] = nr;
+      a.nrmx[j] = nx;
+      if (from_s) a.piv[j] = x.piv_s;
+    }
+    if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
+  };
+  Col A, B;
+  int64_t it = next_valid(0);
+  if (it < x.cnt) fetch(A, col_of(it));
+  while (it < x.cnt) {
+    const int64_t it2 = next_valid(it + 1);
+    if (it2 < x.cnt) fetch(B, col_of(it2));
+    process(A, col_of(it));
+    if (it2 >= x.cnt) break;
+    const int64_t it3 = next_valid(it2 + 1);
+    if (it3 < x.cnt) fetch(A, col_of(it3));
+    process(B, col_of(it2));
+    it = it3;
+  }
+}
+
+// TC0 / NLD: the panel's first active 64-row chunk (t0 / 64; a 32-step panel
+// never crosses a chunk) and ld / 64, or -1 for the generic runtime version
+template <int TC0, int NLD>
+__global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dyn[];
+  __shared__ double sh_red[PW];
+  __shared__ double sh_bv[PW];
+  __shared__ long long sh_bp[PW];
+  __shared__ double sh_hdr[kHdr];
+  __shared__ long long sh_piv[2];
+  __shared__ long long sh_state[2];
+  __shared__ double sh_nst[4];
+  __shared__ double wsh[NB];    // w = V^T v of the current step
+  __shared__ double vrow[NB];   // V(s, 0:NB)
+  __shared__ double Fs[NB];     // F row of the column swapped out of position s
+  __shared__ double fb[NB];     // F row of the staged candidate column
+  __shared__ double sh_alpha;
+
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = a.m, n = a.n, ld = a.ld;
+  const int64_t c0 = n * cta / G, c1 = n * (cta + 1) / G;
+  const int64_t cand_sz = kHdr + ld + NB;
+  const int nld = (int)(ld >> 6);
+  double* vv = dyn;              // [ld] current reflector, zero outside [s, m)
+  double* Vs = dyn + ld;         // [NB][ld] panel reflectors (column-major, zero outside support)
+  double* olds = Vs + NB * ld;   // [ld]
+  double* pivr = olds + ld;      // [ld]
+  for (int64_t i = threadIdx.x; i < (NB + 3) * ld; i += PT) dyn[i] = 0.0;
+  const int64_t cnt = (c1 - c0 - warp + PW - 1) / PW;
+  unsigned long long my_recomputes = 0;
+  __syncthreads();
+
+  // candidate staging: reflector of column b for step s1 from A_p - V F^T
+  // (c_used = number of panel reflectors already applied); w = V^T v when the
+  // next step continues this panel
+  auto stage = [&](double* cd, int64_t s1, long long b, int c_used, bool same_panel) {
+    if (b >= n || s1 >= m) {
+      __syncthreads();
+      return;
+    }
+    if (threadIdx.x < NB) fb[threadIdx.x] = threadIdx.x < c_used ? a.F[b * NB + threadIdx.x] : 0.0;
+    __syncthreads();
+    const double* x = a.W + b * ld;
+    // rows r = threadIdx.x + PT * q (ld <= 512 <= 2 PT)
+    double xr[kRowsPerThread];
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+      const int64_t r = threadIdx.x + PT * q;
+      xr[q] = 0.0;
+      if (r >= s1 && r < m) {
+        double v = x[r];
+        for (int i = 0; i < c_used; ++i) v = fma(-Vs[i * ld + r], fb[i], v);
+        xr[q] = v;
+        if (r == s1) sh_alpha = v;
+      }
+      part = fma(xr[q], xr[q], part);
+    }
+    const double cn2 = cta_sum(part, sh_red);  // (its barriers publish sh_alpha)
+    const double colnorm = sqrt(cn2);
+    const double alpha = sh_alpha;
+    const bool apply = colnorm > 0.0;
+    double beta = alpha, tau = 0.0, scale = 1.0;
+    if (apply) {
+      beta = alpha >= 0.0 ? -colnorm : colnorm;
+      tau = (beta - alpha) / beta;
+      scale = alpha - beta;
+    }
+    double vr[kRowsPerThread];
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+      const int64_t r = threadIdx.x + PT * q;
+      vr[q] = 0.0;
+      if (r >= s1 && r < m) vr[q] = apply ? ((r == s1) ? 1.0 : xr[q] / scale) : xr[q];
+      if (r < ld) cd[kHdr + r] = vr[q];
+    }
+    if (threadIdx.x == 0) {
+      cd[0] = alpha;
+      cd[1] = beta;
+      cd[2] = tau;
+      cd[3] = apply ? 1.0 : 0.0;
+    }
+    // w_i = V(:, i)^T v for the reflectors of this panel (warp i, i < c_used)
+    if (same_panel) {
+      double* vtmp = pivr;  // free scratch at this point of the step
+#pragma unroll
+      for (int q = 0; q < kRowsPerThread; ++q)
+        if (threadIdx.x + PT * q < ld) vtmp[threadIdx.x + PT * q] = vr[q];
+      __syncthreads();
+      for (int i = warp; i < NB; i += PW) {
+        double acc = 0.0;
+        if (i < c_used)
+          for (int64_t rr = s1 + lane; rr < m; rr += 32) acc = fma(Vs[i * ld + rr], vtmp[rr], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) cd[kHdr + ld + i] = acc;
+      }
+    }
+    __syncthreads();
+  };
+
+  // ------------------------------------------------------------ init (first launch)
+  if (a.init) {
+    double bv = -INFINITY;
+    long long bp = INT64_MAX;
+    int bad = 0;
+    for (int64_t j = c0 + warp; j < c1; j += PW) {
+      const double* col = a.W + j * ld;
+      double acc = 0.0;
+      for (int t = 0; t < nld; ++t) {
+        const double2 xx = *reinterpret_cast<const double2*>(col + 64 * t + 2 * lane);
+        bad |= !isfinite(xx.x) | !isfinite(xx.y);
+        acc = fma(xx.x, xx.x, acc);
+        acc = fma(xx.y, xx.y, acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        a.nrm[j] = acc;
+        a.nrmx[j] = acc;
+        a.piv[j] = j;
+      }
+      if (better(acc, j, bv, bp)) { bv = acc; bp = j; }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags, 1);
+    if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cv = sh_bv[0];
+      long long cp = sh_bp[0];
+      for (int w = 1; w < PW; ++w)
+        if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      a.pval[cta] = cv;  // parity 0 = step 0
+      a.ppos[cta] = cp;
+      sh_piv[0] = cp;
+    }
+    __syncthreads();
+    stage(a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0], 0, false);
+    grid.sync();
+    if (__ldcg(a.flags) != 0) return;
+  }
+
+  // ------------------------------------------------------------ steps of this panel
+  for (int64_t s = a.t0; s < a.t1; ++s) {
+    const int c = (int)(s - a.t0);  // panel column of this step's reflector
+    const int par = (int)(s & 1), nxt = par ^ 1;
+    // (1) global argmax over the per-CTA partials
+    if (warp == 0) {
+      double pv[kMaxG / 32];
+      long long pp[kMaxG / 32];
+#pragma unroll
+      for (int r = 0; r < kMaxG / 32; ++r) {
+        const int cc = lane + 32 * r;
+        pv[r] = cc < G ? __ldcg(a.pval + (int64_t)par * G + cc) : -INFINITY;
+        pp[r] = cc < G ? __ldcg(a.ppos + (int64_t)par * G + cc) : INT64_MAX;
+      }
+      double bv = pv[0];
+      long long bp = pp[0];
+      int bc = lane;
+#pragma unroll
+      for (int r = 1; r < kMaxG / 32; ++r)
+        if (better(pv[r], pp[r], bv, bp)) { bv = pv[r]; bp = pp[r]; bc = lane + 32 * r; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const long long op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (better(ov, op, bv, bp)) { bv = ov; bp = op; bc = oc; }
+      }
+      if (lane == 0) { sh_piv[0] = bp; sh_piv[1] = bc; }
+    }
+    __syncthreads();
+    const int64_t p = sh_piv[0];
+    const double* cd = a.cand + ((int64_t)par * G + sh_piv[1]) * cand_sz;
+
+    // (2) the winner's reflector -> vv, Vs(:, c), w, V(s, :)
+    {
+      const double tau_b = __ldcg(cd + 2);
+      const bool apply_b = __ldcg(cd + 3) != 0.0;
+      if (s > 0 && threadIdx.x == 0) vv[s - 1] = 0.0;
+      for (int64_t i = s + threadIdx.x; i < m; i += PT) {
+        const double vi = __ldcg(cd + kHdr + i);
+        vv[i] = vi;
+        Vs[c * ld + i] = (apply_b && tau_b != 0.0) ? vi : 0.0;
+      }
+      if (threadIdx.x < kHdr) sh_hdr[threadIdx.x] = __ldcg(cd + threadIdx.x);
+      if (threadIdx.x < NB) wsh[threadIdx.x] = threadIdx.x < c ? __ldcg(cd + kHdr + ld + threadIdx.x) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < NB) vrow[threadIdx.x] = threadIdx.x <= c ? Vs[threadIdx.x * ld + s] : 0.0;
+    // (3) swap bookkeeping by the owner of position p
+    const bool owner = (p >= c0 && p < c1);
+    const bool swapped = owner && p != s;
+    if (swapped) {
+      for (int64_t i = threadIdx.x; i < ld; i += PT) olds[i] = __ldcg(a.W + s * ld + i);
+      for (int64_t i = threadIdx.x; i < s; i += PT) pivr[i] = a.W[p * ld + i];
+      if (threadIdx.x < NB) Fs[threadIdx.x] = threadIdx.x < c ? __ldcg(a.F + s * NB + threadIdx.x) : 0.0;
+      if (threadIdx.x == 0) {
+        sh_state[0] = a.piv[p];
+        sh_state[1] = __ldcg(a.piv + s);
+        sh_nst[0] = a.nrm[p];
+        sh_nst[1] = a.nrmx[p];
+        sh_nst[2] = __ldcg(a.nrm + s);
+        sh_nst[3] = __ldcg(a.nrmx + s);
+      }
+    }
+    __syncthreads();
+    const double tau = sh_hdr[2];
+    const bool apply = sh_hdr[3] != 0.0 && tau != 0.0;
+    if (cta == 0 && threadIdx.x == 0) a.tau[s] = tau;
+    const double w_l = wsh[lane];
+    const double vr_l = vrow[lane];
+    const double vr_c = vrow[c];  // V(s, c): 1 when applied
+
+    // (4) fused pass over owned positions j in (s, n): read-only except row s and F(j, c)
+    double bv = -INFINITY;
+    long long bp = INT64_MAX;
+    {
+      PassCtx x{a, s, c, p, swapped, apply, tau, w_l, vr_l, vr_c, c0, cnt, warp, lane, vv, Vs, olds, Fs, sh_nst,
+                sh_state[1], 0ull};
+      pass_cols<TC0, NLD>(x, bv, bp);
+      my_recomputes += x.recomputes;
+    }
+
+    // (5) CTA argmax, pivot column write-back, V row-major copy for the panel GEMM
+    if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cv = sh_bv[0];
+      long long cp = sh_bp[0];
+      for (int w = 1; w < PW; ++w)
+        if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      a.pval[(int64_t)nxt * G + cta] = cv;
+      a.ppos[(int64_t)nxt * G + cta] = cp;
+      sh_piv[0] = cp;
+    }
+    if (owner) {
+      double* ps = a.W + s * ld;
+      if (swapped) {
+        for (int64_t i = threadIdx.x; i < s; i += PT) ps[i] = pivr[i];
+        if (threadIdx.x == 0) {
+          a.piv[s] = sh_state[0];
+          a.nrm[s] = sh_nst[0];
+          a.nrmx[s] = sh_nst[1];
+        }
+      }
+      const double beta = sh_hdr[1];
+      for (int64_t i = s + threadIdx.x; i < m; i += PT) ps[i] = (sh_hdr[3] != 0.0 && i == s) ? beta : vv[i];
+    }
+    if (cta == 0)
+      for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
+    __syncthreads();
+    if (s + 1 < a.k)
+      stage(a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0], c + 1, s + 1 < a.t1);
+    grid.sync();
+  }
+  if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
+}
+
+// Panel update A_p(r0:m, j0:n) -= V(r0:m, 0:nc) F(j0:n, 0:nc)^T (rank <= 32,
+// HBM-bound: one read + one write of the block).  A thread owns one row
+// (m - r0 <= 512) and keeps its V entries in registers; the F rows of a batch
+// of columns are staged in shared memory and read as broadcasts; 8 columns
+// are loaded before any is reduced (memory-level parallelism).
+constexpr int UT = 512;       // threads per CTA: row r0 + tid
+constexpr int UB = 64;        // columns per F batch
+constexpr int UG = 8;         // columns in flight per thread
+__global__ void __launch_bounds__(UT, 1) panel_update_kernel(double* __restrict__ W, int64_t ld, int64_t r0,
+                                                             int64_t m, int64_t j0, int64_t n,
+                                                             const double* __restrict__ Vg,
+                                                             const double* __restrict__ F, int nc) {
+  __shared__ double Fb[UB][NB];
+  const int tid = threadIdx.x;
+  const int64_t r = r0 + tid;
+  const bool has = r < m;
+  double v[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) v[i] = (has && i < nc) ? Vg[r * NB + i] : 0.0;
+  const int64_t nbatch = (n - j0 + UB - 1) / UB;
+  for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+    const int64_t jb = j0 + bt * UB;
+    const int cols = (int)(n - jb < UB ? n - jb : UB);
+    __syncthreads();
+    for (int e = tid; e < UB * NB; e += UT) {
+      const int jj = e / NB, i = e % NB;
+      Fb[jj][i] = (jj < cols && i < nc) ? F[(jb + jj) * NB + i] : 0.0;
+    }
+    __syncthreads();
+    if (!has) continue;
+    for (int g = 0; g < cols; g += UG) {
+      double x[UG];
+#pragma unroll
+      for (int u = 0; u < UG; ++u) x[u] = g + u < cols ? W[(jb + g + u) * ld + r] : 0.0;
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const double2* f2 = reinterpret_cast<const double2*>(Fb[g + u < UB ? g + u : 0]);
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NB / 2; ++i) {
+          const double2 f = f2[i];
+          s0 = fma(v[2 * i], f.x, s0);
+          s1 = fma(v[2 * i + 1], f.y, s1);
+        }
+        if (g + u < cols) W[(jb + g + u) * ld + r] = x[u] - (s0 + s1);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool cpqr_panel_supported(int64_t m, int64_t ld, bool padded) {
+  static const bool off = [] {
+    const char* e = getenv("LRB_CPQR_PANEL");
+    return e && atoi(e) == 0;
+  }();
+  return !off && padded && ld % 64 == 0 && ld <= 64 * CH && m <= ld;
+}
+
+void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
+                double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)(NB + 3) * ld;
+  using KernT = void (*)(PanelArgs);
+  const bool spec = ld == 64 * CH;
+  auto kern_for = [&](int64_t t0) -> KernT {
+    if (!spec) return cpqr_panel_kernel<-1, -1>;
+    switch (t0 / 64) {
+      case 0: return cpqr_panel_kernel<0, CH>;
+      case 1: return cpqr_panel_kernel<1, CH>;
+      case 2: return cpqr_panel_kernel<2, CH>;
+      case 3: return cpqr_panel_kernel<3, CH>;
+      case 4: return cpqr_panel_kernel<4, CH>;
+      case 5: return cpqr_panel_kernel<5, CH>;
+      case 6: return cpqr_panel_kernel<6, CH>;
+      default: return cpqr_panel_kernel<7, CH>;
+    }
+  };
+  static bool attr = false;
+  if (!attr) {
+    const KernT all[] = {cpqr_panel_kernel<-1, -1>, cpqr_panel_kernel<0, CH>, cpqr_panel_kernel<1, CH>,
+                         cpqr_panel_kernel<2, CH>,  cpqr_panel_kernel<3, CH>, cpqr_panel_kernel<4, CH>,
+                         cpqr_panel_kernel<5, CH>,  cpqr_panel_kernel<6, CH>, cpqr_panel_kernel<7, CH>};
+    for (KernT kf : all)
+      LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+    attr = true;
+  }
+  int per_sm = 0;
+  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_panel_kernel<-1, -1>, PT, smem));
+  per_sm = std::max(1, per_sm);
+  int G = std::min(std::min(per_sm, 1) * num_sms(), kMaxG);
+  G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + PW - 1) / PW));
+  const size_t cand_sz = kHdr + (size_t)ld + NB;
+  const size_t nd = 2 * (size_t)n + 2 * (size_t)G + 2 * (size_t)G * cand_sz + (size_t)n * NB + (size_t)ld * NB;
+  const size_t bytes = sizeof(double) * nd + sizeof(long long) * 2 * (size_t)G + 256;
+  uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
+  PanelArgs a{};
+  a.W = W;
+  a.m = m;
+  a.n = n;
+  a.ld = ld;
+  a.k = k;
+  a.piv = pivots;
+  a.tau = tau;
+  double* d = reinterpret_cast<double*>(base);
+  a.nrm = d;
+  a.nrmx = d + n;
+  a.pval = d + 2 * n;
+  a.cand = a.pval + 2 * G;
+  a.F = a.cand + 2 * (size_t)G * cand_sz;
+  a.Vg = a.F + (size_t)n * NB;
+  a.ppos = reinterpret_cast<long long*>(a.Vg + (size_t)ld * NB);
+  a.flags = d_flags;
+  a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
+  for (int64_t t0 = 0; t0 < k; t0 += NB) {
+    const int64_t t1 = std::min<int64_t>(k, t0 + NB);
+    a.t0 = t0;
+    a.t1 = t1;
+    a.init = t0 == 0 ? 1 : 0;
+    void* params[] = {&a};
+    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0), dim3(G), dim3(PT), params, smem, st));
+    LRB_CHECK_LAUNCH();
+    // A_p(t1:m, t1:n) -= V(t1:m, 0:c) F(t1:n, 0:c)^T  (rows/cols of later panels only)
+    if (t1 < k && t1 < m && t1 < n) {
+      const int64_t nbatch = (n - t1 + UB - 1) / UB;
+      const int ug = (int)std::min<int64_t>(nbatch, num_sms());  // persistent: V loaded once per CTA
+      panel_update_kernel<<<ug, UT, 0, st>>>(W, ld, t1, m, t1, n, a.Vg, a.F, (int)(t1 - t0));
+      LRB_CHECK_LAUNCH();
+    }
+  }
+}
+
+}  // namespace lrb
