@@ -110,18 +110,25 @@ constexpr int kSplitRows = 4;  // K entries per thread per tile
 constexpr int kSplitThreads = 256;
 constexpr int kSplitTile = kSplitRows * kSplitThreads;
 
+constexpr int kMaxRowsPerThread = 32;  // colmax: 8192-row tiles, 16 double2 loads in flight per thread
 __global__ void __launch_bounds__(256) colmax_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
-                                                     int64_t ldx, unsigned long long* __restrict__ cmax) {
+                                                     int64_t ldx, bool vec2, unsigned long long* __restrict__ cmax) {
   __shared__ double sh[8];
-  const int64_t tiles_k = (K + kSplitTile - 1) / kSplitTile;
+  constexpr int64_t kTile = (int64_t)kMaxRowsPerThread * kSplitThreads;
+  const int64_t tiles_k = (K + kTile - 1) / kTile;
   for (int64_t t = blockIdx.x; t < tiles_k * cols; t += gridDim.x) {
-    const int64_t j = t / tiles_k, i0 = (t % tiles_k) * kSplitTile;
+    const int64_t j = t / tiles_k, i0 = (t % tiles_k) * kTile;
     const double* x = X + j * ldx;
     double mx = 0.0;
+    if (vec2 && i0 + kTile <= K) {
+      double2 r[kMaxRowsPerThread / 2];
 #pragma unroll
-    for (int e = 0; e < kSplitRows; ++e) {
-      const int64_t i = i0 + e * kSplitThreads + threadIdx.x;
-      if (i < K) mx = fmax(mx, fabs(x[i]));
+      for (int e = 0; e < kMaxRowsPerThread / 2; ++e)
+        r[e] = __ldcs(reinterpret_cast<const double2*>(x + i0 + 2 * (e * kSplitThreads + threadIdx.x)));
+#pragma unroll
+      for (int e = 0; e < kMaxRowsPerThread / 2; ++e) mx = fmax(mx, fmax(fabs(r[e].x), fabs(r[e].y)));
+    } else {
+      for (int64_t i = i0 + threadIdx.x; i < K && i < i0 + kTile; i += kSplitThreads) mx = fmax(mx, fabs(x[i]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -148,7 +155,28 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
   constexpr double M52 = 6755399441055744.0;  // 1.5 * 2^52
   constexpr float M23 = 12582912.0f;          // 1.5 * 2^23
   const int64_t tiles_k = (K + kSplitTile - 1) / kSplitTile;
-  for (int64_t t = blockIdx.x; t < tiles_k * cols; t += gridDim.x) {
+  const int64_t total = tiles_k * cols;
+  // software pipeline: the next tile's 4 values are in flight while this
+  // tile's 64 residues are computed and stored
+  auto load = [&](int64_t t, double (&v)[kSplitRows]) {
+    const int64_t j = t / tiles_k, tk = t % tiles_k;
+    const int64_t i0 = tk * kSplitTile + (int64_t)kSplitRows * threadIdx.x;
+    const double* x = X + j * ldx + i0;
+    if (vec2 && i0 + kSplitRows <= K) {
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(x));
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(x + 2));
+      v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q) v[q] = i0 + q < K ? x[q] : 0.0;
+    }
+  };
+  double v[kSplitRows], vn[kSplitRows];
+  int64_t t = blockIdx.x;
+  if (t < total) load(t, v);
+  for (; t < total; t += gridDim.x) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < total) load(tn, vn);
     const int64_t j = t / tiles_k, tk = t % tiles_k;
     const int64_t i0 = tk * kSplitTile + (int64_t)kSplitRows * threadIdx.x;
     const double mx = __longlong_as_double((long long)cmax[j]);
@@ -156,45 +184,39 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     const int sft = mx > 0.0 ? beta - e : 0;
     if (tk == 0 && threadIdx.x == 0) shift[j] = sft;
-    if (i0 >= K) continue;
-    const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
-    const double* x = X + j * ldx + i0;
-    double v[kSplitRows];
-    if (vec2 && i0 + kSplitRows <= K) {
-      const double2 a = *reinterpret_cast<const double2*>(x);
-      const double2 b = *reinterpret_cast<const double2*>(x + 2);
-      v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
-    } else {
+    if (i0 < K) {
+      const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
+      uint32_t byte[kOzakiModuli][kSplitRows];
 #pragma unroll
-      for (int q = 0; q < kSplitRows; ++q) v[q] = i0 + q < K ? x[q] : 0.0;
-    }
-    uint32_t byte[kOzakiModuli][kSplitRows];
+      for (int q = 0; q < kSplitRows; ++q) {
+        const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
 #pragma unroll
-    for (int q = 0; q < kSplitRows; ++q) {
-      const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
+        for (int g = 0; g < kOzakiModuli / 2; ++g) {
+          const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
+          const double invP = 1.0 / P;
+          const double qg = fma(xp, invP, M52) - M52;
+          const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
+          const int lo = __double2loint(r + M52);
+          const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
+          const float rf = fb - M23;                           // r
 #pragma unroll
-      for (int g = 0; g < kOzakiModuli / 2; ++g) {
-        const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
-        const double invP = 1.0 / P;
-        const double qg = fma(xp, invP, M52) - M52;
-        const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
-        const int lo = __double2loint(r + M52);
-        const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
-        const float rf = fb - M23;                           // r
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int tt = 2 * g + h;
-          const float m = (float)kmod(tt);
-          const float qq = fmaf(rf, 1.0f / m, M23) - M23;
-          const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
-          byte[tt][q] = (uint32_t)__float_as_int(y);
+          for (int h = 0; h < 2; ++h) {
+            const int tt = 2 * g + h;
+            const float m = (float)kmod(tt);
+            const float qq = fmaf(rf, 1.0f / m, M23) - M23;
+            const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
+            byte[tt][q] = (uint32_t)__float_as_int(y);
+          }
         }
       }
-    }
-    int8_t* out = planes + j * ldp + i0;
+      int8_t* out = planes + j * ldp + i0;
 #pragma unroll
-    for (int tt = 0; tt < kOzakiModuli; ++tt)
-      *reinterpret_cast<uint32_t*>(out + tt * plane_stride) = pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]);
+      for (int tt = 0; tt < kOzakiModuli; ++tt)
+        __stcs(reinterpret_cast<unsigned int*>(out + tt * plane_stride),
+               pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]));
+    }
+#pragma unroll
+    for (int q = 0; q < kSplitRows; ++q) v[q] = vn[q];
   }
 }
 
@@ -456,9 +478,11 @@ void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cuda
   LRB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st));
   const int64_t tiles = (K + kSplitTile - 1) / kSplitTile * cols;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 8 * num_sms()));
-  colmax_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, cmax);
-  LRB_CHECK_LAUNCH();
   const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
+  const int64_t mtiles = (K + kMaxRowsPerThread * kSplitThreads - 1) / (kMaxRowsPerThread * kSplitThreads) * cols;
+  const int gm = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, 8 * num_sms()));
+  colmax_kernel<<<gm, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, cmax);
+  LRB_CHECK_LAUNCH();
   split_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, op.beta, cmax, op.planes, op.ld, op.plane_stride,
                                             op.shift);
   LRB_CHECK_LAUNCH();
