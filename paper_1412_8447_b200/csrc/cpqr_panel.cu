@@ -40,7 +40,7 @@ namespace {
 
 constexpr int NB = 32;       // panel width (one F entry per lane)
 constexpr int CH = 8;        // 64-row chunks held in registers: ld <= 512
-constexpr int PT = 384;      // threads per CTA (12 warps, one CTA per SM; 170 registers)
+constexpr int PT = 256;      // threads per CTA (8 warps, one CTA per SM; up to 255 registers)
 constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
 constexpr int PW = PT / 32;
 constexpr int kMaxG = 512;
@@ -93,20 +93,23 @@ struct PassCtx {
   int c;
   int64_t p;
   bool swapped, apply;
-  double tau, w_l, vr_l, vr_c;
+  double tau, vr_c;
   int64_t c0, cnt;
   int warp, lane;
   const double* vv;
   const double* Vs;
   const double* olds;
   const double* Fs;
+  const double* wsh;     // w = V^T v (NB)
+  const double* vrow;    // V(s, 0:NB)
   const double* nst;     // nrm[p], nrmx[p], nrm[s], nrmx[s]
   long long piv_s;
   unsigned long long recomputes;
 };
 
 // exact squared norm of A_cur(s+1:m, j) = A_p - V(:, 0:c] F(j, 0:c]^T (the rare
-// recompute branch of cpqr.hpp:80-83); src = the column's A_p values
+// recompute branch of cpqr.hpp:80-83) for the swapped column: full warp,
+// src = the column's A_p values, lane i holds F(j, i)
 __device__ __noinline__ double recompute_norm(const double* src, int64_t s, int64_t m, int64_t ld, int c,
                                               const double* Vs, double f_lane, int lane) {
   double f[NB];
@@ -123,98 +126,205 @@ __device__ __noinline__ double recompute_norm(const double* src, int64_t s, int6
   return warp_sum(q);
 }
 
-// One step's pass over a warp's columns.  TC0 = first active 64-row chunk
-// (s / 64) and NLD = ld / 64 as compile-time constants: the chunk loop has no
-// per-column predicates (rows [m, ld) and v outside [s, m) are zero).
-// TC0 = -1: runtime chunk range.
+// group version of the recompute (L lanes per column): rows s+1..m-1 of the
+// column re-read from W (L2-hot), F(j, 0:c] from global (written by the group)
+template <int L>
+__device__ __noinline__ double group_recompute(const double* col, const double* Fj, int64_t s, int64_t m,
+                                               int64_t ld, int c, const double* Vs, int l) {
+  double q = 0.0;
+  for (int64_t r = s + 1 + l; r < m; r += L) {
+    double x = col[r];
+    for (int i = 0; i <= c; ++i) x = fma(-Vs[i * ld + r], Fj[i], x);
+    q = fma(x, x, q);
+  }
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  return q;
+}
+
+// The column moved from position s to position p this step (at most one per
+// CTA): full warp, A_p values from olds, F row from Fs.  Writes the whole
+// column to position p with row s updated, its F row, norms and pivot.
+__device__ __noinline__ void process_swapped(PassCtx& x, double& bv, long long& bp) {
+  const PanelArgs& a = x.a;
+  const int64_t s = x.s, ld = a.ld, m = a.m, j = x.p;
+  const int lane = x.lane, c = x.c;
+  double d = 0.0;
+  for (int64_t r = s + lane; r < m; r += 32) d = fma(x.olds[r], x.vv[r], d);
+  double f = lane < c ? x.Fs[lane] : 0.0;
+  double e0 = d - f * x.wsh[lane];
+  double e1 = f * x.vrow[lane];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+    e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+  }
+  const double fnew = x.apply ? x.tau * e0 : 0.0;
+  const double xs = x.olds[s] - e1 - x.vr_c * fnew;
+  double* dst = a.W + j * ld;
+  for (int64_t r = lane; r < ld; r += 32) dst[r] = r == s ? xs : x.olds[r];
+  if (lane == c) f = fnew;
+  if (lane <= c) a.F[j * NB + lane] = f;
+  double nr = x.nst[2] - xs * xs;
+  double nx = x.nst[3];
+  if (nr < 1e-6 * nx) {
+    nr = recompute_norm(x.olds, s, m, ld, c, x.Vs, f, lane);
+    nx = nr;
+    ++x.recomputes;
+  }
+  if (lane == 0) {
+    a.nrm[j] = nr;
+    a.nrmx[j] = nx;
+    a.piv[j] = x.piv_s;
+  }
+  if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
+}
+
+// One step's pass over a warp's columns (all but the swapped one).
+// TC0 = first active 64-row chunk (s / 64, constant over a 32-step panel),
+// NLD = ld / 64; TC0 = -1: runtime chunk range.
+// Specialised layout: a column is handled by a group of L = 4 * (active
+// chunks) lanes, 32 / L columns per warp instruction; lane l of a group holds
+// rows base + 2(l + L k) + {0, 1}, k < KP (<= 16 rows), and F(j, l S .. l S + S - 1)
+// (S = NB / L).  Late panels (few active rows) thus run up to 8 columns per
+// warp instruction with log2(L)-round reductions.
 template <int TC0, int NLD>
 __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp) {
+  constexpr bool SPEC = TC0 >= 0;
+  constexpr int NA = SPEC ? NLD - TC0 : CH;
+  // lanes per column: a power of two with 16 rows (8 row pairs) or fewer per lane
+  constexpr int L = !SPEC ? 32 : (NA >= 5 ? 32 : (NA >= 3 ? 16 : 4 * NA));
+  constexpr int KP = SPEC ? 32 * NA / L : CH;  // row pairs per lane
+  constexpr int GPW = 32 / L;
+  constexpr int S = NB / L;
+  constexpr int D = S == 1 ? 4 : (S == 2 ? 3 : 2);  // warp-iterations in flight
   const PanelArgs& a = x.a;
   const int64_t s = x.s, ld = a.ld, m = a.m;
   const int lane = x.lane, c = x.c;
-  const int tc0 = TC0 >= 0 ? TC0 : (int)(s >> 6);
-  const int nld = NLD >= 0 ? NLD : (int)(ld >> 6);
-  const int lsel = (int)((s & 63) >> 1);
-  auto col_of = [&](int64_t it) { return x.c0 + x.warp + PW * ((s & 1) ? (x.cnt - 1 - it) : it); };
-  auto next_valid = [&](int64_t it) {
-    while (it < x.cnt && col_of(it) <= s) ++it;
-    return it;
-  };
-  auto fetch = [&](Col& cb, int64_t j) {
-    const bool from_s = x.swapped && j == x.p;
-    const double* src = from_s ? x.olds : a.W + j * ld;
+  const int l = lane & (L - 1), g = lane / L;
+  const int gbase = lane & ~(L - 1);
+  const int tc0 = SPEC ? TC0 : (int)(s >> 6);
+  const int nld = SPEC ? NLD : (int)(ld >> 6);
+  const int base = SPEC ? 64 * TC0 : 0;
+  // rows of this lane: base + 2(l + L k) + e; the generic layout (L = 32) keeps
+  // chunk k at rows 64k + 2 lane and predicates k in [tc0, nld)
+  auto active = [&](int k) { return SPEC ? k < KP : (k >= tc0 && k < nld); };
+  const int rel = (int)(s - base);
+  const int kk_s = rel / (2 * L), lo_s = (rel >> 1) & (L - 1), e_s = rel & 1;
+  // per-lane slices of w and V(s, :)
+  double wl[S], vl[S];
 #pragma unroll
-    for (int t = 0; t < CH; ++t)
-      if (t >= tc0 && t < nld) {
-        const double2* q = reinterpret_cast<const double2*>(src + 64 * t + 2 * lane);
-        const double2 xx = from_s ? *q : __ldcs(q);
-        cb.c[t][0] = xx.x;
-        cb.c[t][1] = xx.y;
-      }
-    cb.f = lane < c ? (from_s ? x.Fs[lane] : a.F[j * NB + lane]) : 0.0;
-    cb.nr = from_s ? x.nst[2] : a.nrm[j];
-    cb.nx = from_s ? x.nst[3] : a.nrmx[j];
+  for (int t = 0; t < S; ++t) {
+    wl[t] = x.wsh[l * S + t];
+    vl[t] = x.vrow[l * S + t];
+  }
+  const int lc = c / S, tcs = c % S;  // owner lane / slot of F(j, c)
+  // the warp's columns c0 + warp + PW*it; valid ones (> s) are a contiguous run
+  const int64_t first = x.c0 + x.warp;
+  int64_t it_min = s >= first ? (s - first) / PW + 1 : 0;
+  if (it_min > x.cnt) it_min = x.cnt;
+  const int64_t n_valid = x.cnt - it_min;
+  auto col_at = [&](int64_t q) { return first + PW * ((s & 1) ? (x.cnt - 1 - q) : (it_min + q)); };
+  struct Slot {
+    double c[CH][2];
+    double f[S];
+    double nr, nx;
+    int64_t j;
+    bool ok;
   };
-  auto process = [&](Col& cb, int64_t j) {
-    const bool from_s = x.swapped && j == x.p;
-    double* dst = a.W + j * ld;
-    const double2* v2 = reinterpret_cast<const double2*>(x.vv);
+  auto fetch = [&](Slot& cb, int64_t qi) {
+    const int64_t q = qi * GPW + g;
+    cb.ok = q < n_valid;
+    cb.j = cb.ok ? col_at(q) : x.c0;  // any owned column for the (unused) loads
+    if (x.swapped && cb.j == x.p) cb.ok = false;
+    const double* src = a.W + cb.j * ld + base;
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+      if (active(k)) {
+        const double2 xx = __ldcs(reinterpret_cast<const double2*>(src + 2 * (l + L * k)));
+        cb.c[k][0] = xx.x;
+        cb.c[k][1] = xx.y;
+      }
+    const double* fr = a.F + cb.j * NB + l * S;
+#pragma unroll
+    for (int t = 0; t < S; ++t) cb.f[t] = (l * S + t < c) ? fr[t] : 0.0;
+    cb.nr = a.nrm[cb.j];
+    cb.nx = a.nrmx[cb.j];
+  };
+  const double2* v2 = reinterpret_cast<const double2*>(x.vv + base);
+  auto process = [&](Slot& cb) {
     double d0 = 0.0, d1 = 0.0, xs = 0.0;
 #pragma unroll
-    for (int t = 0; t < CH; ++t)
-      if (t >= tc0 && t < nld) {
-        const double2 vx = v2[32 * t + lane];
-        d0 = fma(cb.c[t][0], vx.x, d0);
-        d1 = fma(cb.c[t][1], vx.y, d1);
-        if (t == tc0) xs = (s & 1) ? cb.c[t][1] : cb.c[t][0];
+    for (int k = 0; k < KP; ++k)
+      if (active(k)) {
+        const double2 vx = v2[l + L * k];
+        d0 = fma(cb.c[k][0], vx.x, d0);
+        d1 = fma(cb.c[k][1], vx.y, d1);
+        if (k == kk_s) xs = e_s ? cb.c[k][1] : cb.c[k][0];
       }
-    // dot - sum_i F(j,i) w_i   and   sum_{i<c} V(s,i) F(j,i): one pair of reductions
-    double e0 = d0 + d1 - cb.f * x.w_l;
-    double e1 = cb.f * x.vr_l;
+    double e0 = d0 + d1, e1 = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int t = 0; t < S; ++t) {
+      e0 = fma(-cb.f[t], wl[t], e0);
+      e1 = fma(cb.f[t], vl[t], e1);
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) {
       e0 += __shfl_xor_sync(0xffffffffu, e0, o);
       e1 += __shfl_xor_sync(0xffffffffu, e1, o);
     }
     const double fnew = x.apply ? x.tau * e0 : 0.0;
     // R(s, j) = A_p(s, j) - sum_{i<c} V(s,i) F(j,i) - V(s,c) F(j,c)
-    xs = __shfl_sync(0xffffffffu, xs, lsel);
+    xs = __shfl_sync(0xffffffffu, xs, gbase | lo_s);
     xs = xs - e1 - x.vr_c * fnew;
-    if (lane == lsel) dst[s] = xs;
-    if (lane == c) cb.f = fnew;
-    if (lane == 0) a.F[j * NB + c] = fnew;
-    if (from_s) {
-      // position p receives the column of position s: every row, and its F row
-      for (int64_t r = lane; r < ld; r += 32)
-        if (r != s) dst[r] = x.olds[r];
-      if (lane < c) a.F[j * NB + lane] = cb.f;
-    }
+    const int64_t j = cb.j;
+    if (cb.ok && l == lo_s) a.W[j * ld + s] = xs;
+    if (cb.ok && l == lc) a.F[j * NB + c] = fnew;
+#pragma unroll
+    for (int t = 0; t < S; ++t)
+      if (l == lc && t == tcs) cb.f[t] = fnew;
     double nr = cb.nr - xs * xs;
     double nx = cb.nx;
-    if (nr < 1e-6 * nx) {
-      nr = recompute_norm(from_s ? x.olds : dst, s, m, ld, c, x.Vs, cb.f, lane);
-      nx = nr;
-      ++x.recomputes;
+    const bool need = cb.ok && nr < 1e-6 * nx;
+    if (__any_sync(0xffffffffu, need)) {  // rare: exact norm from A_p - V F^T (L2-hot re-read)
+      __syncwarp();
+      const double qq = group_recompute<L>(a.W + j * ld, a.F + j * NB, s, m, ld, c, x.Vs, l);
+      if (need) {
+        nr = qq;
+        nx = qq;
+        ++x.recomputes;
+      }
     }
-    if (lane == 0) {
-      a.nrm[j] = nr;
-      a.nrmx[j] = nx;
-      if (from_s) a.piv[j] = x.piv_s;
+    if (cb.ok) {
+      if (l == 0) {
+        a.nrm[j] = nr;
+        a.nrmx[j] = nx;
+      }
+      if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
     }
-    if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
   };
-  Col A, B;
-  int64_t it = next_valid(0);
-  if (it < x.cnt) fetch(A, col_of(it));
-  while (it < x.cnt) {
-    const int64_t it2 = next_valid(it + 1);
-    if (it2 < x.cnt) fetch(B, col_of(it2));
-    process(A, col_of(it));
-    if (it2 >= x.cnt) break;
-    const int64_t it3 = next_valid(it2 + 1);
-    if (it3 < x.cnt) fetch(A, col_of(it3));
-    process(B, col_of(it2));
-    it = it3;
+  const int64_t iters = (n_valid + GPW - 1) / GPW;
+  Slot buf[D];
+#pragma unroll
+  for (int u = 0; u < D - 1; ++u)
+    if (u < iters) fetch(buf[u], u);
+  for (int64_t q0 = 0; q0 < iters; q0 += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int64_t q = q0 + u;
+      if (q >= iters) break;
+      if (q + D - 1 < iters) fetch(buf[(u + D - 1) % D], q + D - 1);
+      process(buf[u]);
+    }
+  }
+  // the column moved into position p by the swap, if this warp owns p
+  if (x.swapped && x.p >= first && (x.p - first) % PW == 0) process_swapped(x, bv, bp);
+  // per-lane best -> warp best (the caller publishes lane 0's)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const long long op = __shfl_xor_sync(0xffffffffu, bp, o);
+    if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
   }
 }
 
@@ -260,9 +370,15 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       __syncthreads();
       return;
     }
+    const double* x = a.W + b * ld;
+    double xl[kRowsPerThread];  // issued before the F row is published
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+      const int64_t r = threadIdx.x + PT * q;
+      xl[q] = (r >= s1 && r < m) ? x[r] : 0.0;
+    }
     if (threadIdx.x < NB) fb[threadIdx.x] = threadIdx.x < c_used ? a.F[b * NB + threadIdx.x] : 0.0;
     __syncthreads();
-    const double* x = a.W + b * ld;
     // rows r = threadIdx.x + PT * q (ld <= 512 <= 2 PT)
     double xr[kRowsPerThread];
     double part = 0.0;
@@ -271,7 +387,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       const int64_t r = threadIdx.x + PT * q;
       xr[q] = 0.0;
       if (r >= s1 && r < m) {
-        double v = x[r];
+        double v = xl[q];
         for (int i = 0; i < c_used; ++i) v = fma(-Vs[i * ld + r], fb[i], v);
         xr[q] = v;
         if (r == s1) sh_alpha = v;
@@ -436,7 +552,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     double bv = -INFINITY;
     long long bp = INT64_MAX;
     {
-      PassCtx x{a, s, c, p, swapped, apply, tau, w_l, vr_l, vr_c, c0, cnt, warp, lane, vv, Vs, olds, Fs, sh_nst,
+      PassCtx x{a, s, c, p, swapped, apply, tau, vr_c, c0, cnt, warp, lane, vv, Vs, olds, Fs, wsh, vrow, sh_nst,
                 sh_state[1], 0ull};
       pass_cols<TC0, NLD>(x, bv, bp);
       my_recomputes += x.recomputes;
