@@ -216,6 +216,7 @@ const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const doub
     c->oz_shift = DBuf<int>((size_t)cols, c->st);
     c->oz_op.planes = c->oz_planes;
     c->oz_op.shift = c->oz_shift;
+    c->oz_op.unsigned_res = K <= kOzakiMaxKUnsigned;  // A: the cheap u8 split (its partner stays s8)
     ozaki_split(K, cols, X, ldx, beta, c->oz_op, c->st);
     c->oz_src = X;
     c->oz_K = K;
@@ -781,6 +782,7 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
     c->oz_op.ld = (m + 15) / 16 * 16;
     c->oz_op.plane_stride = c->oz_op.ld * n;
     c->oz_op.beta = ozaki_beta(m);
+    c->oz_op.unsigned_res = m <= kOzakiMaxKUnsigned;
     c->oz_src = d;
     c->oz_K = m;
     c->oz_cols = n;

@@ -142,7 +142,11 @@ struct OzakiOperand {
   int* shift = nullptr;
   int64_t K = 0, cols = 0, ld = 0, plane_stride = 0;
   int beta = 0;
+  // residues in [0, m) read as u8 (cheaper split) instead of symmetric s8;
+  // allowed on one operand of a product when K <= kOzakiMaxKUnsigned
+  bool unsigned_res = false;
 };
+constexpr int64_t kOzakiMaxKUnsigned = 65536;  // K * 255 * 128 < 2^31
 int ozaki_beta(int64_t K);
 size_t ozaki_plane_bytes(int64_t K, int64_t cols);
 void ozaki_split(int64_t K, int64_t cols, const double* X, int64_t ldx, int beta, OzakiOperand& op, cudaStream_t st);

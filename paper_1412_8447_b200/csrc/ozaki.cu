@@ -147,6 +147,12 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
+// UNS: residues t = x' mod m in [0, m) for the u8 operand: the pair remainder
+// comes out of the FP64 stage already biased positive (u = r + B_P, B_P a
+// multiple of P >= 2^17, folded into the low-word constant) and t = u - m
+// umulhi(u, ceil(2^32/m)) is exact for u < 2^24.  Two integer ops per
+// modulus instead of three FP32 ones plus the rebias.
+template <bool UNS>
 __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
                                                     int64_t ldx, bool vec2, int beta,
                                                     const unsigned long long* __restrict__ cmax,
@@ -196,16 +202,29 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
           const double invP = 1.0 / P;
           const double qg = fma(xp, invP, M52) - M52;
           const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
-          const int lo = __double2loint(r + M52);
-          const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
-          const float rf = fb - M23;                           // r
+          if constexpr (UNS) {
+            const int iP = kmod(2 * g) * kmod(2 * g + 1);
+            const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
+            const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int tt = 2 * g + h;
-            const float m = (float)kmod(tt);
-            const float qq = fmaf(rf, 1.0f / m, M23) - M23;
-            const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
-            byte[tt][q] = (uint32_t)__float_as_int(y);
+            for (int h = 0; h < 2; ++h) {
+              const int tt = 2 * g + h;
+              const uint32_t mm = (uint32_t)kmod(tt);
+              const uint32_t magic = (uint32_t)((0x100000000ull + mm - 1) / mm);
+              byte[tt][q] = u - mm * __umulhi(u, magic);  // u mod m
+            }
+          } else {
+            const int lo = __double2loint(r + M52);
+            const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
+            const float rf = fb - M23;                           // r
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int tt = 2 * g + h;
+              const float m = (float)kmod(tt);
+              const float qq = fmaf(rf, 1.0f / m, M23) - M23;
+              const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
+              byte[tt][q] = (uint32_t)__float_as_int(y);
+            }
           }
         }
       }
@@ -274,7 +293,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 
 __global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
     imma_gemm_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
-                     int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride) {
+                     int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride, uint32_t ab_fmt) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ISTAGES * ISTAGE_BYTES);
@@ -324,8 +343,8 @@ __global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // kind::i8: D s32, A/B signed int8, K-major, N = 256, M = 128
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+      // kind::i8: D s32; A/B u8 (0) or s8 (1) per operand (ab_fmt bits 7, 10)
+      const uint32_t idesc = (2u << 4) | ab_fmt | ((uint32_t)(256 >> 3) << 17) |
                              ((uint32_t)(IBM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ISTAGES;
@@ -483,7 +502,9 @@ void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cuda
   const int gm = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, 8 * num_sms()));
   colmax_kernel<<<gm, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, cmax);
   LRB_CHECK_LAUNCH();
-  split_kernel<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, op.beta, cmax, op.planes, op.ld, op.plane_stride,
+  if (op.unsigned_res && K > kOzakiMaxKUnsigned) throw CudaError("ozaki_split: unsigned residues need K <= 65536");
+  auto kern = op.unsigned_res ? split_kernel<true> : split_kernel<false>;
+  kern<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, op.beta, cmax, op.planes, op.ld, op.plane_stride,
                                             op.shift);
   LRB_CHECK_LAUNCH();
   LRB_CUDA(cudaFreeAsync(cmax, st));
@@ -523,7 +544,11 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
   const int tiles_m = (int)((M + IBM - 1) / IBM), tiles_n = (int)((N + IBN - 1) / IBN);
   // clusters of ICL CTAs along M: pad the M grid (extra CTAs compute zero rows and store nothing)
   dim3 grid((tiles_m + ICL - 1) / ICL * ICL, tiles_n, kOzakiModuli);
-  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, M * N);
+  if (P.unsigned_res && Q.unsigned_res) throw CudaError("ozaki_gemm_tn: at most one unsigned-residue operand");
+  if ((P.unsigned_res || Q.unsigned_res) && P.K > kOzakiMaxKUnsigned)
+    throw CudaError("ozaki_gemm_tn: K too large for an unsigned-residue operand");
+  const uint32_t ab_fmt = (P.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
+  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, M * N, ab_fmt);
   LRB_CHECK_LAUNCH();
   const int64_t total = M * N;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * num_sms()));
