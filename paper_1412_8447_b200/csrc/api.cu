@@ -102,8 +102,6 @@ struct lr_ctx {
   const double* oz_src = nullptr;
   int64_t oz_K = 0, oz_cols = 0, oz_ld = 0;
   lrb::OzakiOperand oz_op;
-  DBuf<int8_t> oz_planes;
-  DBuf<int> oz_shift;
   // auxiliary streams of the host-pointer entry points: host->device upload
   // of A (overlapped with the sketch) and device->host of finished factors
   cudaStream_t up_st = nullptr, down_st = nullptr;
@@ -200,22 +198,18 @@ void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t l
 // that (and in the default mode) the DMMA GEMM runs.
 constexpr int64_t kOzakiMaxK = int64_t(1) << 17;
 
-struct OzakiTmp {
-  DBuf<int8_t> planes;
-  DBuf<int> shift;
-};
-
-// Residue planes of X (K x cols, K-contiguous).  `cacheable` operands (A of
-// the current CUR call) are split once and reused while an OzakiScope is open.
+// Residue planes of X (K x cols, K-contiguous) in grow-only workspace slots
+// (a 68.7 GB plane set re-allocated from the stream pool every call fragments
+// it; persistent slots keep steady-state calls allocation-free).  `cacheable`
+// operands (A of the current CUR call) are split once and reused while an
+// OzakiScope is open; `tmp_slot` 0/1 picks the slots of the other operand.
 const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
-                                  OzakiTmp& tmp, OzakiOperand& out) {
+                                  int tmp_slot, OzakiOperand& out) {
   const int beta = ozaki_beta(K);
   if (cacheable && c->oz_cache_on) {
     if (c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx) return c->oz_op;
-    c->oz_planes = DBuf<int8_t>(ozaki_plane_bytes(K, cols), c->st);
-    c->oz_shift = DBuf<int>((size_t)cols, c->st);
-    c->oz_op.planes = c->oz_planes;
-    c->oz_op.shift = c->oz_shift;
+    c->oz_op.planes = static_cast<int8_t*>(c->ws.get(WsSlot::kOzA, ozaki_plane_bytes(K, cols)));
+    c->oz_op.shift = static_cast<int*>(c->ws.get(WsSlot::kOzAShift, sizeof(int) * (size_t)cols));
     c->oz_op.unsigned_res = K <= kOzakiMaxKUnsigned;  // A: the cheap u8 split (its partner stays s8)
     ozaki_split(K, cols, X, ldx, beta, c->oz_op, c->st);
     c->oz_src = X;
@@ -224,10 +218,9 @@ const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const doub
     c->oz_ld = ldx;
     return c->oz_op;
   }
-  tmp.planes = DBuf<int8_t>(ozaki_plane_bytes(K, cols), c->st);
-  tmp.shift = DBuf<int>((size_t)cols, c->st);
-  out.planes = tmp.planes;
-  out.shift = tmp.shift;
+  out.planes = static_cast<int8_t*>(c->ws.get(tmp_slot ? WsSlot::kOzQ : WsSlot::kOzP, ozaki_plane_bytes(K, cols)));
+  out.shift = static_cast<int*>(c->ws.get(tmp_slot ? WsSlot::kOzQShift : WsSlot::kOzPShift, sizeof(int) * (size_t)cols));
+  out.unsigned_res = false;
   ozaki_split(K, cols, X, ldx, beta, out, c->st);
   return out;
 }
@@ -239,10 +232,9 @@ void gemm_a(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t
     gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
     return;
   }
-  OzakiTmp tp, tq;
   OzakiOperand op, oq;
-  const OzakiOperand& Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, tp, op);
-  const OzakiOperand& Qo = ozaki_operand(c, K, N, Q, ldq, a_side == 1, tq, oq);
+  const OzakiOperand& Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, 0, op);
+  const OzakiOperand& Qo = ozaki_operand(c, K, N, Q, ldq, a_side == 1, 1, oq);
   mark(c, "ozaki_split");
   ozaki_gemm_tn(c->ws, Po, Qo, M, N, out, ldo, 1.0, 0.0, c->st);
 }
@@ -253,9 +245,7 @@ struct OzakiScope {
   explicit OzakiScope(lr_ctx* cc) : c(cc) { c->oz_cache_on = true; }
   ~OzakiScope() {
     c->oz_cache_on = false;
-    c->oz_src = nullptr;
-    c->oz_planes.reset();
-    c->oz_shift.reset();
+    c->oz_src = nullptr;  // the planes stay allocated in the workspace for the next call
   }
 };
 
@@ -768,15 +758,12 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
   DBuf<double> omt((size_t)m * even(ell), c->st);
   gaussian_matrix(ell, m, seed, omt, m, true, c->st);
   const bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
-  OzakiTmp tp;
   OzakiOperand om;
   if (oz) {
-    ozaki_operand(c, m, ell, omt, m, false, tp, om);
+    ozaki_operand(c, m, ell, omt, m, false, 0, om);
     // the cached operand of A, filled chunk by chunk
-    c->oz_planes = DBuf<int8_t>(ozaki_plane_bytes(m, n), c->st);
-    c->oz_shift = DBuf<int>((size_t)n, c->st);
-    c->oz_op.planes = c->oz_planes;
-    c->oz_op.shift = c->oz_shift;
+    c->oz_op.planes = static_cast<int8_t*>(c->ws.get(WsSlot::kOzA, ozaki_plane_bytes(m, n)));
+    c->oz_op.shift = static_cast<int*>(c->ws.get(WsSlot::kOzAShift, sizeof(int) * (size_t)n));
     c->oz_op.K = m;
     c->oz_op.cols = n;
     c->oz_op.ld = (m + 15) / 16 * 16;

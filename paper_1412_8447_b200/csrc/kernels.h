@@ -33,6 +33,12 @@ enum class WsSlot : int {
   kPartials,
   kHostCopyA,
   kHostCopyB,
+  kOzA,        // Ozaki residue planes of the input matrix (kept across calls: no pool churn)
+  kOzAShift,
+  kOzP,        // residue planes of the other operand(s) of a contraction
+  kOzPShift,
+  kOzQ,
+  kOzQShift,
   kCount
 };
 
