@@ -106,17 +106,17 @@ def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None, co
     col_range=(lo, width) builds only the column block A(:, lo:lo+width)."""
     import torch
 
-    from .lowrank import default_context, empty_colmajor
+    from .lowrank import default_context, empty_colmajor, on_torch_stream
 
     ctx = default_context()
     lib = ctx.lib
 
     def gauss(rows, cols, seed):
         g = empty_colmajor(rows, cols, device)
-        rc = lib.lr_gaussian_matrix_d(ctx.h, rows, cols, seed, g.data_ptr(), rows)
+        with on_torch_stream(ctx):  # g may reuse memory torch's stream is still reading
+            rc = lib.lr_gaussian_matrix_d(ctx.h, rows, cols, seed, g.data_ptr(), rows)
         if rc != 0:
             raise RuntimeError(lib.lr_last_error().decode())
-        ctx.synchronize()
         return g
 
     def haar(rows, cols, seed):

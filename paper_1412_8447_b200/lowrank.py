@@ -10,6 +10,7 @@ tensors; they are what bench.py times.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 from typing import Optional
@@ -229,6 +230,7 @@ class Context:
         _raise(self.lib.lr_ctx_create(ctypes.byref(h), int(device)))
         self.h = h
         self.device = device
+        self._stream = None  # None: the context's own stream
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -242,7 +244,13 @@ class Context:
             pass
 
     def set_stream(self, stream_handle: int) -> None:
+        """Run subsequent device calls on this cudaStream_t (0 = the legacy default stream)."""
         _raise(self.lib.lr_ctx_set_stream(self.h, ctypes.c_void_p(stream_handle)))
+        self._stream = stream_handle
+
+    def use_own_stream(self) -> None:
+        _raise(self.lib.lr_ctx_use_own_stream(self.h))
+        self._stream = None
 
     GEMM_DMMA = 0
     GEMM_OZAKI_INT8 = 1
@@ -280,6 +288,23 @@ class Context:
 
 
 _default: Optional[Context] = None
+
+
+@contextlib.contextmanager
+def on_torch_stream(c: "Context"):
+    """Device entry points called on torch tensors run in torch's current
+    stream order (inputs written and outputs allocated by torch are then
+    ordered with the library's kernels), unless the context was bound to a
+    stream explicitly with set_stream."""
+    if c._stream is not None:
+        yield
+        return
+    import torch
+    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    try:
+        yield
+    finally:
+        c.use_own_stream()
 
 
 def default_context() -> Context:
@@ -634,11 +659,12 @@ def randomized_cur_device(a, k: int, cfg: Optional[SketchConfig] = None, strateg
             "col_coeff": empty_colmajor(k, max(n - k, 1), dev), "row_coeff": empty_colmajor(k, max(m - k, 1), dev),
             "skeleton": empty_colmajor(k, k, dev),
         }
-    _raise(c.lib.lr_randomized_cur_d(
-        c.h, m, n, _dptr(a), lda, k, (cfg or SketchConfig())._c(), (strategy or SolveStrategy.automatic())._c(),
-        float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]), _dptr(out["row_pivots"]), _dptr(out["c"]),
-        _dptr(out["u"]), _dptr(out["r"]), _dptr(out["col_coeff"]), _dptr(out["row_coeff"]),
-        _dptr(out["skeleton"])))
+    with on_torch_stream(c):
+        _raise(c.lib.lr_randomized_cur_d(
+            c.h, m, n, _dptr(a), lda, k, (cfg or SketchConfig())._c(), (strategy or SolveStrategy.automatic())._c(),
+            float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]), _dptr(out["row_pivots"]), _dptr(out["c"]),
+            _dptr(out["u"]), _dptr(out["r"]), _dptr(out["col_coeff"]), _dptr(out["row_coeff"]),
+            _dptr(out["skeleton"])))
     return out
 
 
@@ -647,8 +673,9 @@ def cur_error_fro_device(a, cur: dict, ctx: Optional[Context] = None):
     m, n = a.shape
     k = cur["u"].shape[0]
     res = np.empty(2)
-    _raise(c.lib.lr_cur_error_fro_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(cur["c"]), _dptr(cur["u"]),
-                                    _dptr(cur["r"]), _ptr(res)))
+    with on_torch_stream(c):
+        _raise(c.lib.lr_cur_error_fro_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(cur["c"]), _dptr(cur["u"]),
+                                        _dptr(cur["r"]), _ptr(res)))
     return float(res[0]), float(res[1])
 
 
@@ -675,12 +702,13 @@ def randomized_cur_csr_device(row_ptr, col_idx, val, shape, k: int, cfg: Optiona
         "col_coeff": empty_colmajor(k, max(n - k, 1), dev), "row_coeff": empty_colmajor(k, max(m - k, 1), dev),
         "skeleton": empty_colmajor(k, k, dev),
     }
-    _raise(c.lib.lr_randomized_cur_csr_d(
-        c.h, m, n, nnz, _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, (cfg or SketchConfig())._c(),
-        (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]),
-        _dptr(out["row_pivots"]), _dptr(out["u"]), _dptr(out["c_col_ptr"]), _dptr(out["c_row_idx"]),
-        _dptr(out["c_val"]), _dptr(out["r_row_ptr"]), _dptr(out["r_col_idx"]), _dptr(out["r_val"]),
-        _dptr(out["col_coeff"]), _dptr(out["row_coeff"]), _dptr(out["skeleton"])))
+    with on_torch_stream(c):
+        _raise(c.lib.lr_randomized_cur_csr_d(
+            c.h, m, n, nnz, _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, (cfg or SketchConfig())._c(),
+            (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]),
+            _dptr(out["row_pivots"]), _dptr(out["u"]), _dptr(out["c_col_ptr"]), _dptr(out["c_row_idx"]),
+            _dptr(out["c_val"]), _dptr(out["r_row_ptr"]), _dptr(out["r_col_idx"]), _dptr(out["r_val"]),
+            _dptr(out["col_coeff"]), _dptr(out["row_coeff"]), _dptr(out["skeleton"])))
     out["shape"] = (m, n)
     return out
 
@@ -690,8 +718,9 @@ def cur_error_fro_csr_device(row_ptr, col_idx, val, shape, cur: dict, ctx: Optio
     m, n = shape
     k = cur["u"].shape[0]
     res = np.empty(2)
-    _raise(c.lib.lr_cur_error_fro_csr_d(
-        c.h, m, n, int(val.numel()), _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, _dptr(cur["c_col_ptr"]),
-        _dptr(cur["c_row_idx"]), _dptr(cur["c_val"]), _dptr(cur["u"]), _dptr(cur["r_row_ptr"]),
-        _dptr(cur["r_col_idx"]), _dptr(cur["r_val"]), _ptr(res)))
+    with on_torch_stream(c):
+        _raise(c.lib.lr_cur_error_fro_csr_d(
+            c.h, m, n, int(val.numel()), _dptr(row_ptr), _dptr(col_idx), _dptr(val), k, _dptr(cur["c_col_ptr"]),
+            _dptr(cur["c_row_idx"]), _dptr(cur["c_val"]), _dptr(cur["u"]), _dptr(cur["r_row_ptr"]),
+            _dptr(cur["r_col_idx"]), _dptr(cur["r_val"]), _ptr(res)))
     return float(res[0]), float(res[1])

@@ -35,6 +35,7 @@ def _gemm(lr, ctx, P, Q):
     Pc = lr.empty_colmajor(K, M, "cuda"); Pc.copy_(torch.as_tensor(P, device="cuda"))
     Qc = lr.empty_colmajor(K, N, "cuda"); Qc.copy_(torch.as_tensor(Q, device="cuda"))
     out = lr.empty_colmajor(M, N, "cuda")
+    torch.cuda.synchronize()  # inputs copied on torch's stream
     rc = ctx.lib.lr_gemm_tn_d(ctx.h, M, N, K, Pc.data_ptr(), Pc.stride(1), Qc.data_ptr(), Qc.stride(1),
                               out.data_ptr(), out.stride(1))
     assert rc == 0, ctx.lib.lr_last_error()

@@ -73,6 +73,7 @@ def test_gemm_kernel_vs_numpy(lr):
         Qc = lr.empty_colmajor(K, N, "cuda"); Qc.copy_(Q)
         out = lr.empty_colmajor(M, N, "cuda")
         ctx = lr.default_context()
+        torch.cuda.synchronize()  # inputs copied on torch's stream
         rc = ctx.lib.lr_gemm_tn_d(ctx.h, M, N, K, Pc.data_ptr(), Pc.stride(1), Qc.data_ptr(), Qc.stride(1),
                                   out.data_ptr(), out.stride(1))
         assert rc == 0, ctx.lib.lr_last_error()
