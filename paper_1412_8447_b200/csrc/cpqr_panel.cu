@@ -28,6 +28,9 @@
 // the CTA's best column's reflector for the next step -> one grid barrier),
 // then panel_update_kernel for the block update.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -43,7 +46,7 @@ constexpr int CH = 8;        // 64-row chunks held in registers: ld <= 512
 constexpr int PT = 256;      // threads per CTA (8 warps, one CTA per SM; up to 255 registers)
 constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
 constexpr int PW = PT / 32;
-constexpr int kMaxG = 512;
+constexpr int kMaxG = 256;       // per-CTA partials read by one warp (8 per lane)
 constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
 constexpr int kSmemMax = (NB + 3) * 64 * CH * (int)sizeof(double);
 
@@ -63,7 +66,33 @@ struct PanelArgs {
   double* Vg;                // [ld][NB] row-major copy of the panel's V (GEMM operand)
   int* flags;
   unsigned long long* recomputes;
+  unsigned long long* trace;  // optional per-phase ns of CTA 0 (LRB_CPQR_TRACE), 8 slots
+  unsigned int* bar;          // grid barrier counter (zeroed before each launch)
 };
+
+// Grid barrier for the co-resident (cooperative) grid: one release atomic per
+// CTA on a monotonic counter and an acquire spin without back-off.  (The
+// cooperative-groups grid.sync measured ~9 us per barrier here; this one is
+// the latency of an L2 atomic round trip plus the last arrival.)
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& target) {
+  target += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // release: the CTA's writes (ordered before this thread by the barrier) become visible gpu-wide
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
@@ -129,7 +158,7 @@ __device__ __noinline__ double recompute_norm(const double* src, int64_t s, int6
 // group version of the recompute (L lanes per column): rows s+1..m-1 of the
 // column re-read from W (L2-hot), F(j, 0:c] from global (written by the group)
 template <int L>
-__device__ __noinline__ double group_recompute(const double* col, const double* Fj, int64_t s, int64_t m,
+__device__ __forceinline__ double group_recompute(const double* col, const double* Fj, int64_t s, int64_t m,
                                                int64_t ld, int c, const double* Vs, int l) {
   double q = 0.0;
   for (int64_t r = s + 1 + l; r < m; r += L) {
@@ -197,7 +226,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
   constexpr int KP = SPEC ? 32 * NA / L : CH;  // row pairs per lane
   constexpr int GPW = 32 / L;
   constexpr int S = NB / L;
-  constexpr int D = S == 1 ? 4 : (S == 2 ? 3 : 2);  // warp-iterations in flight
+  constexpr int D = (S == 1 && NA <= 4) ? 4 : (S <= 2 ? 3 : 2);  // warp-iterations in flight
   const PanelArgs& a = x.a;
   const int64_t s = x.s, ld = a.ld, m = a.m;
   const int lane = x.lane, c = x.c;
@@ -219,33 +248,39 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     vl[t] = x.vrow[l * S + t];
   }
   const int lc = c / S, tcs = c % S;  // owner lane / slot of F(j, c)
-  // the warp's columns c0 + warp + PW*it; valid ones (> s) are a contiguous run
-  const int64_t first = x.c0 + x.warp;
-  int64_t it_min = s >= first ? (s - first) / PW + 1 : 0;
-  if (it_min > x.cnt) it_min = x.cnt;
-  const int64_t n_valid = x.cnt - it_min;
-  auto col_at = [&](int64_t q) { return first + PW * ((s & 1) ? (x.cnt - 1 - q) : (it_min + q)); };
+  // the warp's columns c0 + warp + PW*it; valid ones (> s) are a contiguous
+  // run, visited as j = jstart + dj * q (32-bit indices, n < 2^31)
+  const int first = (int)(x.c0 + x.warp);
+  const int cnt = (int)x.cnt;
+  int it_min = s >= first ? (int)((s - first) / PW) + 1 : 0;
+  if (it_min > cnt) it_min = cnt;
+  const int n_valid = cnt - it_min;
+  const int jstart = (s & 1) ? first + PW * (cnt - 1) : first + PW * it_min;
+  const int dj = (s & 1) ? -PW : PW;
+  const int jp = x.swapped ? (int)x.p : -1;
+  const double* Wb = a.W + base + 2 * l;
+  const double* Fb = a.F + l * S;
   struct Slot {
     double c[CH][2];
     double f[S];
     double nr, nx;
-    int64_t j;
+    int j;
     bool ok;
   };
-  auto fetch = [&](Slot& cb, int64_t qi) {
-    const int64_t q = qi * GPW + g;
+  auto fetch = [&](Slot& cb, int qi) {
+    const int q = qi * GPW + g;
     cb.ok = q < n_valid;
-    cb.j = cb.ok ? col_at(q) : x.c0;  // any owned column for the (unused) loads
-    if (x.swapped && cb.j == x.p) cb.ok = false;
-    const double* src = a.W + cb.j * ld + base;
+    cb.j = jstart + dj * (cb.ok ? q : 0);  // an owned column for the (unused) loads
+    if (cb.j == jp) cb.ok = false;
+    const double* src = Wb + (size_t)cb.j * (size_t)ld;
 #pragma unroll
     for (int k = 0; k < KP; ++k)
       if (active(k)) {
-        const double2 xx = __ldcs(reinterpret_cast<const double2*>(src + 2 * (l + L * k)));
+        const double2 xx = __ldcs(reinterpret_cast<const double2*>(src + 2 * L * k));
         cb.c[k][0] = xx.x;
         cb.c[k][1] = xx.y;
       }
-    const double* fr = a.F + cb.j * NB + l * S;
+    const double* fr = Fb + (size_t)cb.j * NB;
 #pragma unroll
     for (int t = 0; t < S; ++t) cb.f[t] = (l * S + t < c) ? fr[t] : 0.0;
     cb.nr = a.nrm[cb.j];
@@ -277,9 +312,9 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     // R(s, j) = A_p(s, j) - sum_{i<c} V(s,i) F(j,i) - V(s,c) F(j,c)
     xs = __shfl_sync(0xffffffffu, xs, gbase | lo_s);
     xs = xs - e1 - x.vr_c * fnew;
-    const int64_t j = cb.j;
-    if (cb.ok && l == lo_s) a.W[j * ld + s] = xs;
-    if (cb.ok && l == lc) a.F[j * NB + c] = fnew;
+    const int j = cb.j;
+    if (cb.ok && l == lo_s) a.W[(size_t)j * ld + s] = xs;
+    if (cb.ok && l == lc) a.F[(size_t)j * NB + c] = fnew;
 #pragma unroll
     for (int t = 0; t < S; ++t)
       if (l == lc && t == tcs) cb.f[t] = fnew;
@@ -288,7 +323,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     const bool need = cb.ok && nr < 1e-6 * nx;
     if (__any_sync(0xffffffffu, need)) {  // rare: exact norm from A_p - V F^T (L2-hot re-read)
       __syncwarp();
-      const double qq = group_recompute<L>(a.W + j * ld, a.F + j * NB, s, m, ld, c, x.Vs, l);
+      const double qq = group_recompute<L>(a.W + (size_t)j * ld, a.F + (size_t)j * NB, s, m, ld, c, x.Vs, l);
       if (need) {
         nr = qq;
         nx = qq;
@@ -303,15 +338,15 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
       if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
     }
   };
-  const int64_t iters = (n_valid + GPW - 1) / GPW;
+  const int iters = (n_valid + GPW - 1) / GPW;
   Slot buf[D];
 #pragma unroll
   for (int u = 0; u < D - 1; ++u)
     if (u < iters) fetch(buf[u], u);
-  for (int64_t q0 = 0; q0 < iters; q0 += D) {
+  for (int q0 = 0; q0 < iters; q0 += D) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
-      const int64_t q = q0 + u;
+      const int q = q0 + u;
       if (q >= iters) break;
       if (q + D - 1 < iters) fetch(buf[(u + D - 1) % D], q + D - 1);
       process(buf[u]);
@@ -332,7 +367,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
 // never crosses a chunk) and ld / 64, or -1 for the generic runtime version
 template <int TC0, int NLD>
 __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned int bar_target = 0;
   extern __shared__ double dyn[];
   __shared__ double sh_red[PW];
   __shared__ double sh_bv[PW];
@@ -472,11 +507,20 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     }
     __syncthreads();
     stage(a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0], 0, false);
-    grid.sync();
+    grid_barrier(a.bar, bar_target);
     if (__ldcg(a.flags) != 0) return;
   }
 
   // ------------------------------------------------------------ steps of this panel
+  const bool tr = a.trace != nullptr && threadIdx.x == 0;
+  unsigned long long tprev = tr ? gtimer() : 0;
+  auto stamp = [&](int slot) {
+    if (tr) {
+      const unsigned long long t = gtimer();
+      a.trace[cta * 8 + slot] += t - tprev;
+      tprev = t;
+    }
+  };
   for (int64_t s = a.t0; s < a.t1; ++s) {
     const int c = (int)(s - a.t0);  // panel column of this step's reflector
     const int par = (int)(s & 1), nxt = par ^ 1;
@@ -521,10 +565,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       }
       if (threadIdx.x < kHdr) sh_hdr[threadIdx.x] = __ldcg(cd + threadIdx.x);
       if (threadIdx.x < NB) wsh[threadIdx.x] = threadIdx.x < c ? __ldcg(cd + kHdr + ld + threadIdx.x) : 0.0;
+      // V(s, 0:c) of the earlier reflectors (V(s, c) = 1 when applied: vr_c below)
+      if (threadIdx.x < NB) vrow[threadIdx.x] = threadIdx.x < c ? Vs[threadIdx.x * ld + s] : 0.0;
     }
-    __syncthreads();
-    if (threadIdx.x < NB) vrow[threadIdx.x] = threadIdx.x <= c ? Vs[threadIdx.x * ld + s] : 0.0;
-    // (3) swap bookkeeping by the owner of position p
+    // (3) swap bookkeeping by the owner of position p: its loads are issued
+    // together with the candidate's (one L2 round trip, one barrier)
     const bool owner = (p >= c0 && p < c1);
     const bool swapped = owner && p != s;
     if (swapped) {
@@ -541,12 +586,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       }
     }
     __syncthreads();
+    stamp(1);  // argmax + candidate / swap loads
     const double tau = sh_hdr[2];
     const bool apply = sh_hdr[3] != 0.0 && tau != 0.0;
     if (cta == 0 && threadIdx.x == 0) a.tau[s] = tau;
-    const double w_l = wsh[lane];
-    const double vr_l = vrow[lane];
-    const double vr_c = vrow[c];  // V(s, c): 1 when applied
+    const double vr_c = apply ? 1.0 : 0.0;  // V(s, c)
 
     // (4) fused pass over owned positions j in (s, n): read-only except row s and F(j, c)
     double bv = -INFINITY;
@@ -558,6 +602,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       my_recomputes += x.recomputes;
     }
 
+    stamp(2);  // pass
     // (5) CTA argmax, pivot column write-back, V row-major copy for the panel GEMM
     if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
     __syncthreads();
@@ -586,9 +631,12 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     if (cta == 0)
       for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
     __syncthreads();
+    stamp(3);  // CTA argmax, pivot write-back
     if (s + 1 < a.k)
       stage(a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0], c + 1, s + 1 < a.t1);
-    grid.sync();
+    stamp(4);  // stage
+    grid_barrier(a.bar, bar_target);
+    stamp(5);  // grid barrier
   }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
 }
@@ -705,13 +753,21 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   a.F = a.cand + 2 * (size_t)G * cand_sz;
   a.Vg = a.F + (size_t)n * NB;
   a.ppos = reinterpret_cast<long long*>(a.Vg + (size_t)ld * NB);
+  a.bar = reinterpret_cast<unsigned int*>(a.ppos + 2 * (size_t)G);
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
+  static const bool trace = getenv("LRB_CPQR_TRACE") != nullptr;
+  a.trace = nullptr;
+  if (trace) {
+    LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 8 * sizeof(unsigned long long) * G, st));
+    LRB_CUDA(cudaMemsetAsync(a.trace, 0, 8 * sizeof(unsigned long long) * G, st));
+  }
   for (int64_t t0 = 0; t0 < k; t0 += NB) {
     const int64_t t1 = std::min<int64_t>(k, t0 + NB);
     a.t0 = t0;
     a.t1 = t1;
     a.init = t0 == 0 ? 1 : 0;
+    LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
     void* params[] = {&a};
     LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
@@ -722,6 +778,25 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       panel_update_kernel<<<ug, UT, 0, st>>>(W, ld, t1, m, t1, n, a.Vg, a.F, (int)(t1 - t0));
       LRB_CHECK_LAUNCH();
     }
+  }
+  if (trace) {
+    std::vector<unsigned long long> h(8 * (size_t)G);
+    LRB_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    LRB_CUDA(cudaStreamSynchronize(st));
+    const char* names[6] = {"", "loads", "pass", "argmax+wb", "stage", "barrier"};
+    for (int slot = 1; slot <= 5; ++slot) {
+      double mn = 1e30, mx = 0, sum = 0;
+      int arg = 0;
+      for (int g = 0; g < G; ++g) {
+        const double v = h[g * 8 + slot] / 1e3 / k;
+        mn = std::min(mn, v);
+        sum += v;
+        if (v > mx) { mx = v; arg = g; }
+      }
+      fprintf(stderr, "cpqr_panel trace %-10s us/step: min %.2f mean %.2f max %.2f (cta %d)\n", names[slot], mn,
+              sum / G, mx, arg);
+    }
+    cudaFreeAsync(a.trace, st);
   }
 }
 
