@@ -28,8 +28,13 @@ struct LrError {
 };
 [[noreturn]] void fail(int code, const std::string& msg, int64_t index = -1) { throw LrError{code, msg, index}; }
 
+void arena_close();
+
 template <typename F>
 int guard(F&& f) {
+  struct Close {
+    ~Close() { arena_close(); }
+  } close_arena;
   try {
     f();
     return LR_OK;
@@ -51,28 +56,55 @@ int guard(F&& f) {
 
 inline int64_t even(int64_t x) { return x + (x & 1); }
 
-// stream-ordered device buffer from the (caching) default memory pool
+// Per-context call arena: every DBuf of a public call on the context's stream
+// is a bump allocation in one grow-only device block, reset at the next call
+// (stream order makes the reuse safe; switching streams synchronises the old
+// one).  Re-allocating multi-GB temporaries from the stream-ordered pool every
+// call fragmented it and made some calls map fresh memory (~100 ms).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0, overflow = 0, want = 0;
+  cudaStream_t st = nullptr;
+  bool active = false;
+};
+thread_local Arena* tl_arena = nullptr;
+
+// stream-ordered device buffer: from the call arena, else the default pool
 template <typename T>
 struct DBuf {
   T* p = nullptr;
   cudaStream_t st = nullptr;
+  bool from_arena = false;
   DBuf() = default;
   DBuf(size_t n, cudaStream_t s) : st(s) {
-    LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(n, 1), s));
+    const size_t bytes = sizeof(T) * std::max<size_t>(n, 1);
+    Arena* ar = tl_arena;
+    if (ar && ar->active && s == ar->st) {
+      const size_t off = (ar->used + 255) & ~size_t(255);
+      if (off + bytes <= ar->cap) {
+        p = reinterpret_cast<T*>(ar->base + off);
+        ar->used = off + bytes;
+        from_arena = true;
+        return;
+      }
+      ar->overflow += bytes + 256;  // grow the arena before the next call
+    }
+    LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s));
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DBuf(DBuf&& o) noexcept : p(o.p), st(o.st), from_arena(o.from_arena) { o.p = nullptr; }
   DBuf& operator=(DBuf&& o) noexcept {
     reset();
     p = o.p;
     st = o.st;
+    from_arena = o.from_arena;
     o.p = nullptr;
     return *this;
   }
   ~DBuf() { reset(); }
   void reset() {
-    if (p) cudaFreeAsync(p, st);
+    if (p && !from_arena) cudaFreeAsync(p, st);
     p = nullptr;
   }
   operator T*() const { return p; }
@@ -105,6 +137,7 @@ struct lr_ctx {
   // auxiliary streams of the host-pointer entry points: host->device upload
   // of A (overlapped with the sketch) and device->host of finished factors
   cudaStream_t up_st = nullptr, down_st = nullptr;
+  Arena arena;
 };
 
 namespace {
@@ -863,7 +896,38 @@ struct Downloads {
 lr_ctx* checked(lr_ctx* c) {
   if (!c) fail(LR_EINVAL, "null lr_ctx");
   LRB_CUDA(cudaSetDevice(c->device));
+  // open the call arena (grown to the previous calls' high-water mark)
+  Arena& ar = c->arena;
+  if (!ar.active) {
+    if (ar.want > ar.cap) {
+      LRB_CUDA(cudaDeviceSynchronize());
+      if (ar.base) LRB_CUDA(cudaFree(ar.base));
+      ar.base = nullptr;
+      ar.cap = 0;
+      const size_t bytes = (ar.want + ar.want / 8 + (64u << 20)) & ~size_t((2u << 20) - 1);
+      if (cudaMalloc(reinterpret_cast<void**>(&ar.base), bytes) == cudaSuccess) {
+        ar.cap = bytes;
+      } else {
+        cudaGetLastError();  // no room: this call allocates from the pool
+        ar.base = nullptr;
+        ar.want = 0;
+      }
+    }
+    ar.used = 0;
+    ar.overflow = 0;
+    ar.st = c->st;
+    ar.active = true;
+    tl_arena = &ar;
+  }
   return c;
+}
+
+void arena_close() {
+  Arena* ar = tl_arena;
+  if (!ar) return;
+  ar->want = std::max(ar->want, ar->used + ar->overflow);
+  ar->active = false;
+  tl_arena = nullptr;
 }
 
 }  // namespace
@@ -907,7 +971,9 @@ int lr_ctx_destroy(lr_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
+    cudaDeviceSynchronize();
     c->ws.release_all();
+    if (c->arena.base) cudaFree(c->arena.base);
     cudaFreeHost(c->h_flags);
     cudaFreeHost(c->h_scal);
     cudaFreeHost(c->h_ll);
@@ -920,7 +986,12 @@ int lr_ctx_destroy(lr_ctx* c) {
 
 int lr_ctx_set_stream(lr_ctx* c, void* s) {
   // NULL is the CUDA legacy default stream (what torch reports for its default stream)
-  return guard([&] { checked(c)->st = s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy; });
+  return guard([&] {
+    const cudaStream_t ns = s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy;
+    // the call arena is reused in stream order: finish the old stream's work first
+    if (checked(c)->st != ns) LRB_CUDA(cudaStreamSynchronize(c->st));
+    c->st = ns;
+  });
 }
 int lr_ctx_set_gemm_mode(lr_ctx* c, int mode) {
   return guard([&] {
@@ -931,7 +1002,10 @@ int lr_ctx_set_gemm_mode(lr_ctx* c, int mode) {
 }
 int lr_ctx_get_gemm_mode(lr_ctx* c) { return c ? c->gemm_mode : -1; }
 int lr_ctx_use_own_stream(lr_ctx* c) {
-  return guard([&] { checked(c)->st = c->own; });
+  return guard([&] {
+    if (checked(c)->st != c->own) LRB_CUDA(cudaStreamSynchronize(c->st));
+    c->st = c->own;
+  });
 }
 int lr_ctx_get_stats(lr_ctx* c, lr_stats* out) {
   return guard([&] { *out = checked(c)->stats; });

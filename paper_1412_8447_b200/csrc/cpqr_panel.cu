@@ -698,34 +698,37 @@ bool cpqr_panel_supported(int64_t m, int64_t ld, bool padded) {
     const char* e = getenv("LRB_CPQR_PANEL");
     return e && atoi(e) == 0;
   }();
-  return !off && padded && ld % 64 == 0 && ld <= 64 * CH && m <= ld;
+  // specialised widths only (the generic-width panel kernel is slower than cpqr.cu's)
+  return !off && padded && (ld == 256 || ld == 320 || ld == 512) && m <= ld;
 }
 
 void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                 double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)(NB + 3) * ld;
   using KernT = void (*)(PanelArgs);
-  const bool spec = ld == 64 * CH;
+  // specialised kernels per (ld / 64, first active chunk); ld in {256, 320, 512}
+  static const KernT k4[] = {cpqr_panel_kernel<0, 4>, cpqr_panel_kernel<1, 4>, cpqr_panel_kernel<2, 4>,
+                             cpqr_panel_kernel<3, 4>};
+  static const KernT k5[] = {cpqr_panel_kernel<0, 5>, cpqr_panel_kernel<1, 5>, cpqr_panel_kernel<2, 5>,
+                             cpqr_panel_kernel<3, 5>, cpqr_panel_kernel<4, 5>};
+  static const KernT k8[] = {cpqr_panel_kernel<0, 8>, cpqr_panel_kernel<1, 8>, cpqr_panel_kernel<2, 8>,
+                             cpqr_panel_kernel<3, 8>, cpqr_panel_kernel<4, 8>, cpqr_panel_kernel<5, 8>,
+                             cpqr_panel_kernel<6, 8>, cpqr_panel_kernel<7, 8>};
+  const int nld = (int)(ld / 64);
   auto kern_for = [&](int64_t t0) -> KernT {
-    if (!spec) return cpqr_panel_kernel<-1, -1>;
-    switch (t0 / 64) {
-      case 0: return cpqr_panel_kernel<0, CH>;
-      case 1: return cpqr_panel_kernel<1, CH>;
-      case 2: return cpqr_panel_kernel<2, CH>;
-      case 3: return cpqr_panel_kernel<3, CH>;
-      case 4: return cpqr_panel_kernel<4, CH>;
-      case 5: return cpqr_panel_kernel<5, CH>;
-      case 6: return cpqr_panel_kernel<6, CH>;
-      default: return cpqr_panel_kernel<7, CH>;
-    }
+    const int tc = (int)(t0 / 64);
+    if (nld == 8) return k8[tc];
+    if (nld == 5) return k5[tc];
+    if (nld == 4) return k4[tc];
+    return cpqr_panel_kernel<-1, -1>;
   };
   static bool attr = false;
   if (!attr) {
-    const KernT all[] = {cpqr_panel_kernel<-1, -1>, cpqr_panel_kernel<0, CH>, cpqr_panel_kernel<1, CH>,
-                         cpqr_panel_kernel<2, CH>,  cpqr_panel_kernel<3, CH>, cpqr_panel_kernel<4, CH>,
-                         cpqr_panel_kernel<5, CH>,  cpqr_panel_kernel<6, CH>, cpqr_panel_kernel<7, CH>};
-    for (KernT kf : all)
-      LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+    for (KernT kf : k4) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+    for (KernT kf : k5) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+    for (KernT kf : k8) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+    LRB_CUDA(cudaFuncSetAttribute(cpqr_panel_kernel<-1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemMax));
     attr = true;
   }
   int per_sm = 0;

@@ -115,7 +115,8 @@ def test_cpqr_rank_deficient_and_det(lr, oracle):
     assert np.prod(np.abs(np.diag(q.s))) == pytest.approx(abs(np.linalg.det(a)), rel=1e-8)
 
 
-@pytest.mark.parametrize("shape,k", [((510, 3000), 510), ((500, 4096), 500), ((1000, 800), 50),
+@pytest.mark.parametrize("shape,k", [((510, 3000), 510), ((500, 4096), 500), ((300, 5000), 300), ((310, 2000), 137),
+                                     ((210, 6000), 210), ((256, 1500), 256), ((1000, 800), 50),
                                      ((4000, 300), 100), ((64, 64), 64), ((3, 1000), 3), ((777, 5), 5)])
 def test_cpqr_matches_oracle(lr, oracle, shape, k):
     a = inputs.synthetic_np(inputs.scaled(inputs.CONFIGS["c4"], shape[0], shape[1], width=min(shape), k=k))
