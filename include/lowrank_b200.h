@@ -125,6 +125,11 @@ int lr_sketch_gaussian(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64
                        uint64_t seed, double* y);
 int lr_sketch_gaussian_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
                          uint64_t seed, double* y, int64_t ldy);
+/* sketch.hpp:148-164 sketch_power: y (ell x n, ld ell) = Omega A (A^T A)^q with
+   optional row re-orthonormalisation (svd.hpp:216-235); *rows = final row
+   count (orth_rows drops numerically dependent rows) */
+int lr_sketch_power(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q,
+                    int reorth, uint64_t seed, double* y, int64_t* rows);
 
 /* cpqr.hpp:32-114 cpqr_partial(a, k): q m x k (may be NULL), s k x n, pivots n */
 int lr_cpqr_partial(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q,

@@ -11,7 +11,7 @@
 //   ColumnId / RowId / TwoSidedId / id_*     id.hpp:12-159
 //   CurDecomposition / cur_from_two_sided / cur_id / reconstruct  cur.hpp:9-80
 //   SketchConfig / SampleMatrix / sketch_gaussian / randomized_id /
-//   randomized_cur          sketch.hpp:21-234 (Gaussian, power 0)
+//   randomized_cur          sketch.hpp:21-234 (Gaussian sketch, power q >= 0)
 // Templates accept any Eigen::MatrixBase<Derived> with Scalar = double (the
 // B200 path is FP64; other scalars fail at compile time -- there is no CPU
 // fallback).  Needs <Eigen/Dense> (Eigen 3.4, or oracle/eigen_subset).

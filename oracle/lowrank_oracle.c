@@ -13,6 +13,7 @@
  */
 #include "lowrank_oracle.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -702,6 +703,125 @@ int lro_randomized_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_
   rc = lro_cpqr(ell, n, y, ell, steps, NULL, s, pivots, NULL, stats);
   if (!rc) {
     /* s1 = top k rows (sketch.hpp:213-215) */
+    double* s1 = NEW(double, k * n);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < k; ++i) s1[IDX(i, j, k)] = s[IDX(i, j, steps)];
+    rc = lro_coeff_solve(k, n - k, s1, k, s1 + (size_t)k * k, k, strat, coeff);
+    free(s1);
+  }
+  free(s); free(y);
+  return rc;
+}
+
+/* svd.hpp:216-235.  Eigen's HouseholderQR on y^T with makeHouseholder's
+ * convention (beta = -sign(c0)|x|, tau = (beta - c0)/beta, v = x/(c0 - beta);
+ * no reflection when the tail is exactly zero), then householderQ() applied to
+ * the first r columns of the identity. */
+int lro_orth_rows(int64_t ell, int64_t n, const double* y, int64_t ldy, double* out, int64_t* r_out) {
+  if (ell < 1 || n < 1) return fail(LRO_EINVAL, "orth_rows: matrix must be nonempty");
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < ell; ++i)
+      if (!isfinite(y[IDX(i, j, ldy)])) return fail(LRO_EINVAL, "orth_rows: matrix has non-finite entries");
+  const int64_t rows = n, cols = ell, rmax = n < ell ? n : ell;
+  double* x = NEW(double, rows * cols); /* x = y^T, rows x cols */
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t i = 0; i < rows; ++i) x[IDX(i, j, rows)] = y[IDX(j, i, ldy)];
+  double* tau = NEW(double, rmax);
+  double* diag = NEW(double, rmax);
+  for (int64_t j = 0; j < rmax; ++j) {
+    double* cj = x + (size_t)j * rows;
+    const double c0 = cj[j];
+    double tail = 0.0;
+    for (int64_t i = j + 1; i < rows; ++i) tail += cj[i] * cj[i];
+    double beta, t;
+    if (tail == 0.0) {
+      t = 0.0;
+      beta = c0;
+      for (int64_t i = j + 1; i < rows; ++i) cj[i] = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail);
+      if (c0 >= 0.0) beta = -beta;
+      for (int64_t i = j + 1; i < rows; ++i) cj[i] /= (c0 - beta);
+      t = (beta - c0) / beta;
+    }
+    tau[j] = t;
+    diag[j] = fabs(beta);
+    cj[j] = beta;
+    /* apply H = I - t v v^T (v_j = 1) to the trailing columns */
+    for (int64_t c = j + 1; c < cols; ++c) {
+      double* cc = x + (size_t)c * rows;
+      double w = cc[j];
+      for (int64_t i = j + 1; i < rows; ++i) w += cj[i] * cc[i];
+      w *= t;
+      cc[j] -= w;
+      for (int64_t i = j + 1; i < rows; ++i) cc[i] -= w * cj[i];
+    }
+  }
+  double dmax = 0.0;
+  for (int64_t j = 0; j < rmax; ++j) dmax = diag[j] > dmax ? diag[j] : dmax;
+  const double tol = dmax * DBL_EPSILON * (double)(rows > cols ? rows : cols);
+  int64_t r = rmax;
+  while (r > 0 && diag[r - 1] <= tol) --r;
+  /* thin Q (rows x r) = H_0 ... H_{rmax-1} [I_r; 0] */
+  double* q = NEW(double, rows * (r > 0 ? r : 1));
+  for (int64_t c = 0; c < r; ++c)
+    for (int64_t i = 0; i < rows; ++i) q[IDX(i, c, rows)] = (i == c) ? 1.0 : 0.0;
+  for (int64_t j = rmax - 1; j >= 0; --j) {
+    const double* vj = x + (size_t)j * rows;
+    if (tau[j] == 0.0) continue;
+    for (int64_t c = 0; c < r; ++c) {
+      double* qc = q + (size_t)c * rows;
+      double w = qc[j];
+      for (int64_t i = j + 1; i < rows; ++i) w += vj[i] * qc[i];
+      w *= tau[j];
+      qc[j] -= w;
+      for (int64_t i = j + 1; i < rows; ++i) qc[i] -= w * vj[i];
+    }
+  }
+  for (int64_t c = 0; c < r; ++c)
+    for (int64_t i = 0; i < rows; ++i) out[IDX(c, i, ldy)] = q[IDX(i, c, rows)];
+  *r_out = r;
+  free(q); free(diag); free(tau); free(x);
+  return LRO_OK;
+}
+
+/* sketch.hpp:148-164 */
+int lro_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                     uint64_t seed, double* y, int64_t* rows_out) {
+  if (q < 0) return fail(LRO_EINVAL, "sketch_power: q must be nonnegative");
+  int rc = lro_sketch_gaussian(m, n, a, lda, ell, seed, y);
+  if (rc) return rc;
+  int64_t rows = ell;
+  double* z = NEW(double, ell * m);   /* ell x m, ld ell */
+  double* at = NEW(double, n * m);    /* A^T, n x m */
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i) at[IDX(j, i, n)] = a[IDX(i, j, lda)];
+  for (int round = 0; round < q && !rc; ++round) {
+    if (reorth && (rc = lro_orth_rows(rows, n, y, ell, y, &rows))) break;
+    lro_gemm_nn(rows, m, n, y, ell, at, n, z, ell);  /* z = y A^T */
+    if (reorth && (rc = lro_orth_rows(rows, m, z, ell, z, &rows))) break;
+    lro_gemm_nn(rows, n, m, z, ell, a, lda, y, ell);  /* y = z A */
+  }
+  free(at); free(z);
+  *rows_out = rows;
+  return rc;
+}
+
+int lro_randomized_id_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int oversample,
+                            int q, int reorth, uint64_t seed, lro_solve_strategy strat, int64_t* pivots,
+                            double* coeff, int64_t* stats) {
+  int rc;
+  if ((rc = require_rank_in_range(k, m, n, "randomized_id"))) return rc;
+  const int64_t ell = k + (int64_t)oversample;
+  if (ell < k) return fail(LRO_EINVAL, "build_sample: sample count below target rank");
+  double* y = NEW(double, ell * n);
+  int64_t rows = ell;
+  if ((rc = lro_sketch_power(m, n, a, lda, ell, q, reorth, seed, y, &rows))) { free(y); return rc; }
+  const int64_t steps = rows < n ? rows : n;
+  if (steps < k) { free(y); return fail(LRO_ERUNTIME, "randomized_id: sample rank collapsed below target rank"); }
+  double* s = NEW(double, steps * n);
+  rc = lro_cpqr(rows, n, y, ell, steps, NULL, s, pivots, NULL, stats);
+  if (!rc) {
     double* s1 = NEW(double, k * n);
     for (int64_t j = 0; j < n; ++j)
       for (int64_t i = 0; i < k; ++i) s1[IDX(i, j, k)] = s[IDX(i, j, steps)];

@@ -97,6 +97,19 @@ int lro_randomized_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_
                       int oversample, uint64_t seed, lro_solve_strategy strat,
                       int64_t* pivots, double* coeff, int64_t* stats);
 
+/* svd.hpp:216-235 orth_rows: Householder QR of y^T (n x ell), numerical rank
+ * r (trailing |R_ii| <= max|R_ii| eps max(n, ell) dropped), out = thin Q^T:
+ * r x n (ld ell; rows r..ell-1 untouched); *r_out = r */
+int lro_orth_rows(int64_t ell, int64_t n, const double* y, int64_t ldy, double* out, int64_t* r_out);
+/* sketch.hpp:148-164 sketch_power: y (ell x n, ld ell) = Omega A (A^T A)^q,
+ * optional re-orthonormalisation; *rows_out = the sample's final row count */
+int lro_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                     uint64_t seed, double* y, int64_t* rows_out);
+/* sketch.hpp:200-223 with the Gaussian power sketch (q >= 0) */
+int lro_randomized_id_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int oversample,
+                            int q, int reorth, uint64_t seed, lro_solve_strategy strat, int64_t* pivots,
+                            double* coeff, int64_t* stats);
+
 /* id.hpp:124-134 given col pivots (n) and k: row pivots (m), row coeff
  * k x (m-k), skeleton k x k */
 int lro_tsid_from_column_id(int64_t m, int64_t n, const double* a, int64_t lda,

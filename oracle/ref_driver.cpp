@@ -142,6 +142,32 @@ int lref_randomized_id(int64_t m, int64_t n, const double* a, int64_t lda, int64
   });
 }
 
+// sketch.hpp:148-164 power sketch: y (ell x n, ld ell); *rows = final row count
+int lref_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                      uint64_t seed, double* y, int64_t* rows) {
+  return guard([&] {
+    auto out = sketch_power(from_ptr(m, n, a, lda), ell, q, reorth != 0, seed);
+    *rows = out.y.rows();
+    for (int64_t j = 0; j < out.y.cols(); ++j)
+      for (int64_t i = 0; i < out.y.rows(); ++i) y[i + j * ell] = out.y(i, j);
+  });
+}
+
+// sketch.hpp:200-223 with power iterations
+int lref_randomized_id_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int oversample, int q,
+                             int reorth, uint64_t seed, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    SketchConfig cfg;
+    cfg.oversample = oversample;
+    cfg.seed = seed;
+    cfg.power = q;
+    cfg.reorthonormalize = reorth != 0;
+    auto id = randomized_id(from_ptr(m, n, a, lda), k, cfg);
+    to_idx(id.pivots, pivots);
+    to_ptr(id.coeff, coeff);
+  });
+}
+
 // tsID from a column ID: row pivots, row coeff, skeleton
 int lref_tsid_from_column_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                              const int64_t* col_pivots, const double* col_coeff, int64_t* row_pivots,

@@ -239,13 +239,14 @@ constexpr int64_t kOzakiMaxK = int64_t(1) << 17;
 const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
                                   int tmp_slot, OzakiOperand& out) {
   const int beta = ozaki_beta(K);
-  if (cacheable && c->oz_cache_on) {
-    if (c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx) return c->oz_op;
+  if (cacheable) {  // the input matrix: kOzA slot, reused while an OzakiScope is open
+    if (c->oz_cache_on && c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx)
+      return c->oz_op;
     c->oz_op.planes = static_cast<int8_t*>(c->ws.get(WsSlot::kOzA, ozaki_plane_bytes(K, cols)));
     c->oz_op.shift = static_cast<int*>(c->ws.get(WsSlot::kOzAShift, sizeof(int) * (size_t)cols));
     c->oz_op.unsigned_res = K <= kOzakiMaxKUnsigned;  // A: the cheap u8 split (its partner stays s8)
     ozaki_split(K, cols, X, ldx, beta, c->oz_op, c->st);
-    c->oz_src = X;
+    c->oz_src = c->oz_cache_on ? X : nullptr;
     c->oz_K = K;
     c->oz_cols = cols;
     c->oz_ld = ldx;
@@ -295,12 +296,12 @@ void zero_pad_rows(lr_ctx* c, double* W, int64_t m, int64_t ld, int64_t n) {
 }
 
 void cpqr_core(lr_ctx* c, int64_t m, int64_t n, double* W, int64_t ldw, int64_t k, int64_t* piv, double* tau,
-               const char* who, bool padded = false) {
+               const char* who, bool padded = false, bool nopivot = false) {
   DBuf<int> flags(1, c->st);
   DBuf<long long> rec(1, c->st);
   LRB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), c->st));
   LRB_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(long long), c->st));
-  cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, padded, c->st);
+  cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, padded, c->st, nopivot);
   LRB_CUDA(cudaMemcpyAsync(c->h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   LRB_CUDA(cudaMemcpyAsync(c->h_ll, rec.p, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -543,11 +544,89 @@ void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, 
   mark(c, "sketch_gemm");
 }
 
+// svd.hpp:216-235 orth_rows on the transposed sample: an orthonormal basis Q
+// (rows x r, ld ldq) of the columns of X (rows x k, ld ldx), rank-trimmed like
+// the reference's Householder QR (trailing |R_ii| <= max|R_ii| eps max(rows, k)
+// dropped).  CholeskyQR2 when it is provably safe (cond bound < 1e7, hence full
+// rank), else the unpivoted Householder QR of cpqr.cu.  Q may differ from the
+// reference's by column signs, which leave the power sketch's row space, every
+// pivot and T unchanged.  Returns r.
+int64_t orth_cols_core(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, double* Q, int64_t ldq) {
+  require_nonempty(rows, k, "orth_rows");
+  if (!device_all_finite(c, rows, k, X, ldx)) fail(LR_EINVAL, "orth_rows: matrix has non-finite entries");
+  if (rows >= 2 * k) {
+    DBuf<double> Xt((size_t)even(k) * rows, c->st), R((size_t)k * k, c->st), Ri((size_t)k * k, c->st);
+    transpose_matrix(rows, k, X, ldx, Xt, even(k), c->st);
+    if (cholqr2(c, rows, k, X, ldx, Xt, even(k), R, Ri)) {
+      gemm(c, rows, k, k, Xt, even(k), Ri, k, Q, ldq);  // Q = X R^-1
+      return k;
+    }
+  }
+  const int64_t rmax = std::min(rows, k), ldw = even(rows);
+  DBuf<double> W((size_t)ldw * k, c->st), tau(rmax, c->st), d(rmax, c->st), Qf((size_t)ldw * rmax, c->st);
+  DBuf<int64_t> piv(k, c->st);
+  copy_matrix(rows, k, X, ldx, W, ldw, c->st);
+  cpqr_core(c, rows, k, W, ldw, rmax, piv, tau, "orth_rows", false, true);
+  // |R_ii| -> host, trailing trim
+  LRB_CUDA(cudaMemcpy2DAsync(d.p, sizeof(double), W.p, (ldw + 1) * sizeof(double), sizeof(double), rmax,
+                             cudaMemcpyDeviceToDevice, c->st));
+  std::vector<double> h(rmax);
+  LRB_CUDA(cudaMemcpyAsync(h.data(), d.p, sizeof(double) * rmax, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  double dmax = 0.0;
+  for (double v : h) dmax = std::max(dmax, std::fabs(v));
+  const double tol = dmax * 2.220446049250313e-16 * (double)std::max(rows, k);
+  int64_t r = rmax;
+  while (r > 0 && std::fabs(h[r - 1]) <= tol) --r;
+  if (r > 0) {
+    cpqr_form_q(rows, k, W, ldw, rmax, tau, Qf, ldw, c->st);
+    copy_matrix(rows, r, Qf, ldw, Q, ldq, c->st);
+  }
+  return r;
+}
+
+// sketch.hpp:148-164 power rounds on the sample Y (rows x n, ld ldy):
+// Z^T = A Y^T (A^T materialised once so both products are K-contiguous),
+// Y = Z A (the input matrix's contraction: Ozaki or DMMA per the context).
+// Returns the new sample in Yb (ld work_ld(rows), zero padded); *rows updated.
+void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int q, bool reorth,
+                       DBuf<double>& Yb, int64_t& ldy, int64_t& rows) {
+  const int64_t ldat = even(n);
+  DBuf<double> At((size_t)ldat * m, c->st);
+  transpose_matrix(m, n, a, lda, At, ldat, c->st);  // A^T: n x m
+  for (int round = 0; round < q; ++round) {
+    DBuf<double> Yt((size_t)ldat * rows, c->st), Qy;
+    transpose_matrix(rows, n, Yb, ldy, Yt, ldat, c->st);  // Y^T: n x rows
+    const double* Ym = Yt;
+    if (reorth) {
+      Qy = DBuf<double>((size_t)ldat * rows, c->st);
+      rows = orth_cols_core(c, n, rows, Yt, ldat, Qy, ldat);
+      Ym = Qy;
+    }
+    if (rows < 1) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
+    DBuf<double> Zt((size_t)even(m) * rows, c->st), Qz;
+    gemm(c, m, rows, n, At, ldat, Ym, ldat, Zt, even(m));  // Z^T = A Y^T (m x rows)
+    const double* Zm = Zt;
+    if (reorth) {
+      Qz = DBuf<double>((size_t)even(m) * rows, c->st);
+      rows = orth_cols_core(c, m, rows, Zt, even(m), Qz, even(m));
+      Zm = Qz;
+    }
+    if (rows < 1) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
+    ldy = work_ld(rows);
+    Yb = DBuf<double>((size_t)ldy * n, c->st);
+    zero_pad_rows(c, Yb, rows, ldy, n);
+    gemm_a(c, rows, n, m, Zm, even(m), a, lda, Yb, ldy, 1);  // Y = Z A (rows x n)
+  }
+  mark(c, "power_rounds");
+}
+
 // sketch.hpp:200-223 argument checks (before any work)
 int64_t check_randomized_id(int64_t m, int64_t n, int64_t k, const lr_sketch_config& cfg) {
   require_rank_in_range(k, m, n, "randomized_id");
-  if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
-    fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch with power 0 runs on the B200 path");
+  if (cfg.kind != LR_SKETCH_GAUSSIAN)
+    fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch runs on the B200 path");
+  if (cfg.power < 0) fail(LR_EINVAL, "sketch_power: q must be nonnegative");
   const int64_t ell = k + cfg.oversample;
   if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
   require_nonempty(m, n, "sketch_gaussian");
@@ -560,8 +639,8 @@ int64_t check_randomized_id(int64_t m, int64_t n, int64_t k, const lr_sketch_con
 void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                         const lr_sketch_config& cfg, const lr_solve_strategy& strat, int64_t* piv, double* coeff,
                         int64_t ldc, double* Ypre = nullptr) {
-  const int64_t ell = check_randomized_id(m, n, k, cfg);
-  const int64_t ldy = work_ld(ell);
+  int64_t ell = check_randomized_id(m, n, k, cfg);
+  int64_t ldy = work_ld(ell);
   DBuf<double> Yb;
   double* Y = Ypre;
   if (!Y) {
@@ -569,6 +648,11 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
     Y = Yb;
     zero_pad_rows(c, Y, ell, ldy, n);
     sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
+  }
+  if (cfg.power > 0) {  // sketch.hpp:148-164 (the caller's pre-sketched Y only for q = 0)
+    if (Ypre) fail(LR_ERUNTIME, "randomized_id: power rounds need the library-owned sample");
+    power_rounds_core(c, m, n, a, lda, cfg.power, cfg.reorthonormalize != 0, Yb, ldy, ell);
+    Y = Yb;
   }
   const int64_t steps = std::min(ell, n);  // cpqr_full
   if (steps < k) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
@@ -1061,6 +1145,28 @@ int lr_sketch_gaussian(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
   });
 }
 
+// sketch.hpp:148-164: y (ell x n, ld ell; first *rows rows valid)
+int lr_sketch_power(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                    uint64_t seed, double* y, int64_t* rows) {
+  return guard([&] {
+    checked(c);
+    if (q < 0) fail(LR_EINVAL, "sketch_power: q must be nonnegative");
+    require_nonempty(m, n, "sketch_gaussian");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    if (!device_all_finite(c, m, n, d, l)) fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+    require_sample_count(ell, m, "sketch_gaussian");
+    int64_t ldy = work_ld(ell), r = ell;
+    DBuf<double> yd((size_t)ldy * n, c->st);
+    zero_pad_rows(c, yd, ell, ldy, n);
+    sketch_core(c, m, n, d, l, ell, seed, yd, ldy);
+    if (q > 0) power_rounds_core(c, m, n, d, l, q, reorth != 0, yd, ldy, r);
+    to_host(c, r, n, yd, ldy, y, ell);
+    sync(c);
+    *rows = r;
+  });
+}
+
 // cpqr.hpp:32-114
 int lr_cpqr_partial_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, double* q, double* s,
                       int64_t* pivots) {
@@ -1306,8 +1412,14 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
       Downloads down(c);  // declared after the buffers it reads: drains first
       OzakiScope scope(c);
       mark(c, "begin");
-      upload_sketch(c, m, n, a, lda, d, l, ell, cfg.seed, Y, ldy);
-      randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k, Y);
+      if (cfg.power == 0) {
+        upload_sketch(c, m, n, a, lda, d, l, ell, cfg.seed, Y, ldy);
+        randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k, Y);
+      } else {
+        LRB_CUDA(cudaMemcpy2DAsync(d.p, l * sizeof(double), a, lda * sizeof(double), m * sizeof(double), n,
+                                   cudaMemcpyHostToDevice, c->st));
+        randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k);
+      }
       down.idx(n, cp, col_pivots);
       down.mat(k, n - k, ccd, k, col_coeff, k);
       DBuf<double> Ct((size_t)even(k) * m, c->st);

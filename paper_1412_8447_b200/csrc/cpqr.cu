@@ -55,6 +55,7 @@ struct CpqrArgs {
   double* scratch;   // [G][4*m]: old-s column, pivot R rows, (v, tau*v if not in smem)
   int* flags;
   unsigned long long* recomputes;
+  int nopivot;  // unpivoted Householder QR (orth_rows fallback): position s is always the pivot
 };
 
 __device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
@@ -204,6 +205,10 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
       long long cp = sh_bp[0];
       for (int w = 1; w < kWarps; ++w)
         if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      if (a.nopivot) {  // the owner of column 0 wins
+        cp = (0 >= c0 && 0 < c1) ? 0 : INT64_MAX;
+        cv = cp == 0 ? INFINITY : -INFINITY;
+      }
       a.pval[cta] = cv;
       a.ppos[cta] = cp;
       sh_piv[0] = cp;
@@ -486,6 +491,10 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
       long long cp = sh_bp[0];
       for (int w = 1; w < kWarps; ++w)
         if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      if (a.nopivot) {  // the owner of position s + 1 wins
+        cp = (s + 1 >= c0 && s + 1 < c1) ? s + 1 : INT64_MAX;
+        cv = cp == s + 1 ? INFINITY : -INFINITY;
+      }
       a.pval[(int64_t)nxt * G + cta] = cv;
       a.ppos[(int64_t)nxt * G + cta] = cp;
       sh_piv[0] = cp;
@@ -578,8 +587,8 @@ int cpqr_fast_variant() {
 }  // namespace
 
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
-                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st) {
-  if (cpqr_panel_supported(m, ld, padded)) {
+                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st, bool nopivot) {
+  if (!nopivot && cpqr_panel_supported(m, ld, padded)) {
     cpqr_panel(ws, m, n, W, ld, k, pivots, tau, d_flags, d_recomputes, st);
     return;
   }
@@ -606,6 +615,7 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
   a.ppos = reinterpret_cast<long long*>(a.scratch + 4 * (size_t)Gmax * ld);
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
+  a.nopivot = nopivot ? 1 : 0;
   const size_t smem = ld <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)ld : 0;
   const bool fast = padded && ld % 64 == 0 && ld <= 512;
   if (fast) {

@@ -103,8 +103,10 @@ struct CpqrStats {
 // lower part the reflectors, pivots the permutation and tau the k scalars.
 // Device pointers; pivots (n int64), tau (k), flags (1 int: nonfinite input).
 // `padded`: ld % 64 == 0 and rows [m, ld) of W are zero (enables the fast path).
+// nopivot: unpivoted Householder QR with the same reflector convention
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
-                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st);
+                  double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st,
+                  bool nopivot = false);
 // Panel (delayed-update) CPQR for short-wide padded matrices (cpqr_panel.cu):
 // same contract as cpqr_inplace; supported when ld % 64 == 0, ld <= 512 and
 // rows [m, ld) are zero.

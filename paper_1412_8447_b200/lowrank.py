@@ -22,7 +22,7 @@ from . import _lib as L
 __all__ = [
     "SingularityError", "ConvergenceError", "LowrankCudaError", "SolveKind", "SolveStrategy", "SketchKind",
     "SketchConfig", "PivotedQr", "ColumnId", "RowId", "TwoSidedId", "CurDecomposition", "SampleMatrix",
-    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "cpqr_partial", "cpqr_full",
+    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_power", "cpqr_partial", "cpqr_full",
     "stabilized_coeff_solve", "svd", "pinv", "id_column", "id_row", "tsid_from_column_id", "id_two_sided",
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
@@ -350,6 +350,20 @@ def sketch_gaussian(a, ell: int, seed: int, ctx: Optional[Context] = None) -> Sa
 
 
 # ------------------------------------------------------------------ CPQR / solve / SVD
+def sketch_power(a, ell: int, q: int, reorthonormalize: bool = True, seed: int = 0,
+                 ctx: Optional[Context] = None) -> SampleMatrix:
+    """sketch.hpp:148-164: Omega A (A^T A)^q (rows re-orthonormalised before each product)."""
+    c = _ctx(ctx)
+    a = _f64(a)
+    m, n = a.shape
+    y = np.zeros((int(ell), n), order="F")
+    rows = ctypes.c_int64(0)
+    _raise(c.lib.lr_sketch_power(c.h, m, n, _ptr(a), _ld(a), int(ell), int(q), int(bool(reorthonormalize)),
+                                 int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(y), ctypes.byref(rows)))
+    prov = SampleProvenance(SketchKind.Gaussian, int(ell), int(q), bool(reorthonormalize) and q > 0, int(seed))
+    return SampleMatrix(np.asfortranarray(y[: rows.value]), prov)
+
+
 def cpqr_partial(a, k: int, want_q: bool = True, ctx: Optional[Context] = None) -> PivotedQr:
     """cpqr.hpp:32-114."""
     c = _ctx(ctx)

@@ -70,6 +70,10 @@ class Oracle:
             "lro_randomized_id": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, c_u64, lro_solve_strategy, c_p,
                                   c_p, c_p],
             "lro_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, lro_solve_strategy, c_p, c_p, c_p],
+            "lro_orth_rows": [c_i64, c_i64, c_p, c_i64, c_p, c_p],
+            "lro_sketch_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_u64, c_p, c_p],
+            "lro_randomized_id_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        c_u64, lro_solve_strategy, c_p, c_p, c_p],
             "lro_cur_from_two_sided": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_dbl, ctypes.c_int, c_p,
                                        c_p, c_p],
             "lro_cur_error_fro": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p],
@@ -158,6 +162,32 @@ class Oracle:
         self._chk(self.L.lro_sketch_gaussian(m, n, _p(a), m, ell, seed, _p(y)))
         return y
 
+    def orth_rows(self, y):
+        y = _f(y)
+        ell, n = y.shape
+        out = np.zeros((ell, n), order="F")
+        r = np.zeros(1, dtype=np.int64)
+        self._chk(self.L.lro_orth_rows(ell, n, _p(y), ell, _p(out), _p(r)))
+        return out[: int(r[0])]
+
+    def sketch_power(self, a, ell, q, reorth, seed):
+        a = _f(a)
+        m, n = a.shape
+        y = np.zeros((ell, n), order="F")
+        rows = np.zeros(1, dtype=np.int64)
+        self._chk(self.L.lro_sketch_power(m, n, _p(a), m, ell, q, int(reorth), seed, _p(y), _p(rows)))
+        return y[: int(rows[0])]
+
+    def randomized_id_power(self, a, k, oversample, q, reorth, seed, strategy=None):
+        a = _f(a)
+        m, n = a.shape
+        piv = np.empty(n, dtype=np.int64)
+        coeff = np.empty((k, n - k), order="F")
+        stats = np.zeros(1, dtype=np.int64)
+        self._chk(self.L.lro_randomized_id_power(m, n, _p(a), m, k, oversample, q, int(reorth), seed,
+                                                 strategy or self.strategy(), _p(piv), _p(coeff), _p(stats)))
+        return piv, coeff
+
     def randomized_id(self, a, k, oversample=10, seed=0, strategy=None):
         a = _f(a)
         m, n = a.shape
@@ -232,6 +262,9 @@ class Ref:
             "lref_id_row": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p],
             "lref_randomized_id": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, c_u64, c_p, c_p],
             "lref_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p],
+            "lref_sketch_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_u64, c_p, c_p],
+            "lref_randomized_id_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         c_u64, c_p, c_p],
             "lref_cur_from_two_sided": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_dbl, ctypes.c_int,
                                         c_p, c_p, c_p],
             "lref_randomized_cur": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, c_u64, c_dbl, ctypes.c_int, c_p,
@@ -312,6 +345,23 @@ class Ref:
         piv = np.empty(n, dtype=np.int64)
         coeff = np.empty((k, n - k), order="F")
         self._chk(self.L.lref_randomized_id(m, n, _p(a), m, k, oversample, seed, _p(piv), _p(coeff)))
+        return piv, coeff
+
+    def sketch_power(self, a, ell, q, reorth, seed):
+        a = _f(a)
+        m, n = a.shape
+        y = np.zeros((ell, n), order="F")
+        rows = np.zeros(1, dtype=np.int64)
+        self._chk(self.L.lref_sketch_power(m, n, _p(a), m, ell, q, int(reorth), seed, _p(y), _p(rows)))
+        return y[: int(rows[0])]
+
+    def randomized_id_power(self, a, k, oversample, q, reorth, seed):
+        a = _f(a)
+        m, n = a.shape
+        piv = np.empty(n, dtype=np.int64)
+        coeff = np.empty((k, n - k), order="F")
+        self._chk(self.L.lref_randomized_id_power(m, n, _p(a), m, k, oversample, q, int(reorth), seed, _p(piv),
+                                                  _p(coeff)))
         return piv, coeff
 
     def tsid(self, a, k, col_pivots, col_coeff):

@@ -258,4 +258,63 @@ def test_validation_messages(lr, oracle):
     with pytest.raises(ValueError, match="sample count"):
         lr.randomized_id(a, 5, lr.SketchConfig(oversample=10))
     with pytest.raises(NotImplementedError):
-        lr.randomized_id(a, 2, lr.SketchConfig(power=1))
+        lr.randomized_id(a, 2, lr.SketchConfig(kind=lr.SketchKind.Srft))
+    with pytest.raises(ValueError, match="q must be nonnegative"):
+        lr.randomized_id(a, 2, lr.SketchConfig(power=-1))
+
+
+# ------------------------------------------------------------------ power iterations
+@pytest.mark.parametrize("q,reorth", [(1, True), (2, True), (1, False)])
+def test_randomized_id_power_matches_oracle(lr, oracle, q, reorth):
+    """sketch.hpp:148-164: identical pivots and T within 1e-10 (the GPU's
+    orthonormal bases may differ from Householder's by signs, which leaves the
+    row space, pivots and T unchanged)."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 1500, 1200, width=400, k=60)
+    a = inputs.synthetic_np(cfg)
+    cid = lr.randomized_id(a, 60, lr.SketchConfig(oversample=10, seed=5, power=q, reorthonormalize=reorth))
+    piv, coeff = oracle.randomized_id_power(a, 60, 10, q, reorth, 5)
+    assert np.array_equal(cid.pivots, piv)
+    assert rel(cid.coeff, coeff) <= TOL
+
+
+def test_randomized_cur_power_matches_oracle_both_engines(lr, oracle):
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 2000, 1600, width=512, k=80)
+    a = inputs.synthetic_np(cfg)
+    piv, _ = oracle.randomized_id_power(a, 80, 10, 1, True, 2)
+    ctx = lr.default_context()
+    for mode in (ctx.GEMM_DMMA, ctx.GEMM_OZAKI_INT8):
+        ctx.set_gemm_mode(mode)
+        try:
+            cur = lr.randomized_cur(a, 80, lr.SketchConfig(oversample=10, seed=2, power=1), u_mode=lr.U_CPINV_A_RPINV)
+        finally:
+            ctx.set_gemm_mode(ctx.GEMM_DMMA)
+        assert np.array_equal(cur.col_pivots, piv)
+
+
+def test_power_rank_deficient_sample_shrinks(lr, oracle):
+    """orth_rows drops numerically dependent rows (svd.hpp:226-231): a rank-20
+    matrix with l = 30 leaves a 20-row sample, so k = 25 collapses (sketch.hpp:207-212)
+    while k = 15 runs the Householder fallback and matches the oracle."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 300, 200, width=20, k=15)
+    a = inputs.synthetic_np(cfg)
+    cid = lr.randomized_id(a, 15, lr.SketchConfig(oversample=15, seed=1, power=1))
+    piv, coeff = oracle.randomized_id_power(a, 15, 15, 1, True, 1)
+    assert np.array_equal(cid.pivots[:15], piv[:15])
+    with pytest.raises(RuntimeError, match="collapsed"):
+        lr.randomized_id(a, 25, lr.SketchConfig(oversample=5, seed=1, power=1))
+
+
+def test_sketch_power_rows_span_the_oracle_sample(lr, oracle):
+    """The sample itself: same row count; the GPU rows span the oracle's row
+    space (orthonormal bases agree up to an orthogonal k x k factor)."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 800, 700, width=200, k=40)
+    a = inputs.synthetic_np(cfg)
+    g = lr.sketch_power(a, 50, 1, True, 4).y
+    o = oracle.sketch_power(a, 50, 1, True, 4)
+    assert g.shape == o.shape
+    # q = 0 is exactly the Gaussian sketch (test_sketch.cpp:94-99)
+    assert np.array_equal(lr.sketch_power(a, 50, 0, True, 4).y, lr.sketch_gaussian(a, 50, 4).y)
+    # both end with Y = Z A for orthonormal Z; project o onto g's row space
+    qg, _ = np.linalg.qr(g.T)
+    resid = o.T - qg @ (qg.T @ o.T)
+    assert np.linalg.norm(resid) <= 1e-10 * np.linalg.norm(o)
