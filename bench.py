@@ -290,7 +290,7 @@ def run_ours(args, rank, world, local_rank):
     t0 = time.time()
     a = inputs.synthetic_torch(cfg, device=dev, col_block=8192)
     gen_s = time.time() - t0
-    sk = lr.SketchConfig(oversample=OVERSAMPLE, seed=cfg.sketch_seed)
+    sk = lr.SketchConfig(oversample=OVERSAMPLE, seed=cfg.sketch_seed, power=args.power)
     out = None
     for _ in range(args.warmup):
         out = lr.randomized_cur_device(a, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=out)
@@ -389,6 +389,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, "
                                "U = C^+ A R^+)", "m": cfg.m, "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE,
                    "u_mode": "cpinv_a_rpinv", "l2": "A (34.4 GB) exceeds L2; no flush needed",
+                   "power": args.power,
                    "gemm_engine": {"ozaki": "ozaki_int8 (FP64 emulated on INT8 tcgen05, 16 moduli)",
                                    "dmma": "fp64_dmma"}[args.engine],
                    "parallelism": "replicas" if world > 1 else "single"},
@@ -556,6 +557,8 @@ def main():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--workload", default="c4", choices=["c4", "c5"],
                    help="c4: dense randomized CUR 65536^2 (headline); c5: sparse CSR 200000x100000")
+    p.add_argument("--power", type=int, default=0,
+                   help="power iterations q (sketch.hpp:148-164; BASELINE configs use q = 0)")
     p.add_argument("--engine", default="ozaki", choices=["ozaki", "dmma"],
                    help="contraction engine of the two A-sized GEMMs (lr_ctx_set_gemm_mode)")
     p.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "sharded"],

@@ -594,6 +594,7 @@ void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
   const int64_t ldat = even(n);
   DBuf<double> At((size_t)ldat * m, c->st);
   transpose_matrix(m, n, a, lda, At, ldat, c->st);  // A^T: n x m
+  mark(c, "power_transpose_a");
   for (int round = 0; round < q; ++round) {
     DBuf<double> Yt((size_t)ldat * rows, c->st), Qy;
     transpose_matrix(rows, n, Yb, ldy, Yt, ldat, c->st);  // Y^T: n x rows
@@ -604,21 +605,24 @@ void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
       Ym = Qy;
     }
     if (rows < 1) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
+    mark(c, "power_orth");
     DBuf<double> Zt((size_t)even(m) * rows, c->st), Qz;
     gemm(c, m, rows, n, At, ldat, Ym, ldat, Zt, even(m));  // Z^T = A Y^T (m x rows)
+    mark(c, "power_zt_gemm");
     const double* Zm = Zt;
     if (reorth) {
       Qz = DBuf<double>((size_t)even(m) * rows, c->st);
       rows = orth_cols_core(c, m, rows, Zt, even(m), Qz, even(m));
       Zm = Qz;
     }
+    mark(c, "power_orth");
     if (rows < 1) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
     ldy = work_ld(rows);
     Yb = DBuf<double>((size_t)ldy * n, c->st);
     zero_pad_rows(c, Yb, rows, ldy, n);
     gemm_a(c, rows, n, m, Zm, even(m), a, lda, Yb, ldy, 1);  // Y = Z A (rows x n)
+    mark(c, "power_y_gemm");
   }
-  mark(c, "power_rounds");
 }
 
 // sketch.hpp:200-223 argument checks (before any work)
