@@ -125,6 +125,10 @@ int lr_sketch_gaussian(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64
                        uint64_t seed, double* y);
 int lr_sketch_gaussian_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
                          uint64_t seed, double* y, int64_t ldy);
+/* sketch.hpp:84-143 sketch_srft: y (ell x n, ld ell) = sqrt(m/ell) R H D A (random
+   signs D, orthonormal Hartley transform H, ell sampled rows R) */
+int lr_sketch_srft(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
+                   double* y);
 /* sketch.hpp:148-164 sketch_power: y (ell x n, ld ell) = Omega A (A^T A)^q with
    optional row re-orthonormalisation (svd.hpp:216-235); *rows = final row
    count (orth_rows drops numerically dependent rows) */

@@ -713,6 +713,100 @@ int lro_randomized_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_
   return rc;
 }
 
+static const double kPi = 3.14159265358979323846; /* std::numbers::pi */
+
+/* rng.hpp:53-62 */
+void lro_sample_without_replacement(uint64_t seed, int64_t population, int64_t count, int64_t* out) {
+  int64_t* pool = NEW(int64_t, population);
+  for (int64_t i = 0; i < population; ++i) pool[i] = i;
+  uint64_t next = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t j = i + (int64_t)(lro_stream_value(seed, next++) % (uint64_t)(population - i));
+    const int64_t t = pool[i];
+    pool[i] = pool[j];
+    pool[j] = t;
+  }
+  memcpy(out, pool, sizeof(int64_t) * (size_t)count);
+  free(pool);
+}
+
+static double srft_sign(uint64_t sign_seed, int64_t i) {
+  return (lro_stream_value(sign_seed, (uint64_t)i) & 1u) ? -1.0 : 1.0;
+}
+
+/* sketch.hpp:84-100 with hartley.hpp:60-73 */
+int lro_srft_operator(int64_t m, int64_t ell, uint64_t seed, double* out) {
+  if (ell < 1 || ell > m) return fail(LRO_EINVAL, "srft_operator: sample count %lld out of range for %lld rows",
+                                      (long long)ell, (long long)m);
+  const uint64_t sseed = lro_derive_seed(seed, 1), rseed = lro_derive_seed(seed, 2);
+  int64_t* rows = NEW(int64_t, ell);
+  lro_sample_without_replacement(rseed, m, ell, rows);
+  const double hs = 1.0 / sqrt((double)m), scale = sqrt((double)m / (double)ell);
+  for (int64_t q = 0; q < m; ++q) {
+    const double sg = srft_sign(sseed, q);
+    for (int64_t i = 0; i < ell; ++i) {
+      const int64_t p = rows[i];
+      const double t = 2.0 * kPi * (double)((p * q) % m) / (double)m;
+      out[IDX(i, q, ell)] = scale * ((hs * (cos(t) + sin(t))) * sg);
+    }
+  }
+  free(rows);
+  return LRO_OK;
+}
+
+/* hartley.hpp:17-43: unnormalised radix-2 DIT fast Hartley transform */
+static void fht_unnormalized(double* data, double* scratch, int64_t n) {
+  if (n == 1) return;
+  const int64_t half = n / 2;
+  for (int64_t j = 0; j < half; ++j) {
+    scratch[j] = data[2 * j];
+    scratch[half + j] = data[2 * j + 1];
+  }
+  fht_unnormalized(scratch, data, half);
+  fht_unnormalized(scratch + half, data, half);
+  const double* even = scratch;
+  const double* odd = scratch + half;
+  for (int64_t k = 0; k < half; ++k) {
+    const double angle = 2.0 * kPi * (double)k / (double)n;
+    const double c = cos(angle), s = sin(angle);
+    const int64_t mirror = k == 0 ? 0 : half - k;
+    const double cross = c * odd[k] + s * odd[mirror];
+    data[k] = even[k] + cross;
+    data[k + half] = even[k] - cross;
+  }
+}
+
+/* sketch.hpp:110-143 */
+int lro_sketch_srft(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed, double* y) {
+  if (m < 1 || n < 1) return fail(LRO_EINVAL, "sketch_srft: matrix must be nonempty");
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i)
+      if (!isfinite(a[IDX(i, j, lda)])) return fail(LRO_EINVAL, "sketch_srft: matrix has non-finite entries");
+  if (ell < 1 || ell > m) return fail(LRO_EINVAL, "sketch_srft: sample count %lld out of range for %lld rows",
+                                      (long long)ell, (long long)m);
+  if ((m & (m - 1)) == 0) {
+    const uint64_t sseed = lro_derive_seed(seed, 1), rseed = lro_derive_seed(seed, 2);
+    int64_t* rows = NEW(int64_t, ell);
+    lro_sample_without_replacement(rseed, m, ell, rows);
+    double* col = NEW(double, m);
+    double* scr = NEW(double, m);
+    const double hs = 1.0 / sqrt((double)m), scale = sqrt((double)m / (double)ell);
+    for (int64_t j = 0; j < n; ++j) {
+      for (int64_t i = 0; i < m; ++i) col[i] = srft_sign(sseed, i) * a[IDX(i, j, lda)];
+      fht_unnormalized(col, scr, m);
+      for (int64_t i = 0; i < m; ++i) col[i] *= hs;
+      for (int64_t i = 0; i < ell; ++i) y[IDX(i, j, ell)] = scale * col[rows[i]];
+    }
+    free(scr); free(col); free(rows);
+    return LRO_OK;
+  }
+  double* om = NEW(double, ell * m);
+  int rc = lro_srft_operator(m, ell, seed, om);
+  if (!rc) lro_gemm_nn(ell, n, m, om, ell, a, lda, y, ell);
+  free(om);
+  return rc;
+}
+
 /* svd.hpp:216-235.  Eigen's HouseholderQR on y^T with makeHouseholder's
  * convention (beta = -sign(c0)|x|, tau = (beta - c0)/beta, v = x/(c0 - beta);
  * no reflection when the tail is exactly zero), then householderQ() applied to
@@ -786,12 +880,26 @@ int lro_orth_rows(int64_t ell, int64_t n, const double* y, int64_t ldy, double* 
 }
 
 /* sketch.hpp:148-164 */
+static int power_rounds(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                        double* y, int64_t* rows_out);
+
 int lro_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
                      uint64_t seed, double* y, int64_t* rows_out) {
   if (q < 0) return fail(LRO_EINVAL, "sketch_power: q must be nonnegative");
   int rc = lro_sketch_gaussian(m, n, a, lda, ell, seed, y);
   if (rc) return rc;
+  return power_rounds(m, n, a, lda, ell, q, reorth, y, rows_out);
+}
+
+/* the power rounds of sketch_power / build_sample (sketch.hpp:155-160, :180-185) */
+static int power_rounds(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, int q, int reorth,
+                        double* y, int64_t* rows_out) {
+  int rc = 0;
   int64_t rows = ell;
+  if (q == 0) {
+    *rows_out = ell;
+    return 0;
+  }
   double* z = NEW(double, ell * m);   /* ell x m, ld ell */
   double* at = NEW(double, n * m);    /* A^T, n x m */
   for (int64_t j = 0; j < n; ++j)
@@ -810,13 +918,23 @@ int lro_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t
 int lro_randomized_id_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int oversample,
                             int q, int reorth, uint64_t seed, lro_solve_strategy strat, int64_t* pivots,
                             double* coeff, int64_t* stats) {
+  return lro_randomized_id_cfg(m, n, a, lda, k, 0, oversample, 0, q, reorth, seed, strat, pivots, coeff, stats);
+}
+
+int lro_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                          int64_t srft_samples, int q, int reorth, uint64_t seed, lro_solve_strategy strat,
+                          int64_t* pivots, double* coeff, int64_t* stats) {
   int rc;
   if ((rc = require_rank_in_range(k, m, n, "randomized_id"))) return rc;
-  const int64_t ell = k + (int64_t)oversample;
+  /* SketchConfig::sample_count, sketch.hpp:29-32 */
+  const int64_t ell = kind == 0 ? k + (int64_t)oversample : (srft_samples > 0 ? srft_samples : 2 * k);
   if (ell < k) return fail(LRO_EINVAL, "build_sample: sample count below target rank");
+  if (q < 0) return fail(LRO_EINVAL, "sketch_power: q must be nonnegative");
   double* y = NEW(double, ell * n);
   int64_t rows = ell;
-  if ((rc = lro_sketch_power(m, n, a, lda, ell, q, reorth, seed, y, &rows))) { free(y); return rc; }
+  rc = kind == 0 ? lro_sketch_gaussian(m, n, a, lda, ell, seed, y) : lro_sketch_srft(m, n, a, lda, ell, seed, y);
+  if (!rc) rc = power_rounds(m, n, a, lda, ell, q, reorth, y, &rows);
+  if (rc) { free(y); return rc; }
   const int64_t steps = rows < n ? rows : n;
   if (steps < k) { free(y); return fail(LRO_ERUNTIME, "randomized_id: sample rank collapsed below target rank"); }
   double* s = NEW(double, steps * n);

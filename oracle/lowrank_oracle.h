@@ -97,6 +97,20 @@ int lro_randomized_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_
                       int oversample, uint64_t seed, lro_solve_strategy strat,
                       int64_t* pivots, double* coeff, int64_t* stats);
 
+/* rng.hpp:53-62 CounterRng::sample_without_replacement (partial Fisher-Yates):
+ * out[0..count) */
+void lro_sample_without_replacement(uint64_t seed, int64_t population, int64_t count, int64_t* out);
+/* sketch.hpp:84-100 srft_operator: ell x m dense operator, ld ell */
+int lro_srft_operator(int64_t m, int64_t ell, uint64_t seed, double* out);
+/* sketch.hpp:110-143 sketch_srft: y (ell x n, ld ell); radix-2 fast Hartley
+ * transform (hartley.hpp:17-43) when m is a power of two, else the dense operator */
+int lro_sketch_srft(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed, double* y);
+/* sketch.hpp:167-223 randomized_id with a full SketchConfig: kind 0 Gaussian / 1
+ * SRFT, sample count k + oversample (Gaussian) or srft_samples (0 -> 2k), q power rounds */
+int lro_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                          int64_t srft_samples, int q, int reorth, uint64_t seed, lro_solve_strategy strat,
+                          int64_t* pivots, double* coeff, int64_t* stats);
+
 /* svd.hpp:216-235 orth_rows: Householder QR of y^T (n x ell), numerical rank
  * r (trailing |R_ii| <= max|R_ii| eps max(n, ell) dropped), out = thin Q^T:
  * r x n (ld ell; rows r..ell-1 untouched); *r_out = r */

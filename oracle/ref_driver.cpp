@@ -153,6 +153,32 @@ int lref_sketch_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_
   });
 }
 
+// sketch.hpp:110-143: y (ell x n, ld ell)
+int lref_sketch_srft(int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed, double* y) {
+  return guard([&] { to_ptr(sketch_srft(from_ptr(m, n, a, lda), ell, seed).y, y); });
+}
+
+int lref_srft_operator(int64_t m, int64_t ell, uint64_t seed, double* out) {
+  return guard([&] { to_ptr(srft_operator<double>(m, ell, seed), out); });
+}
+
+// sketch.hpp:200-223 with a full SketchConfig
+int lref_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                           int64_t srft_samples, int q, int reorth, uint64_t seed, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    SketchConfig cfg;
+    cfg.kind = kind == 0 ? SketchKind::Gaussian : SketchKind::Srft;
+    cfg.oversample = oversample;
+    cfg.srft_samples = srft_samples;
+    cfg.seed = seed;
+    cfg.power = q;
+    cfg.reorthonormalize = reorth != 0;
+    auto id = randomized_id(from_ptr(m, n, a, lda), k, cfg);
+    to_idx(id.pivots, pivots);
+    to_ptr(id.coeff, coeff);
+  });
+}
+
 // sketch.hpp:200-223 with power iterations
 int lref_randomized_id_power(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int oversample, int q,
                              int reorth, uint64_t seed, int64_t* pivots, double* coeff) {

@@ -534,11 +534,48 @@ void id_column_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
 }
 
 // sketch.hpp:67-78 into y (ell x n, ldy); a must be validated by the caller
+// rng.hpp:14-62 on the host (SRFT row sampling)
+uint64_t host_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+uint64_t host_stream_value(uint64_t seed, uint64_t index) { return host_mix64(seed + (index + 1) * 0x9E3779B97F4A7C15ULL); }
+uint64_t host_derive_seed(uint64_t seed, uint64_t tag) { return host_stream_value(seed, tag ^ 0xD1B54A32D192ED03ULL); }
+// CounterRng::sample_without_replacement (partial Fisher-Yates), rng.hpp:53-62
+std::vector<int64_t> sample_without_replacement(uint64_t seed, int64_t population, int64_t count) {
+  std::vector<int64_t> pool((size_t)population);
+  for (int64_t i = 0; i < population; ++i) pool[(size_t)i] = i;
+  uint64_t next = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t j = i + (int64_t)(host_stream_value(seed, next++) % (uint64_t)(population - i));
+    std::swap(pool[(size_t)i], pool[(size_t)j]);
+  }
+  pool.resize((size_t)count);
+  return pool;
+}
+
+// Omega^T (m x ell, ld m) of the sketch kind: Gaussian (rng.hpp:74-94) or the
+// SRFT operator (sketch.hpp:84-100; the reference applies it through a fast
+// Hartley transform when m is a power of two -- same operator, the GPU
+// contracts with it on the tensor cores like the Gaussian one)
+void sketch_operator_t(lr_ctx* c, int64_t m, int64_t ell, int kind, uint64_t seed, double* omt) {
+  if (kind == LR_SKETCH_SRFT) {
+    const std::vector<int64_t> rows = sample_without_replacement(host_derive_seed(seed, 2), m, ell);
+    DBuf<int64_t> dr(ell, c->st);
+    LRB_CUDA(cudaMemcpyAsync(dr.p, rows.data(), sizeof(int64_t) * ell, cudaMemcpyHostToDevice, c->st));
+    srft_operator_t(m, ell, host_derive_seed(seed, 1), dr, omt, m, c->st);
+    sync(c);  // rows (host vector) must outlive the copy
+  } else {
+    gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  }
+}
+
 void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
-                 double* y, int64_t ldy) {
+                 double* y, int64_t ldy, int kind = LR_SKETCH_GAUSSIAN) {
   DBuf<double> omt((size_t)m * even(ell), c->st);
   // Omega^T (m x ell): element (i,j) of Omega stored at omt[j + i*m]
-  gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  sketch_operator_t(c, m, ell, kind, seed, omt);
   mark(c, "omega");
   gemm_a(c, ell, n, m, omt, m, a, lda, y, ldy, 1);
   mark(c, "sketch_gemm");
@@ -628,13 +665,16 @@ void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
 // sketch.hpp:200-223 argument checks (before any work)
 int64_t check_randomized_id(int64_t m, int64_t n, int64_t k, const lr_sketch_config& cfg) {
   require_rank_in_range(k, m, n, "randomized_id");
-  if (cfg.kind != LR_SKETCH_GAUSSIAN)
-    fail(LR_EUNSUPPORTED, "randomized_id: only the Gaussian sketch runs on the B200 path");
+  if (cfg.kind != LR_SKETCH_GAUSSIAN && cfg.kind != LR_SKETCH_SRFT)
+    fail(LR_EINVAL, "randomized_id: unknown sketch kind");
   if (cfg.power < 0) fail(LR_EINVAL, "sketch_power: q must be nonnegative");
-  const int64_t ell = k + cfg.oversample;
+  // SketchConfig::sample_count, sketch.hpp:29-32
+  const int64_t ell = cfg.kind == LR_SKETCH_GAUSSIAN ? k + cfg.oversample
+                                                      : (cfg.srft_samples > 0 ? cfg.srft_samples : 2 * k);
   if (ell < k) fail(LR_EINVAL, "build_sample: sample count below target rank");
-  require_nonempty(m, n, "sketch_gaussian");
-  require_sample_count(ell, m, "sketch_gaussian");
+  const char* who = cfg.kind == LR_SKETCH_GAUSSIAN ? "sketch_gaussian" : "sketch_srft";
+  require_nonempty(m, n, who);
+  require_sample_count(ell, m, who);
   return ell;
 }
 
@@ -651,7 +691,7 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
     Yb = DBuf<double>((size_t)ldy * n, c->st);
     Y = Yb;
     zero_pad_rows(c, Y, ell, ldy, n);
-    sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy);
+    sketch_core(c, m, n, a, lda, ell, cfg.seed, Y, ldy, cfg.kind);
   }
   if (cfg.power > 0) {  // sketch.hpp:148-164 (the caller's pre-sketched Y only for q = 0)
     if (Ypre) fail(LR_ERUNTIME, "randomized_id: power rounds need the library-owned sample");
@@ -666,7 +706,8 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
   } catch (const LrError& e) {
     // Y is non-finite: distinguish a non-finite A (sketch_gaussian's check) from overflow in Y
     if (e.code == LR_EINVAL && !device_all_finite(c, m, n, a, lda))
-      fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+      fail(LR_EINVAL, std::string(cfg.kind == LR_SKETCH_SRFT ? "sketch_srft" : "sketch_gaussian") +
+                          ": matrix has non-finite entries");
     throw;
   }
   mark(c, "cpqr_sample");
@@ -874,10 +915,10 @@ bool is_pinned(const void* h) {
 // the sketch (and, on the Ozaki engine, the residue split of A, which is kept
 // in the context's cache for the A^T Q contraction of the same call).
 void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double* d, int64_t l, int64_t ell,
-                   uint64_t seed, double* Y, int64_t ldy) {
+                   uint64_t seed, double* Y, int64_t ldy, int kind) {
   cudaStream_t up = aux_stream(c->up_st);
   DBuf<double> omt((size_t)m * even(ell), c->st);
-  gaussian_matrix(ell, m, seed, omt, m, true, c->st);
+  sketch_operator_t(c, m, ell, kind, seed, omt);
   const bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
   OzakiOperand om;
   if (oz) {
@@ -1144,6 +1185,23 @@ int lr_sketch_gaussian(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
     require_sample_count(ell, m, "sketch_gaussian");
     DBuf<double> yd((size_t)ell * n, c->st);
     sketch_core(c, m, n, d, l, ell, seed, yd, ell);
+    to_host(c, ell, n, yd, ell, y, ell);
+    sync(c);
+  });
+}
+
+// sketch.hpp:110-143: y (ell x n, ld ell)
+int lr_sketch_srft(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
+                   double* y) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "sketch_srft");
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    if (!device_all_finite(c, m, n, d, l)) fail(LR_EINVAL, "sketch_srft: matrix has non-finite entries");
+    require_sample_count(ell, m, "sketch_srft");
+    DBuf<double> yd((size_t)ell * n, c->st);
+    sketch_core(c, m, n, d, l, ell, seed, yd, ell, LR_SKETCH_SRFT);
     to_host(c, ell, n, yd, ell, y, ell);
     sync(c);
   });
@@ -1417,7 +1475,7 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
       OzakiScope scope(c);
       mark(c, "begin");
       if (cfg.power == 0) {
-        upload_sketch(c, m, n, a, lda, d, l, ell, cfg.seed, Y, ldy);
+        upload_sketch(c, m, n, a, lda, d, l, ell, cfg.seed, Y, ldy, cfg.kind);
         randomized_id_core(c, m, n, d, l, k, cfg, strat, cp, ccd, k, Y);
       } else {
         LRB_CUDA(cudaMemcpy2DAsync(d.p, l * sizeof(double), a, lda * sizeof(double), m * sizeof(double), n,

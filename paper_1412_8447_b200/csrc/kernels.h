@@ -72,6 +72,10 @@ void gemm_tn_resid_sq(Workspace& ws, int M, int N, int K, const double* P, int64
 void gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ldo, bool transposed,
                      cudaStream_t st);
 
+// sketch.hpp:84-100 SRFT operator transposed (m x ell, ld ldo) for sampled rows `rows` (device, ell)
+void srft_operator_t(int64_t m, int64_t ell, uint64_t sign_seed, const int64_t* rows, double* out, int64_t ldo,
+                     cudaStream_t st);
+
 // ---------------------------------------------------------------- elementwise / data movement
 void scale_matrix(int M, int N, double* a, int64_t lda, double beta, cudaStream_t st);
 void copy_matrix(int64_t m, int64_t n, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t st);

@@ -60,4 +60,29 @@ void gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int
   LRB_CHECK_LAUNCH();
 }
 
+// sketch.hpp:84-100 srft_operator, stored transposed (out[i + j*ldo] = Omega(j, i)):
+// Omega(j, i) = sqrt(m/ell) * (cas(2 pi ((rows_j i) mod m) / m) / sqrt(m)) * sign_i,
+// sign_i = -1 if stream_value(sign_seed, i) is odd (hartley.hpp:60-73).
+__global__ void srft_operator_t_kernel(int64_t m, int64_t ell, uint64_t sign_seed, const int64_t* __restrict__ rows,
+                                       double* __restrict__ out, int64_t ldo) {
+  const double hs = 1.0 / sqrt((double)m), scale = sqrt((double)m / (double)ell);
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * ell; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % m, j = t / m;
+    const double sg = (stream_value(sign_seed, (uint64_t)i) & 1u) ? -1.0 : 1.0;
+    const double ang = two_pi * (double)((rows[j] * i) % m) / (double)m;
+    double sn, cs;
+    sincos(ang, &sn, &cs);
+    out[i + j * ldo] = scale * ((hs * (cs + sn)) * sg);
+  }
+}
+
+void srft_operator_t(int64_t m, int64_t ell, uint64_t sign_seed, const int64_t* rows, double* out, int64_t ldo,
+                     cudaStream_t st) {
+  if (m <= 0 || ell <= 0) return;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((m * ell + 255) / 256, 32 * num_sms()));
+  srft_operator_t_kernel<<<g, 256, 0, st>>>(m, ell, sign_seed, rows, out, ldo);
+  LRB_CHECK_LAUNCH();
+}
+
 }  // namespace lrb

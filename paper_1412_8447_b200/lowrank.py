@@ -22,7 +22,7 @@ from . import _lib as L
 __all__ = [
     "SingularityError", "ConvergenceError", "LowrankCudaError", "SolveKind", "SolveStrategy", "SketchKind",
     "SketchConfig", "PivotedQr", "ColumnId", "RowId", "TwoSidedId", "CurDecomposition", "SampleMatrix",
-    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_power", "cpqr_partial", "cpqr_full",
+    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_srft", "sketch_power", "cpqr_partial", "cpqr_full",
     "stabilized_coeff_solve", "svd", "pinv", "id_column", "id_row", "tsid_from_column_id", "id_two_sided",
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
@@ -350,6 +350,16 @@ def sketch_gaussian(a, ell: int, seed: int, ctx: Optional[Context] = None) -> Sa
 
 
 # ------------------------------------------------------------------ CPQR / solve / SVD
+def sketch_srft(a, ell: int, seed: int, ctx: Optional[Context] = None) -> SampleMatrix:
+    """sketch.hpp:110-143: sqrt(m/ell) R H D A (subsampled randomized Hartley transform)."""
+    c = _ctx(ctx)
+    a = _f64(a)
+    m, n = a.shape
+    y = np.empty((int(ell), n), order="F")
+    _raise(c.lib.lr_sketch_srft(c.h, m, n, _ptr(a), _ld(a), int(ell), int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(y)))
+    return SampleMatrix(y, SampleProvenance(SketchKind.Srft, int(ell), 0, False, int(seed)))
+
+
 def sketch_power(a, ell: int, q: int, reorthonormalize: bool = True, seed: int = 0,
                  ctx: Optional[Context] = None) -> SampleMatrix:
     """sketch.hpp:148-164: Omega A (A^T A)^q (rows re-orthonormalised before each product)."""

@@ -71,6 +71,10 @@ class Oracle:
                                   c_p, c_p],
             "lro_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, lro_solve_strategy, c_p, c_p, c_p],
             "lro_orth_rows": [c_i64, c_i64, c_p, c_i64, c_p, c_p],
+            "lro_srft_operator": [c_i64, c_i64, c_u64, c_p],
+            "lro_sketch_srft": [c_i64, c_i64, c_p, c_i64, c_i64, c_u64, c_p],
+            "lro_randomized_id_cfg": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
+                                      ctypes.c_int, c_u64, lro_solve_strategy, c_p, c_p, c_p],
             "lro_sketch_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_u64, c_p, c_p],
             "lro_randomized_id_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_u64, lro_solve_strategy, c_p, c_p, c_p],
@@ -170,6 +174,29 @@ class Oracle:
         self._chk(self.L.lro_orth_rows(ell, n, _p(y), ell, _p(out), _p(r)))
         return out[: int(r[0])]
 
+    def srft_operator(self, m, ell, seed):
+        out = np.empty((ell, m), order="F")
+        self._chk(self.L.lro_srft_operator(m, ell, seed, _p(out)))
+        return out
+
+    def sketch_srft(self, a, ell, seed):
+        a = _f(a)
+        m, n = a.shape
+        y = np.empty((ell, n), order="F")
+        self._chk(self.L.lro_sketch_srft(m, n, _p(a), m, ell, seed, _p(y)))
+        return y
+
+    def randomized_id_cfg(self, a, k, kind=0, oversample=10, srft_samples=0, q=0, reorth=True, seed=0,
+                          strategy=None):
+        a = _f(a)
+        m, n = a.shape
+        piv = np.empty(n, dtype=np.int64)
+        coeff = np.empty((k, n - k), order="F")
+        stats = np.zeros(1, dtype=np.int64)
+        self._chk(self.L.lro_randomized_id_cfg(m, n, _p(a), m, k, kind, oversample, srft_samples, q, int(reorth),
+                                               seed, strategy or self.strategy(), _p(piv), _p(coeff), _p(stats)))
+        return piv, coeff
+
     def sketch_power(self, a, ell, q, reorth, seed):
         a = _f(a)
         m, n = a.shape
@@ -262,6 +289,10 @@ class Ref:
             "lref_id_row": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p],
             "lref_randomized_id": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, c_u64, c_p, c_p],
             "lref_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p],
+            "lref_sketch_srft": [c_i64, c_i64, c_p, c_i64, c_i64, c_u64, c_p],
+            "lref_srft_operator": [c_i64, c_i64, c_u64, c_p],
+            "lref_randomized_id_cfg": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
+                                       ctypes.c_int, c_u64, c_p, c_p],
             "lref_sketch_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_u64, c_p, c_p],
             "lref_randomized_id_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          c_u64, c_p, c_p],
@@ -345,6 +376,27 @@ class Ref:
         piv = np.empty(n, dtype=np.int64)
         coeff = np.empty((k, n - k), order="F")
         self._chk(self.L.lref_randomized_id(m, n, _p(a), m, k, oversample, seed, _p(piv), _p(coeff)))
+        return piv, coeff
+
+    def sketch_srft(self, a, ell, seed):
+        a = _f(a)
+        m, n = a.shape
+        y = np.empty((ell, n), order="F")
+        self._chk(self.L.lref_sketch_srft(m, n, _p(a), m, ell, seed, _p(y)))
+        return y
+
+    def srft_operator(self, m, ell, seed):
+        out = np.empty((ell, m), order="F")
+        self._chk(self.L.lref_srft_operator(m, ell, seed, _p(out)))
+        return out
+
+    def randomized_id_cfg(self, a, k, kind=0, oversample=10, srft_samples=0, q=0, reorth=True, seed=0):
+        a = _f(a)
+        m, n = a.shape
+        piv = np.empty(n, dtype=np.int64)
+        coeff = np.empty((k, n - k), order="F")
+        self._chk(self.L.lref_randomized_id_cfg(m, n, _p(a), m, k, kind, oversample, srft_samples, q, int(reorth),
+                                                seed, _p(piv), _p(coeff)))
         return piv, coeff
 
     def sketch_power(self, a, ell, q, reorth, seed):

@@ -257,8 +257,6 @@ def test_validation_messages(lr, oracle):
         lr.randomized_id(a, 0)
     with pytest.raises(ValueError, match="sample count"):
         lr.randomized_id(a, 5, lr.SketchConfig(oversample=10))
-    with pytest.raises(NotImplementedError):
-        lr.randomized_id(a, 2, lr.SketchConfig(kind=lr.SketchKind.Srft))
     with pytest.raises(ValueError, match="q must be nonnegative"):
         lr.randomized_id(a, 2, lr.SketchConfig(power=-1))
 
@@ -318,3 +316,22 @@ def test_sketch_power_rows_span_the_oracle_sample(lr, oracle):
     qg, _ = np.linalg.qr(g.T)
     resid = o.T - qg @ (qg.T @ o.T)
     assert np.linalg.norm(resid) <= 1e-10 * np.linalg.norm(o)
+
+
+# ------------------------------------------------------------------ SRFT sketch
+@pytest.mark.parametrize("m", [1024, 1000])
+def test_sketch_srft_matches_oracle(lr, oracle, m):
+    """sketch.hpp:110-143: the GPU contracts A with the SRFT operator on the
+    tensor cores; the reference uses the fast Hartley transform when m is a
+    power of two (same operator, roundoff-level differences)."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], m, 700, width=300, k=50)
+    a = inputs.synthetic_np(cfg)
+    y = lr.sketch_srft(a, 100, 11).y
+    assert rel(y, oracle.sketch_srft(a, 100, 11)) <= 1e-12
+    cid = lr.randomized_id(a, 50, lr.SketchConfig(kind=lr.SketchKind.Srft, seed=11))
+    piv, coeff = oracle.randomized_id_cfg(a, 50, kind=1, seed=11)
+    assert np.array_equal(cid.pivots, piv) and rel(cid.coeff, coeff) <= TOL
+    cur = lr.randomized_cur(a, 50, lr.SketchConfig(kind=lr.SketchKind.Srft, srft_samples=80, power=1, seed=2),
+                            u_mode=lr.U_CPINV_A_RPINV)
+    piv2, _ = oracle.randomized_id_cfg(a, 50, kind=1, srft_samples=80, q=1, seed=2)
+    assert np.array_equal(cur.col_pivots, piv2)
