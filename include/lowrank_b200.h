@@ -125,6 +125,9 @@ int lr_sketch_gaussian(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64
                        uint64_t seed, double* y);
 int lr_sketch_gaussian_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
                          uint64_t seed, double* y, int64_t ldy);
+/* sketch.hpp:238-254 randomized_svd: u (m x k), sigma (k), v (n x k) */
+int lr_randomized_svd(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                      lr_sketch_config cfg, double* u, double* sigma, double* v);
 /* sketch.hpp:84-143 sketch_srft: y (ell x n, ld ell) = sqrt(m/ell) R H D A (random
    signs D, orthonormal Hartley transform H, ell sampled rows R) */
 int lr_sketch_srft(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,

@@ -950,6 +950,40 @@ int lro_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, in
   return rc;
 }
 
+/* sketch.hpp:238-254 */
+int lro_randomized_svd(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                       int64_t srft_samples, int q, int reorth, uint64_t seed, double* u, double* sigma, double* v) {
+  int rc;
+  if ((rc = require_rank_in_range(k, m, n, "randomized_svd"))) return rc;
+  const int64_t ell = kind == 0 ? k + (int64_t)oversample : (srft_samples > 0 ? srft_samples : 2 * k);
+  if (ell < k) return fail(LRO_EINVAL, "build_sample: sample count below target rank");
+  double* y = NEW(double, ell * n);
+  int64_t rows = ell, r = 0;
+  rc = kind == 0 ? lro_sketch_gaussian(m, n, a, lda, ell, seed, y) : lro_sketch_srft(m, n, a, lda, ell, seed, y);
+  if (!rc) rc = power_rounds(m, n, a, lda, ell, q, reorth, y, &rows);
+  if (!rc) rc = lro_orth_rows(rows, n, y, ell, y, &r);  /* q (r x n, ld ell) */
+  if (!rc && r < k) rc = fail(LRO_ERUNTIME, "randomized_svd: sample rank collapsed below target rank");
+  if (rc) { free(y); return rc; }
+  /* projected = a q^T (m x r) */
+  double* qt = NEW(double, n * r);
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < n; ++j) qt[IDX(j, i, n)] = y[IDX(i, j, ell)];
+  double* pr = NEW(double, m * r);
+  lro_gemm_nn(m, r, n, a, lda, qt, n, pr, m);
+  const int64_t rr = m < r ? m : r;
+  double* su = NEW(double, m * rr);
+  double* ss = NEW(double, rr);
+  double* sv = NEW(double, r * rr);
+  rc = lro_svd(m, r, pr, m, su, ss, sv);
+  if (!rc) {
+    memcpy(u, su, sizeof(double) * (size_t)(m * k));
+    memcpy(sigma, ss, sizeof(double) * (size_t)k);
+    lro_gemm_nn(n, k, r, qt, n, sv, r, v, n);  /* v = q^T small.v(:, :k) */
+  }
+  free(sv); free(ss); free(su); free(pr); free(qt); free(y);
+  return rc;
+}
+
 /* id.hpp:124-134 */
 int lro_tsid_from_column_id(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                             const int64_t* col_pivots, lro_solve_strategy strat, int64_t* row_pivots,

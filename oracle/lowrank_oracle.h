@@ -111,6 +111,11 @@ int lro_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, in
                           int64_t srft_samples, int q, int reorth, uint64_t seed, lro_solve_strategy strat,
                           int64_t* pivots, double* coeff, int64_t* stats);
 
+/* sketch.hpp:238-254 randomized_svd: u m x k, sigma k, v n x k (kind/oversample/
+ * srft_samples/q/reorth/seed as lro_randomized_id_cfg) */
+int lro_randomized_svd(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                       int64_t srft_samples, int q, int reorth, uint64_t seed, double* u, double* sigma, double* v);
+
 /* svd.hpp:216-235 orth_rows: Householder QR of y^T (n x ell), numerical rank
  * r (trailing |R_ii| <= max|R_ii| eps max(n, ell) dropped), out = thin Q^T:
  * r x n (ld ell; rows r..ell-1 untouched); *r_out = r */

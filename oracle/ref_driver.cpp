@@ -162,6 +162,24 @@ int lref_srft_operator(int64_t m, int64_t ell, uint64_t seed, double* out) {
   return guard([&] { to_ptr(srft_operator<double>(m, ell, seed), out); });
 }
 
+// sketch.hpp:238-254
+int lref_randomized_svd(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
+                        int64_t srft_samples, int q, int reorth, uint64_t seed, double* u, double* sigma, double* v) {
+  return guard([&] {
+    SketchConfig cfg;
+    cfg.kind = kind == 0 ? SketchKind::Gaussian : SketchKind::Srft;
+    cfg.oversample = oversample;
+    cfg.srft_samples = srft_samples;
+    cfg.seed = seed;
+    cfg.power = q;
+    cfg.reorthonormalize = reorth != 0;
+    auto s = randomized_svd(from_ptr(m, n, a, lda), k, cfg);
+    to_ptr(s.u, u);
+    for (int64_t i = 0; i < k; ++i) sigma[i] = s.sigma(i);
+    to_ptr(s.v, v);
+  });
+}
+
 // sketch.hpp:200-223 with a full SketchConfig
 int lref_randomized_id_cfg(int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, int kind, int oversample,
                            int64_t srft_samples, int q, int reorth, uint64_t seed, int64_t* pivots, double* coeff) {

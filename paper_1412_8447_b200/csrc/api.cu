@@ -1190,6 +1190,45 @@ int lr_sketch_gaussian(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
   });
 }
 
+// sketch.hpp:238-254 randomized_svd: u (m x k), sigma (k), v (n x k), all host
+int lr_randomized_svd(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_sketch_config cfg,
+                      double* u, double* sigma, double* v) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "randomized_svd");
+    require_rank_in_range(k, m, n, "randomized_svd");
+    int64_t ell = check_randomized_id(m, n, k, cfg);
+    int64_t l;
+    DBuf<double> d = to_dev(c, m, n, a, lda, &l);
+    int64_t ldy = work_ld(ell);
+    DBuf<double> Y((size_t)ldy * n, c->st);
+    zero_pad_rows(c, Y, ell, ldy, n);
+    sketch_core(c, m, n, d, l, ell, cfg.seed, Y, ldy, cfg.kind);
+    if (cfg.power > 0) power_rounds_core(c, m, n, d, l, cfg.power, cfg.reorthonormalize != 0, Y, ldy, ell);
+    // q = orth_rows(y): Q_y = q^T (n x r)
+    const int64_t ldn = even(n);
+    DBuf<double> Yt((size_t)ldn * ell, c->st), Qy((size_t)ldn * ell, c->st);
+    transpose_matrix(ell, n, Y, ldy, Yt, ldn, c->st);
+    const int64_t r = orth_cols_core(c, n, ell, Yt, ldn, Qy, ldn);
+    if (r < k) fail(LR_ERUNTIME, "randomized_svd: sample rank collapsed below target rank");
+    // projected = a q^T (m x r) = (A^T)^T Q_y with A^T materialised (K = n contiguous)
+    DBuf<double> At((size_t)ldn * m, c->st), Pm((size_t)even(m) * r, c->st);
+    transpose_matrix(m, n, d, l, At, ldn, c->st);
+    gemm(c, m, r, n, At, ldn, Qy, ldn, Pm, even(m));
+    const int64_t rr = std::min(m, r);
+    DBuf<double> su((size_t)m * rr, c->st), ss(rr, c->st), sv((size_t)r * rr, c->st);
+    svd_core(c, m, r, Pm, even(m), su, ss, sv);
+    // v = q^T small.v(:, :k): out (n x k) = P^T Q with P = Q_y^T (r x n), Q = small.v (r x k)
+    DBuf<double> Qyt((size_t)even(r) * n, c->st), vd((size_t)n * k, c->st);
+    transpose_matrix(n, r, Qy, ldn, Qyt, even(r), c->st);
+    gemm(c, n, k, r, Qyt, even(r), sv, r, vd, n);
+    to_host(c, m, k, su, m, u, m);
+    to_host(c, k, 1, ss, k, sigma, k);
+    to_host(c, n, k, vd, n, v, n);
+    sync(c);
+  });
+}
+
 // sketch.hpp:110-143: y (ell x n, ld ell)
 int lr_sketch_srft(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
                    double* y) {

@@ -24,7 +24,7 @@ __all__ = [
     "SketchConfig", "PivotedQr", "ColumnId", "RowId", "TwoSidedId", "CurDecomposition", "SampleMatrix",
     "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_srft", "sketch_power", "cpqr_partial", "cpqr_full",
     "stabilized_coeff_solve", "svd", "pinv", "id_column", "id_row", "tsid_from_column_id", "id_two_sided",
-    "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "select_columns", "select_rows",
+    "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "randomized_svd", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
     "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
@@ -350,6 +350,20 @@ def sketch_gaussian(a, ell: int, seed: int, ctx: Optional[Context] = None) -> Sa
 
 
 # ------------------------------------------------------------------ CPQR / solve / SVD
+def randomized_svd(a, k: int, cfg: Optional[SketchConfig] = None, ctx: Optional[Context] = None) -> Svd:
+    """sketch.hpp:238-254: orth_rows of the sample, SVD of A Q^T, truncated to rank k."""
+    c = _ctx(ctx)
+    a = _f64(a)
+    m, n = a.shape
+    kk = max(int(k), 1)
+    u = np.empty((m, kk), order="F")
+    s = np.empty(kk)
+    v = np.empty((n, kk), order="F")
+    _raise(c.lib.lr_randomized_svd(c.h, m, n, _ptr(a), _ld(a), int(k), (cfg or SketchConfig())._c(), _ptr(u), _ptr(s),
+                                   _ptr(v)))
+    return Svd(u, s, v)
+
+
 def sketch_srft(a, ell: int, seed: int, ctx: Optional[Context] = None) -> SampleMatrix:
     """sketch.hpp:110-143: sqrt(m/ell) R H D A (subsampled randomized Hartley transform)."""
     c = _ctx(ctx)

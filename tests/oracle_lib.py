@@ -72,6 +72,8 @@ class Oracle:
             "lro_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, lro_solve_strategy, c_p, c_p, c_p],
             "lro_orth_rows": [c_i64, c_i64, c_p, c_i64, c_p, c_p],
             "lro_srft_operator": [c_i64, c_i64, c_u64, c_p],
+            "lro_randomized_svd": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
+                                   ctypes.c_int, c_u64, c_p, c_p, c_p],
             "lro_sketch_srft": [c_i64, c_i64, c_p, c_i64, c_i64, c_u64, c_p],
             "lro_randomized_id_cfg": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
                                       ctypes.c_int, c_u64, lro_solve_strategy, c_p, c_p, c_p],
@@ -173,6 +175,16 @@ class Oracle:
         r = np.zeros(1, dtype=np.int64)
         self._chk(self.L.lro_orth_rows(ell, n, _p(y), ell, _p(out), _p(r)))
         return out[: int(r[0])]
+
+    def randomized_svd(self, a, k, kind=0, oversample=10, srft_samples=0, q=0, reorth=True, seed=0):
+        a = _f(a)
+        m, n = a.shape
+        u = np.empty((m, k), order="F")
+        s = np.empty(k)
+        v = np.empty((n, k), order="F")
+        self._chk(self.L.lro_randomized_svd(m, n, _p(a), m, k, kind, oversample, srft_samples, q, int(reorth), seed, _p(u),
+                            _p(s), _p(v)))
+        return u, s, v
 
     def srft_operator(self, m, ell, seed):
         out = np.empty((ell, m), order="F")
@@ -291,6 +303,8 @@ class Ref:
             "lref_tsid_from_column_id": [c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p],
             "lref_sketch_srft": [c_i64, c_i64, c_p, c_i64, c_i64, c_u64, c_p],
             "lref_srft_operator": [c_i64, c_i64, c_u64, c_p],
+            "lref_randomized_svd": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
+                                    ctypes.c_int, c_u64, c_p, c_p, c_p],
             "lref_randomized_id_cfg": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int,
                                        ctypes.c_int, c_u64, c_p, c_p],
             "lref_sketch_power": [c_i64, c_i64, c_p, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_u64, c_p, c_p],
@@ -384,6 +398,16 @@ class Ref:
         y = np.empty((ell, n), order="F")
         self._chk(self.L.lref_sketch_srft(m, n, _p(a), m, ell, seed, _p(y)))
         return y
+
+    def randomized_svd(self, a, k, kind=0, oversample=10, srft_samples=0, q=0, reorth=True, seed=0):
+        a = _f(a)
+        m, n = a.shape
+        u = np.empty((m, k), order="F")
+        s = np.empty(k)
+        v = np.empty((n, k), order="F")
+        self._chk(self.L.lref_randomized_svd(m, n, _p(a), m, k, kind, oversample, srft_samples, q, int(reorth), seed, _p(u),
+                            _p(s), _p(v)))
+        return u, s, v
 
     def srft_operator(self, m, ell, seed):
         out = np.empty((ell, m), order="F")

@@ -335,3 +335,18 @@ def test_sketch_srft_matches_oracle(lr, oracle, m):
                             u_mode=lr.U_CPINV_A_RPINV)
     piv2, _ = oracle.randomized_id_cfg(a, 50, kind=1, srft_samples=80, q=1, seed=2)
     assert np.array_equal(cur.col_pivots, piv2)
+
+
+# ------------------------------------------------------------------ randomized SVD
+@pytest.mark.parametrize("kw", [dict(), dict(power=1), dict(kind=1, seed=5)])
+def test_randomized_svd_matches_oracle(lr, oracle, kw):
+    """sketch.hpp:238-254: sigma within 1e-10; U and V columns equal up to sign
+    (the GPU's orthonormal sample basis may differ from Householder's by signs)."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 900, 700, width=300, k=40)
+    a = inputs.synthetic_np(cfg)
+    sk = lr.SketchConfig(kind=kw.get("kind", 0), power=kw.get("power", 0), seed=kw.get("seed", 1))
+    g = lr.randomized_svd(a, 30, sk)
+    uo, so, vo = oracle.randomized_svd(a, 30, kind=sk.kind, q=sk.power, seed=sk.seed)
+    assert rel(g.sigma, so) <= TOL
+    sgn = np.sign(np.sum(g.u * uo, axis=0))
+    assert rel(g.u * sgn, uo) <= 1e-9 and rel(g.v * sgn, vo) <= 1e-9
