@@ -125,6 +125,11 @@ int lr_sketch_gaussian(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64
                        uint64_t seed, double* y);
 int lr_sketch_gaussian_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell,
                          uint64_t seed, double* y, int64_t ldy);
+/* sketch.hpp:84-100 srft_operator: out (ell x m, ld ell) */
+int lr_srft_operator(lr_ctx* ctx, int64_t m, int64_t ell, uint64_t seed, double* out);
+/* svd.hpp:216-235 orth_rows: thin Q^T of the Householder QR of y^T, rank-trimmed:
+   out (ell x n, ld ell; first *r rows) */
+int lr_orth_rows(lr_ctx* ctx, int64_t ell, int64_t n, const double* y, int64_t ldy, double* out, int64_t* r);
 /* sketch.hpp:238-254 randomized_svd: u (m x k), sigma (k), v (n x k) */
 int lr_randomized_svd(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                       lr_sketch_config cfg, double* u, double* sigma, double* v);

@@ -10,8 +10,9 @@
 //   Svd / svd / pinv / spectral_norm         svd.hpp:16-207
 //   ColumnId / RowId / TwoSidedId / id_*     id.hpp:12-159
 //   CurDecomposition / cur_from_two_sided / cur_id / reconstruct  cur.hpp:9-80
-//   SketchConfig / SampleMatrix / sketch_gaussian / randomized_id /
-//   randomized_cur          sketch.hpp:21-234 (Gaussian sketch, power q >= 0)
+//   SketchConfig / SampleMatrix / sketch_gaussian / sketch_srft /
+//   srft_operator / sketch_power / randomized_id / randomized_cur /
+//   randomized_svd          sketch.hpp:21-254; orth_rows svd.hpp:216-235
 // Templates accept any Eigen::MatrixBase<Derived> with Scalar = double (the
 // B200 path is FP64; other scalars fail at compile time -- there is no CPU
 // fallback).  Needs <Eigen/Dense> (Eigen 3.4, or oracle/eigen_subset).
@@ -532,6 +533,66 @@ SampleMatrix<typename Derived::Scalar> sketch_gaussian(const Eigen::MatrixBase<D
   b200::check(lr_sketch_gaussian(b200::context(), d.rows(), d.cols(), d.data(), b200::ld(d), ell, seed,
                                  out.y.data()));
   out.provenance = {SketchKind::Gaussian, ell, 0, false, seed};
+  return out;
+}
+
+// sketch.hpp:84-100
+template <typename Scalar = double>
+MatrixX<Scalar> srft_operator(Index m, Index ell, std::uint64_t seed) {
+  static_assert(std::is_same_v<Scalar, double>, "the B200 path is FP64 only");
+  MatrixX<double> out(std::max<Index>(ell, 0), std::max<Index>(m, 0));
+  b200::check(lr_srft_operator(b200::context(), m, ell, seed, out.data()));
+  return out;
+}
+
+// sketch.hpp:110-143
+template <typename Derived>
+SampleMatrix<typename Derived::Scalar> sketch_srft(const Eigen::MatrixBase<Derived>& a, Index ell,
+                                                   std::uint64_t seed) {
+  MatrixX<double> d = b200::dense(a);
+  SampleMatrix<double> out;
+  out.y.resize(std::max<Index>(ell, 0), d.cols());
+  b200::check(lr_sketch_srft(b200::context(), d.rows(), d.cols(), d.data(), b200::ld(d), ell, seed, out.y.data()));
+  out.provenance = {SketchKind::Srft, ell, 0, false, seed};
+  return out;
+}
+
+// svd.hpp:216-235
+template <typename Derived>
+MatrixX<typename Derived::Scalar> orth_rows(const Eigen::MatrixBase<Derived>& y) {
+  MatrixX<double> d = b200::dense(y);
+  MatrixX<double> out(d.rows(), d.cols());
+  int64_t r = 0;
+  b200::check(lr_orth_rows(b200::context(), d.rows(), d.cols(), d.data(), b200::ld(d), out.data(), &r));
+  return MatrixX<double>(out.topRows(r));
+}
+
+// sketch.hpp:148-164
+template <typename Derived>
+SampleMatrix<typename Derived::Scalar> sketch_power(const Eigen::MatrixBase<Derived>& a, Index ell, int q,
+                                                    bool reorthonormalize, std::uint64_t seed) {
+  MatrixX<double> d = b200::dense(a);
+  MatrixX<double> y(std::max<Index>(ell, 0), d.cols());
+  int64_t rows = 0;
+  b200::check(lr_sketch_power(b200::context(), d.rows(), d.cols(), d.data(), b200::ld(d), ell, q,
+                              reorthonormalize ? 1 : 0, seed, y.data(), &rows));
+  SampleMatrix<double> out;
+  out.y = y.topRows(rows);
+  out.provenance = {SketchKind::Gaussian, ell, q, reorthonormalize && q > 0, seed};
+  return out;
+}
+
+// sketch.hpp:238-254
+template <typename Derived>
+Svd<typename Derived::Scalar> randomized_svd(const Eigen::MatrixBase<Derived>& a, Index k, const SketchConfig& cfg) {
+  MatrixX<double> d = b200::dense(a);
+  const Index m = d.rows(), n = d.cols(), kk = std::max<Index>(k, 0);
+  Svd<double> out;
+  out.u.resize(m, kk);
+  out.sigma.resize(kk);
+  out.v.resize(n, kk);
+  b200::check(lr_randomized_svd(b200::context(), m, n, d.data(), b200::ld(d), k, cfg.c_abi(), out.u.data(),
+                                out.sigma.data(), out.v.data()));
   return out;
 }
 

@@ -61,6 +61,8 @@ SIGNATURES = {
     "lr_gaussian_matrix": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
     "lr_gaussian_matrix_d": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp, c_i64], ctypes.c_int),
     "lr_sketch_gaussian": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
+    "lr_srft_operator": ([ctypes.c_void_p, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),
+    "lr_orth_rows": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, ctypes.POINTER(c_i64)], ctypes.c_int),
     "lr_randomized_svd": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config, c_dp, c_dp, c_dp],
                           ctypes.c_int),
     "lr_sketch_srft": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_u64, c_dp], ctypes.c_int),

@@ -1190,6 +1190,39 @@ int lr_sketch_gaussian(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
   });
 }
 
+// sketch.hpp:84-100 srft_operator: out (ell x m, ld ell), host
+int lr_srft_operator(lr_ctx* c, int64_t m, int64_t ell, uint64_t seed, double* out) {
+  return guard([&] {
+    checked(c);
+    require_sample_count(ell, m, "srft_operator");
+    DBuf<double> omt((size_t)m * ell, c->st), om((size_t)ell * m, c->st);
+    sketch_operator_t(c, m, ell, LR_SKETCH_SRFT, seed, omt);
+    transpose_matrix(m, ell, omt, m, om, ell, c->st);
+    to_host(c, ell, m, om, ell, out, ell);
+    sync(c);
+  });
+}
+
+// svd.hpp:216-235 orth_rows: out (first *r rows of ell x n, ld ell), host
+int lr_orth_rows(lr_ctx* c, int64_t ell, int64_t n, const double* y, int64_t ldy, double* out, int64_t* r) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(ell, n, "orth_rows");
+    int64_t l;
+    DBuf<double> d = to_dev(c, ell, n, y, ldy, &l);
+    const int64_t ldn = even(n);
+    DBuf<double> Yt((size_t)ldn * ell, c->st), Q((size_t)ldn * ell, c->st), Qt((size_t)ell * n, c->st);
+    transpose_matrix(ell, n, d, l, Yt, ldn, c->st);
+    const int64_t rr = orth_cols_core(c, n, ell, Yt, ldn, Q, ldn);
+    if (rr > 0) {
+      transpose_matrix(n, rr, Q, ldn, Qt, rr, c->st);
+      to_host(c, rr, n, Qt, rr, out, ell);
+    }
+    sync(c);
+    *r = rr;
+  });
+}
+
 // sketch.hpp:238-254 randomized_svd: u (m x k), sigma (k), v (n x k), all host
 int lr_randomized_svd(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_sketch_config cfg,
                       double* u, double* sigma, double* v) {
