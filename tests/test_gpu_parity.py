@@ -350,3 +350,14 @@ def test_randomized_svd_matches_oracle(lr, oracle, kw):
     assert rel(g.sigma, so) <= TOL
     sgn = np.sign(np.sum(g.u * uo, axis=0))
     assert rel(g.u * sgn, uo) <= 1e-9 and rel(g.v * sgn, vo) <= 1e-9
+
+
+def test_srft_dense_fallback_roundoff(lr, oracle):
+    """test_sketch.cpp:76-81 asks sketch_srft(a) == srft_operator(m, l, s) * a bitwise for
+    non-power-of-two m (the reference's fallback IS that host product); on the GPU the
+    contraction runs on the tensor cores, so the identity holds to roundoff."""
+    a = oracle.gaussian_matrix(48, 10, 70)
+    y = lr.sketch_srft(a, 12, 8).y
+    om = oracle.srft_operator(48, 12, 8)
+    assert np.max(np.abs(y - om @ a)) <= 1e-14 * np.max(np.abs(om @ a)) * 48
+    assert rel(y, oracle.sketch_srft(a, 12, 8)) <= 1e-14
