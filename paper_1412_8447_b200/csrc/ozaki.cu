@@ -160,13 +160,13 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
                                                     int* __restrict__ shift) {
   constexpr double M52 = 6755399441055744.0;  // 1.5 * 2^52
   constexpr float M23 = 12582912.0f;          // 1.5 * 2^23
-  const int64_t tiles_k = (K + kSplitTile - 1) / kSplitTile;
-  const int64_t total = tiles_k * cols;
-  // software pipeline: the next tile's 4 values are in flight while this
-  // tile's 64 residues are computed and stored
-  auto load = [&](int64_t t, double (&v)[kSplitRows]) {
-    const int64_t j = t / tiles_k, tk = t % tiles_k;
-    const int64_t i0 = tk * kSplitTile + (int64_t)kSplitRows * threadIdx.x;
+  // a CTA walks whole columns (j += gridDim.x) tile by tile: no index
+  // division, one scale per column, and a software pipeline: the next tile's
+  // 4 values are in flight while this tile's 64 residues are computed and stored
+  const int tiles_k = (int)((K + kSplitTile - 1) / kSplitTile);
+  const int64_t r_off = (int64_t)kSplitRows * threadIdx.x;
+  auto load = [&](int64_t j, int tk, double (&v)[kSplitRows]) {
+    const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
     const double* x = X + j * ldx + i0;
     if (vec2 && i0 + kSplitRows <= K) {
       const double2 a = __ldcs(reinterpret_cast<const double2*>(x));
@@ -178,64 +178,72 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
     }
   };
   double v[kSplitRows], vn[kSplitRows];
-  int64_t t = blockIdx.x;
-  if (t < total) load(t, v);
-  for (; t < total; t += gridDim.x) {
-    const int64_t tn = t + gridDim.x;
-    if (tn < total) load(tn, vn);
-    const int64_t j = t / tiles_k, tk = t % tiles_k;
-    const int64_t i0 = tk * kSplitTile + (int64_t)kSplitRows * threadIdx.x;
+  int64_t j = blockIdx.x;
+  int tk = 0;
+  if (j < cols) load(j, 0, v);
+  while (j < cols) {
     const double mx = __longlong_as_double((long long)cmax[j]);
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     const int sft = mx > 0.0 ? beta - e : 0;
-    if (tk == 0 && threadIdx.x == 0) shift[j] = sft;
-    if (i0 < K) {
-      const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
-      uint32_t byte[kOzakiModuli][kSplitRows];
+    if (threadIdx.x == 0) shift[j] = sft;
+    const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
+    int8_t* colp = planes + j * ldp;
+    for (; tk < tiles_k; ++tk) {
+      // prefetch the next tile (this column's next one, or the next column's first)
+      const bool last = tk + 1 == tiles_k;
+      const int64_t jn = last ? j + gridDim.x : j;
+      const int tkn = last ? 0 : tk + 1;
+      if (jn < cols) load(jn, tkn, vn);
+      const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
+      if (i0 < K) {
+        uint32_t byte[kOzakiModuli][kSplitRows];
 #pragma unroll
-      for (int q = 0; q < kSplitRows; ++q) {
-        const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
+        for (int q = 0; q < kSplitRows; ++q) {
+          const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
 #pragma unroll
-        for (int g = 0; g < kOzakiModuli / 2; ++g) {
-          const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
-          const double invP = 1.0 / P;
-          const double qg = fma(xp, invP, M52) - M52;
-          const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
-          if constexpr (UNS) {
-            const int iP = kmod(2 * g) * kmod(2 * g + 1);
-            const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
-            const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
+          for (int g = 0; g < kOzakiModuli / 2; ++g) {
+            const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
+            const double invP = 1.0 / P;
+            const double qg = fma(xp, invP, M52) - M52;
+            const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
+            if constexpr (UNS) {
+              const int iP = kmod(2 * g) * kmod(2 * g + 1);
+              const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
+              const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int tt = 2 * g + h;
-              const uint32_t mm = (uint32_t)kmod(tt);
-              const uint32_t magic = (uint32_t)((0x100000000ull + mm - 1) / mm);
-              byte[tt][q] = u - mm * __umulhi(u, magic);  // u mod m
-            }
-          } else {
-            const int lo = __double2loint(r + M52);
-            const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
-            const float rf = fb - M23;                           // r
+              for (int h = 0; h < 2; ++h) {
+                const int tt = 2 * g + h;
+                const uint32_t mm = (uint32_t)kmod(tt);
+                const uint32_t magic = (uint32_t)((0x100000000ull + mm - 1) / mm);
+                byte[tt][q] = u - mm * __umulhi(u, magic);  // u mod m
+              }
+            } else {
+              const int lo = __double2loint(r + M52);
+              const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
+              const float rf = fb - M23;                           // r
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int tt = 2 * g + h;
-              const float m = (float)kmod(tt);
-              const float qq = fmaf(rf, 1.0f / m, M23) - M23;
-              const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
-              byte[tt][q] = (uint32_t)__float_as_int(y);
+              for (int h = 0; h < 2; ++h) {
+                const int tt = 2 * g + h;
+                const float m = (float)kmod(tt);
+                const float qq = fmaf(rf, 1.0f / m, M23) - M23;
+                const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
+                byte[tt][q] = (uint32_t)__float_as_int(y);
+              }
             }
           }
         }
+        int8_t* out = colp + i0;
+#pragma unroll
+        for (int tt = 0; tt < kOzakiModuli; ++tt)
+          __stcs(reinterpret_cast<unsigned int*>(out + tt * plane_stride),
+                 pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]));
       }
-      int8_t* out = planes + j * ldp + i0;
 #pragma unroll
-      for (int tt = 0; tt < kOzakiModuli; ++tt)
-        __stcs(reinterpret_cast<unsigned int*>(out + tt * plane_stride),
-               pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]));
+      for (int q = 0; q < kSplitRows; ++q) v[q] = vn[q];
     }
-#pragma unroll
-    for (int q = 0; q < kSplitRows; ++q) v[q] = vn[q];
+    tk = 0;
+    j += gridDim.x;
   }
 }
 
@@ -495,8 +503,7 @@ void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cuda
   unsigned long long* cmax = nullptr;
   LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cmax), sizeof(unsigned long long) * cols, st));
   LRB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st));
-  const int64_t tiles = (K + kSplitTile - 1) / kSplitTile * cols;
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 8 * num_sms()));
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cols, 8 * num_sms()));  // split: whole columns per CTA
   const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
   const int64_t mtiles = (K + kMaxRowsPerThread * kSplitThreads - 1) / (kMaxRowsPerThread * kSplitThreads) * cols;
   const int gm = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, 8 * num_sms()));
