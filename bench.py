@@ -71,10 +71,24 @@ def ozaki_split_bytes(rows, cols):
     return 32.0 * rows * cols
 
 
+def measured_traffic(cfg):
+    """DRAM bytes per stage launch from the committed ncu capture
+    (profiles/r01_traffic.json, C4 shapes only), else None."""
+    if (cfg.m, cfg.n, cfg.k) != (M, N, K_RANK):
+        return {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f).get("per_launch", {})
+    except Exception:
+        return {}
+
+
 def kernel_rooflines(cfg, st, stages, engine):
     """Roofline entries of the step's big kernels from their CUDA-event stage
-    times (average per launch)."""
+    times (average per launch).  `traffic`: DRAM bytes per launch measured by
+    ncu (profiles/r01_traffic.json) where captured."""
     peaks = read_peaks()
+    traffic = measured_traffic(cfg) if engine == "ozaki" else {}
     hbm = peaks.get("hbm_gbs", 6548.5)
     ell = cfg.k + OVERSAMPLE
     out = {}
@@ -88,7 +102,7 @@ def kernel_rooflines(cfg, st, stages, engine):
                 ach = ops / (st[name] * 1e-3) / 1e12
                 out[name] = {"kernel": f"imma_gemm_kernel + crt_kernel ({what}, 16 INT8 residue GEMMs)",
                              "bound": "tensor", "achieved": round(ach, 1), "peak": round(i8, 1), "unit": "TOP/s",
-                             "frac": round(ach / i8, 4), "traffic": None,
+                             "frac": round(ach / i8, 4), "traffic": traffic.get(name),
                              "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (INT8 = 2x bf16 rate)",
                              "algorithmic": f"16 moduli x 2*{cols}*m*n = {ops:.4e} int8 op per launch"}
         if st.get("ozaki_split"):
@@ -97,7 +111,7 @@ def kernel_rooflines(cfg, st, stages, engine):
             ach = b / (stages["ozaki_split"]["ms"] / calls * 2 * 1e-3) / 1e9
             out["ozaki_split"] = {"kernel": "colmax_kernel + split_kernel (A, Omega^T, Q_c residue planes)",
                                   "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                                  "frac": round(ach / hbm, 4), "traffic": None,
+                                  "frac": round(ach / hbm, 4), "traffic": traffic.get("ozaki_split"),
                                   "algorithmic": "32 B per element of each split operand (read 8 + 8, write 16)"}
     else:
         for name, key, what in (("sketch_gemm", "sketch", "Y = Omega A"), ("ctA_gemm", "cta", "X^T = A^T Q_c")):
@@ -112,10 +126,14 @@ def kernel_rooflines(cfg, st, stages, engine):
         if st.get(name):
             b = cpqr_bytes(rows, cols, steps)
             ach = b / (st[name] * 1e-3) / 1e9
-            out[name] = {"kernel": "cpqr_kernel (persistent fused Householder step + norm downdate + argmax)",
+            out[name] = {"kernel": "cpqr_panel_kernel x16 + panel_update_kernel x15 (delayed-update CPQR, one "
+                                   "cooperative launch per 32 steps)",
                          "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(ach / hbm, 4), "traffic": None,
-                         "algorithmic": f"sum_s 16 (rows-s)(cols-s) + 32 (cols-s) = {b:.4e} B per launch"}
+                         "frac": round(ach / hbm, 4), "traffic": traffic.get(name),
+                         "algorithmic": f"SURVEY 8d right-looking count sum_s 16 (rows-s)(cols-s) + 32 (cols-s) "
+                                        f"= {b:.4e} B per launch (the panel form moves less: see traffic)",
+                         "note": "step-latency floor ~16 us/step (argmax -> reflector broadcast -> grid barrier) "
+                                 "x 510 steps; tools/bench_cpqr.py with LRB_CPQR_TRACE=1 breaks it down"}
     return out
 
 
