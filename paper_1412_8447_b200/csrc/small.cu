@@ -88,6 +88,59 @@ __global__ void backsub_operator_axpy_kernel(int64_t k, const double* __restrict
   }
 }
 
+// Register-pipelined variant for k <= 512: column i-1 of S11 (rows < i-1) and
+// its diagonal are loaded while the axpy of column i runs, so each step costs
+// a few shared-memory ops instead of an L2 round trip.  Same arithmetic order.
+constexpr int kPipeMaxK = 512;
+__global__ void backsub_operator_pipe_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11,
+                                             double threshold, double* __restrict__ M, int* __restrict__ zero_rows) {
+  extern __shared__ double xs_all[];
+  __shared__ double sh[32];
+  const double tol = threshold * block_max_abs_diag(k, s11, ld11, sh);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * kAxpyWarps + w;
+  if (blockIdx.x == 0)
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) zero_rows[i] = fabs(s11[i + i * ld11]) <= tol;
+  if (c >= k) return;
+  double* x = xs_all + (int64_t)w * k;
+  for (int64_t i = lane; i <= c; i += 32) x[i] = (i == c) ? 1.0 : 0.0;
+  double* mc = M + c * k;
+  for (int64_t i = c + 1 + lane; i < k; i += 32) mc[i] = 0.0;
+  constexpr int T = kPipeMaxK / 32;
+  double cur[T], nxt[T];
+  auto load = [&](int64_t i, double (&v)[T]) {
+    const double* col = s11 + i * ld11;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int64_t j = lane + 32 * t;
+      v[t] = j < i ? col[j] : 0.0;
+    }
+  };
+  load(c, cur);
+  double d = s11[c + c * ld11];
+  __syncwarp();
+  for (int64_t i = c; i >= 0; --i) {
+    double dn = 0.0;
+    if (i > 0) {
+      load(i - 1, nxt);
+      dn = s11[(i - 1) + (i - 1) * ld11];
+    }
+    const double mi = fabs(d) <= tol ? 0.0 : x[i] / d;
+    if (lane == 0) mc[i] = mi;
+    if (mi != 0.0) {
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int64_t j = lane + 32 * t;
+        if (j < i) x[j] = fma(-cur[t], mi, x[j]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < T; ++t) cur[t] = nxt[t];
+    d = dn;
+  }
+}
+
 __global__ void diag_minmax_kernel(int64_t k, const double* __restrict__ s11, int64_t ld11, double* out) {
   __shared__ double smx[32], smn[32];
   double mx = 0.0, mn = INFINITY;
@@ -301,7 +354,11 @@ __global__ void cholesky_upper_kernel(int64_t k, double* __restrict__ g, int64_t
 
 void launch_backsub_operator(int64_t k, const double* s11, int64_t ld11, double threshold, double* M, int* zr,
                              cudaStream_t st) {
-  if (k <= kAxpyMaxK) {
+  if (k <= kPipeMaxK) {
+    const size_t smem = sizeof(double) * kAxpyWarps * (size_t)k;
+    backsub_operator_pipe_kernel<<<(unsigned)((k + kAxpyWarps - 1) / kAxpyWarps), kAxpyWarps * 32, smem, st>>>(
+        k, s11, ld11, threshold, M, zr);
+  } else if (k <= kAxpyMaxK) {
     const size_t smem = sizeof(double) * kAxpyWarps * (size_t)k;
     static bool attr = false;
     if (!attr) {
