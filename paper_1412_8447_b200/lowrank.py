@@ -315,6 +315,16 @@ def default_context() -> Context:
 
 
 def _f64(a) -> np.ndarray:
+    """float64 column-major input; a column-major view with a padded leading
+    dimension (e.g. big[:m] of a Fortran array) is passed through uncopied."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 2 and a.strides[0] == 8 and a.strides[1] % 8 == 0 and a.strides[1] >= 8 * max(1, a.shape[0]):
+        return a
+    return np.asfortranarray(a)
+
+
+def _fc(a) -> np.ndarray:
+    """compact column-major float64 (arrays the ABI takes without a leading dimension)"""
     return np.asfortranarray(np.asarray(a, dtype=np.float64))
 
 
@@ -323,6 +333,9 @@ def _ptr(x: np.ndarray) -> int:
 
 
 def _ld(a: np.ndarray) -> int:
+    """leading dimension (elements between columns) of a column-major array"""
+    if a.ndim == 2 and a.shape[1] > 1 and a.strides[0] == 8:
+        return max(1, a.strides[1] // 8, a.shape[0])
     return max(1, a.shape[0])
 
 
@@ -521,7 +534,7 @@ def cur_from_two_sided(a, tsid: TwoSidedId, pinv_threshold: float = 1e-12, u_mod
     k = tsid.rank()
     cp = np.ascontiguousarray(tsid.col_pivots(), dtype=np.int64)
     rp = np.ascontiguousarray(tsid.row_pivots(), dtype=np.int64)
-    cc = _f64(tsid.col_id.coeff)
+    cc = _fc(tsid.col_id.coeff)
     C = np.empty((m, k), order="F")
     U = np.empty((k, k), order="F")
     R = np.empty((k, n), order="F")
@@ -620,7 +633,7 @@ def cur_error_fro(a, cur: CurDecomposition, ctx: Optional[Context] = None):
     m, n = a.shape
     k = cur.rank()
     out = np.empty(2)
-    C, U, R = _f64(cur.c), _f64(cur.u), _f64(cur.r)
+    C, U, R = _fc(cur.c), _fc(cur.u), _fc(cur.r)
     _raise(c.lib.lr_cur_error_fro(c.h, m, n, _ptr(a), _ld(a), k, _ptr(C), _ptr(U), _ptr(R), _ptr(out)))
     return float(out[0]), float(out[1])
 

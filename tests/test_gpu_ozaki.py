@@ -177,3 +177,52 @@ def test_host_pipeline_pinned_outputs_match(lr, oracle, engine):
     o = oracle.randomized_cur(a, 120, 10, 3, u_mode=1)
     assert np.array_equal(c2.col_pivots, o["col_pivots"]) and np.array_equal(c2.row_pivots, o["row_pivots"])
     assert rel(c2.u, o["u"]) <= TOL
+
+
+@pytest.mark.parametrize("shape,k", [((333, 257), 1), ((97, 1500), 40), ((1100, 600), 300)])
+def test_host_pipeline_edge_shapes_both_engines(lr, oracle, shape, k):
+    """Ragged shapes through the host entry point (chunked upload, m not a
+    multiple of 16, k = 1, n below one chunk): oracle index sets on both engines."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], shape[0], shape[1], width=min(shape), k=k)
+    a = inputs.synthetic_np(cfg)
+    o = oracle.randomized_cur(a, k, 5, 9, u_mode=1)
+    ctx = lr.default_context()
+    for mode in (ctx.GEMM_DMMA, ctx.GEMM_OZAKI_INT8):
+        ctx.set_gemm_mode(mode)
+        try:
+            cur = lr.randomized_cur(a, k, lr.SketchConfig(oversample=5, seed=9), u_mode=lr.U_CPINV_A_RPINV)
+        finally:
+            ctx.set_gemm_mode(ctx.GEMM_DMMA)
+        assert np.array_equal(cur.col_pivots, o["col_pivots"]) and np.array_equal(cur.row_pivots, o["row_pivots"])
+        assert rel(cur.u, o["u"]) <= TOL
+
+
+def test_host_pipeline_nonfinite_and_strided_input(lr):
+    """A NaN in the last upload chunk is reported with the reference's message;
+    a strided (lda > m) host matrix gives the same factors as its compact copy."""
+    a = np.asfortranarray(np.random.default_rng(3).standard_normal((700, 2100)))
+    big = np.zeros((760, 2100), order="F")
+    big[:700] = a
+    view = big[:700]
+    ctx = lr.default_context()
+    for mode in (ctx.GEMM_DMMA, ctx.GEMM_OZAKI_INT8):
+        ctx.set_gemm_mode(mode)
+        try:
+            c1 = lr.randomized_cur(a, 30, lr.SketchConfig(seed=4))
+            c2 = lr.randomized_cur(view, 30, lr.SketchConfig(seed=4))
+            assert np.array_equal(c1.col_pivots, c2.col_pivots) and np.array_equal(c1.u, c2.u)
+            bad = a.copy()
+            bad[5, 2099] = np.nan
+            with pytest.raises(ValueError, match="non-finite"):
+                lr.randomized_cur(bad, 30, lr.SketchConfig(seed=4))
+        finally:
+            ctx.set_gemm_mode(ctx.GEMM_DMMA)
+
+
+def test_ozaki_gemm_large_k_falls_back(lr, ozaki):
+    """K > 2^17 exceeds exact int32 accumulation: the engine runs DMMA instead."""
+    rng = np.random.default_rng(2)
+    P = rng.standard_normal((140000, 3))
+    Q = rng.standard_normal((140000, 2))
+    out = _gemm(lr, ozaki, P, Q)
+    assert rel(out, P.T @ Q) <= 1e-13
