@@ -15,8 +15,11 @@
 // as accurate as an FP64 GEMM (accumulation itself is exact here).  The scaled
 // residue planes of an operand can be kept and reused: A enters both big
 // contractions of the CUR with the same per-column scaling.
+#include <climits>
 #include <cstring>
 #include <vector>
+
+#include <math_constants.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -107,37 +110,44 @@ void upload_constants() {
 //   * bytes of 4 consecutive K entries are packed per plane (PRMT), one
 //     coalesced 4-byte store per plane.
 constexpr int kSplitRows = 4;  // K entries per thread per tile
+constexpr int kOzakiNonFinite = INT_MIN;  // shift sentinel of a column with NaN / Inf
 constexpr int kSplitThreads = 256;
 constexpr int kSplitTile = kSplitRows * kSplitThreads;
 
 constexpr int kMaxRowsPerThread = 32;  // colmax: 8192-row tiles, 16 double2 loads in flight per thread
 __global__ void __launch_bounds__(256) colmax_kernel(int64_t K, int64_t cols, const double* __restrict__ X,
                                                      int64_t ldx, bool vec2, unsigned long long* __restrict__ cmax) {
-  __shared__ double sh[8];
+  __shared__ unsigned long long sh[8];
   constexpr int64_t kTile = (int64_t)kMaxRowsPerThread * kSplitThreads;
   const int64_t tiles_k = (K + kTile - 1) / kTile;
   for (int64_t t = blockIdx.x; t < tiles_k * cols; t += gridDim.x) {
     const int64_t j = t / tiles_k, i0 = (t % tiles_k) * kTile;
     const double* x = X + j * ldx;
-    double mx = 0.0;
+    // max of |x| as a bit pattern: NaN / Inf patterns exceed every finite one,
+    // so a non-finite column is recognised by the split (fmax would drop NaN)
+    unsigned long long mx = 0;
     if (vec2 && i0 + kTile <= K) {
       double2 r[kMaxRowsPerThread / 2];
 #pragma unroll
       for (int e = 0; e < kMaxRowsPerThread / 2; ++e)
         r[e] = __ldcs(reinterpret_cast<const double2*>(x + i0 + 2 * (e * kSplitThreads + threadIdx.x)));
 #pragma unroll
-      for (int e = 0; e < kMaxRowsPerThread / 2; ++e) mx = fmax(mx, fmax(fabs(r[e].x), fabs(r[e].y)));
+      for (int e = 0; e < kMaxRowsPerThread / 2; ++e) {
+        mx = max(mx, (unsigned long long)__double_as_longlong(fabs(r[e].x)));
+        mx = max(mx, (unsigned long long)__double_as_longlong(fabs(r[e].y)));
+      }
     } else {
-      for (int64_t i = i0 + threadIdx.x; i < K && i < i0 + kTile; i += kSplitThreads) mx = fmax(mx, fabs(x[i]));
+      for (int64_t i = i0 + threadIdx.x; i < K && i < i0 + kTile; i += kSplitThreads)
+        mx = max(mx, (unsigned long long)__double_as_longlong(fabs(x[i])));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double m = sh[0];
-      for (int w = 1; w < kSplitThreads / 32; ++w) m = fmax(m, sh[w]);
-      if (m > 0.0) atomicMax(cmax + j, (unsigned long long)__double_as_longlong(m));
+      unsigned long long m = sh[0];
+      for (int w = 1; w < kSplitThreads / 32; ++w) m = max(m, sh[w]);
+      if (m > 0) atomicMax(cmax + j, m);
     }
     __syncthreads();
   }
@@ -184,9 +194,10 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
   while (j < cols) {
     const double mx = __longlong_as_double((long long)cmax[j]);
     int e = 0;
-    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
-    const int sft = mx > 0.0 ? beta - e : 0;
-    if (threadIdx.x == 0) shift[j] = sft;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);  // mx < 2^e
+    const int sft = (mx > 0.0 && isfinite(mx)) ? beta - e : 0;
+    // non-finite column: the sentinel makes every product entry NaN (crt_kernel)
+    if (threadIdx.x == 0) shift[j] = isfinite(mx) ? sft : kOzakiNonFinite;
     const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
     int8_t* colp = planes + j * ldp;
     for (; tk < tiles_k; ++tk) {
@@ -453,7 +464,8 @@ __global__ void crt_kernel(int64_t M, int64_t N, const int8_t* __restrict__ res,
     const double lo = (double)(unsigned long long)a;
     double v = fma(hi, 18446744073709551616.0, lo);
     if (neg) v = -v;
-    v = ldexp(v, -(shift_p[i] + shift_q[j]));
+    v = (shift_p[i] == kOzakiNonFinite || shift_q[j] == kOzakiNonFinite) ? CUDART_NAN
+                                                                         : ldexp(v, -(shift_p[i] + shift_q[j]));
     double* o = out + i + j * ldo;
     *o = beta == 0.0 ? alpha * v : alpha * v + beta * *o;
   }

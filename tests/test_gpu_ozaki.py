@@ -226,3 +226,18 @@ def test_ozaki_gemm_large_k_falls_back(lr, ozaki):
     Q = rng.standard_normal((140000, 2))
     out = _gemm(lr, ozaki, P, Q)
     assert rel(out, P.T @ Q) <= 1e-13
+
+
+def test_ozaki_gemm_propagates_nonfinite(lr, ozaki):
+    """A NaN or Inf in an operand column makes that product column non-finite
+    (as an FP64 GEMM would), so the pipeline's finiteness checks still fire."""
+    rng = np.random.default_rng(4)
+    P = rng.standard_normal((500, 20))
+    Q = rng.standard_normal((500, 30))
+    P[7, 3] = np.nan
+    Q[11, 5] = np.inf
+    out = _gemm(lr, ozaki, P, Q)
+    assert np.all(np.isnan(out[3, :])) and np.all(~np.isfinite(out[:, 5]))
+    keep = np.ones(20, bool)
+    keep[3] = False
+    assert np.all(np.isfinite(np.delete(out[keep], 5, axis=1)))
