@@ -361,3 +361,16 @@ def test_srft_dense_fallback_roundoff(lr, oracle):
     om = oracle.srft_operator(48, 12, 8)
     assert np.max(np.abs(y - om @ a)) <= 1e-14 * np.max(np.abs(om @ a)) * 48
     assert rel(y, oracle.sketch_srft(a, 12, 8)) <= 1e-14
+
+
+@pytest.mark.parametrize("shape,k", [((250, 37), 37), ((250, 1), 1), ((300, 700), 33), ((512, 1300), 512),
+                                     ((500, 3000), 31)])
+def test_panel_cpqr_edge_shapes(lr, oracle, shape, k):
+    """The delayed-update CPQR (ld 256 / 320 / 512) at ragged panel counts, few
+    columns (fewer than one warp per CTA), a single column, a full 512-row panel
+    set, and k < one panel: the oracle's pivots, S and Q."""
+    a = oracle.gaussian_matrix(shape[0], shape[1], shape[0] + shape[1] + k)
+    q = lr.cpqr_partial(a, k)
+    o = oracle.cpqr(a, k, want_q=True)
+    assert np.array_equal(q.pivots, o["pivots"])
+    assert rel(q.s, o["s"]) <= 1e-12 and rel(q.q, o["q"]) <= 1e-12
