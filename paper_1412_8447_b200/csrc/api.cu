@@ -236,13 +236,16 @@ constexpr int64_t kOzakiMaxK = int64_t(1) << 17;
 // it; persistent slots keep steady-state calls allocation-free).  `cacheable`
 // operands (A of the current CUR call) are split once and reused while an
 // OzakiScope is open; `tmp_slot` 0/1 picks the slots of the other operand.
-const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
+const OzakiOperand* ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
                                   int tmp_slot, OzakiOperand& out) {
   const int beta = ozaki_beta(K);
   if (cacheable) {  // the input matrix: kOzA slot, reused while an OzakiScope is open
     if (c->oz_cache_on && c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx)
-      return c->oz_op;
-    c->oz_op.planes = static_cast<int8_t*>(c->ws.get(WsSlot::kOzA, ozaki_plane_bytes(K, cols)));
+      return &c->oz_op;
+    c->oz_src = nullptr;
+    int8_t* pl = static_cast<int8_t*>(c->ws.try_get(WsSlot::kOzA, ozaki_plane_bytes(K, cols)));
+    if (!pl) return nullptr;  // no room for the planes: the caller runs the DMMA GEMM
+    c->oz_op.planes = pl;
     c->oz_op.shift = static_cast<int*>(c->ws.get(WsSlot::kOzAShift, sizeof(int) * (size_t)cols));
     c->oz_op.unsigned_res = K <= kOzakiMaxKUnsigned;  // A: the cheap u8 split (its partner stays s8)
     ozaki_split(K, cols, X, ldx, beta, c->oz_op, c->st);
@@ -250,13 +253,14 @@ const OzakiOperand& ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const doub
     c->oz_K = K;
     c->oz_cols = cols;
     c->oz_ld = ldx;
-    return c->oz_op;
+    return &c->oz_op;
   }
-  out.planes = static_cast<int8_t*>(c->ws.get(tmp_slot ? WsSlot::kOzQ : WsSlot::kOzP, ozaki_plane_bytes(K, cols)));
+  out.planes = static_cast<int8_t*>(c->ws.try_get(tmp_slot ? WsSlot::kOzQ : WsSlot::kOzP, ozaki_plane_bytes(K, cols)));
+  if (!out.planes) return nullptr;
   out.shift = static_cast<int*>(c->ws.get(tmp_slot ? WsSlot::kOzQShift : WsSlot::kOzPShift, sizeof(int) * (size_t)cols));
   out.unsigned_res = false;
   ozaki_split(K, cols, X, ldx, beta, out, c->st);
-  return out;
+  return &out;
 }
 
 // out (M x N) = P^T Q where P or Q is the input matrix A (`a_side` 0: P, 1: Q)
@@ -267,10 +271,14 @@ void gemm_a(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t
     return;
   }
   OzakiOperand op, oq;
-  const OzakiOperand& Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, 0, op);
-  const OzakiOperand& Qo = ozaki_operand(c, K, N, Q, ldq, a_side == 1, 1, oq);
+  const OzakiOperand* Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, 0, op);
+  const OzakiOperand* Qo = Po ? ozaki_operand(c, K, N, Q, ldq, a_side == 1, 1, oq) : nullptr;
+  if (!Po || !Qo) {  // residue planes do not fit next to the caller's data: FP64 DMMA
+    gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
+    return;
+  }
   mark(c, "ozaki_split");
-  ozaki_gemm_tn(c->ws, Po, Qo, M, N, out, ldo, 1.0, 0.0, c->st);
+  ozaki_gemm_tn(c->ws, *Po, *Qo, M, N, out, ldo, 1.0, 0.0, c->st);
 }
 
 // Scope of one CUR call: A's residue planes live until it closes.
@@ -919,12 +927,16 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
   cudaStream_t up = aux_stream(c->up_st);
   DBuf<double> omt((size_t)m * even(ell), c->st);
   sketch_operator_t(c, m, ell, kind, seed, omt);
-  const bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
+  bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
   OzakiOperand om;
+  int8_t* aplanes = nullptr;
   if (oz) {
-    ozaki_operand(c, m, ell, omt, m, false, 0, om);
-    // the cached operand of A, filled chunk by chunk
-    c->oz_op.planes = static_cast<int8_t*>(c->ws.get(WsSlot::kOzA, ozaki_plane_bytes(m, n)));
+    // the cached operand of A, filled chunk by chunk (DMMA when the planes do not fit)
+    aplanes = static_cast<int8_t*>(c->ws.try_get(WsSlot::kOzA, ozaki_plane_bytes(m, n)));
+    oz = aplanes != nullptr && ozaki_operand(c, m, ell, omt, m, false, 0, om) != nullptr;
+  }
+  if (oz) {
+    c->oz_op.planes = aplanes;
     c->oz_op.shift = static_cast<int*>(c->ws.get(WsSlot::kOzAShift, sizeof(int) * (size_t)n));
     c->oz_op.K = m;
     c->oz_op.cols = n;

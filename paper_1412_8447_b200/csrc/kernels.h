@@ -47,6 +47,8 @@ class Workspace {
   Workspace() : ptr_((size_t)WsSlot::kCount, nullptr), cap_((size_t)WsSlot::kCount, 0) {}
   ~Workspace();
   void* get(WsSlot s, size_t bytes);
+  // like get(), but nullptr instead of an exception when the device is out of memory
+  void* try_get(WsSlot s, size_t bytes);
   double* get_doubles(WsSlot s, size_t n) { return static_cast<double*>(get(s, n * sizeof(double))); }
   void release_all();
 

@@ -23,6 +23,26 @@ void Workspace::release_all() {
   for (auto& c : cap_) c = 0;
 }
 
+void* Workspace::try_get(WsSlot s, size_t bytes) {
+  const size_t i = static_cast<size_t>(s);
+  if (bytes == 0) bytes = 16;
+  if (cap_[i] >= bytes) return ptr_[i];
+  if (ptr_[i]) {
+    LRB_CUDA(cudaDeviceSynchronize());
+    LRB_CUDA(cudaFree(ptr_[i]));
+    ptr_[i] = nullptr;
+    cap_[i] = 0;
+  }
+  const size_t rounded = (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+  if (cudaMalloc(&ptr_[i], rounded) != cudaSuccess) {
+    cudaGetLastError();
+    ptr_[i] = nullptr;
+    return nullptr;
+  }
+  cap_[i] = rounded;
+  return ptr_[i];
+}
+
 void* Workspace::get(WsSlot s, size_t bytes) {
   const size_t i = static_cast<size_t>(s);
   if (bytes == 0) bytes = 16;

@@ -241,3 +241,27 @@ def test_ozaki_gemm_propagates_nonfinite(lr, ozaki):
     keep = np.ones(20, bool)
     keep[3] = False
     assert np.all(np.isfinite(np.delete(out[keep], 5, axis=1)))
+
+
+def test_ozaki_falls_back_to_dmma_when_planes_do_not_fit(lr, oracle):
+    """With too little free HBM for A's residue planes (2 B per byte of A) the
+    Ozaki engine runs the FP64 DMMA GEMM instead of failing."""
+    import torch
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 12000, 12000, width=1024, k=100)
+    a = inputs.synthetic_np(cfg)
+    sk = lr.SketchConfig(oversample=10, seed=6)
+    ref = lr.randomized_cur(a, 100, sk, u_mode=lr.U_CPINV_A_RPINV)
+    ctx = lr.default_context()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    free = torch.cuda.mem_get_info()[0]
+    filler = torch.empty(max(0, free - int(3.2e9)), dtype=torch.uint8, device="cuda")
+    try:
+        ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+        cur = lr.randomized_cur(a, 100, sk, u_mode=lr.U_CPINV_A_RPINV)
+    finally:
+        ctx.set_gemm_mode(ctx.GEMM_DMMA)
+        del filler
+        torch.cuda.empty_cache()
+    assert np.array_equal(cur.col_pivots, ref.col_pivots) and np.array_equal(cur.row_pivots, ref.row_pivots)
+    assert rel(cur.u, ref.u) <= TOL
