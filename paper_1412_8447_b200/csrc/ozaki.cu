@@ -208,47 +208,43 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
       if (jn < cols) load(jn, tkn, vn);
       const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
       if (i0 < K) {
-        uint32_t byte[kOzakiModuli][kSplitRows];
+        // modulus pair outer, element inner: the 4 elements' bytes of a plane
+        // are packed and stored as soon as they exist (few live registers)
+        double xp[kSplitRows];
 #pragma unroll
-        for (int q = 0; q < kSplitRows; ++q) {
-          const double xp = rint((v[q] * sc1) * sc2);  // exact integer, |xp| <= 2^beta
+        for (int q = 0; q < kSplitRows; ++q) xp[q] = rint((v[q] * sc1) * sc2);  // exact, |xp| <= 2^beta
+        int8_t* out = colp + i0;
 #pragma unroll
-          for (int g = 0; g < kOzakiModuli / 2; ++g) {
-            const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
-            const double invP = 1.0 / P;
-            const double qg = fma(xp, invP, M52) - M52;
-            const double r = fma(-qg, P, xp);  // exact, |r| < 2^17
+        for (int g = 0; g < kOzakiModuli / 2; ++g) {
+          const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
+          const double invP = 1.0 / P;
+          uint32_t b0[kSplitRows], b1[kSplitRows];
+#pragma unroll
+          for (int q = 0; q < kSplitRows; ++q) {
+            const double qg = fma(xp[q], invP, M52) - M52;
+            const double r = fma(-qg, P, xp[q]);  // exact, |r| < 2^17
             if constexpr (UNS) {
               const int iP = kmod(2 * g) * kmod(2 * g + 1);
               const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
               const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int tt = 2 * g + h;
-                const uint32_t mm = (uint32_t)kmod(tt);
-                const uint32_t magic = (uint32_t)((0x100000000ull + mm - 1) / mm);
-                byte[tt][q] = u - mm * __umulhi(u, magic);  // u mod m
-              }
+              const uint32_t m0 = (uint32_t)kmod(2 * g), m1 = (uint32_t)kmod(2 * g + 1);
+              b0[q] = u - m0 * __umulhi(u, (uint32_t)((0x100000000ull + m0 - 1) / m0));  // u mod m
+              b1[q] = u - m1 * __umulhi(u, (uint32_t)((0x100000000ull + m1 - 1) / m1));
             } else {
               const int lo = __double2loint(r + M52);
               const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
               const float rf = fb - M23;                           // r
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int tt = 2 * g + h;
-                const float m = (float)kmod(tt);
-                const float qq = fmaf(rf, 1.0f / m, M23) - M23;
-                const float y = fmaf(-qq, m, fb);  // 1.5*2^23 + residue, exact
-                byte[tt][q] = (uint32_t)__float_as_int(y);
-              }
+              const float m0 = (float)kmod(2 * g), m1 = (float)kmod(2 * g + 1);
+              const float q0 = fmaf(rf, 1.0f / m0, M23) - M23;
+              const float q1 = fmaf(rf, 1.0f / m1, M23) - M23;
+              b0[q] = (uint32_t)__float_as_int(fmaf(-q0, m0, fb));  // 1.5*2^23 + residue, exact
+              b1[q] = (uint32_t)__float_as_int(fmaf(-q1, m1, fb));
             }
           }
+          __stcs(reinterpret_cast<unsigned int*>(out + (2 * g) * plane_stride), pack4(b0[0], b0[1], b0[2], b0[3]));
+          __stcs(reinterpret_cast<unsigned int*>(out + (2 * g + 1) * plane_stride),
+                 pack4(b1[0], b1[1], b1[2], b1[3]));
         }
-        int8_t* out = colp + i0;
-#pragma unroll
-        for (int tt = 0; tt < kOzakiModuli; ++tt)
-          __stcs(reinterpret_cast<unsigned int*>(out + tt * plane_stride),
-                 pack4(byte[tt][0], byte[tt][1], byte[tt][2], byte[tt][3]));
       }
 #pragma unroll
       for (int q = 0; q < kSplitRows; ++q) v[q] = vn[q];
