@@ -109,7 +109,7 @@ void upload_constants() {
 //     r/m from a half-integer for odd m; 1/256 is exact);
 //   * bytes of 4 consecutive K entries are packed per plane (PRMT), one
 //     coalesced 4-byte store per plane.
-constexpr int kSplitRows = 4;  // K entries per thread per tile
+constexpr int kSplitRows = 8;  // K entries per thread per tile
 constexpr int kOzakiNonFinite = INT_MIN;  // shift sentinel of a column with NaN / Inf
 constexpr int kSplitThreads = 256;
 constexpr int kSplitTile = kSplitRows * kSplitThreads;
@@ -179,9 +179,12 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
     const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
     const double* x = X + j * ldx + i0;
     if (vec2 && i0 + kSplitRows <= K) {
-      const double2 a = __ldcs(reinterpret_cast<const double2*>(x));
-      const double2 b = __ldcs(reinterpret_cast<const double2*>(x + 2));
-      v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+#pragma unroll
+      for (int h = 0; h < kSplitRows / 2; ++h) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(x + 2 * h));
+        v[2 * h] = a.x;
+        v[2 * h + 1] = a.y;
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < kSplitRows; ++q) v[q] = i0 + q < K ? x[q] : 0.0;
@@ -241,9 +244,11 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
               b1[q] = (uint32_t)__float_as_int(fmaf(-q1, m1, fb));
             }
           }
-          __stcs(reinterpret_cast<unsigned int*>(out + (2 * g) * plane_stride), pack4(b0[0], b0[1], b0[2], b0[3]));
-          __stcs(reinterpret_cast<unsigned int*>(out + (2 * g + 1) * plane_stride),
-                 pack4(b1[0], b1[1], b1[2], b1[3]));
+          static_assert(kSplitRows == 8, "two packed words per plane");
+          __stcs(reinterpret_cast<uint2*>(out + (2 * g) * plane_stride),
+                 make_uint2(pack4(b0[0], b0[1], b0[2], b0[3]), pack4(b0[4], b0[5], b0[6], b0[7])));
+          __stcs(reinterpret_cast<uint2*>(out + (2 * g + 1) * plane_stride),
+                 make_uint2(pack4(b1[0], b1[1], b1[2], b1[3]), pack4(b1[4], b1[5], b1[6], b1[7])));
         }
       }
 #pragma unroll
