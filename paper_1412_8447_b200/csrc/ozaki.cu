@@ -35,6 +35,16 @@ __host__ __device__ constexpr int kmod(int t) {
        : t == 7 ? 233 : t == 8 ? 229 : t == 9 ? 227 : t == 10 ? 223 : t == 11 ? 217 : t == 12 ? 211
        : t == 13 ? 199 : t == 14 ? 197 : 193;
 }
+// CRT constants for the 16 moduli (checked against crt_host() at first use)
+__host__ __device__ constexpr int kcrt_inv(int t) {
+  return t == 0 ? 33 : t == 1 ? 224 : t == 2 ? 195 : t == 3 ? 157 : t == 4 ? 135 : t == 5 ? 5 : t == 6 ? 184 : t == 7 ? 231 : t == 8 ? 30 : t == 9 ? 125 : t == 10 ? 34 : t == 11 ? 69 : t == 12 ? 138 : t == 13 ? 45 : t == 14 ? 125 : 116;
+}
+__host__ __device__ constexpr unsigned long long kcrt_lo(int t) {
+  return t == 0 ? 0x4f49e5694da9b2e1ull : t == 1 ? 0xdc260b74c26c1f00ull : t == 2 ? 0x9d2149451d00b500ull : t == 3 ? 0xce517cd98d6cd300ull : t == 4 ? 0xbf00edc53ccce700ull : t == 5 ? 0xf38f4acb35d0f100ull : t == 6 ? 0x6fb4e8e030e92f00ull : t == 7 ? 0x400adf7d96273900ull : t == 8 ? 0xe460060ca2d64d00ull : t == 9 ? 0x22287b63959c6b00ull : t == 10 ? 0x1d07eaa91a043f00ull : t == 11 ? 0xbe46a92f8bfd4900ull : t == 12 ? 0x163067a0850cfb00ull : t == 13 ? 0x64b68a2d6a571700ull : t == 14 ? 0x20dcc75b5bd36d00ull : 0x104ccb7d161a2100ull;
+}
+__host__ __device__ constexpr unsigned long long kcrt_hi(int t) {
+  return t == 0 ? 0x2984652cbaccc5ull : t == 1 ? 0x29ae133ffac78cull : t == 2 ? 0x2a026c7210ffc4ull : t == 3 ? 0x2a581dc182587full : t == 4 ? 0x2b07aa28241161ull : t == 5 ? 0x2c19e9e0e86b0aull : t == 6 ? 0x2c7863cd5e0b89ull : t == 7 ? 0x2d9d8cd3c1274dull : t == 8 ? 0x2e698658032147ull : t == 9 ? 0x2ed235339261dbull : t == 10 ? 0x2fa93501fc538aull : t == 11 ? 0x30fa914fe6fd5eull : t == 12 ? 0x325f1d5499d7afull : t == 13 ? 0x3568b59c98d3f7ull : t == 14 ? 0x35f384c67897beull : 0x3711c48aea8303ull;
+}
 __constant__ int c_mod[kOzakiModuli];
 __constant__ double c_inv_mod[kOzakiModuli];
 __constant__ unsigned long long c_Mt[kOzakiModuli][2];  // M / m_t (low, high limbs)
@@ -78,6 +88,10 @@ void upload_constants() {
   static bool done = false;
   if (done) return;
   const CrtHost& h = crt_host();
+  for (int t = 0; t < kOzakiModuli; ++t)
+    if (kmod(t) != kMod[t] || kcrt_inv(t) != h.inv[t] || kcrt_lo(t) != (unsigned long long)h.Mt[t] ||
+        kcrt_hi(t) != (unsigned long long)(h.Mt[t] >> 64))
+      throw CudaError("ozaki: compiled CRT constants disagree with the moduli");
   double inv[kOzakiModuli];
   unsigned long long mt[kOzakiModuli][2], mm[2];
   for (int t = 0; t < kOzakiModuli; ++t) {
@@ -444,31 +458,36 @@ __global__ void crt_kernel(int64_t M, int64_t N, const int8_t* __restrict__ res,
                            int64_t ldo, double alpha, double beta) {
   const i128 Mc = (i128)(((u128)c_Mcrt[1] << 64) | (u128)c_Mcrt[0]);
   const i128 half = Mc >> 1;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M * N; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % M, j = t / M;
-    i128 s = 0;
+  // 2D walk (rows fastest): no per-element 64-bit index division; moduli,
+  // inverses and M / m_t are compile-time constants of the unrolled loop
+  for (int64_t j = blockIdx.y; j < N; j += gridDim.y) {
+    const int sq = shift_q[j];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+      const int8_t* r = res + j * ldr + i;
+      i128 s = 0;
 #pragma unroll
-    for (int p = 0; p < kOzakiModuli; ++p) {
-      const int m = c_mod[p];
-      int d = ((int)res[p * plane_stride + j * ldr + i] * c_crt_inv[p]) % m;
-      if (d > m / 2) d -= m;
-      else if (d < -(m / 2)) d += m;
-      const i128 Mt = (i128)(((u128)c_Mt[p][1] << 64) | (u128)c_Mt[p][0]);
-      s += (i128)d * Mt;  // |term| <= M/2
-      if (s > half) s -= Mc;
-      else if (s < -half) s += Mc;
+      for (int p = 0; p < kOzakiModuli; ++p) {
+        const int m = kmod(p);
+        int d = ((int)r[p * plane_stride] * kcrt_inv(p)) % m;
+        if (d > m / 2) d -= m;
+        else if (d < -(m / 2)) d += m;
+        const i128 Mt = (i128)(((u128)kcrt_hi(p) << 64) | (u128)kcrt_lo(p));
+        s += (i128)d * Mt;  // |term| <= M/2
+        if (s > half) s -= Mc;
+        else if (s < -half) s += Mc;
+      }
+      // int128 -> double (round to nearest via the high/low split), then unscale
+      const bool neg = s < 0;
+      const u128 a = neg ? (u128)(-s) : (u128)s;
+      const double hi = (double)(unsigned long long)(a >> 64);
+      const double lo = (double)(unsigned long long)a;
+      double v = fma(hi, 18446744073709551616.0, lo);
+      if (neg) v = -v;
+      const int sp = shift_p[i];
+      v = (sp == kOzakiNonFinite || sq == kOzakiNonFinite) ? CUDART_NAN : ldexp(v, -(sp + sq));
+      double* o = out + i + j * ldo;
+      *o = beta == 0.0 ? alpha * v : alpha * v + beta * *o;
     }
-    // int128 -> double (round to nearest via the high/low split), then unscale
-    const bool neg = s < 0;
-    const u128 a = neg ? (u128)(-s) : (u128)s;
-    const double hi = (double)(unsigned long long)(a >> 64);
-    const double lo = (double)(unsigned long long)a;
-    double v = fma(hi, 18446744073709551616.0, lo);
-    if (neg) v = -v;
-    v = (shift_p[i] == kOzakiNonFinite || shift_q[j] == kOzakiNonFinite) ? CUDART_NAN
-                                                                         : ldexp(v, -(shift_p[i] + shift_q[j]));
-    double* o = out + i + j * ldo;
-    *o = beta == 0.0 ? alpha * v : alpha * v + beta * *o;
   }
 }
 
@@ -570,9 +589,9 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
   const uint32_t ab_fmt = (P.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
   imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, M * N, ab_fmt);
   LRB_CHECK_LAUNCH();
-  const int64_t total = M * N;
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * num_sms()));
-  crt_kernel<<<g, 256, 0, st>>>(M, N, res, ldr, M * N, P.shift, Q.shift, out, ldo, alpha, beta);
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((M + 255) / 256, 64));
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(N, std::max<int64_t>(1, 16 * num_sms() / gx)));
+  crt_kernel<<<dim3(gx, gy), 256, 0, st>>>(M, N, res, ldr, M * N, P.shift, Q.shift, out, ldo, alpha, beta);
   LRB_CHECK_LAUNCH();
 }
 
