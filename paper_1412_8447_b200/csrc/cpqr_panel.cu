@@ -226,7 +226,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
   constexpr int KP = SPEC ? 32 * NA / L : CH;  // row pairs per lane
   constexpr int GPW = 32 / L;
   constexpr int S = NB / L;
-  constexpr int D = (S == 1 && NA <= 4) ? 4 : (S <= 2 ? 3 : 2);  // warp-iterations in flight
+  constexpr int D = S == 1 ? 4 : (S <= 2 ? 3 : 2);  // warp-iterations in flight
   const PanelArgs& a = x.a;
   const int64_t s = x.s, ld = a.ld, m = a.m;
   const int lane = x.lane, c = x.c;
