@@ -102,6 +102,12 @@ int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
 #define LR_GEMM_DMMA 0
 #define LR_GEMM_OZAKI_INT8 1
 int lr_ctx_set_gemm_mode(lr_ctx* ctx, int mode);
+/* The device matrix a (m x n, lda) will be contracted more than once by the
+   following calls (e.g. the column-sharded pipeline's sketch and A^T Q_c):
+   on the Ozaki engine its residue planes are split once and reused until
+   lr_ctx_clear_operand_cache.  The caller must not modify a in between. */
+int lr_ctx_cache_operand(lr_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda);
+int lr_ctx_clear_operand_cache(lr_ctx* ctx);
 int lr_ctx_get_gemm_mode(lr_ctx* ctx);
 /* back to the context's own (non-blocking) stream, the default after creation */
 int lr_ctx_use_own_stream(lr_ctx* ctx);

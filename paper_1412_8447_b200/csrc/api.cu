@@ -131,6 +131,9 @@ struct lr_ctx {
   // Ozaki residue planes of A, kept for the duration of one CUR call so the
   // sketch and the A^T Q contraction split A once (OzakiScope)
   bool oz_cache_on = false;
+  bool oz_pinned = false;  // lr_ctx_cache_operand: the cache outlives single calls
+  const double* pin_src = nullptr;
+  int64_t pin_K = 0, pin_cols = 0, pin_ld = 0;
   const double* oz_src = nullptr;
   int64_t oz_K = 0, oz_cols = 0, oz_ld = 0;
   lrb::OzakiOperand oz_op;
@@ -270,6 +273,10 @@ void gemm_a(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t
     gemm(c, M, N, K, P, ldp, Q, ldq, out, ldo);
     return;
   }
+  if (a_side < 0 && c->oz_pinned) {  // a caller-pinned matrix (lr_ctx_cache_operand) keeps its planes
+    if (P == c->pin_src && K == c->pin_K && M == c->pin_cols && ldp == c->pin_ld) a_side = 0;
+    else if (Q == c->pin_src && K == c->pin_K && N == c->pin_cols && ldq == c->pin_ld) a_side = 1;
+  }
   OzakiOperand op, oq;
   const OzakiOperand* Po = ozaki_operand(c, K, M, P, ldp, a_side == 0, 0, op);
   const OzakiOperand* Qo = Po ? ozaki_operand(c, K, N, Q, ldq, a_side == 1, 1, oq) : nullptr;
@@ -286,6 +293,7 @@ struct OzakiScope {
   lr_ctx* c;
   explicit OzakiScope(lr_ctx* cc) : c(cc) { c->oz_cache_on = true; }
   ~OzakiScope() {
+    if (c->oz_pinned) return;  // a pinned operand's planes stay valid across calls
     c->oz_cache_on = false;
     c->oz_src = nullptr;  // the planes stay allocated in the workspace for the next call
   }
@@ -1142,6 +1150,29 @@ int lr_ctx_set_gemm_mode(lr_ctx* c, int mode) {
   });
 }
 int lr_ctx_get_gemm_mode(lr_ctx* c) { return c ? c->gemm_mode : -1; }
+int lr_ctx_cache_operand(lr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "cache_operand");
+    require_ld(m, lda, "cache_operand");
+    c->oz_pinned = true;
+    c->oz_cache_on = true;
+    if (c->pin_src != a || c->pin_K != m || c->pin_cols != n || c->pin_ld != lda) c->oz_src = nullptr;
+    c->pin_src = a;
+    c->pin_K = m;
+    c->pin_cols = n;
+    c->pin_ld = lda;
+  });
+}
+int lr_ctx_clear_operand_cache(lr_ctx* c) {
+  return guard([&] {
+    checked(c);
+    c->oz_pinned = false;
+    c->oz_cache_on = false;
+    c->oz_src = nullptr;
+    c->pin_src = nullptr;
+  });
+}
 int lr_ctx_use_own_stream(lr_ctx* c) {
   return guard([&] {
     if (checked(c)->st != c->own) LRB_CUDA(cudaStreamSynchronize(c->st));

@@ -99,6 +99,13 @@ class DeviceBackend:
         out.copy_(t)
         return out
 
+    def cache_operand(self, a):
+        m, n = a.shape
+        self._raise(self.lib.lr_ctx_cache_operand(self.ctx.h, a.data_ptr(), m, n, self.ld(a)))
+
+    def clear_operand_cache(self):
+        self._raise(self.lib.lr_ctx_clear_operand_cache(self.ctx.h))
+
     def sketch(self, a, ell, seed):
         m, n = a.shape
         y = self.empty(ell, n)
@@ -201,33 +208,37 @@ def randomized_cur_sharded(be, comm, a_local, col_offset: int, n_total: int, k: 
     strategy = strategy or SolveStrategy.automatic()
     m, n_g = a_local.shape
     ell = k + oversample
-    y_local = be.sketch(a_local, ell, seed)
-    y = comm.all_gather_cols(y_local)
-    assert y.shape[1] == n_total
-    piv, coeff = be.id_from_sample(y, k, strategy)
-    own = be.owned_index(piv[:k], col_offset, n_g)
-    c = comm.all_reduce_sum(be.gather_columns(a_local, own))
-    row_piv, row_coeff, skeleton = be.tsid_from_c(c, k, strategy)
-    r_local = be.gather_rows(a_local, row_piv[:k])
-    # C = Qc Rc (replicated)
-    rc, rci, ok_c = be.cholqr2(c)
-    # R^T = Qr Sr over the column blocks (CholeskyQR2 with all-reduced Gram matrices)
-    rt_local = be.transpose(r_local)
-    s1 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(rt_local, rt_local)))
-    s1i = be.tri_inv(s1)
-    q1_local = be.gemm_tn(r_local, s1i)
-    s2 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(q1_local, q1_local)))
-    s = be.gemm_tn(be.transpose(s2), s1)
-    si = be.tri_inv(s)
-    if not ok_c:
-        raise NotImplementedError("sharded CUR: C is too ill-conditioned for CholeskyQR2 (use the 1-GPU path)")
-    qr_local = be.gemm_tn(r_local, si)
-    qc = be.gemm_tn(be.transpose(c), rci)
-    xt_local = be.gemm_tn(a_local, qc)
-    w = comm.all_reduce_sum(be.gemm_tn(xt_local, qr_local))
-    t1 = be.gemm_tn(be.transpose(rci), w)
-    u = be.gemm_tn(be.transpose(t1), be.transpose(si))
-    r = comm.all_gather_cols(r_local)
+    be.cache_operand(a_local)  # the shard enters the sketch and A^T Q_c: split it once (Ozaki engine)
+    try:
+        y_local = be.sketch(a_local, ell, seed)
+        y = comm.all_gather_cols(y_local)
+        assert y.shape[1] == n_total
+        piv, coeff = be.id_from_sample(y, k, strategy)
+        own = be.owned_index(piv[:k], col_offset, n_g)
+        c = comm.all_reduce_sum(be.gather_columns(a_local, own))
+        row_piv, row_coeff, skeleton = be.tsid_from_c(c, k, strategy)
+        r_local = be.gather_rows(a_local, row_piv[:k])
+        # C = Qc Rc (replicated)
+        rc, rci, ok_c = be.cholqr2(c)
+        # R^T = Qr Sr over the column blocks (CholeskyQR2 with all-reduced Gram matrices)
+        rt_local = be.transpose(r_local)
+        s1 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(rt_local, rt_local)))
+        s1i = be.tri_inv(s1)
+        q1_local = be.gemm_tn(r_local, s1i)
+        s2 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(q1_local, q1_local)))
+        s = be.gemm_tn(be.transpose(s2), s1)
+        si = be.tri_inv(s)
+        if not ok_c:
+            raise NotImplementedError("sharded CUR: C is too ill-conditioned for CholeskyQR2 (use the 1-GPU path)")
+        qr_local = be.gemm_tn(r_local, si)
+        qc = be.gemm_tn(be.transpose(c), rci)
+        xt_local = be.gemm_tn(a_local, qc)
+        w = comm.all_reduce_sum(be.gemm_tn(xt_local, qr_local))
+        t1 = be.gemm_tn(be.transpose(rci), w)
+        u = be.gemm_tn(be.transpose(t1), be.transpose(si))
+        r = comm.all_gather_cols(r_local)
+    finally:
+        be.clear_operand_cache()
     return dict(col_pivots=piv, row_pivots=row_piv, c=c, u=u, r=r, col_coeff=coeff, row_coeff=row_coeff,
                 skeleton=skeleton)
 

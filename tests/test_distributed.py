@@ -66,6 +66,12 @@ def backsub_np(s11, s12):
 
 
 class NumpyBackend:
+    def cache_operand(self, a):
+        pass
+
+    def clear_operand_cache(self):
+        pass
+
     def sketch(self, a, ell, seed):
         return np.asfortranarray(inputs.gaussian_np(ell, a.shape[0], seed) @ a)
 

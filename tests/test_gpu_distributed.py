@@ -11,7 +11,10 @@ from paper_1412_8447_b200 import inputs
 pytestmark = pytest.mark.gpu
 
 
-def test_sharded_pipeline_on_device_matches_oracle(lr, oracle):
+@pytest.mark.parametrize("engine", [0, 1])
+def test_sharded_pipeline_on_device_matches_oracle(lr, oracle, engine):
+    """engine 1: the Ozaki engine with the shard pinned (lr_ctx_cache_operand)
+    so the sketch and A^T Q_c share one residue split."""
     import torch
 
     from paper_1412_8447_b200 import distributed as D
@@ -30,8 +33,14 @@ def test_sharded_pipeline_on_device_matches_oracle(lr, oracle):
         def all_reduce_sum(self, x):
             return x
 
-    res = D.randomized_cur_sharded(be, One(), a, 0, cfg.n, cfg.k, oversample=10, seed=5)
-    torch.cuda.synchronize()
+    ctx = lr.default_context()
+    ctx.set_gemm_mode(engine)
+    try:
+        res = D.randomized_cur_sharded(be, One(), a, 0, cfg.n, cfg.k, oversample=10, seed=5)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_gemm_mode(0)
+        ctx.use_own_stream()
     o = oracle.randomized_cur(a_np, cfg.k, 10, 5, u_mode=1)
     assert np.array_equal(res["col_pivots"].cpu().numpy(), o["col_pivots"])
     assert np.array_equal(res["row_pivots"].cpu().numpy(), o["row_pivots"])
