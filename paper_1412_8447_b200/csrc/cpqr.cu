@@ -588,7 +588,7 @@ int cpqr_fast_variant() {
 
 void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                   double* tau, int* d_flags, long long* d_recomputes, bool padded, cudaStream_t st, bool nopivot) {
-  if (!nopivot && cpqr_panel_supported(m, ld, padded)) {
+  if (!nopivot && cpqr_panel_supported(m, n, ld, padded)) {
     cpqr_panel(ws, m, n, W, ld, k, pivots, tau, d_flags, d_recomputes, st);
     return;
   }

@@ -48,7 +48,8 @@ constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
 constexpr int PW = PT / 32;
 constexpr int kMaxG = 256;       // per-CTA partials read by one warp (8 per lane)
 constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
-constexpr int kSmemMax = (NB + 3) * 64 * CH * (int)sizeof(double);
+// dynamic shared memory: (NB+3) ld + 2 maxcols doubles; the opt-in ceiling (227 KB) also holds the static arrays
+constexpr int kSmemLimit = 216 * 1024;
 
 struct PanelArgs {
   double* W;
@@ -68,6 +69,7 @@ struct PanelArgs {
   unsigned long long* recomputes;
   unsigned long long* trace;  // optional per-phase ns of CTA 0 (LRB_CPQR_TRACE), 8 slots
   unsigned int* bar;          // grid barrier counter (zeroed before each launch)
+  int64_t maxcols;            // columns per CTA bound (shared-memory norm arrays)
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
@@ -132,6 +134,8 @@ struct PassCtx {
   const double* wsh;     // w = V^T v (NB)
   const double* vrow;    // V(s, 0:NB)
   const double* nst;     // nrm[p], nrmx[p], nrm[s], nrmx[s]
+  double* snr;           // this CTA's running / last exact squared norms (shared memory, index j - c0)
+  double* snx;
   long long piv_s;
   unsigned long long recomputes;
 };
@@ -202,8 +206,8 @@ __device__ __noinline__ void process_swapped(PassCtx& x, double& bv, long long& 
     ++x.recomputes;
   }
   if (lane == 0) {
-    a.nrm[j] = nr;
-    a.nrmx[j] = nx;
+    x.snr[j - x.c0] = nr;
+    x.snx[j - x.c0] = nx;
     a.piv[j] = x.piv_s;
   }
   if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
@@ -283,8 +287,8 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     const double* fr = Fb + (size_t)cb.j * NB;
 #pragma unroll
     for (int t = 0; t < S; ++t) cb.f[t] = (l * S + t < c) ? fr[t] : 0.0;
-    cb.nr = a.nrm[cb.j];
-    cb.nx = a.nrmx[cb.j];
+    cb.nr = x.snr[cb.j - x.c0];
+    cb.nx = x.snx[cb.j - x.c0];
   };
   const double2* v2 = reinterpret_cast<const double2*>(x.vv + base);
   auto process = [&](Slot& cb) {
@@ -332,8 +336,8 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     }
     if (cb.ok) {
       if (l == 0) {
-        a.nrm[j] = nr;
-        a.nrmx[j] = nx;
+        x.snr[j - x.c0] = nr;
+        x.snx[j - x.c0] = nx;
       }
       if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
     }
@@ -392,6 +396,8 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   double* Vs = dyn + ld;         // [NB][ld] panel reflectors (column-major, zero outside support)
   double* olds = Vs + NB * ld;   // [ld]
   double* pivr = olds + ld;      // [ld]
+  double* snr = pivr + ld;       // [maxcols] norms of the owned columns for this launch
+  double* snx = snr + a.maxcols;
   for (int64_t i = threadIdx.x; i < (NB + 3) * ld; i += PT) dyn[i] = 0.0;
   const int64_t cnt = (c1 - c0 - warp + PW - 1) / PW;
   unsigned long long my_recomputes = 0;
@@ -510,6 +516,12 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     grid_barrier(a.bar, bar_target);
     if (__ldcg(a.flags) != 0) return;
   }
+  // the owned columns' norms live in shared memory for this launch
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += PT) {
+    snr[j - c0] = __ldcg(a.nrm + j);
+    snx[j - c0] = __ldcg(a.nrmx + j);
+  }
+  __syncthreads();
 
   // ------------------------------------------------------------ steps of this panel
   const bool tr = a.trace != nullptr && threadIdx.x == 0;
@@ -579,8 +591,8 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       if (threadIdx.x == 0) {
         sh_state[0] = a.piv[p];
         sh_state[1] = __ldcg(a.piv + s);
-        sh_nst[0] = a.nrm[p];
-        sh_nst[1] = a.nrmx[p];
+        sh_nst[0] = snr[p - c0];
+        sh_nst[1] = snx[p - c0];
         sh_nst[2] = __ldcg(a.nrm + s);
         sh_nst[3] = __ldcg(a.nrmx + s);
       }
@@ -597,7 +609,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     long long bp = INT64_MAX;
     {
       PassCtx x{a, s, c, p, swapped, apply, tau, vr_c, c0, cnt, warp, lane, vv, Vs, olds, Fs, wsh, vrow, sh_nst,
-                sh_state[1], 0ull};
+                snr, snx, sh_state[1], 0ull};
       pass_cols<TC0, NLD>(x, bv, bp);
       my_recomputes += x.recomputes;
     }
@@ -630,6 +642,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     }
     if (cta == 0)
       for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
+    // the next pivot position's norms, for the owner of the next step's pivot (swap bookkeeping)
+    if (threadIdx.x == 0 && s + 1 >= c0 && s + 1 < c1) {
+      a.nrm[s + 1] = snr[s + 1 - c0];
+      a.nrmx[s + 1] = snx[s + 1 - c0];
+    }
     __syncthreads();
     stamp(3);  // CTA argmax, pivot write-back
     if (s + 1 < a.k)
@@ -637,6 +654,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     stamp(4);  // stage
     grid_barrier(a.bar, bar_target);
     stamp(5);  // grid barrier
+  }
+  // trailing positions' norms back to global for the next panel launch
+  for (int64_t j = (c0 > a.t1 ? c0 : a.t1) + threadIdx.x; j < c1; j += PT) {
+    a.nrm[j] = snr[j - c0];
+    a.nrmx[j] = snx[j - c0];
   }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
 }
@@ -693,18 +715,20 @@ __global__ void __launch_bounds__(UT, 1) panel_update_kernel(double* __restrict_
 
 }  // namespace
 
-bool cpqr_panel_supported(int64_t m, int64_t ld, bool padded) {
+bool cpqr_panel_supported(int64_t m, int64_t n, int64_t ld, bool padded) {
   static const bool off = [] {
     const char* e = getenv("LRB_CPQR_PANEL");
     return e && atoi(e) == 0;
   }();
   // specialised widths only (the generic-width panel kernel is slower than cpqr.cu's)
-  return !off && padded && (ld == 256 || ld == 320 || ld == 512) && m <= ld;
+  // shared memory: V panel + 3 vectors + two norm arrays of ceil(n / SMs) columns
+  const int64_t maxcols = (n + num_sms() - 1) / num_sms() + 1;
+  const bool fits = sizeof(double) * ((NB + 3) * (size_t)ld + 2 * (size_t)maxcols) <= (size_t)kSmemLimit;
+  return !off && padded && (ld == 256 || ld == 320 || ld == 512) && m <= ld && fits;
 }
 
 void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                 double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)(NB + 3) * ld;
   using KernT = void (*)(PanelArgs);
   // specialised kernels per (ld / 64, first active chunk); ld in {256, 320, 512}
   static const KernT k4[] = {cpqr_panel_kernel<0, 4>, cpqr_panel_kernel<1, 4>, cpqr_panel_kernel<2, 4>,
@@ -724,18 +748,25 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   };
   static bool attr = false;
   if (!attr) {
-    for (KernT kf : k4) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-    for (KernT kf : k5) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-    for (KernT kf : k8) LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-    LRB_CUDA(cudaFuncSetAttribute(cpqr_panel_kernel<-1, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemMax));
+    auto set = [](KernT kf) {
+      cudaFuncAttributes fa{};
+      LRB_CUDA(cudaFuncGetAttributes(&fa, kf));
+      LRB_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(fa.maxDynamicSharedSizeBytes > 0 ? 227 * 1024 - fa.sharedSizeBytes
+                                                                           : kSmemLimit)));
+    };
+    for (KernT kf : k4) set(kf);
+    for (KernT kf : k5) set(kf);
+    for (KernT kf : k8) set(kf);
+    set(cpqr_panel_kernel<-1, -1>);
     attr = true;
   }
-  int per_sm = 0;
-  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_panel_kernel<-1, -1>, PT, smem));
-  per_sm = std::max(1, per_sm);
-  int G = std::min(std::min(per_sm, 1) * num_sms(), kMaxG);
+  // one CTA per SM (the shared memory holds the panel's V)
+  int G = std::min(num_sms(), kMaxG);
   G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + PW - 1) / PW));
+  const int64_t maxcols = (n + G - 1) / G + 1;
+  const size_t smem = sizeof(double) * ((size_t)(NB + 3) * ld + 2 * (size_t)maxcols);
+  if (smem > (size_t)kSmemLimit) throw CudaError("cpqr_panel: too many columns per CTA for the shared norms");
   const size_t cand_sz = kHdr + (size_t)ld + NB;
   const size_t nd = 2 * (size_t)n + 2 * (size_t)G + 2 * (size_t)G * cand_sz + (size_t)n * NB + (size_t)ld * NB;
   const size_t bytes = sizeof(double) * nd + sizeof(long long) * 2 * (size_t)G + 256;
@@ -757,6 +788,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   a.Vg = a.F + (size_t)n * NB;
   a.ppos = reinterpret_cast<long long*>(a.Vg + (size_t)ld * NB);
   a.bar = reinterpret_cast<unsigned int*>(a.ppos + 2 * (size_t)G);
+  a.maxcols = maxcols;
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
   static const bool trace = getenv("LRB_CPQR_TRACE") != nullptr;

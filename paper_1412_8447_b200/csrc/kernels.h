@@ -116,7 +116,7 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
 // Panel (delayed-update) CPQR for short-wide padded matrices (cpqr_panel.cu):
 // same contract as cpqr_inplace; supported when ld % 64 == 0, ld <= 512 and
 // rows [m, ld) are zero.
-bool cpqr_panel_supported(int64_t m, int64_t ld, bool padded);
+bool cpqr_panel_supported(int64_t m, int64_t n, int64_t ld, bool padded);
 void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                 double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st);
 // s (k x n, lds) = top k rows of W with strict lower part zeroed and the sign fix
