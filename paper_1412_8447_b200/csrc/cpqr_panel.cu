@@ -22,6 +22,13 @@
 // right-looking pass) plus 256 B of F per column; the panel update is one
 // read+write every NB steps.
 //
+// Column swaps are logical: a column keeps its slot (and its CTA) for the
+// whole factorization; each slot carries its logical position (the position
+// the reference's swaps would have moved it to; ties in the argmax go to the
+// lowest logical position) and a pivoted slot leaves the active set (norm
+// -inf, F row 0).  No step waits on a column move; one permutation pass at
+// the end puts the <= 2k displaced columns at their positions.
+//
 // Structure per panel: ONE persistent cooperative launch for the NB steps
 // (per step: batched argmax of per-CTA partials -> the winner's staged
 // reflector -> fused pass over owned columns -> per-CTA argmax + staging of
@@ -48,8 +55,12 @@ constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
 constexpr int PW = PT / 32;
 constexpr int kMaxG = 256;       // per-CTA partials read by one warp (8 per lane)
 constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
-// dynamic shared memory: (NB+3) ld + 2 maxcols doubles; the opt-in ceiling (227 KB) also holds the static arrays
+// dynamic shared memory: (NB+2) ld doubles (v, V, scratch) + per owned slot two
+// norms and a logical position; the opt-in ceiling (227 KB) also holds the static arrays
 constexpr int kSmemLimit = 216 * 1024;
+inline size_t panel_smem_bytes(int64_t ld, int64_t maxcols) {
+  return sizeof(double) * ((size_t)(NB + 2) * ld + 2 * (size_t)maxcols) + sizeof(int) * (size_t)maxcols;
+}
 
 struct PanelArgs {
   double* W;
@@ -68,8 +79,10 @@ struct PanelArgs {
   int* flags;
   unsigned long long* recomputes;
   unsigned long long* trace;  // optional per-phase ns of CTA 0 (LRB_CPQR_TRACE), 8 slots
+  unsigned long long* tstep;  // optional per-step barrier arrival / departure times [k][G][2]
   unsigned int* bar;          // grid barrier counter (zeroed before each launch)
   int64_t maxcols;            // columns per CTA bound (shared-memory norm arrays)
+  int* posof;                 // [n] logical position of each column slot (between launches)
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
@@ -122,42 +135,20 @@ struct PassCtx {
   const PanelArgs& a;
   int64_t s;
   int c;
-  int64_t p;
-  bool swapped, apply;
+  int64_t p;             // logical position of this step's pivot (the column at position s moves there)
+  bool apply;
   double tau, vr_c;
   int64_t c0, cnt;
   int warp, lane;
   const double* vv;
   const double* Vs;
-  const double* olds;
-  const double* Fs;
   const double* wsh;     // w = V^T v (NB)
   const double* vrow;    // V(s, 0:NB)
-  const double* nst;     // nrm[p], nrmx[p], nrm[s], nrmx[s]
   double* snr;           // this CTA's running / last exact squared norms (shared memory, index j - c0)
   double* snx;
-  long long piv_s;
+  int* spos;             // logical positions of the owned slots (shared memory, index j - c0)
   unsigned long long recomputes;
 };
-
-// exact squared norm of A_cur(s+1:m, j) = A_p - V(:, 0:c] F(j, 0:c]^T (the rare
-// recompute branch of cpqr.hpp:80-83) for the swapped column: full warp,
-// src = the column's A_p values, lane i holds F(j, i)
-__device__ __noinline__ double recompute_norm(const double* src, int64_t s, int64_t m, int64_t ld, int c,
-                                              const double* Vs, double f_lane, int lane) {
-  double f[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) f[i] = __shfl_sync(0xffffffffu, f_lane, i);
-  double q = 0.0;
-  for (int64_t r = s + 1 + lane; r < m; r += 32) {
-    double x = src[r];
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      if (i <= c) x = fma(-Vs[i * ld + r], f[i], x);
-    q = fma(x, x, q);
-  }
-  return warp_sum(q);
-}
 
 // group version of the recompute (L lanes per column): rows s+1..m-1 of the
 // column re-read from W (L2-hot), F(j, 0:c] from global (written by the group)
@@ -175,45 +166,7 @@ __device__ __forceinline__ double group_recompute(const double* col, const doubl
   return q;
 }
 
-// The column moved from position s to position p this step (at most one per
-// CTA): full warp, A_p values from olds, F row from Fs.  Writes the whole
-// column to position p with row s updated, its F row, norms and pivot.
-__device__ __noinline__ void process_swapped(PassCtx& x, double& bv, long long& bp) {
-  const PanelArgs& a = x.a;
-  const int64_t s = x.s, ld = a.ld, m = a.m, j = x.p;
-  const int lane = x.lane, c = x.c;
-  double d = 0.0;
-  for (int64_t r = s + lane; r < m; r += 32) d = fma(x.olds[r], x.vv[r], d);
-  double f = lane < c ? x.Fs[lane] : 0.0;
-  double e0 = d - f * x.wsh[lane];
-  double e1 = f * x.vrow[lane];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    e0 += __shfl_xor_sync(0xffffffffu, e0, o);
-    e1 += __shfl_xor_sync(0xffffffffu, e1, o);
-  }
-  const double fnew = x.apply ? x.tau * e0 : 0.0;
-  const double xs = x.olds[s] - e1 - x.vr_c * fnew;
-  double* dst = a.W + j * ld;
-  for (int64_t r = lane; r < ld; r += 32) dst[r] = r == s ? xs : x.olds[r];
-  if (lane == c) f = fnew;
-  if (lane <= c) a.F[j * NB + lane] = f;
-  double nr = x.nst[2] - xs * xs;
-  double nx = x.nst[3];
-  if (nr < 1e-6 * nx) {
-    nr = recompute_norm(x.olds, s, m, ld, c, x.Vs, f, lane);
-    nx = nr;
-    ++x.recomputes;
-  }
-  if (lane == 0) {
-    x.snr[j - x.c0] = nr;
-    x.snx[j - x.c0] = nx;
-    a.piv[j] = x.piv_s;
-  }
-  if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
-}
-
-// One step's pass over a warp's columns (all but the swapped one).
+// One step's pass over a warp's column slots (pivoted slots: loads only).
 // TC0 = first active 64-row chunk (s / 64, constant over a 32-step panel),
 // NLD = ld / 64; TC0 = -1: runtime chunk range.
 // Specialised layout: a column is handled by a group of L = 4 * (active
@@ -252,30 +205,26 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     vl[t] = x.vrow[l * S + t];
   }
   const int lc = c / S, tcs = c % S;  // owner lane / slot of F(j, c)
-  // the warp's columns c0 + warp + PW*it; valid ones (> s) are a contiguous
-  // run, visited as j = jstart + dj * q (32-bit indices, n < 2^31)
+  // the warp's slots c0 + warp + PW*q, visited as j = jstart + dj * q
+  // (alternating direction: the previous step's last columns are L2-hot;
+  // 32-bit indices, n < 2^31)
   const int first = (int)(x.c0 + x.warp);
-  const int cnt = (int)x.cnt;
-  int it_min = s >= first ? (int)((s - first) / PW) + 1 : 0;
-  if (it_min > cnt) it_min = cnt;
-  const int n_valid = cnt - it_min;
-  const int jstart = (s & 1) ? first + PW * (cnt - 1) : first + PW * it_min;
+  const int n_valid = (int)x.cnt;
+  const int jstart = (s & 1) ? first + PW * (n_valid - 1) : first;
   const int dj = (s & 1) ? -PW : PW;
-  const int jp = x.swapped ? (int)x.p : -1;
   const double* Wb = a.W + base + 2 * l;
   const double* Fb = a.F + l * S;
   struct Slot {
     double c[CH][2];
     double f[S];
     double nr, nx;
-    int j;
+    int j, lp;
     bool ok;
   };
   auto fetch = [&](Slot& cb, int qi) {
     const int q = qi * GPW + g;
     cb.ok = q < n_valid;
     cb.j = jstart + dj * (cb.ok ? q : 0);  // an owned column for the (unused) loads
-    if (cb.j == jp) cb.ok = false;
     const double* src = Wb + (size_t)cb.j * (size_t)ld;
 #pragma unroll
     for (int k = 0; k < KP; ++k)
@@ -289,6 +238,8 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     for (int t = 0; t < S; ++t) cb.f[t] = (l * S + t < c) ? fr[t] : 0.0;
     cb.nr = x.snr[cb.j - x.c0];
     cb.nx = x.snx[cb.j - x.c0];
+    cb.lp = x.spos[cb.j - x.c0];
+    if (cb.nr == -INFINITY) cb.ok = false;  // pivoted slot (its rows hold R / reflector values)
   };
   const double2* v2 = reinterpret_cast<const double2*>(x.vv + base);
   auto process = [&](Slot& cb) {
@@ -335,11 +286,15 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
       }
     }
     if (cb.ok) {
+      // the column at logical position s takes the pivot's position p (the reference's swap)
+      const int lp = cb.lp == (int)s ? (int)x.p : cb.lp;
       if (l == 0) {
         x.snr[j - x.c0] = nr;
         x.snx[j - x.c0] = nx;
+        x.spos[j - x.c0] = lp;
       }
-      if (better(nr, j, bv, bp)) { bv = nr; bp = j; }
+      const long long key = ((long long)lp << 32) | (long long)j;  // ties -> lowest logical position
+      if (better(nr, key, bv, bp)) { bv = nr; bp = key; }
     }
   };
   const int iters = (n_valid + GPW - 1) / GPW;
@@ -356,8 +311,6 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
       process(buf[u]);
     }
   }
-  // the column moved into position p by the swap, if this warp owns p
-  if (x.swapped && x.p >= first && (x.p - first) % PW == 0) process_swapped(x, bv, bp);
   // per-lane best -> warp best (the caller publishes lane 0's)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -378,11 +331,8 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   __shared__ long long sh_bp[PW];
   __shared__ double sh_hdr[kHdr];
   __shared__ long long sh_piv[2];
-  __shared__ long long sh_state[2];
-  __shared__ double sh_nst[4];
   __shared__ double wsh[NB];    // w = V^T v of the current step
   __shared__ double vrow[NB];   // V(s, 0:NB)
-  __shared__ double Fs[NB];     // F row of the column swapped out of position s
   __shared__ double fb[NB];     // F row of the staged candidate column
   __shared__ double sh_alpha;
 
@@ -394,11 +344,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   const int nld = (int)(ld >> 6);
   double* vv = dyn;              // [ld] current reflector, zero outside [s, m)
   double* Vs = dyn + ld;         // [NB][ld] panel reflectors (column-major, zero outside support)
-  double* olds = Vs + NB * ld;   // [ld]
-  double* pivr = olds + ld;      // [ld]
-  double* snr = pivr + ld;       // [maxcols] norms of the owned columns for this launch
+  double* scr = Vs + NB * ld;    // [ld] staging scratch
+  double* snr = scr + ld;        // [maxcols] norms of the owned slots for this launch
   double* snx = snr + a.maxcols;
-  for (int64_t i = threadIdx.x; i < (NB + 3) * ld; i += PT) dyn[i] = 0.0;
+  int* spos = reinterpret_cast<int*>(snx + a.maxcols);  // [maxcols] their logical positions
+  for (int64_t i = threadIdx.x; i < (NB + 2) * ld; i += PT) dyn[i] = 0.0;
   const int64_t cnt = (c1 - c0 - warp + PW - 1) / PW;
   unsigned long long my_recomputes = 0;
   __syncthreads();
@@ -461,7 +411,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     }
     // w_i = V(:, i)^T v for the reflectors of this panel (warp i, i < c_used)
     if (same_panel) {
-      double* vtmp = pivr;  // free scratch at this point of the step
+      double* vtmp = scr;
 #pragma unroll
       for (int q = 0; q < kRowsPerThread; ++q)
         if (threadIdx.x + PT * q < ld) vtmp[threadIdx.x + PT * q] = vr[q];
@@ -495,9 +445,10 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       if (lane == 0) {
         a.nrm[j] = acc;
         a.nrmx[j] = acc;
-        a.piv[j] = j;
+        a.posof[j] = (int)j;
       }
-      if (better(acc, j, bv, bp)) { bv = acc; bp = j; }
+      const long long key = (j << 32) | j;
+      if (better(acc, key, bv, bp)) { bv = acc; bp = key; }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags, 1);
     if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
@@ -512,7 +463,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       sh_piv[0] = cp;
     }
     __syncthreads();
-    stage(a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0], 0, false);
+    stage(a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0] & 0xffffffffll, 0, false);
     grid_barrier(a.bar, bar_target);
     if (__ldcg(a.flags) != 0) return;
   }
@@ -520,6 +471,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   for (int64_t j = c0 + threadIdx.x; j < c1; j += PT) {
     snr[j - c0] = __ldcg(a.nrm + j);
     snx[j - c0] = __ldcg(a.nrmx + j);
+    spos[j - c0] = __ldcg(a.posof + j);
   }
   __syncthreads();
 
@@ -562,7 +514,8 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       if (lane == 0) { sh_piv[0] = bp; sh_piv[1] = bc; }
     }
     __syncthreads();
-    const int64_t p = sh_piv[0];
+    const int64_t p = sh_piv[0] >> 32;            // logical position of the pivot
+    const int64_t sp = sh_piv[0] & 0xffffffffll;  // its slot
     const double* cd = a.cand + ((int64_t)par * G + sh_piv[1]) * cand_sz;
 
     // (2) the winner's reflector -> vv, Vs(:, c), w, V(s, :)
@@ -580,24 +533,15 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       // V(s, 0:c) of the earlier reflectors (V(s, c) = 1 when applied: vr_c below)
       if (threadIdx.x < NB) vrow[threadIdx.x] = threadIdx.x < c ? Vs[threadIdx.x * ld + s] : 0.0;
     }
-    // (3) swap bookkeeping by the owner of position p: its loads are issued
-    // together with the candidate's (one L2 round trip, one barrier)
-    const bool owner = (p >= c0 && p < c1);
-    const bool swapped = owner && p != s;
-    if (swapped) {
-      for (int64_t i = threadIdx.x; i < ld; i += PT) olds[i] = __ldcg(a.W + s * ld + i);
-      for (int64_t i = threadIdx.x; i < s; i += PT) pivr[i] = a.W[p * ld + i];
-      if (threadIdx.x < NB) Fs[threadIdx.x] = threadIdx.x < c ? __ldcg(a.F + s * NB + threadIdx.x) : 0.0;
-      if (threadIdx.x == 0) {
-        sh_state[0] = a.piv[p];
-        sh_state[1] = __ldcg(a.piv + s);
-        sh_nst[0] = snr[p - c0];
-        sh_nst[1] = snx[p - c0];
-        sh_nst[2] = __ldcg(a.nrm + s);
-        sh_nst[3] = __ldcg(a.nrmx + s);
-      }
+    // (3) the pivot's slot leaves the active set (its norm -> -inf; no data moves:
+    // the reference's column swap is the relabelling s <-> p of logical positions)
+    const bool owner = (sp >= c0 && sp < c1);
+    if (owner && threadIdx.x == 0) {
+      snr[sp - c0] = -INFINITY;
+      spos[sp - c0] = (int)s;
     }
     __syncthreads();
+    if (tr && a.tstep) a.tstep[(s * G + cta) * 4 + 1] = gtimer();
     stamp(1);  // argmax + candidate / swap loads
     const double tau = sh_hdr[2];
     const bool apply = sh_hdr[3] != 0.0 && tau != 0.0;
@@ -608,12 +552,12 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     double bv = -INFINITY;
     long long bp = INT64_MAX;
     {
-      PassCtx x{a, s, c, p, swapped, apply, tau, vr_c, c0, cnt, warp, lane, vv, Vs, olds, Fs, wsh, vrow, sh_nst,
-                snr, snx, sh_state[1], 0ull};
+      PassCtx x{a, s, c, p, apply, tau, vr_c, c0, cnt, warp, lane, vv, Vs, wsh, vrow, snr, snx, spos, 0ull};
       pass_cols<TC0, NLD>(x, bv, bp);
       my_recomputes += x.recomputes;
     }
 
+    if (tr && a.tstep) a.tstep[(s * G + cta) * 4 + 2] = gtimer();
     stamp(2);  // pass
     // (5) CTA argmax, pivot column write-back, V row-major copy for the panel GEMM
     if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
@@ -627,40 +571,64 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       a.ppos[(int64_t)nxt * G + cta] = cp;
       sh_piv[0] = cp;
     }
-    if (owner) {
-      double* ps = a.W + s * ld;
-      if (swapped) {
-        for (int64_t i = threadIdx.x; i < s; i += PT) ps[i] = pivr[i];
-        if (threadIdx.x == 0) {
-          a.piv[s] = sh_state[0];
-          a.nrm[s] = sh_nst[0];
-          a.nrmx[s] = sh_nst[1];
-        }
-      }
+    if (owner) {  // the pivot slot: R(s, s) = beta, the reflector below; F row -> 0 (panel update no-op)
+      double* ps = a.W + sp * ld;
       const double beta = sh_hdr[1];
       for (int64_t i = s + threadIdx.x; i < m; i += PT) ps[i] = (sh_hdr[3] != 0.0 && i == s) ? beta : vv[i];
+      if (threadIdx.x < NB) a.F[sp * NB + threadIdx.x] = 0.0;
     }
     if (cta == 0)
       for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
-    // the next pivot position's norms, for the owner of the next step's pivot (swap bookkeeping)
-    if (threadIdx.x == 0 && s + 1 >= c0 && s + 1 < c1) {
-      a.nrm[s + 1] = snr[s + 1 - c0];
-      a.nrmx[s + 1] = snx[s + 1 - c0];
-    }
     __syncthreads();
     stamp(3);  // CTA argmax, pivot write-back
     if (s + 1 < a.k)
-      stage(a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0], c + 1, s + 1 < a.t1);
+      stage(a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0] & 0xffffffffll, c + 1, s + 1 < a.t1);
     stamp(4);  // stage
+    if (tr && a.tstep) a.tstep[(s * G + cta) * 4 + 3] = (gtimer() & ~3ull) | (owner ? 1 : 0);
     grid_barrier(a.bar, bar_target);
+    if (tr && a.tstep && s + 1 < a.k) a.tstep[((s + 1) * G + cta) * 4] = gtimer();
     stamp(5);  // grid barrier
   }
-  // trailing positions' norms back to global for the next panel launch
-  for (int64_t j = (c0 > a.t1 ? c0 : a.t1) + threadIdx.x; j < c1; j += PT) {
+  // the owned slots' state back to global for the next launch / the final permutation
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += PT) {
     a.nrm[j] = snr[j - c0];
     a.nrmx[j] = snx[j - c0];
+    a.posof[j] = spos[j - c0];
   }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
+}
+
+// Final permutation: piv[posof[j]] = j; slots with posof[j] != j are listed
+// (at most 2 per step; overflow -> flags bit 2, never expected)
+__global__ void perm_scatter_kernel(const int* __restrict__ posof, int64_t n, int64_t* __restrict__ piv,
+                                    int* __restrict__ list, int* __restrict__ count, int cap, int* flags) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int p = posof[j];
+    piv[p] = j;
+    if (p != (int)j) {
+      const int e = atomicAdd(count, 1);
+      if (e < cap) list[e] = (int)j;
+      else atomicOr(flags, 4);
+    }
+  }
+}
+
+__global__ void iota_positions_kernel(int* posof, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    posof[j] = (int)j;
+}
+
+// listed slots -> scratch (scatter = false), scratch -> their logical positions (scatter = true)
+__global__ void move_slots_kernel(double* __restrict__ W, int64_t ld, const int* __restrict__ list,
+                                  const int* __restrict__ count, const int* __restrict__ posof,
+                                  double* __restrict__ tmp, bool scatter) {
+  const int cnt = *count;
+  for (int e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const int j = list[e];
+    double* src = scatter ? tmp + (size_t)e * ld : W + (size_t)j * ld;
+    double* dst = scatter ? W + (size_t)posof[j] * ld : tmp + (size_t)e * ld;
+    for (int64_t r = threadIdx.x; r < ld; r += blockDim.x) dst[r] = src[r];
+  }
 }
 
 // Panel update A_p(r0:m, j0:n) -= V(r0:m, 0:nc) F(j0:n, 0:nc)^T (rank <= 32,
@@ -721,9 +689,9 @@ bool cpqr_panel_supported(int64_t m, int64_t n, int64_t ld, bool padded) {
     return e && atoi(e) == 0;
   }();
   // specialised widths only (the generic-width panel kernel is slower than cpqr.cu's)
-  // shared memory: V panel + 3 vectors + two norm arrays of ceil(n / SMs) columns
+  // shared memory: V panel + 2 vectors + the state of ceil(n / SMs) column slots
   const int64_t maxcols = (n + num_sms() - 1) / num_sms() + 1;
-  const bool fits = sizeof(double) * ((NB + 3) * (size_t)ld + 2 * (size_t)maxcols) <= (size_t)kSmemLimit;
+  const bool fits = panel_smem_bytes(ld, maxcols) <= (size_t)kSmemLimit;
   return !off && padded && (ld == 256 || ld == 320 || ld == 512) && m <= ld && fits;
 }
 
@@ -765,11 +733,13 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   int G = std::min(num_sms(), kMaxG);
   G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + PW - 1) / PW));
   const int64_t maxcols = (n + G - 1) / G + 1;
-  const size_t smem = sizeof(double) * ((size_t)(NB + 3) * ld + 2 * (size_t)maxcols);
+  const size_t smem = panel_smem_bytes(ld, maxcols);
   if (smem > (size_t)kSmemLimit) throw CudaError("cpqr_panel: too many columns per CTA for the shared norms");
   const size_t cand_sz = kHdr + (size_t)ld + NB;
   const size_t nd = 2 * (size_t)n + 2 * (size_t)G + 2 * (size_t)G * cand_sz + (size_t)n * NB + (size_t)ld * NB;
-  const size_t bytes = sizeof(double) * nd + sizeof(long long) * 2 * (size_t)G + 256;
+  const size_t ndisp = 2 * (size_t)k + 2;  // slots away from their final position: <= 2 per step
+  const size_t bytes = sizeof(double) * (nd + ndisp * (size_t)ld) + sizeof(long long) * 2 * (size_t)G + 256 +
+                       sizeof(int) * ((size_t)n + ndisp + 2);
   uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
   PanelArgs a{};
   a.W = W;
@@ -788,14 +758,23 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   a.Vg = a.F + (size_t)n * NB;
   a.ppos = reinterpret_cast<long long*>(a.Vg + (size_t)ld * NB);
   a.bar = reinterpret_cast<unsigned int*>(a.ppos + 2 * (size_t)G);
+  double* disp_cols = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(a.bar) + 256);
+  a.posof = reinterpret_cast<int*>(disp_cols + ndisp * (size_t)ld);
+  int* disp_list = a.posof + n;
+  int* disp_count = disp_list + ndisp;
   a.maxcols = maxcols;
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
   static const bool trace = getenv("LRB_CPQR_TRACE") != nullptr;
+  static const bool trace_panels = getenv("LRB_CPQR_TRACE_PANELS") != nullptr;
+  std::vector<unsigned long long> prev;
   a.trace = nullptr;
+  a.tstep = nullptr;
   if (trace) {
     LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 8 * sizeof(unsigned long long) * G, st));
     LRB_CUDA(cudaMemsetAsync(a.trace, 0, 8 * sizeof(unsigned long long) * G, st));
+    if (trace_panels)
+      LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.tstep), 4 * sizeof(unsigned long long) * G * k, st));
   }
   for (int64_t t0 = 0; t0 < k; t0 += NB) {
     const int64_t t1 = std::min<int64_t>(k, t0 + NB);
@@ -806,14 +785,44 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     void* params[] = {&a};
     LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
+    if (trace && trace_panels) {  // per-panel phase means / maxima over CTAs (diagnostic)
+      std::vector<unsigned long long> h(8 * (size_t)G);
+      LRB_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      LRB_CUDA(cudaStreamSynchronize(st));
+      if (t0 == 0) prev.assign(h.size(), 0ull);
+      fprintf(stderr, "cpqr_panel t0=%4ld us/step (mean/max):", (long)t0);
+      for (int slot = 1; slot <= 5; ++slot) {
+        double sum = 0, mx = 0;
+        for (int g = 0; g < G; ++g) {
+          const double v = (double)(h[g * 8 + slot] - prev[g * 8 + slot]) / 1e3 / (double)(t1 - t0);
+          sum += v;
+          mx = std::max(mx, v);
+        }
+        fprintf(stderr, " %.2f/%.2f", sum / G, mx);
+      }
+      fprintf(stderr, "\n");
+      prev = h;
+    }
     // A_p(t1:m, t1:n) -= V(t1:m, 0:c) F(t1:n, 0:c)^T  (rows/cols of later panels only)
     if (t1 < k && t1 < m && t1 < n) {
-      const int64_t nbatch = (n - t1 + UB - 1) / UB;
+      const int64_t nbatch = (n + UB - 1) / UB;  // every slot (pivoted ones have F = 0)
       const int ug = (int)std::min<int64_t>(nbatch, num_sms());  // persistent: V loaded once per CTA
-      panel_update_kernel<<<ug, UT, 0, st>>>(W, ld, t1, m, t1, n, a.Vg, a.F, (int)(t1 - t0));
+      panel_update_kernel<<<ug, UT, 0, st>>>(W, ld, t1, m, 0, n, a.Vg, a.F, (int)(t1 - t0));
       LRB_CHECK_LAUNCH();
     }
   }
+  // logical -> physical: pivots, and the few slots not at their final position
+  // move there through a scratch copy (the reference's swapped layout)
+  LRB_CUDA(cudaMemsetAsync(disp_count, 0, sizeof(int), st));
+  const int pg = (int)std::min<int64_t>((n + 255) / 256, 4 * (int64_t)num_sms());
+  if (k == 0) iota_positions_kernel<<<pg, 256, 0, st>>>(a.posof, n);
+  perm_scatter_kernel<<<pg, 256, 0, st>>>(a.posof, n, pivots, disp_list, disp_count, (int)ndisp,
+                                                        d_flags);
+  LRB_CHECK_LAUNCH();
+  const int dg = (int)std::min<size_t>(ndisp, 4 * (size_t)num_sms());
+  move_slots_kernel<<<dg, 256, 0, st>>>(W, ld, disp_list, disp_count, a.posof, disp_cols, false);
+  move_slots_kernel<<<dg, 256, 0, st>>>(W, ld, disp_list, disp_count, a.posof, disp_cols, true);
+  LRB_CHECK_LAUNCH();
   if (trace) {
     std::vector<unsigned long long> h(8 * (size_t)G);
     LRB_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -830,6 +839,41 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       }
       fprintf(stderr, "cpqr_panel trace %-10s us/step: min %.2f mean %.2f max %.2f (cta %d)\n", names[slot], mn,
               sum / G, mx, arg);
+    }
+    if (a.tstep) {  // per step: the last-arriving CTA's phases vs the CTA mean (steps 1..k-1)
+      std::vector<unsigned long long> t(4 * (size_t)G * k);
+      LRB_CUDA(cudaMemcpyAsync(t.data(), a.tstep, t.size() * 8, cudaMemcpyDeviceToHost, st));
+      LRB_CUDA(cudaStreamSynchronize(st));
+      for (int64_t b0 = 0; b0 < k; b0 += 64) {
+        const int64_t b1 = std::min<int64_t>(k, b0 + 64);
+        double wait = 0, dl[3] = {0, 0, 0}, dstart = 0;
+        int cnt = 0, own_p = 0, own_s = 0;
+        for (int64_t s = std::max<int64_t>(b0, 1); s < b1; ++s) {
+          if (s % NB == 0) continue;  // first step of a launch: no departure stamp
+          double mean[4] = {0, 0, 0, 0};
+          int am = 0;
+          for (int g = 0; g < G; ++g) {
+            const unsigned long long* q = &t[(s * G + g) * 4];
+            for (int e = 0; e < 4; ++e) mean[e] += ((double)q[e] - (double)t[(s * G) * 4]) / G;
+            if (q[3] > t[(s * G + am) * 4 + 3]) am = g;
+          }
+          const unsigned long long* L = &t[(s * G + am) * 4];
+          own_p += (int)(L[3] & 1);
+          own_s += (int)((L[3] >> 1) & 1);
+          const double base0 = (double)t[(s * G) * 4];
+          wait += (double)L[3] - base0 - mean[3];
+          dstart += (double)L[0] - base0 - mean[0];
+          for (int e = 1; e < 4; ++e)
+            dl[e - 1] += ((double)L[e] - (double)L[e - 1]) - (mean[e] - mean[e - 1]);
+          ++cnt;
+        }
+        if (!cnt) continue;
+        const double ns = 1e3 * cnt;
+        fprintf(stderr, "cpqr_panel steps %4ld-%4ld last CTA vs mean (us): arrival %+.2f = start %+.2f loads %+.2f "
+                "pass %+.2f tail %+.2f; last CTA owns p %d / s %d of %d\n", (long)b0, (long)b1, wait / ns, dstart / ns,
+                dl[0] / ns, dl[1] / ns, dl[2] / ns, own_p, own_s, cnt);
+      }
+      cudaFreeAsync(a.tstep, st);
     }
     cudaFreeAsync(a.trace, st);
   }

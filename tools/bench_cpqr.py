@@ -14,8 +14,16 @@ def run(rows, n, reps=3):
     ctx = lr.default_context()
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     a = lr.empty_colmajor(rows, n, "cuda")
-    g = torch.randn(n, rows, dtype=torch.float64, device="cuda")
-    a.copy_(g.T)
+    if os.environ.get("SPECTRUM") == "c4":  # sketch of a C4-spectrum matrix: G diag(s) V^T
+        w = 1024
+        sv = (1.0 + torch.arange(w, dtype=torch.float64, device="cuda") / 50.0) ** -3
+        v, _ = torch.linalg.qr(torch.randn(n, w, dtype=torch.float64, device="cuda"))
+        g = torch.randn(rows, w, dtype=torch.float64, device="cuda") * sv
+        a.copy_(g @ v.T)
+        del v, g
+    else:
+        g = torch.randn(n, rows, dtype=torch.float64, device="cuda")
+        a.copy_(g.T)
     k = min(rows, n)
     s = lr.empty_colmajor(k, n, "cuda")
     piv = torch.empty(n, dtype=torch.int64, device="cuda")
@@ -29,7 +37,8 @@ def run(rows, n, reps=3):
         assert rc == 0, ctx.lib.lr_last_error()
         best = min(best, e0.elapsed_time(e1))
     byts = sum(16.0 * (rows - t) * (n - t) + 32.0 * (n - t) for t in range(k))
-    return {"rows": rows, "n": n, "steps": k, "ms": best, "us_per_step": 1e3 * best / k,
+    st = ctx.stats() if hasattr(ctx, "stats") else {}
+    return {"stats": st, "rows": rows, "n": n, "steps": k, "ms": best, "us_per_step": 1e3 * best / k,
             "GBps_alg": byts / (best * 1e-3) / 1e9}
 
 
