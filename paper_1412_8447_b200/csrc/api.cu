@@ -209,7 +209,7 @@ bool device_all_finite(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
 
 // GEMM wrapper: pads misaligned operands (TMA needs 16B-aligned base and ld)
 void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-          double* out, int64_t ldo, double alpha = 1.0, double beta = 0.0, int splits = -1) {
+          double* out, int64_t ldo, double alpha = 1.0, double beta = 0.0, int splits = -1, bool upper = false) {
   auto ok = [](const double* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0); };
   DBuf<double> pp, qq;
   if (!ok(P, ldp)) {
@@ -226,7 +226,7 @@ void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t l
     Q = qq;
     ldq = l;
   }
-  gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st);
+  gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st, upper);
 }
 
 // ---------------------------------------------------------------- A-sized contractions
@@ -467,15 +467,15 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
              double* R, double* Rinv) {
   DBuf<double> G((size_t)k * k, c->st), R1inv((size_t)k * k, c->st), Q1((size_t)even(rows) * k, c->st);
   DBuf<int> info(2, c->st);
-  gemm(c, k, k, rows, X, ldx, X, ldx, G, k);  // G1 = X^T X
+  gemm(c, k, k, rows, X, ldx, X, ldx, G, k, 1.0, 0.0, -1, true);  // G1 = X^T X (upper tiles)
   cholesky_upper(c->ws, k, G, k, info, c->st);  // G <- R1
   LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   sync(c);
   if (c->h_flags[0] != 0) return false;
-  tri_upper_inverse(k, G, k, R1inv, k, c->st);
+  tri_upper_inverse_blocked(k, G, k, R1inv, k, c->st);
   gemm(c, rows, k, k, Xt, ldxt, R1inv, k, Q1, even(rows));  // Q1 = X R1^-1
   DBuf<double> G2((size_t)k * k, c->st), R2t((size_t)k * k, c->st);
-  gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k);  // G2 = Q1^T Q1
+  gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k, 1.0, 0.0, -1, true);  // G2 = Q1^T Q1
   cholesky_upper(c->ws, k, G2, k, info.p + 1, c->st);
   LRB_CUDA(cudaMemcpyAsync(c->h_flags + 1, info.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -483,7 +483,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   // R = R2 R1: R(i,j) = sum_l R2(i,l) R1(l,j) -> P = R2^T
   transpose_matrix(k, k, G2, k, R2t, k, c->st);
   gemm(c, k, k, k, R2t, k, G, k, R, k);
-  tri_upper_inverse(k, R, k, Rinv, k, c->st);
+  tri_upper_inverse_blocked(k, R, k, Rinv, k, c->st);
   DBuf<double> part(4 * num_sms() + 4, c->st), f(2, c->st);
   frob2(k, k, R, k, part, f, c->st);
   frob2(k, k, Rinv, k, part, f.p + 1, c->st);

@@ -17,7 +17,7 @@
 //     F(j, c)   = tau (A_p(s:m, j)^T v - sum_{i<c} F(j, i) w_i),  w = V^T v
 //     R(s, j)   = A_p(s, j) - sum_{i<=c} V(s, i) F(j, i)          (row s only)
 //     norm2(j) -= R(s, j)^2  (exact recompute from A_p - V F^T when flagged)
-//   per panel: A_p(s1:m, s1:n) -= V(s1:m, :) F(s1:n, :)^T (panel_update_kernel).
+//   per panel: A_p(s1:m, :) -= V(s1:m, :) F(:, :)^T (panel_update_dmma_kernel).
 // HBM traffic per step is one read of the trailing block (half of the
 // right-looking pass) plus 256 B of F per column; the panel update is one
 // read+write every NB steps.
@@ -33,7 +33,7 @@
 // (per step: batched argmax of per-CTA partials -> the winner's staged
 // reflector -> fused pass over owned columns -> per-CTA argmax + staging of
 // the CTA's best column's reflector for the next step -> one grid barrier),
-// then panel_update_kernel for the block update.
+// then panel_update_dmma_kernel for the block update.
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <vector>
@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   // ------------------------------------------------------------ steps of this panel
   const bool tr = a.trace != nullptr && threadIdx.x == 0;
   unsigned long long tprev = tr ? gtimer() : 0;
+  const unsigned long long tk0 = tprev, ck0 = tr ? clock64() : 0;
   auto stamp = [&](int slot) {
     if (tr) {
       const unsigned long long t = gtimer();
@@ -595,7 +596,70 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     a.nrmx[j] = snx[j - c0];
     a.posof[j] = spos[j - c0];
   }
+  if (tr) {  // SM clock over this launch: cycles / ns
+    a.trace[cta * 8 + 6] += clock64() - ck0;
+    a.trace[cta * 8 + 7] += gtimer() - tk0;
+  }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
+}
+
+// Panel update on the DMMA pipe: W(r0:r1, :) -= V(r0:r1, 0:nc) F(:, 0:nc)^T as
+// m8n8k4 tiles with the W tile itself as the accumulator.  A warp owns an
+// 8-column group and walks the 8-row blocks; -V's A fragments are pre-swizzled
+// in shared memory ([row block][k step][lane]), F's B fragments sit in
+// registers, and U row blocks of W are loaded before any is multiplied.
+constexpr int PUW = 16;  // warps per CTA
+constexpr int PUU = 8;   // row blocks in flight per warp
+__global__ void __launch_bounds__(PUW * 32, 1)
+    panel_update_dmma_kernel(double* __restrict__ W, int64_t ld, int64_t r0, int64_t r1, int64_t n,
+                             const double* __restrict__ Vg, const double* __restrict__ F, int nc) {
+  extern __shared__ double vfrag[];
+  const int nrb = (int)((r1 - r0) >> 3);
+  for (int e = threadIdx.x; e < nrb * 256; e += blockDim.x) {
+    const int rb = e >> 8, ks = (e >> 5) & 7, ln = e & 31;
+    const int kc = 4 * ks + (ln & 3);
+    vfrag[e] = kc < nc ? -Vg[(r0 + 8 * rb + (ln >> 2)) * NB + kc] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ngroups = (n + 7) >> 3;
+  for (int64_t gi = (int64_t)blockIdx.x * PUW + warp; gi < ngroups; gi += (int64_t)gridDim.x * PUW) {
+    const int64_t j0 = gi * 8;
+    double b[8];
+    const int64_t jb = j0 + (lane >> 2);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int kc = 4 * ks + (lane & 3);
+      b[ks] = (jb < n && kc < nc) ? __ldg(F + jb * NB + kc) : 0.0;
+    }
+    const int64_t jc = j0 + 2 * (lane & 3);
+    const bool v0 = jc < n, v1 = jc + 1 < n;
+    double* w0 = W + jc * ld + r0 + (lane >> 2);
+    double* w1 = w0 + ld;
+    for (int rb0 = 0; rb0 < nrb; rb0 += PUU) {
+      double c[PUU][2];
+#pragma unroll
+      for (int u = 0; u < PUU; ++u) {
+        const bool ok = rb0 + u < nrb;
+        c[u][0] = (ok && v0) ? __ldcs(w0 + 8 * (rb0 + u)) : 0.0;
+        c[u][1] = (ok && v1) ? __ldcs(w1 + 8 * (rb0 + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PUU; ++u) {
+        if (rb0 + u < nrb) {
+          const double* af = vfrag + ((rb0 + u) * 8) * 32 + lane;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) dmma_8x8x4(c[u][0], c[u][1], af[ks * 32], b[ks]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PUU; ++u)
+        if (rb0 + u < nrb) {
+          if (v0) __stcs(w0 + 8 * (rb0 + u), c[u][0]);
+          if (v1) __stcs(w1 + 8 * (rb0 + u), c[u][1]);
+        }
+    }
+  }
 }
 
 // Final permutation: piv[posof[j]] = j; slots with posof[j] != j are listed
@@ -631,55 +695,6 @@ __global__ void move_slots_kernel(double* __restrict__ W, int64_t ld, const int*
   }
 }
 
-// Panel update A_p(r0:m, j0:n) -= V(r0:m, 0:nc) F(j0:n, 0:nc)^T (rank <= 32,
-// HBM-bound: one read + one write of the block).  A thread owns one row
-// (m - r0 <= 512) and keeps its V entries in registers; the F rows of a batch
-// of columns are staged in shared memory and read as broadcasts; 8 columns
-// are loaded before any is reduced (memory-level parallelism).
-constexpr int UT = 512;       // threads per CTA: row r0 + tid
-constexpr int UB = 64;        // columns per F batch
-constexpr int UG = 8;         // columns in flight per thread
-__global__ void __launch_bounds__(UT, 1) panel_update_kernel(double* __restrict__ W, int64_t ld, int64_t r0,
-                                                             int64_t m, int64_t j0, int64_t n,
-                                                             const double* __restrict__ Vg,
-                                                             const double* __restrict__ F, int nc) {
-  __shared__ double Fb[UB][NB];
-  const int tid = threadIdx.x;
-  const int64_t r = r0 + tid;
-  const bool has = r < m;
-  double v[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) v[i] = (has && i < nc) ? Vg[r * NB + i] : 0.0;
-  const int64_t nbatch = (n - j0 + UB - 1) / UB;
-  for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
-    const int64_t jb = j0 + bt * UB;
-    const int cols = (int)(n - jb < UB ? n - jb : UB);
-    __syncthreads();
-    for (int e = tid; e < UB * NB; e += UT) {
-      const int jj = e / NB, i = e % NB;
-      Fb[jj][i] = (jj < cols && i < nc) ? F[(jb + jj) * NB + i] : 0.0;
-    }
-    __syncthreads();
-    if (!has) continue;
-    for (int g = 0; g < cols; g += UG) {
-      double x[UG];
-#pragma unroll
-      for (int u = 0; u < UG; ++u) x[u] = g + u < cols ? W[(jb + g + u) * ld + r] : 0.0;
-#pragma unroll
-      for (int u = 0; u < UG; ++u) {
-        const double2* f2 = reinterpret_cast<const double2*>(Fb[g + u < UB ? g + u : 0]);
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int i = 0; i < NB / 2; ++i) {
-          const double2 f = f2[i];
-          s0 = fma(v[2 * i], f.x, s0);
-          s1 = fma(v[2 * i + 1], f.y, s1);
-        }
-        if (g + u < cols) W[(jb + g + u) * ld + r] = x[u] - (s0 + s1);
-      }
-    }
-  }
-}
 
 }  // namespace
 
@@ -727,6 +742,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     for (KernT kf : k5) set(kf);
     for (KernT kf : k8) set(kf);
     set(cpqr_panel_kernel<-1, -1>);
+    LRB_CUDA(cudaFuncSetAttribute(panel_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 256 * 64)));
     attr = true;
   }
   // one CTA per SM (the shared memory holds the panel's V)
@@ -805,9 +822,12 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     }
     // A_p(t1:m, t1:n) -= V(t1:m, 0:c) F(t1:n, 0:c)^T  (rows/cols of later panels only)
     if (t1 < k && t1 < m && t1 < n) {
-      const int64_t nbatch = (n + UB - 1) / UB;  // every slot (pivoted ones have F = 0)
-      const int ug = (int)std::min<int64_t>(nbatch, num_sms());  // persistent: V loaded once per CTA
-      panel_update_kernel<<<ug, UT, 0, st>>>(W, ld, t1, m, 0, n, a.Vg, a.F, (int)(t1 - t0));
+      // every slot (pivoted ones have F = 0); rows t1..m rounded up to 8 (padding rows stay 0)
+      const int64_t r1 = std::min<int64_t>(ld, (m + 7) & ~int64_t(7));
+      const int64_t ngroups = (n + 7) / 8;
+      const int ug = (int)std::min<int64_t>((ngroups + PUW - 1) / PUW, num_sms());  // persistent
+      const size_t usm = sizeof(double) * 256 * (size_t)((r1 - t1) / 8);
+      panel_update_dmma_kernel<<<ug, PUW * 32, usm, st>>>(W, ld, t1, r1, n, a.Vg, a.F, (int)(t1 - t0));
       LRB_CHECK_LAUNCH();
     }
   }
@@ -839,6 +859,11 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       }
       fprintf(stderr, "cpqr_panel trace %-10s us/step: min %.2f mean %.2f max %.2f (cta %d)\n", names[slot], mn,
               sum / G, mx, arg);
+    }
+    {
+      double cyc = 0, ns = 0;
+      for (int g = 0; g < G; ++g) { cyc += (double)h[g * 8 + 6]; ns += (double)h[g * 8 + 7]; }
+      fprintf(stderr, "cpqr_panel trace SM clock %.0f MHz over %.3f ms\n", 1e3 * cyc / ns, ns / G / 1e6);
     }
     if (a.tstep) {  // per step: the last-arriving CTA's phases vs the CTA mean (steps 1..k-1)
       std::vector<unsigned long long> t(4 * (size_t)G * k);

@@ -48,7 +48,7 @@ struct EpiArgs {
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
-                   int K, int tiles_m, int tiles_n, int m_fast, int kt_per_split, EpiArgs ep) {
+                   int K, int tiles_m, int tiles_n, int m_fast, int kt_per_split, EpiArgs ep, int upper) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -57,7 +57,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bid = blockIdx.x;
   int tm, tn;
-  if (m_fast) { tm = bid % tiles_m; tn = bid / tiles_m; }
+  if (upper) {  // tiles on or above the diagonal only (Gram products; tiles_m == tiles_n)
+    int t = bid;
+    tn = 0;
+    while (t > tn) { t -= tn + 1; ++tn; }
+    tm = t;
+  } else if (m_fast) { tm = bid % tiles_m; tn = bid / tiles_m; }
   else { tn = bid % tiles_n; tm = bid / tiles_n; }
   const int m0 = tm * BM, n0 = tn * BN;
   const int KT = (K + BK - 1) / BK;
@@ -205,9 +210,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 // deterministic split-K reduction: out = alpha * sum_s ws[s] + beta * out
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int M, int N, double* out,
-                                     int64_t ldo, double alpha, double beta) {
+                                     int64_t ldo, double alpha, double beta, int upper) {
   const int64_t total = (int64_t)M * N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (upper && (t % M) / BM > (t / M) / BN) continue;  // tile below the diagonal: not computed
     double s = 0.0;
     for (int p = 0; p < splits; ++p) s += ws[p * total + t];
     const int64_t m = t % M, n = t / M;
@@ -220,7 +226,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
 
 template <int EPI>
 void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, int splits, const EpiArgs& ep,
-            cudaStream_t st) {
+            cudaStream_t st, bool upper = false) {
   static bool attr = false;
   if (!attr) {
     LRB_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -229,9 +235,9 @@ void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, i
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
   const int KT = (K + BK - 1) / BK;
   const int kt_per_split = (KT + splits - 1) / splits;
-  dim3 grid(tiles_m * tiles_n, splits);
+  dim3 grid(upper ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n, splits);
   gemm_tn_kernel<EPI><<<grid, THREADS, SMEM_BYTES, st>>>(tp, tq, M, N, K, tiles_m, tiles_n, tiles_m <= tiles_n ? 1 : 0,
-                                                         kt_per_split, ep);
+                                                         kt_per_split, ep, upper ? 1 : 0);
   LRB_CHECK_LAUNCH();
 }
 
@@ -240,7 +246,8 @@ void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, i
 int gemm_tn_grid_ctas(int M, int N) { return ((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
 
 void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st) {
+             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper) {
+  if (upper && M != N) throw CudaError("gemm_tn: upper-tile mode needs a square output");
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {
     scale_matrix(M, N, out, ldo, beta, st);
@@ -256,21 +263,21 @@ void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, c
   const int KT = (K + BK - 1) / BK;
   if (splits <= 0) {
     // auto: fill ~2 waves when the output tile count is small
-    const int tiles = gemm_tn_grid_ctas(M, N);
+    const int tiles = upper ? ((N + BN - 1) / BN) * ((N + BN - 1) / BN + 1) / 2 : gemm_tn_grid_ctas(M, N);
     splits = 1;
     while (tiles * splits < 2 * num_sms() && KT / (splits * 2) >= 8) splits *= 2;
   }
   splits = std::max(1, std::min(splits, KT));
   if (splits == 1) {
-    launch<kEpiStore>(tp, tq, M, N, K, 1, ep, st);
+    launch<kEpiStore>(tp, tq, M, N, K, 1, ep, st, upper);
     return;
   }
   double* w = ws.get_doubles(WsSlot::kSplitK, (size_t)splits * M * N);
   ep.ws = w;
-  launch<kEpiSplitK>(tp, tq, M, N, K, splits, ep, st);
+  launch<kEpiSplitK>(tp, tq, M, N, K, splits, ep, st, upper);
   const int64_t total = (int64_t)M * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * num_sms());
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(w, splits, M, N, out, ldo, alpha, beta);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(w, splits, M, N, out, ldo, alpha, beta, upper ? 1 : 0);
   LRB_CHECK_LAUNCH();
 }
 

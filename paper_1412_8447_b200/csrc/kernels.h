@@ -60,9 +60,11 @@ class Workspace {
 // ---------------------------------------------------------------- GEMM
 int gemm_tn_grid_ctas(int M, int N);
 // out(MxN) = alpha P^T Q + beta out; P: KxM (ldp), Q: KxN (ldq), K-contiguous.
-// splits <= 0 chooses a deterministic split-K factor from the shape.
+// splits <= 0 chooses a deterministic split-K factor from the shape.  upper:
+// only the output tiles on/above the diagonal (Gram products, M == N; the
+// strictly-lower tiles are left unwritten).
 void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st);
+             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper = false);
 // per-CTA partial sums of (R - P^T Q)^2 written to partials_out[0..*num_partials)
 void gemm_tn_resid_sq(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q,
                       int64_t ldq, const double* R, int64_t ldr, double* partials_out, int* num_partials,
@@ -146,6 +148,9 @@ void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld1
 void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st);
 // inverse of an upper-triangular R (k x k) -> Rinv (upper)
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
+// same for a nonzero diagonal (no singular-row handling), blocked: CholeskyQR factors
+void tri_upper_inverse_blocked(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi,
+                               cudaStream_t st);
 
 // ---------------------------------------------------------------- Ozaki-II FP64 emulation on INT8 tcgen05
 constexpr int kOzakiModuli = 16;

@@ -212,7 +212,11 @@ __global__ void max_reduce_kernel(const double* __restrict__ p, int n, double* o
 constexpr int kCholB = 64;
 
 __global__ void chol_diag_kernel(int64_t j0, int jb, double* __restrict__ g, int64_t ldg, int* info) {
+  // 256 threads own fixed 4x4 element sets (rows tr + 16u, columns tc + 16v):
+  // per column j, threads 0..jb-1 scale row j (one division each), then every
+  // thread applies the rank-1 update to its own elements
   __shared__ double a[kCholB][kCholB + 1];
+  __shared__ double srow[kCholB];
   __shared__ int fail;
   if (info[0] != 0) return;
   for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
@@ -221,27 +225,37 @@ __global__ void chol_diag_kernel(int64_t j0, int jb, double* __restrict__ g, int
   }
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
+  const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
   for (int j = 0; j < jb; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = a[j][j];
-      if (!(d > 0.0) || !isfinite(d)) {
-        fail = j + 1;
-      } else {
-        a[j][j] = sqrt(d);
+    const double d = a[j][j];
+    if (!(d > 0.0) || !isfinite(d)) {  // uniform
+      if (threadIdx.x == 0) fail = j + 1;
+      break;
+    }
+    const double ri = rsqrt(d);  // 1/sqrt(d): multiplications instead of a division chain
+    const int x = threadIdx.x;
+    if (x > j && x < jb) {
+      const double v = a[j][x] * ri;
+      srow[x] = v;
+      a[j][x] = v;
+    }
+    __syncthreads();
+    if (x == j) a[j][j] = sqrt(d);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = tc + 16 * v;
+      if (c > j && c < jb) {
+        const double sc = srow[c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = tr + 16 * u;
+          if (r > j && r <= c) a[r][c] = fma(-srow[r], sc, a[r][c]);
+        }
       }
     }
     __syncthreads();
-    if (fail) break;
-    const double rd = a[j][j];
-    for (int c = j + 1 + threadIdx.x; c < jb; c += blockDim.x) a[j][c] /= rd;
-    __syncthreads();
-    const int nt = jb - j - 1;
-    for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
-      const int r = j + 1 + t % nt, c = j + 1 + t / nt;
-      if (r <= c) a[r][c] = fma(-a[j][r], a[j][c], a[r][c]);
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (fail) {
     if (threadIdx.x == 0) info[0] = (int)(j0 + fail);
     return;
@@ -252,27 +266,39 @@ __global__ void chol_diag_kernel(int64_t j0, int jb, double* __restrict__ g, int
   }
 }
 
-// X(:, c) = R_JJ^-T G(J, c) for the columns right of the diagonal block
-__global__ void chol_panel_kernel(int64_t k, int64_t j0, int jb, double* __restrict__ g, int64_t ldg,
-                                  const int* info) {
-  __shared__ double r[kCholB][kCholB + 1];
-  if (info[0] != 0) return;
-  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
-    const int i = t % jb, j = t / jb;
-    r[i][j] = g[(j0 + i) + (j0 + j) * ldg];
-  }
-  __syncthreads();
-  const int64_t c = j0 + jb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k) return;
-  double x[kCholB];
-  double* col = g + c * ldg + j0;
+// C = beta C + alpha A^T B (column-major, small K): the Cholesky trailing update
+__global__ void gemm_tn_small_kernel(int m, int n, int kk, double alpha, const double* __restrict__ A, int64_t lda,
+                                     const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C,
+                                     int64_t ldc, bool upper_only) {
+  __shared__ double As[32][33];  // As[l][i] = A(l0 + l, i0 + i)
+  __shared__ double Bs[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (upper_only && i0 > j0 + 31) return;
+  const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int l0 = 0; l0 < kk; l0 += 32) {
+    for (int t = threadIdx.x; t < 32 * 32; t += blockDim.x) {
+      const int a = t & 31, b = t >> 5;
+      As[a][b] = (l0 + a < kk && i0 + b < m) ? A[(l0 + a) + (int64_t)(i0 + b) * lda] : 0.0;
+      Bs[a][b] = (l0 + a < kk && j0 + b < n) ? B[(l0 + a) + (int64_t)(j0 + b) * ldb] : 0.0;
+    }
+    __syncthreads();
 #pragma unroll 8
-  for (int i = 0; i < jb; ++i) {
-    double v = col[i];
-    for (int l = 0; l < i; ++l) v = fma(-r[l][i], x[l], v);
-    x[i] = v / r[i][i];
+    for (int l = 0; l < 32; ++l) {
+      const double av = As[l][ti];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(av, Bs[l][tj + 8 * q], acc[q]);
+    }
+    __syncthreads();
   }
-  for (int i = 0; i < jb; ++i) col[i] = x[i];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ti, j = j0 + tj + 8 * q;
+    if (i < m && j < n && (!upper_only || i <= j)) {
+      double* cp = C + i + (int64_t)j * ldc;
+      *cp = beta == 0.0 ? alpha * acc[q] : fma(alpha, acc[q], beta * *cp);
+    }
+  }
 }
 
 // Panel by forward substitution, one warp per column (axpy form, two rows per
@@ -432,10 +458,107 @@ void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info,
     // G(J+, J+) -= X^T X with X = R(J, J+) (jb x nt): TN GEMM with K = jb
     const double* X = g + j0 + (j0 + jb) * ldg;
     double* T = g + (j0 + jb) + (j0 + jb) * ldg;
-    gemm_tn(ws, (int)nt, (int)nt, jb, X, ldg, X, ldg, T, ldg, -1.0, 1.0, 1, st);
+    (void)ws;
+    gemm_tn_small_kernel<<<dim3((unsigned)((nt + 31) / 32), (unsigned)((nt + 31) / 32)), 256, 0, st>>>(
+        (int)nt, (int)nt, jb, -1.0, X, ldg, X, ldg, 1.0, T, ldg, true);
+    LRB_CHECK_LAUNCH();
   }
   zero_strict_lower_kernel<<<(unsigned)std::min<int64_t>((k * k + 255) / 256, 4096), 256, 0, st>>>(k, g, ldg);
   LRB_CHECK_LAUNCH();
+}
+
+namespace {
+constexpr int kInvB = 64;
+
+// inverse of each kInvB diagonal block: thread c back-substitutes column c
+__global__ void tri_inv_leaf_kernel(int64_t k, const double* __restrict__ r, int64_t ldr, double* __restrict__ ri,
+                                    int64_t ldi) {
+  extern __shared__ double inv_smem[];
+  auto a = reinterpret_cast<double(*)[kInvB + 1]>(inv_smem);
+  auto x = reinterpret_cast<double(*)[kInvB + 1]>(inv_smem + kInvB * (kInvB + 1));
+  const int64_t b0 = (int64_t)blockIdx.x * kInvB;
+  const int nb = (int)(k - b0 < kInvB ? k - b0 : kInvB);
+  for (int t = threadIdx.x; t < kInvB * kInvB; t += blockDim.x) {
+    const int i = t % kInvB, j = t / kInvB;
+    a[i][j] = (i < nb && j < nb) ? r[(b0 + i) + (b0 + j) * ldr] : 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < nb) {
+    for (int i = c; i >= 0; --i) {
+      double v = i == c ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) v = fma(-a[i][l], x[l][c], v);
+      x[i][c] = v / a[i][i];
+    }
+    for (int i = 0; i < nb; ++i) ri[(b0 + i) + (b0 + c) * ldi] = i <= c ? x[i][c] : 0.0;
+  }
+}
+
+// C = alpha A B (column-major, small): 32x32 tiles, 256 threads x 4 outputs
+__global__ void gemm_nn_small_kernel(int m, int n, int kk, double alpha, const double* __restrict__ A, int64_t lda,
+                                     const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
+                                     int64_t ldc) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;  // rows ti, columns tj + 8q
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int l0 = 0; l0 < kk; l0 += 32) {
+    for (int t = threadIdx.x; t < 32 * 32; t += blockDim.x) {
+      const int a = t & 31, b = t >> 5;
+      As[a][b] = (i0 + a < m && l0 + b < kk) ? A[(i0 + a) + (int64_t)(l0 + b) * lda] : 0.0;
+      Bs[a][b] = (l0 + a < kk && j0 + b < n) ? B[(l0 + a) + (int64_t)(j0 + b) * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) {
+      const double av = As[ti][l];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(av, Bs[l][tj + 8 * q], acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ti, j = j0 + tj + 8 * q;
+    if (i < m && j < n) C[i + (int64_t)j * ldc] = alpha * acc[q];
+  }
+}
+
+void gemm_nn_small(int m, int n, int kk, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double* C, int64_t ldc, cudaStream_t st) {
+  gemm_nn_small_kernel<<<dim3((m + 31) / 32, (n + 31) / 32), 256, 0, st>>>(m, n, kk, alpha, A, lda, B, ldb, C, ldc);
+  LRB_CHECK_LAUNCH();
+}
+}  // namespace
+
+// R^-1 of an upper-triangular R with a nonzero diagonal by blocks: diagonal
+// blocks by back substitution, then [A B; 0 C]^-1 = [A^-1, -A^-1 B C^-1; 0, C^-1]
+// level by level (the serial chain is kInvB steps, not k).
+void tri_upper_inverse_blocked(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi,
+                               cudaStream_t st) {
+  LRB_CUDA(cudaMemset2DAsync(rinv, sizeof(double) * ldi, 0, sizeof(double) * k, k, st));
+  constexpr int smem = 2 * kInvB * (kInvB + 1) * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    LRB_CUDA(cudaFuncSetAttribute(tri_inv_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  tri_inv_leaf_kernel<<<(unsigned)((k + kInvB - 1) / kInvB), kInvB, smem, st>>>(k, r, ldr, rinv, ldi);
+  LRB_CHECK_LAUNCH();
+  if (k <= kInvB) return;
+  double* T = nullptr;
+  LRB_CUDA(cudaMallocAsync(&T, sizeof(double) * k * k, st));
+  for (int64_t h = kInvB; h < k; h *= 2)
+    for (int64_t p0 = 0; p0 + h < k; p0 += 2 * h) {
+      const int64_t hc = std::min<int64_t>(h, k - p0 - h);
+      // T = B C^-1, then the block = -A^-1 T
+      gemm_nn_small((int)h, (int)hc, (int)hc, 1.0, r + p0 + (p0 + h) * ldr, ldr, rinv + (p0 + h) + (p0 + h) * ldi,
+                    ldi, T, h, st);
+      gemm_nn_small((int)h, (int)hc, (int)h, -1.0, rinv + p0 + p0 * ldi, ldi, T, h, rinv + p0 + (p0 + h) * ldi, ldi,
+                    st);
+    }
+  LRB_CUDA(cudaFreeAsync(T, st));
 }
 
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st) {
