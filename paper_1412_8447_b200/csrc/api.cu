@@ -4,6 +4,8 @@
 // meaning, validation order and error class; the arithmetic runs on the GPU
 // only (no CPU fallback: a missing device is LR_ECUDA).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -148,6 +150,12 @@ namespace {
 // Close the interval since the previous mark and label it `stage`.
 void mark(lr_ctx* c, const char* stage) {
   if (!c->timing) return;
+  static const bool host_trace = getenv("LRB_MARK_HOST") != nullptr;
+  if (host_trace) {  // host-side timeline of the marks (diagnostic)
+    static const auto h0 = std::chrono::steady_clock::now();
+    fprintf(stderr, "mark %-16s host %10.3f ms\n", stage,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+  }
   cudaEvent_t e;
   LRB_CUDA(cudaEventCreate(&e));
   LRB_CUDA(cudaEventRecord(e, c->st));

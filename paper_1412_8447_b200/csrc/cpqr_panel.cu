@@ -35,6 +35,7 @@
 // the CTA's best column's reflector for the next step -> one grid barrier),
 // then panel_update_dmma_kernel for the block update.
 #include <cooperative_groups.h>
+#include <chrono>
 #include <cstdio>
 #include <vector>
 #include <algorithm>
@@ -713,6 +714,14 @@ bool cpqr_panel_supported(int64_t m, int64_t n, int64_t ld, bool padded) {
 void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int64_t k, int64_t* pivots,
                 double* tau, int* d_flags, long long* d_recomputes, cudaStream_t st) {
   using KernT = void (*)(PanelArgs);
+  static const bool evdiag0 = getenv("LRB_CPQR_EVENTS") != nullptr;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  const auto host_t0 = std::chrono::steady_clock::now();
+  if (evdiag0) {
+    LRB_CUDA(cudaEventCreate(&ev_begin));
+    LRB_CUDA(cudaEventCreate(&ev_end));
+    LRB_CUDA(cudaEventRecord(ev_begin, st));
+  }
   // specialised kernels per (ld / 64, first active chunk); ld in {256, 320, 512}
   static const KernT k4[] = {cpqr_panel_kernel<0, 4>, cpqr_panel_kernel<1, 4>, cpqr_panel_kernel<2, 4>,
                              cpqr_panel_kernel<3, 4>};
@@ -793,15 +802,28 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     if (trace_panels)
       LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.tstep), 4 * sizeof(unsigned long long) * G * k, st));
   }
+  // LRB_CPQR_EVENTS: CUDA events around every launch (kernel vs gap time, diagnostic)
+  static const bool evdiag = getenv("LRB_CPQR_EVENTS") != nullptr;
+  std::vector<cudaEvent_t> ev;
+  auto evrec = [&]() {
+    if (!evdiag) return;
+    cudaEvent_t e;
+    LRB_CUDA(cudaEventCreate(&e));
+    LRB_CUDA(cudaEventRecord(e, st));
+    ev.push_back(e);
+  };
+  evrec();
   for (int64_t t0 = 0; t0 < k; t0 += NB) {
     const int64_t t1 = std::min<int64_t>(k, t0 + NB);
     a.t0 = t0;
     a.t1 = t1;
     a.init = t0 == 0 ? 1 : 0;
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
+    evrec();
     void* params[] = {&a};
     LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
+    evrec();
     if (trace && trace_panels) {  // per-panel phase means / maxima over CTAs (diagnostic)
       std::vector<unsigned long long> h(8 * (size_t)G);
       LRB_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -830,6 +852,19 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       panel_update_dmma_kernel<<<ug, PUW * 32, usm, st>>>(W, ld, t1, r1, n, a.Vg, a.F, (int)(t1 - t0));
       LRB_CHECK_LAUNCH();
     }
+    evrec();
+  }
+  if (evdiag) {  // per panel: [memset] [cooperative kernel] [update]
+    LRB_CUDA(cudaStreamSynchronize(st));
+    double tm = 0, tk = 0, tu = 0;
+    for (size_t i = 0; i + 3 < ev.size(); i += 3) {
+      float x = 0;
+      LRB_CUDA(cudaEventElapsedTime(&x, ev[i], ev[i + 1])); tm += x;
+      LRB_CUDA(cudaEventElapsedTime(&x, ev[i + 1], ev[i + 2])); tk += x;
+      LRB_CUDA(cudaEventElapsedTime(&x, ev[i + 2], ev[i + 3])); tu += x;
+    }
+    fprintf(stderr, "cpqr_panel events: memset+gap %.3f ms, panel kernels %.3f ms, updates %.3f ms\n", tm, tk, tu);
+    for (auto e : ev) cudaEventDestroy(e);
   }
   // logical -> physical: pivots, and the few slots not at their final position
   // move there through a scratch copy (the reference's swapped layout)
@@ -843,6 +878,17 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   move_slots_kernel<<<dg, 256, 0, st>>>(W, ld, disp_list, disp_count, a.posof, disp_cols, false);
   move_slots_kernel<<<dg, 256, 0, st>>>(W, ld, disp_list, disp_count, a.posof, disp_cols, true);
   LRB_CHECK_LAUNCH();
+  if (evdiag0) {
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    LRB_CUDA(cudaEventRecord(ev_end, st));
+    LRB_CUDA(cudaEventSynchronize(ev_end));
+    float x = 0;
+    LRB_CUDA(cudaEventElapsedTime(&x, ev_begin, ev_end));
+    fprintf(stderr, "cpqr_panel events: whole call %.3f ms on the stream, host enqueue %.3f ms\n", x, host_ms);
+    cudaEventDestroy(ev_begin);
+    cudaEventDestroy(ev_end);
+  }
   if (trace) {
     std::vector<unsigned long long> h(8 * (size_t)G);
     LRB_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));

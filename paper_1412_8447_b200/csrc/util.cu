@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // util.cu -- workspace, TMA descriptors and the HBM-bound data-movement
 // kernels (gathers for C / R / A_skel, transposes, validation, reductions).
 // All reductions use a fixed grid and a fixed tree so results are bitwise
@@ -27,6 +29,8 @@ void* Workspace::try_get(WsSlot s, size_t bytes) {
   const size_t i = static_cast<size_t>(s);
   if (bytes == 0) bytes = 16;
   if (cap_[i] >= bytes) return ptr_[i];
+  static const bool dbg = getenv("LRB_WS_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "workspace slot %zu grows %zu -> %zu bytes (try)\n", i, cap_[i], bytes);
   if (ptr_[i]) {
     LRB_CUDA(cudaDeviceSynchronize());
     LRB_CUDA(cudaFree(ptr_[i]));
@@ -47,6 +51,8 @@ void* Workspace::get(WsSlot s, size_t bytes) {
   const size_t i = static_cast<size_t>(s);
   if (bytes == 0) bytes = 16;
   if (cap_[i] < bytes) {
+    static const bool dbg = getenv("LRB_WS_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "workspace slot %zu grows %zu -> %zu bytes\n", i, cap_[i], bytes);
     if (ptr_[i]) {
       LRB_CUDA(cudaDeviceSynchronize());
       LRB_CUDA(cudaFree(ptr_[i]));
