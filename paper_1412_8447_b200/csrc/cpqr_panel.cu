@@ -379,8 +379,17 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       const int64_t r = threadIdx.x + PT * q;
       xr[q] = 0.0;
       if (r >= s1 && r < m) {
-        double v = xl[q];
-        for (int i = 0; i < c_used; ++i) v = fma(-Vs[i * ld + r], fb[i], v);
+        // four independent chains over the panel's reflectors (latency)
+        double v0 = xl[q], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int i = 0;
+        for (; i + 4 <= c_used; i += 4) {
+          v0 = fma(-Vs[i * ld + r], fb[i], v0);
+          v1 = fma(-Vs[(i + 1) * ld + r], fb[i + 1], v1);
+          v2 = fma(-Vs[(i + 2) * ld + r], fb[i + 2], v2);
+          v3 = fma(-Vs[(i + 3) * ld + r], fb[i + 3], v3);
+        }
+        for (; i < c_used; ++i) v0 = fma(-Vs[i * ld + r], fb[i], v0);
+        const double v = (v0 + v1) + (v2 + v3);
         xr[q] = v;
         if (r == s1) sh_alpha = v;
       }
@@ -417,12 +426,18 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       for (int q = 0; q < kRowsPerThread; ++q)
         if (threadIdx.x + PT * q < ld) vtmp[threadIdx.x + PT * q] = vr[q];
       __syncthreads();
-      for (int i = warp; i < NB; i += PW) {
-        double acc = 0.0;
-        if (i < c_used)
-          for (int64_t rr = s1 + lane; rr < m; rr += 32) acc = fma(Vs[i * ld + rr], vtmp[rr], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) cd[kHdr + ld + i] = acc;
+      static_assert(NB == 4 * PW, "four reflectors per warp");
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};  // reflectors warp + PW t, interleaved
+      for (int64_t rr = s1 + lane; rr < m; rr += 32) {
+        const double vt = vtmp[rr];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[t] = fma(Vs[(warp + PW * t) * ld + rr], vt, acc[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = warp + PW * t;
+        const double w = warp_sum(i < c_used ? acc[t] : 0.0);
+        if (lane == 0) cd[kHdr + ld + i] = w;
       }
     }
     __syncthreads();
