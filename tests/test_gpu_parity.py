@@ -374,3 +374,41 @@ def test_panel_cpqr_edge_shapes(lr, oracle, shape, k):
     o = oracle.cpqr(a, k, want_q=True)
     assert np.array_equal(q.pivots, o["pivots"])
     assert rel(q.s, o["s"]) <= 1e-12 and rel(q.q, o["q"]) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(250, 600), (300, 1000), (500, 1400)])
+def test_panel_cpqr_exact_ties(lr, oracle, shape):
+    """Exact norm ties on the panel path (logical column swaps): every column
+    has a duplicate (negated or not) at a random position, so each pivot's
+    twin carries a bitwise-equal norm in any implementation; about a third of
+    the columns sit left of k and are moved by the reference's swaps before
+    their tie is decided, so the lowest *current* position must win.  k stops
+    at rank m: beyond it only rounding noise is left."""
+    m, n = shape
+    h = n // 2
+    rng = np.random.default_rng(m + n)
+    g = oracle.gaussian_matrix(m, h, m + h) * (2.0 ** (-rng.random(h) * 8))[None, :]
+    pos = rng.permutation(n)
+    a = np.zeros((m, n))
+    a[:, pos[:h]] = g
+    a[:, pos[h:]] = g * np.where(rng.random(h) < 0.5, -1.0, 1.0)[None, :]
+    a = np.asfortranarray(a)
+    q = lr.cpqr_partial(a, m)
+    o = oracle.cpqr(a, m)
+    assert np.array_equal(q.pivots, o["pivots"])
+    assert rel(q.s, o["s"]) <= 1e-12
+
+
+def test_panel_cpqr_tie_after_swap(lr):
+    """A tie decided by a moved column: v at position 0, -v at position 4, the
+    largest column w at position 10.  Step 0 takes w and moves v to position
+    10, so step 1's tie goes to -v at position 4 (slot order would pick 0)."""
+    m, n = 300, 700
+    rng = np.random.default_rng(5)
+    a = 0.01 * rng.standard_normal((m, n))
+    v = rng.standard_normal(m)
+    w = rng.standard_normal(m)
+    w -= (w @ v) / (v @ v) * v  # w orthogonal to v: v's residual norm stays exact
+    a[:, 0], a[:, 4], a[:, 10] = v, -v, 3.0 * w / np.linalg.norm(w) * np.linalg.norm(v)
+    q = lr.cpqr_partial(np.asfortranarray(a), 2)
+    assert list(q.pivots[:2]) == [10, 4]
