@@ -82,6 +82,8 @@ typedef struct {
   long long norm_recomputes; /* exact norm recomputations (cpqr.hpp:80-83)       */
   int solve_escalated;       /* 1 if the last coefficient solve took the pinv path */
   int pinv_fast_path;        /* 1 if the last CUR U used the CholeskyQR2 route    */
+  int concurrent_tail;       /* 1 if the last CUR ran its row-ID and A^T Q_c chains
+                                concurrently on two SM partitions (LRB_CUR_SPLIT)  */
 } lr_stats;
 
 lr_solve_strategy lr_solve_strategy_default(void);

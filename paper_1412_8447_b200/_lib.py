@@ -37,7 +37,8 @@ class lr_sketch_config(ctypes.Structure):
 
 class lr_stats(ctypes.Structure):
     _fields_ = [("cpqr_steps", ctypes.c_longlong), ("norm_recomputes", ctypes.c_longlong),
-                ("solve_escalated", ctypes.c_int), ("pinv_fast_path", ctypes.c_int)]
+                ("solve_escalated", ctypes.c_int), ("pinv_fast_path", ctypes.c_int),
+                ("concurrent_tail", ctypes.c_int)]
 
 
 # every exported symbol of include/lowrank_b200.h with its argument types

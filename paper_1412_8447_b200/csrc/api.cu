@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/lowrank_b200.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -143,6 +145,13 @@ struct lr_ctx {
   // of A (overlapped with the sketch) and device->host of finished factors
   cudaStream_t up_st = nullptr, down_st = nullptr;
   Arena arena;
+  // two disjoint SM partitions (green contexts) for the concurrent CUR tail
+  struct SmSplit {
+    bool tried = false, ok = false;
+    int n1 = 0, n2 = 0;  // SMs of partition 1 (row ID chain) / 2 (A^T Q_c chain)
+    CUgreenCtx g1 = nullptr, g2 = nullptr;
+    CUstream s1 = nullptr, s2 = nullptr;
+  } split;
 };
 
 namespace {
@@ -793,6 +802,7 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
   const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
   mark(c, "cholqr2_r");
   c->stats.pinv_fast_path = 0;
+  c->stats.concurrent_tail = 0;
   if (u_mode == LR_U_CPINV_A_RPINV) {
     DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st);
     DBuf<double> Cm((size_t)even(m) * k, c->st);
@@ -863,6 +873,199 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
     gemm(c, k, k, nr, Grt, even(nr), cft, even(nr), Ut, k, 1.0, 1.0);
   }
   transpose_matrix(k, k, Ut, k, U, k, c->st);
+}
+
+// ---------------------------------------------------------------- concurrent CUR tail
+// After C = A(:, J) the tail of the randomized CUR is two independent chains:
+//   (1) row ID of C (CPQR of C^T, k steps, latency-bound) -> R = A(I, :) ->
+//       CholeskyQR2 of R^T -> Q_r
+//   (2) Q_c = C R_c^-1 -> X^T = A^T Q_c (the second A-sized contraction,
+//       tensor-bound)
+// joined by U = R_c^-1 (X^T ... Q_r) S_r^-T.  They run concurrently on two
+// disjoint SM partitions (green contexts; CUDA driver API through the
+// runtime's entry points), each chain's grids sized to its partition
+// (g_sm_budget).  Same kernels, same arithmetic, same results as the
+// sequential tsid_core + cur_core; LRB_CUR_SPLIT=<SMs of chain 1> enables it
+// (default off, see sm_split).
+namespace {
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+}  // namespace
+
+void release_sm_split(lr_ctx* c) {
+  auto& sp = c->split;
+  using StreamDestroy = CUresult (*)(CUstream);
+  using GreenDestroy = CUresult (*)(CUgreenCtx);
+  auto sdestroy = driver_fn<StreamDestroy>("cuStreamDestroy");
+  auto gdestroy = driver_fn<GreenDestroy>("cuGreenCtxDestroy");
+  if (sdestroy) {
+    if (sp.s1) sdestroy(sp.s1);
+    if (sp.s2) sdestroy(sp.s2);
+  }
+  if (gdestroy) {
+    if (sp.g1) gdestroy(sp.g1);
+    if (sp.g2) gdestroy(sp.g2);
+  }
+  sp = lr_ctx::SmSplit{};
+}
+
+bool sm_split(lr_ctx* c) {
+  auto& sp = c->split;
+  if (sp.tried) return sp.ok;
+  sp.tried = true;
+  // off by default: at C4 both chains scale ~linearly with their SM share, so
+  // the concurrent schedule measured slower than the sequential one (71 vs 62 ms)
+  const char* e = getenv("LRB_CUR_SPLIT");
+  const int want = e ? atoi(e) : 0;
+  if (want <= 0) return false;
+  using DeviceGet = CUresult (*)(CUdevice*, int);
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                             unsigned int);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+  using GreenCreate = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+  using GreenStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+  auto device_get = driver_fn<DeviceGet>("cuDeviceGet");
+  auto get_res = driver_fn<GetRes>("cuDeviceGetDevResource");
+  auto split = driver_fn<Split>("cuDevSmResourceSplitByCount");
+  auto gen = driver_fn<GenDesc>("cuDevResourceGenerateDesc");
+  auto gcreate = driver_fn<GreenCreate>("cuGreenCtxCreate");
+  auto gstream = driver_fn<GreenStream>("cuGreenCtxStreamCreate");
+  if (!device_get || !get_res || !split || !gen || !gcreate || !gstream) return false;
+  CUdevice dev;
+  CUdevResource all{}, part[1], rest{};
+  unsigned nb = 1;
+  CUdevResourceDesc d1, d2;
+  if (device_get(&dev, c->device) != CUDA_SUCCESS || get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(part, &nb, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || nb != 1 ||
+      gen(&d1, &part[0], 1) != CUDA_SUCCESS || gen(&d2, &rest, 1) != CUDA_SUCCESS ||
+      gcreate(&sp.g1, d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      gcreate(&sp.g2, d2, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      gstream(&sp.s1, sp.g1, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+      gstream(&sp.s2, sp.g2, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    release_sm_split(c);
+    sp.tried = true;
+    return false;
+  }
+  sp.n1 = (int)part[0].sm.smCount;
+  sp.n2 = (int)rest.sm.smCount;
+  sp.ok = sp.n1 >= 8 && sp.n2 >= 8;
+  return sp.ok;
+}
+
+// Enqueue on a partition stream: the context stream, the call arena's stream
+// and the grid budget follow it; timing marks pause (intervals across streams
+// mean nothing).  The stream first waits for everything enqueued so far.
+struct OnPartition {
+  lr_ctx* c;
+  cudaStream_t prev_st, prev_ar;
+  int prev_budget;
+  bool prev_timing;
+  OnPartition(lr_ctx* cc, CUstream s, int sms, cudaEvent_t fork) : c(cc) {
+    prev_st = c->st;
+    prev_ar = c->arena.st;
+    prev_budget = g_sm_budget;
+    prev_timing = c->timing;
+    LRB_CUDA(cudaStreamWaitEvent((cudaStream_t)s, fork, 0));
+    c->st = (cudaStream_t)s;
+    c->arena.st = (cudaStream_t)s;
+    g_sm_budget = sms;
+    c->timing = false;
+  }
+  ~OnPartition() {
+    c->st = prev_st;
+    c->arena.st = prev_ar;
+    g_sm_budget = prev_budget;
+    c->timing = prev_timing;
+  }
+};
+
+cudaEvent_t record_event(cudaStream_t s) {
+  cudaEvent_t e;
+  LRB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventRecord(e, s));
+  return e;
+}
+
+bool split_applies(lr_ctx* c, int64_t m, int64_t n, int64_t k, int u_mode) {
+  return u_mode == LR_U_CPINV_A_RPINV && m >= 16384 && n >= 16384 && k > 192 && k <= 512 && sm_split(c);
+}
+
+// tsid_core + cur_core (u_mode LR_U_CPINV_A_RPINV) with the two chains
+// concurrent.  on_rows: row pivots / row coefficients / skeleton are final
+// (called with c->st = chain 1's stream); on_r: R is final (same).
+void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                    const int64_t* col_piv, const double* col_coeff, int64_t ldcc, const lr_solve_strategy& strat,
+                    int64_t* row_piv, double* row_coeff, int64_t ldrc, double* skeleton, double thr, double* C,
+                    double* U, double* R, const std::function<void()>& on_rows, const std::function<void()>& on_r) {
+  if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+  c->stats.concurrent_tail = 0;
+  const int64_t ldk = even(k), ldct = work_ld(k);
+  gather_columns(m, k, a, lda, col_piv, C, m, c->st);
+  DBuf<double> Ctp((size_t)ldct * m, c->st), Ct((size_t)ldk * m, c->st);
+  zero_pad_rows(c, Ctp, k, ldct, m);
+  transpose_matrix(m, k, C, m, Ctp, ldct, c->st);
+  copy_matrix(k, m, Ctp, ldct, Ct, ldk, c->st);
+  require_rank_in_range(k, k, m, "id_column");
+  mark(c, "gather_c");
+  DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st), Cm((size_t)even(m) * k, c->st);
+  copy_matrix(m, k, C, m, Cm, even(m), c->st);
+  const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci);
+  mark(c, "cholqr2_c");
+  DBuf<double> Qc((size_t)even(m) * k, c->st), Xt((size_t)even(n) * k, c->st);
+  DBuf<double> tau(k, c->st), Rt((size_t)even(n) * k, c->st), Rk((size_t)ldk * n, c->st);
+  DBuf<double> Sr((size_t)k * k, c->st), Sri((size_t)k * k, c->st), Qr((size_t)even(n) * k, c->st);
+  cudaEvent_t fork = record_event(c->st);
+  cudaEvent_t done2 = nullptr, done1 = nullptr;
+  const auto& sp = c->split;
+  if (c_ok) {  // chain 2 first: it has no host synchronisation, so it is fully enqueued before chain 1 blocks
+    OnPartition on(c, sp.s2, sp.n2, fork);
+    gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m));         // Qc = C Rc^-1
+    gemm_a(c, n, k, m, a, lda, Qc, even(m), Xt, even(n), 0);  // X^T = A^T Qc
+    done2 = record_event(c->st);
+  }
+  bool r_ok = false;
+  {
+    OnPartition on(c, sp.s1, sp.n1, fork);
+    cpqr_core(c, k, m, Ctp, ldct, k, row_piv, tau, "cpqr_partial", work_padded(k, ldct));
+    solve_core(c, k, m - k, Ctp, ldct, Ctp.p + k * ldct, ldct, strat, row_coeff, ldrc, false);
+    if (skeleton) gather_rows(k, k, C, m, row_piv, skeleton, k, c->st);
+    on_rows();
+    gather_rows(k, n, a, lda, row_piv, R, k, c->st);
+    on_r();
+    transpose_matrix(k, n, R, k, Rt, even(n), c->st);
+    copy_matrix(k, n, R, k, Rk, ldk, c->st);
+    r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
+    if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n));  // Qr = R^T Sr^-1
+    done1 = record_event(c->st);
+  }
+  LRB_CUDA(cudaStreamWaitEvent(c->st, done1, 0));
+  if (done2) LRB_CUDA(cudaStreamWaitEvent(c->st, done2, 0));
+  for (cudaEvent_t e : {fork, done1, done2})
+    if (e) cudaEventDestroy(e);
+  mark(c, "tsid_ctA_split");
+  if (!(c_ok && r_ok)) {  // rare: the general U path, sequentially
+    u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, LR_U_CPINV_A_RPINV, U, Ct,
+           [&](const double* Q, int64_t ldq, double* X, int64_t ldx) { gemm_a(c, n, k, m, a, lda, Q, ldq, X, ldx, 0); });
+    return;
+  }
+  c->stats.pinv_fast_path = 1;
+  c->stats.concurrent_tail = 1;
+  DBuf<double> W((size_t)k * k, c->st), t1((size_t)k * k, c->st), tt((size_t)k * k, c->st),
+      st((size_t)k * k, c->st);
+  gemm(c, k, k, n, Xt, even(n), Qr, even(n), W, k);  // W = Qc^T A Qr
+  transpose_matrix(k, k, Rci, k, tt, k, c->st);
+  gemm(c, k, k, k, tt, k, W, k, t1, k);              // t1 = Rc^-1 W
+  transpose_matrix(k, k, t1, k, tt, k, c->st);
+  transpose_matrix(k, k, Sri, k, st, k, c->st);
+  gemm(c, k, k, k, tt, k, st, k, U, k);              // U = t1 Sr^-T
+  mark(c, "u_small");
 }
 
 // cur.hpp:23-34 / lowrank_main.cpp:215 on a dense A given the skeleton index sets
@@ -1136,6 +1339,7 @@ int lr_ctx_destroy(lr_ctx* c) {
     cudaFreeHost(c->h_ll);
     if (c->up_st) cudaStreamDestroy(c->up_st);
     if (c->down_st) cudaStreamDestroy(c->down_st);
+    release_sm_split(c);
     cudaStreamDestroy(c->own);
     delete c;
   });
@@ -1572,6 +1776,11 @@ int lr_randomized_cur_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
     mark(c, "begin");
     OzakiScope scope(c);
     randomized_id_core(c, m, n, a, lda, k, cfg, strat, col_pivots, col_coeff, k);
+    if (split_applies(c, m, n, k, u_mode)) {
+      tsid_cur_split(c, m, n, a, lda, k, col_pivots, col_coeff, k, strat, row_pivots, row_coeff, k, skeleton, thr, C,
+                     U, R, [] {}, [] {});
+      return;
+    }
     DBuf<double> Ct((size_t)even(k) * m, c->st);
     tsid_core(c, m, n, a, lda, k, col_pivots, strat, row_pivots, row_coeff, k, skeleton, C, Ct);
     cur_core(c, m, n, a, lda, k, col_pivots, col_coeff, k, row_pivots, thr, u_mode, C, U, R, Ct);
@@ -1607,15 +1816,24 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
       }
       down.idx(n, cp, col_pivots);
       down.mat(k, n - k, ccd, k, col_coeff, k);
-      DBuf<double> Ct((size_t)even(k) * m, c->st);
-      tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
-      down.idx(m, rp, row_pivots);
-      down.mat(m, k, Cd, m, C, m);
-      down.mat(k, m - k, rcd, k, row_coeff, k);
-      down.mat(k, k, skd, k, skeleton, k);
-      cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
-      down.mat(k, k, Ud, k, U, k);
-      down.mat(k, n, Rd, k, R, k);
+      auto rows_done = [&] {
+        down.idx(m, rp, row_pivots);
+        down.mat(m, k, Cd, m, C, m);
+        down.mat(k, m - k, rcd, k, row_coeff, k);
+        down.mat(k, k, skd, k, skeleton, k);
+      };
+      if (split_applies(c, m, n, k, u_mode)) {
+        tsid_cur_split(c, m, n, d, l, k, cp, ccd, k, strat, rp, rcd, k, skd, thr, Cd, Ud, Rd, rows_done,
+                       [&] { down.mat(k, n, Rd, k, R, k); });
+        down.mat(k, k, Ud, k, U, k);
+      } else {
+        DBuf<double> Ct((size_t)even(k) * m, c->st);
+        tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
+        rows_done();
+        cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+        down.mat(k, k, Ud, k, U, k);
+        down.mat(k, n, Rd, k, R, k);
+      }
       down.finish();
     }
     sync(c);

@@ -36,6 +36,10 @@ extern unsigned long long g_kernel_launches;
 
 constexpr int kNumSMsB200 = 148;
 
+// SMs of the partition the calling thread is enqueueing for (a green-context
+// stream, see api.cu tsid_cur_split), else 0 = the whole device
+extern thread_local int g_sm_budget;
+
 inline int num_sms() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -43,7 +47,7 @@ inline int num_sms() {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v > 0 ? v : kNumSMsB200;
   }();
-  return n;
+  return g_sm_budget > 0 && g_sm_budget < n ? g_sm_budget : n;
 }
 
 // ------------------------------------------------------------ device utils

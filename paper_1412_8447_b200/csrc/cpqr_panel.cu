@@ -771,7 +771,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     attr = true;
   }
   // one CTA per SM (the shared memory holds the panel's V)
-  int G = std::min(num_sms(), kMaxG);
+  static const int grid_cap = getenv("LRB_CPQR_GRID") ? atoi(getenv("LRB_CPQR_GRID")) : 0;  // diagnostic
+  int G = std::min(grid_cap > 0 ? std::min(grid_cap, num_sms()) : num_sms(), kMaxG);
   G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + PW - 1) / PW));
   const int64_t maxcols = (n + G - 1) / G + 1;
   const size_t smem = panel_smem_bytes(ld, maxcols);

@@ -11,6 +11,9 @@
 
 namespace lrb {
 
+thread_local int g_sm_budget = 0;
+
+
 unsigned long long g_kernel_launches = 0;
 
 // ---------------------------------------------------------------- workspace
