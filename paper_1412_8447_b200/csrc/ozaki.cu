@@ -50,6 +50,10 @@ __constant__ double c_inv_mod[kOzakiModuli];
 __constant__ unsigned long long c_Mt[kOzakiModuli][2];  // M / m_t (low, high limbs)
 __constant__ int c_crt_inv[kOzakiModuli];               // (M / m_t)^-1 mod m_t
 __constant__ unsigned long long c_Mcrt[2];
+// c_t = (M / m_t) ((M / m_t)^-1 mod m_t) < M as 32-bit limbs; C' = sum_t r_t c_t mod M
+__constant__ uint32_t c_crt_c[kOzakiModuli][4];
+__constant__ unsigned long long c_crt_k0[2];  // 128 sum_t c_t mod 2^128 (residue offset r + 128)
+__constant__ double c_crt_invM, c_crt_k0M;    // 1 / M, 128 sum_t c_t / M
 
 typedef unsigned __int128 u128;
 typedef __int128 i128;
@@ -106,6 +110,21 @@ void upload_constants() {
   LRB_CUDA(cudaMemcpyToSymbol(c_Mt, mt, sizeof mt));
   LRB_CUDA(cudaMemcpyToSymbol(c_crt_inv, h.inv, sizeof h.inv));
   LRB_CUDA(cudaMemcpyToSymbol(c_Mcrt, mm, sizeof mm));
+  uint32_t cl[kOzakiModuli][4];
+  u128 k0 = 0;
+  double k0M = 0.0;
+  for (int t = 0; t < kOzakiModuli; ++t) {
+    const u128 ct = h.Mt[t] * (u128)h.inv[t];  // < M: inv < m_t
+    for (int i = 0; i < 4; ++i) cl[t][i] = (uint32_t)(ct >> (32 * i));
+    k0 += (u128)128 * ct;  // mod 2^128
+    k0M += 128.0 * ((double)ct / (double)h.M);
+  }
+  const unsigned long long k0w[2] = {(unsigned long long)k0, (unsigned long long)(k0 >> 64)};
+  const double invM = 1.0 / (double)h.M;
+  LRB_CUDA(cudaMemcpyToSymbol(c_crt_c, cl, sizeof cl));
+  LRB_CUDA(cudaMemcpyToSymbol(c_crt_k0, k0w, sizeof k0w));
+  LRB_CUDA(cudaMemcpyToSymbol(c_crt_invM, &invM, sizeof invM));
+  LRB_CUDA(cudaMemcpyToSymbol(c_crt_k0M, &k0M, sizeof k0M));
   done = true;
 }
 
@@ -464,18 +483,28 @@ __global__ void crt_kernel(int64_t M, int64_t N, const int8_t* __restrict__ res,
     const int sq = shift_q[j];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
       const int8_t* r = res + j * ldr + i;
-      i128 s = 0;
+      // T = sum_t (r_t + 128) c_t exactly in four 64-bit limb accumulators
+      // (32x32 -> 64 multiply-adds; each limb sum < 2^44), then one quotient
+      // q = round((T - K0) / M) in FP64 (|C'| <= 0.39 M at the largest K, far
+      // from the rounding boundary) and C' = T - K0 - q M in wrapping 128-bit
+      // arithmetic; the final +-M step only guards the quotient
+      unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
       for (int p = 0; p < kOzakiModuli; ++p) {
-        const int m = kmod(p);
-        int d = ((int)r[p * plane_stride] * kcrt_inv(p)) % m;
-        if (d > m / 2) d -= m;
-        else if (d < -(m / 2)) d += m;
-        const i128 Mt = (i128)(((u128)kcrt_hi(p) << 64) | (u128)kcrt_lo(p));
-        s += (i128)d * Mt;  // |term| <= M/2
-        if (s > half) s -= Mc;
-        else if (s < -half) s += Mc;
+        const uint32_t rp = (uint32_t)((int)r[p * plane_stride] + 128);
+        a0 += (unsigned long long)c_crt_c[p][0] * rp;
+        a1 += (unsigned long long)c_crt_c[p][1] * rp;
+        a2 += (unsigned long long)c_crt_c[p][2] * rp;
+        a3 += (unsigned long long)c_crt_c[p][3] * rp;
       }
+      const double td = fma(fma(fma((double)a3, 4294967296.0, (double)a2), 4294967296.0, (double)a1), 4294967296.0,
+                            (double)a0);
+      const long long q = __double2ll_rn(fma(td, c_crt_invM, -c_crt_k0M));
+      const u128 T = (u128)a0 + ((u128)a1 << 32) + ((u128)a2 << 64) + ((u128)a3 << 96);
+      const u128 K0 = ((u128)c_crt_k0[1] << 64) | (u128)c_crt_k0[0];
+      i128 s = (i128)(T - K0 - (u128)(i128)q * (u128)Mc);
+      if (s > half) s -= Mc;
+      else if (s < -half) s += Mc;
       // int128 -> double (round to nearest via the high/low split), then unscale
       const bool neg = s < 0;
       const u128 a = neg ? (u128)(-s) : (u128)s;
