@@ -126,14 +126,16 @@ def kernel_rooflines(cfg, st, stages, engine):
         if st.get(name):
             b = cpqr_bytes(rows, cols, steps)
             ach = b / (st[name] * 1e-3) / 1e9
-            out[name] = {"kernel": "cpqr_panel_kernel x16 + panel_update_kernel x15 (delayed-update CPQR, one "
-                                   "cooperative launch per 32 steps)",
+            out[name] = {"kernel": "cpqr_panel_kernel x16 + panel_update_dmma_kernel x15 (delayed-update CPQR, one "
+                                   "cooperative launch per 32 steps, logical column swaps)",
                          "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "traffic": traffic.get(name),
                          "algorithmic": f"SURVEY 8d right-looking count sum_s 16 (rows-s)(cols-s) + 32 (cols-s) "
                                         f"= {b:.4e} B per launch (the panel form moves less: see traffic)",
-                         "note": "step-latency floor ~16 us/step (argmax -> reflector broadcast -> grid barrier) "
-                                 "x 510 steps; tools/bench_cpqr.py with LRB_CPQR_TRACE=1 breaks it down"}
+                         "note": "per step ~7 us of fixed latency (argmax -> reflector broadcast -> candidate "
+                                 "staging -> grid barrier) on top of the HBM-bound pass; runs at the power-capped "
+                                 "SM clock left by the INT8 GEMMs; tools/bench_cpqr.py with LRB_CPQR_TRACE=1 "
+                                 "breaks it down"}
     return out
 
 
@@ -360,8 +362,11 @@ def run_ours(args, rank, world, local_rank):
         cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=hout)  # warm-up
         barrier()
         t0 = time.perf_counter()
+        step_s = []
         for _ in range(e2e_steps):
+            ts = time.perf_counter()
             cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=hout)
+            step_s.append(round(time.perf_counter() - ts, 4))
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         if world > 1:
             import torch.distributed as dist
@@ -371,7 +376,7 @@ def run_ours(args, rank, world, local_rank):
         k = cfg.k
         d2h = 8 * (cfg.n + cfg.m) + 8 * (cfg.m * k + k * k + k * cfg.n + k * (cfg.n - k) + k * (cfg.m - k) + k * k)
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * cfg.m * cfg.n, "d2h_bytes_per_step": d2h,
-               "steps": e2e_steps, "host_buffer": "pinned A and pinned result buffers",
+               "steps": e2e_steps, "step_s": step_s, "host_buffer": "pinned A and pinned result buffers",
                "pipeline": "A uploaded in column chunks on a copy stream, each chunk sketched as it lands; "
                            "finished factors copied back on a second stream during the rest of the CUR"}
 
