@@ -361,6 +361,10 @@ def run_ours(args, rank, world, local_rank):
         hout = lr.pinned_cur_outputs(cfg.m, cfg.n, cfg.k)  # reused page-locked result buffers
         cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=hout)  # warm-up
         barrier()
+        e2e_timing = os.environ.get("BENCH_E2E_TIMING") is not None  # diagnostic: stage marks in the e2e calls
+        if e2e_timing:
+            ctx.reset_stats()
+            ctx.enable_timing(True)
         t0 = time.perf_counter()
         step_s = []
         for _ in range(e2e_steps):
@@ -368,6 +372,9 @@ def run_ours(args, rank, world, local_rank):
             cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=hout)
             step_s.append(round(time.perf_counter() - ts, 4))
         e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if e2e_timing:
+            print(json.dumps({"e2e_stages": ctx.stage_report()}), file=sys.stderr)
+            ctx.enable_timing(False)
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)

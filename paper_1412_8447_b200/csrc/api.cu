@@ -156,6 +156,12 @@ struct lr_ctx {
 
 namespace {
 
+// Small device -> host reads of control values (flags, norms) go through a
+// one-warp kernel into the context's mapped pinned words instead of
+// cudaMemcpyAsync: a copy would queue on the copy engine behind the
+// megabyte-sized factor downloads in flight on the download stream.
+void d2h_mapped(lr_ctx* c, void* h, const void* d, size_t bytes) { copy_bytes_mapped(h, d, bytes, c->st); }
+
 // Close the interval since the previous mark and label it `stage`.
 void mark(lr_ctx* c, const char* stage) {
   if (!c->timing) return;
@@ -219,7 +225,7 @@ bool device_all_finite(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
   DBuf<int> f(1, c->st);
   LRB_CUDA(cudaMemsetAsync(f.p, 0, sizeof(int), c->st));
   check_finite(m, n, a, lda, f, c->st);
-  LRB_CUDA(cudaMemcpyAsync(c->h_flags, f.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  d2h_mapped(c, c->h_flags, f.p, sizeof(int));
   sync(c);
   return c->h_flags[0] == 0;
 }
@@ -335,8 +341,8 @@ void cpqr_core(lr_ctx* c, int64_t m, int64_t n, double* W, int64_t ldw, int64_t 
   LRB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), c->st));
   LRB_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(long long), c->st));
   cpqr_inplace(c->ws, m, n, W, ldw, k, piv, tau, flags, rec, padded, c->st, nopivot);
-  LRB_CUDA(cudaMemcpyAsync(c->h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  LRB_CUDA(cudaMemcpyAsync(c->h_ll, rec.p, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  d2h_mapped(c, c->h_flags, flags.p, sizeof(int));
+  d2h_mapped(c, c->h_ll, rec.p, sizeof(long long));
   sync(c);
   if (c->h_flags[0]) fail(LR_EINVAL, std::string(who) + ": matrix has non-finite entries");
   c->stats.cpqr_steps += k;
@@ -355,7 +361,7 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
     LRB_CUDA(cudaMemsetAsync(fl.p, 0, 2 * sizeof(int), c->st));
     check_upper_triangular(k, s11, ld11, fl, c->st);
     check_finite(k, nc, s12, ld12, fl.p + 1, c->st);
-    LRB_CUDA(cudaMemcpyAsync(c->h_flags, fl.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    d2h_mapped(c, c->h_flags, fl.p, 2 * sizeof(int));
     sync(c);
     if (c->h_flags[1]) fail(LR_EINVAL, "stabilized_coeff_solve: non-finite entries");
     if (c->h_flags[0]) fail(LR_EINVAL, "stabilized_coeff_solve: block is not upper triangular");
@@ -366,7 +372,7 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
   if (kind == LR_SOLVE_BACKSUB && strat.escalate) {
     DBuf<double> mm(2, c->st);
     diag_absminmax(k, s11, ld11, mm, c->st);
-    LRB_CUDA(cudaMemcpyAsync(c->h_scal, mm.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    d2h_mapped(c, c->h_scal, mm.p, 2 * sizeof(double));
     sync(c);
     const double dmax = c->h_scal[0], dmin = c->h_scal[1];
     if (dmax == 0.0 || dmin == 0.0 || dmax / dmin > 1e10) kind = LR_SOLVE_PINV;
@@ -486,7 +492,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   DBuf<int> info(2, c->st);
   gemm(c, k, k, rows, X, ldx, X, ldx, G, k, 1.0, 0.0, -1, true);  // G1 = X^T X (upper tiles)
   cholesky_upper(c->ws, k, G, k, info, c->st);  // G <- R1
-  LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  d2h_mapped(c, c->h_flags, info.p, sizeof(int));
   sync(c);
   if (c->h_flags[0] != 0) return false;
   tri_upper_inverse_blocked(k, G, k, R1inv, k, c->st);
@@ -494,7 +500,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   DBuf<double> G2((size_t)k * k, c->st), R2t((size_t)k * k, c->st);
   gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k, 1.0, 0.0, -1, true);  // G2 = Q1^T Q1
   cholesky_upper(c->ws, k, G2, k, info.p + 1, c->st);
-  LRB_CUDA(cudaMemcpyAsync(c->h_flags + 1, info.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  d2h_mapped(c, c->h_flags + 1, info.p + 1, sizeof(int));
   sync(c);
   if (c->h_flags[1] != 0) return false;
   // R = R2 R1: R(i,j) = sum_l R2(i,l) R1(l,j) -> P = R2^T
@@ -504,7 +510,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   DBuf<double> part(4 * num_sms() + 4, c->st), f(2, c->st);
   frob2(k, k, R, k, part, f, c->st);
   frob2(k, k, Rinv, k, part, f.p + 1, c->st);
-  LRB_CUDA(cudaMemcpyAsync(c->h_scal, f.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  d2h_mapped(c, c->h_scal, f.p, 2 * sizeof(double));
   sync(c);
   const double cond_bound = std::sqrt(c->h_scal[0]) * std::sqrt(c->h_scal[1]);
   return std::isfinite(cond_bound) && cond_bound < 1e7;
@@ -1071,10 +1077,12 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
 // cur.hpp:23-34 / lowrank_main.cpp:215 on a dense A given the skeleton index sets
 void cur_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
               const double* col_coeff, int64_t ldcc, const int64_t* row_piv, double thr, int u_mode, double* C,
-              double* U, double* R, const double* Ct_in /* k x m ld even(k), may be null */) {
+              double* U, double* R, const double* Ct_in /* k x m ld even(k), may be null */,
+              const std::function<void()>& on_r = {} /* R is final (e.g. start its download) */) {
   if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
   gather_columns(m, k, a, lda, col_piv, C, m, c->st);
   gather_rows(k, n, a, lda, row_piv, R, k, c->st);
+  if (on_r) on_r();
   u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, u_mode, U, Ct_in,
          [&](const double* Q, int64_t ldq, double* Xt, int64_t ldxt) {
            gemm_a(c, n, k, m, a, lda, Q, ldq, Xt, ldxt, 0);
@@ -1169,16 +1177,28 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
     c->oz_ld = l;
   }
   mark(c, "omega");
-  // ~8 chunks, whole 512-column tiles of the INT8 GEMM
+  // ~8 chunks, whole 512-column tiles of the INT8 GEMM; the last full chunk
+  // is cut into halving pieces so that the sketch left after the final
+  // transfer (the only part not hidden behind PCIe) is one small piece
   const int64_t chunk = std::max<int64_t>(512, ((n + 7) / 8 + 511) / 512 * 512);
+  std::vector<int64_t> pieces;
+  for (int64_t o = 0; o < n; o += chunk) pieces.push_back(std::min(chunk, n - o));
+  int64_t last = pieces.back();
+  pieces.pop_back();
+  while (last > 1024) {
+    const int64_t h = ((last / 2) + 511) / 512 * 512;
+    pieces.push_back(h);
+    last -= h;
+  }
+  pieces.push_back(last);
   cudaEvent_t ready;
   LRB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   cudaEvent_t start;
   LRB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
   LRB_CUDA(cudaEventRecord(start, c->st));  // d is allocated on the compute stream
   LRB_CUDA(cudaStreamWaitEvent(up, start, 0));
-  for (int64_t off = 0; off < n; off += chunk) {
-    const int64_t nc = std::min(chunk, n - off);
+  int64_t off = 0;
+  for (const int64_t nc : pieces) {
     LRB_CUDA(cudaMemcpy2DAsync(d + off * l, l * sizeof(double), a + off * lda, lda * sizeof(double),
                                m * sizeof(double), nc, cudaMemcpyHostToDevice, up));
     LRB_CUDA(cudaEventRecord(ready, up));
@@ -1190,6 +1210,7 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
     } else {
       gemm(c, ell, nc, m, omt, m, d + off * l, l, Y + off * ldy, ldy);
     }
+    off += nc;
   }
   cudaEventDestroy(ready);
   cudaEventDestroy(start);
@@ -1830,9 +1851,9 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
         DBuf<double> Ct((size_t)even(k) * m, c->st);
         tsid_core(c, m, n, d, l, k, cp, strat, rp, rcd, k, skd, Cd, Ct);
         rows_done();
-        cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct);
+        cur_core(c, m, n, d, l, k, cp, ccd, k, rp, thr, u_mode, Cd, Ud, Rd, Ct,
+                 [&] { down.mat(k, n, Rd, k, R, k); });
         down.mat(k, k, Ud, k, U, k);
-        down.mat(k, n, Rd, k, R, k);
       }
       down.finish();
     }
@@ -2129,7 +2150,7 @@ int lr_cholesky_upper_d(lr_ctx* c, int64_t k, double* g, int64_t ldg) {
     checked(c);
     DBuf<int> info(1, c->st);
     cholesky_upper(c->ws, k, g, ldg, info, c->st);
-    LRB_CUDA(cudaMemcpyAsync(c->h_flags, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    d2h_mapped(c, c->h_flags, info.p, sizeof(int));
     sync(c);
     if (c->h_flags[0]) fail(LR_ERUNTIME, "cholesky: leading minor " + std::to_string(c->h_flags[0]) + " not positive");
   });

@@ -201,4 +201,8 @@ void dot_sum(int64_t m, int64_t n, const double* x, int64_t ldx, const double* y
 bool jacobi_svd(Workspace& ws, int64_t m, int64_t n, const double* a, int64_t lda, double* u, double* sigma,
                 double* v, cudaStream_t st);
 
+// bytes (<= a few KB) from device memory to mapped pinned host memory by a
+// one-warp kernel (no copy-engine queueing behind bulk transfers)
+void copy_bytes_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 }  // namespace lrb

@@ -332,4 +332,15 @@ void max_abs(int64_t m, int64_t n, const double* a, int64_t lda, double* partial
   LRB_CHECK_LAUNCH();
 }
 
+namespace {
+__global__ void copy_bytes_kernel(char* __restrict__ dst, const char* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+void copy_bytes_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  copy_bytes_kernel<<<1, 32, 0, st>>>(static_cast<char*>(dst), static_cast<const char*>(src), (int)bytes);
+  LRB_CHECK_LAUNCH();
+}
+
 }  // namespace lrb
