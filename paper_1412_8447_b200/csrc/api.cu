@@ -610,13 +610,22 @@ void sketch_operator_t(lr_ctx* c, int64_t m, int64_t ell, int kind, uint64_t see
   }
 }
 
+// sketch.hpp:137-141: for a row count that is not a power of two the
+// reference forms the SRFT sample as the plain dense product operator * A;
+// that product is reproduced with its exact arithmetic (ascending k, no FMA),
+// the power-of-two (fast Hartley) case is contracted on the tensor cores
+inline bool srft_dense_fallback(int kind, int64_t m) { return kind == LR_SKETCH_SRFT && (m & (m - 1)) != 0; }
+
 void sketch_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t ell, uint64_t seed,
                  double* y, int64_t ldy, int kind = LR_SKETCH_GAUSSIAN) {
   DBuf<double> omt((size_t)m * even(ell), c->st);
   // Omega^T (m x ell): element (i,j) of Omega stored at omt[j + i*m]
   sketch_operator_t(c, m, ell, kind, seed, omt);
   mark(c, "omega");
-  gemm_a(c, ell, n, m, omt, m, a, lda, y, ldy, 1);
+  if (srft_dense_fallback(kind, m))
+    gemm_tn_ordered((int)ell, (int)n, (int)m, omt, m, a, lda, y, ldy, c->st);
+  else
+    gemm_a(c, ell, n, m, omt, m, a, lda, y, ldy, 1);
   mark(c, "sketch_gemm");
 }
 
@@ -1154,7 +1163,8 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
   cudaStream_t up = aux_stream(c->up_st);
   DBuf<double> omt((size_t)m * even(ell), c->st);
   sketch_operator_t(c, m, ell, kind, seed, omt);
-  bool oz = c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
+  const bool ordered = srft_dense_fallback(kind, m);
+  bool oz = !ordered && c->gemm_mode == LR_GEMM_OZAKI_INT8 && m <= kOzakiMaxK;
   OzakiOperand om;
   int8_t* aplanes = nullptr;
   if (oz) {
@@ -1207,6 +1217,8 @@ void upload_sketch(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
       const OzakiOperand view = ozaki_cols(c->oz_op, off, nc);
       ozaki_split_into(d + off * l, l, view, c->st);
       ozaki_gemm_tn(c->ws, om, view, ell, nc, Y + off * ldy, ldy, 1.0, 0.0, c->st);
+    } else if (ordered) {
+      gemm_tn_ordered((int)ell, (int)nc, (int)m, omt, m, d + off * l, l, Y + off * ldy, ldy, c->st);
     } else {
       gemm(c, ell, nc, m, omt, m, d + off * l, l, Y + off * ldy, ldy);
     }

@@ -205,4 +205,10 @@ bool jacobi_svd(Workspace& ws, int64_t m, int64_t n, const double* a, int64_t ld
 // one-warp kernel (no copy-engine queueing behind bulk transfers)
 void copy_bytes_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st);
 
+// out = P^T Q (P: K x M, Q: K x N) summed in ascending k without fused
+// multiply-add: the host triple-loop arithmetic of the reference's dense
+// SRFT fallback, reproduced bit for bit
+void gemm_tn_ordered(int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq, double* out,
+                     int64_t ldo, cudaStream_t st);
+
 }  // namespace lrb

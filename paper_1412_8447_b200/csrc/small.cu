@@ -532,6 +532,48 @@ void gemm_nn_small(int m, int n, int kk, double alpha, const double* A, int64_t 
 }
 }  // namespace
 
+namespace {
+// out = P^T Q with every entry summed in ascending k as fl(acc + fl(p q)) --
+// no fused multiply-add, the arithmetic of a plain host triple loop (the
+// reference's dense SRFT fallback is such a product, sketch.hpp:137-141)
+__global__ void gemm_tn_ordered_kernel(int M, int N, int K, const double* __restrict__ P, int64_t ldp,
+                                       const double* __restrict__ Q, int64_t ldq, double* __restrict__ out,
+                                       int64_t ldo) {
+  __shared__ double Ps[32][33];  // Ps[k][i] = P(k0 + k, i0 + i)
+  __shared__ double Qs[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int t = threadIdx.x; t < 32 * 32; t += blockDim.x) {
+      const int kk = t & 31, b = t >> 5;
+      Ps[kk][b] = (k0 + kk < K && i0 + b < M) ? P[(k0 + kk) + (int64_t)(i0 + b) * ldp] : 0.0;
+      Qs[kk][b] = (k0 + kk < K && j0 + b < N) ? Q[(k0 + kk) + (int64_t)(j0 + b) * ldq] : 0.0;
+    }
+    __syncthreads();
+    const int kn = K - k0 < 32 ? K - k0 : 32;
+    for (int kk = 0; kk < kn; ++kk) {
+      const double pv = Ps[kk][ti];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(pv, Qs[kk][tj + 8 * q]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ti, j = j0 + tj + 8 * q;
+    if (i < M && j < N) out[i + (int64_t)j * ldo] = acc[q];
+  }
+}
+}  // namespace
+
+void gemm_tn_ordered(int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq, double* out,
+                     int64_t ldo, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  gemm_tn_ordered_kernel<<<dim3((M + 31) / 32, (N + 31) / 32), 256, 0, st>>>(M, N, K, P, ldp, Q, ldq, out, ldo);
+  LRB_CHECK_LAUNCH();
+}
+
 // R^-1 of an upper-triangular R with a nonzero diagonal by blocks: diagonal
 // blocks by back substitution, then [A B; 0 C]^-1 = [A^-1, -A^-1 B C^-1; 0, C^-1]
 // level by level (the serial chain is kInvB steps, not k).

@@ -22,7 +22,7 @@ from . import _lib as L
 __all__ = [
     "SingularityError", "ConvergenceError", "LowrankCudaError", "SolveKind", "SolveStrategy", "SketchKind",
     "SketchConfig", "PivotedQr", "ColumnId", "RowId", "TwoSidedId", "CurDecomposition", "SampleMatrix",
-    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_srft", "sketch_power", "cpqr_partial", "cpqr_full",
+    "Context", "default_context", "gaussian_matrix", "sketch_gaussian", "sketch_srft", "srft_operator", "sketch_power", "cpqr_partial", "cpqr_full",
     "stabilized_coeff_solve", "svd", "pinv", "id_column", "id_row", "tsid_from_column_id", "id_two_sided",
     "cur_from_two_sided", "cur_id", "randomized_id", "randomized_cur", "randomized_svd", "select_columns", "select_rows",
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
@@ -385,6 +385,14 @@ def sketch_srft(a, ell: int, seed: int, ctx: Optional[Context] = None) -> Sample
     y = np.empty((int(ell), n), order="F")
     _raise(c.lib.lr_sketch_srft(c.h, m, n, _ptr(a), _ld(a), int(ell), int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(y)))
     return SampleMatrix(y, SampleProvenance(SketchKind.Srft, int(ell), 0, False, int(seed)))
+
+
+def srft_operator(m: int, ell: int, seed: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """sketch.hpp:84-100: the dense SRFT operator sqrt(m/ell) R H D (ell x m)."""
+    c = _ctx(ctx)
+    out = np.empty((int(ell), int(m)), order="F")
+    _raise(c.lib.lr_srft_operator(c.h, int(m), int(ell), int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(out)))
+    return out
 
 
 def sketch_power(a, ell: int, q: int, reorthonormalize: bool = True, seed: int = 0,

@@ -352,15 +352,26 @@ def test_randomized_svd_matches_oracle(lr, oracle, kw):
     assert rel(g.u * sgn, uo) <= 1e-9 and rel(g.v * sgn, vo) <= 1e-9
 
 
-def test_srft_dense_fallback_roundoff(lr, oracle):
-    """test_sketch.cpp:76-81 asks sketch_srft(a) == srft_operator(m, l, s) * a bitwise for
-    non-power-of-two m (the reference's fallback IS that host product); on the GPU the
-    contraction runs on the tensor cores, so the identity holds to roundoff."""
-    a = oracle.gaussian_matrix(48, 10, 70)
-    y = lr.sketch_srft(a, 12, 8).y
-    om = oracle.srft_operator(48, 12, 8)
-    assert np.max(np.abs(y - om @ a)) <= 1e-14 * np.max(np.abs(om @ a)) * 48
-    assert rel(y, oracle.sketch_srft(a, 12, 8)) <= 1e-14
+def _ordered_product(om, a):
+    """operator * a summed in ascending k as fl(acc + fl(p q)): a host triple loop."""
+    y = np.zeros((om.shape[0], a.shape[1]))
+    for k in range(om.shape[1]):
+        y = y + np.outer(om[:, k], a[k, :])  # elementwise IEEE products, then one rounding per add
+    return y
+
+
+@pytest.mark.parametrize("m,ell,n", [(48, 12, 10), (100, 30, 7), (777, 40, 33)])
+def test_srft_dense_fallback_bitwise(lr, oracle, m, ell, n):
+    """test_sketch.cpp:76-81: for non-power-of-two m the reference's sketch_srft IS the
+    dense product srft_operator(m, l, s) * a (sketch.hpp:137-141), and the test demands
+    bitwise equality with that host product.  The GPU reproduces the product's
+    arithmetic (ascending k, no FMA) on the library's own operator; against the
+    oracle's operator (host libm cos/sin) the sample agrees to roundoff."""
+    a = oracle.gaussian_matrix(m, n, m + n)
+    y = lr.sketch_srft(a, ell, 8).y
+    om = lr.srft_operator(m, ell, 8)
+    assert np.array_equal(y, _ordered_product(om, a))
+    assert rel(y, oracle.sketch_srft(a, ell, 8)) <= 1e-14
 
 
 @pytest.mark.parametrize("shape,k", [((250, 37), 37), ((250, 1), 1), ((300, 700), 33), ((512, 1300), 512),
