@@ -180,11 +180,11 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
   constexpr bool SPEC = TC0 >= 0;
   constexpr int NA = SPEC ? NLD - TC0 : CH;
   // lanes per column: a power of two with 16 rows (8 row pairs) or fewer per lane
-  constexpr int L = !SPEC ? 32 : (NA >= 5 ? 32 : (NA >= 3 ? 16 : 4 * NA));
+  constexpr int L = !SPEC ? 32 : (NA >= 5 ? 16 : (NA >= 2 ? 8 : 4));
   constexpr int KP = SPEC ? 32 * NA / L : CH;  // row pairs per lane
   constexpr int GPW = 32 / L;
   constexpr int S = NB / L;
-  constexpr int D = S == 1 ? 4 : (S <= 2 ? 3 : 2);  // warp-iterations in flight
+  constexpr int D = S == 1 ? 4 : (S <= 2 ? (KP > 8 ? 2 : 3) : 2);  // warp-iterations in flight
   const PanelArgs& a = x.a;
   const int64_t s = x.s, ld = a.ld, m = a.m;
   const int lane = x.lane, c = x.c;
@@ -216,7 +216,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
   const double* Wb = a.W + base + 2 * l;
   const double* Fb = a.F + l * S;
   struct Slot {
-    double c[CH][2];
+    double c[KP][2];
     double f[S];
     double nr, nx;
     int j, lp;
