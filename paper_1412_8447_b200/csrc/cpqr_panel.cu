@@ -170,16 +170,19 @@ __device__ __forceinline__ double group_recompute(const double* col, const doubl
 // One step's pass over a warp's column slots (pivoted slots: loads only).
 // TC0 = first active 64-row chunk (s / 64, constant over a 32-step panel),
 // NLD = ld / 64; TC0 = -1: runtime chunk range.
-// Specialised layout: a column is handled by a group of L = 4 * (active
-// chunks) lanes, 32 / L columns per warp instruction; lane l of a group holds
-// rows base + 2(l + L k) + {0, 1}, k < KP (<= 16 rows), and F(j, l S .. l S + S - 1)
-// (S = NB / L).  Late panels (few active rows) thus run up to 8 columns per
-// warp instruction with log2(L)-round reductions.
+// Specialised layout: a column is handled by a group of L lanes (16 for 5-8
+// active 64-row chunks, 8 for 2-4, 4 for one), 32 / L columns per warp
+// instruction; lane l of a group holds rows base + 2(l + L k) + {0, 1},
+// k < KP (<= 16 row pairs), and F(j, l S .. l S + S - 1) (S = NB / L).  The
+// pass is latency-bound per warp (load -> dot -> log2(L)-round reduction ->
+// norm), so several columns per instruction buy memory-level parallelism:
+// 16 lanes instead of 32 on the early panels took the CPQR of Y from 19.4 to
+// 16.9 ms.
 template <int TC0, int NLD>
 __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp) {
   constexpr bool SPEC = TC0 >= 0;
   constexpr int NA = SPEC ? NLD - TC0 : CH;
-  // lanes per column: a power of two with 16 rows (8 row pairs) or fewer per lane
+  // lanes per column: a power of two with at most 16 row pairs per lane
   constexpr int L = !SPEC ? 32 : (NA >= 5 ? 16 : (NA >= 2 ? 8 : 4));
   constexpr int KP = SPEC ? 32 * NA / L : CH;  // row pairs per lane
   constexpr int GPW = 32 / L;
