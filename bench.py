@@ -394,8 +394,10 @@ def run_ours(args, rank, world, local_rank):
     st = {k: v["ms"] / max(1, v["count"]) for k, v in stages.items()}
     per_step = {k: v["ms"] / args.steps for k, v in stages.items()}
     kern = kernel_rooflines(cfg, st, stages, args.engine)
-    # the headline roofline is the kernel with the largest share of the step
-    dom = max(kern, key=lambda n: per_step.get(n, 0.0)) if kern else None
+    # the headline roofline is the dominant kernel: the single stage launch with
+    # the longest duration (the ozaki_split entry sums several split launches
+    # of different operands, so its per-step share is not one kernel's)
+    dom = max(kern, key=lambda n: st.get(n, 0.0)) if kern else None
     roof = dict(kern[dom], share_of_step=round(per_step[dom] / ms, 4)) if dom else None
     secondary = {n: dict(v, share_of_step=round(per_step.get(n, 0.0) / ms, 4)) for n, v in kern.items() if n != dom}
     cpu = None
