@@ -232,7 +232,8 @@ bool device_all_finite(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
 
 // GEMM wrapper: pads misaligned operands (TMA needs 16B-aligned base and ld)
 void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-          double* out, int64_t ldo, double alpha = 1.0, double beta = 0.0, int splits = -1, bool upper = false) {
+          double* out, int64_t ldo, double alpha = 1.0, double beta = 0.0, int splits = -1, bool upper = false,
+          int tri = 0) {
   auto ok = [](const double* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0); };
   DBuf<double> pp, qq;
   if (!ok(P, ldp)) {
@@ -249,7 +250,7 @@ void gemm(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, int64_t l
     Q = qq;
     ldq = l;
   }
-  gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st, upper);
+  gemm_tn(c->ws, (int)M, (int)N, (int)K, P, ldp, Q, ldq, out, ldo, alpha, beta, splits, c->st, upper, tri);
 }
 
 // ---------------------------------------------------------------- A-sized contractions
@@ -381,7 +382,7 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
     DBuf<double> Mt((size_t)k * k, c->st);
     DBuf<int> zr(k, c->st);
     backsub_operator_t(k, s11, ld11, strat.threshold, Mt, zr, c->st);
-    gemm(c, k, nc, k, Mt, k, s12, ld12, t, ldt);
+    gemm(c, k, nc, k, Mt, k, s12, ld12, t, ldt, 1.0, 0.0, -1, false, kTriP);  // M upper triangular
     if (!strat.escalate) {  // allow_singularity_error (solve.hpp:75-83)
       std::vector<int> hz(k);
       LRB_CUDA(cudaMemcpyAsync(hz.data(), zr.p, sizeof(int) * k, cudaMemcpyDeviceToHost, c->st));
@@ -496,7 +497,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   sync(c);
   if (c->h_flags[0] != 0) return false;
   tri_upper_inverse_blocked(k, G, k, R1inv, k, c->st);
-  gemm(c, rows, k, k, Xt, ldxt, R1inv, k, Q1, even(rows));  // Q1 = X R1^-1
+  gemm(c, rows, k, k, Xt, ldxt, R1inv, k, Q1, even(rows), 1.0, 0.0, -1, false, kTriQ);  // Q1 = X R1^-1
   DBuf<double> G2((size_t)k * k, c->st), R2t((size_t)k * k, c->st);
   gemm(c, k, k, rows, Q1, even(rows), Q1, even(rows), G2, k, 1.0, 0.0, -1, true);  // G2 = Q1^T Q1
   cholesky_upper(c->ws, k, G2, k, info.p + 1, c->st);
@@ -643,7 +644,7 @@ int64_t orth_cols_core(lr_ctx* c, int64_t rows, int64_t k, const double* X, int6
     DBuf<double> Xt((size_t)even(k) * rows, c->st), R((size_t)k * k, c->st), Ri((size_t)k * k, c->st);
     transpose_matrix(rows, k, X, ldx, Xt, even(k), c->st);
     if (cholqr2(c, rows, k, X, ldx, Xt, even(k), R, Ri)) {
-      gemm(c, rows, k, k, Xt, even(k), Ri, k, Q, ldq);  // Q = X R^-1
+      gemm(c, rows, k, k, Xt, even(k), Ri, k, Q, ldq, 1.0, 0.0, -1, false, kTriQ);  // Q = X R^-1
       return k;
     }
   }
@@ -830,8 +831,8 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
       // The big contraction uses the orthonormal Qc (not C): applying Rc^-1
       // to C^T A would square cond(C) in the least-squares error.
       DBuf<double> Qc((size_t)even(m) * k, c->st), Qr((size_t)even(n) * k, c->st);
-      gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m));            // Qc = C Rc^-1  (m x k)
-      gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n));            // Qr = R^T Sr^-1 (n x k)
+      gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m), 1.0, 0.0, -1, false, kTriQ);            // Qc = C Rc^-1  (m x k)
+      gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n), 1.0, 0.0, -1, false, kTriQ);            // Qr = R^T Sr^-1 (n x k)
       DBuf<double> Xt((size_t)even(n) * k, c->st), W((size_t)k * k, c->st);
       mark(c, "form_q");
       apply_at(Qc, even(m), Xt, even(n));                        // X^T = A^T Qc  (n x k)
@@ -1041,7 +1042,7 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
   const auto& sp = c->split;
   if (c_ok) {  // chain 2 first: it has no host synchronisation, so it is fully enqueued before chain 1 blocks
     OnPartition on(c, sp.s2, sp.n2, fork);
-    gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m));         // Qc = C Rc^-1
+    gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m), 1.0, 0.0, -1, false, kTriQ);         // Qc = C Rc^-1
     gemm_a(c, n, k, m, a, lda, Qc, even(m), Xt, even(n), 0);  // X^T = A^T Qc
     done2 = record_event(c->st);
   }
@@ -1057,7 +1058,7 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
     transpose_matrix(k, n, R, k, Rt, even(n), c->st);
     copy_matrix(k, n, R, k, Rk, ldk, c->st);
     r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
-    if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n));  // Qr = R^T Sr^-1
+    if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n), 1.0, 0.0, -1, false, kTriQ);  // Qr = R^T Sr^-1
     done1 = record_event(c->st);
   }
   LRB_CUDA(cudaStreamWaitEvent(c->st, done1, 0));

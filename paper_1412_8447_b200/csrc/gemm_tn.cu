@@ -48,7 +48,7 @@ struct EpiArgs {
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
-                   int K, int tiles_m, int tiles_n, int m_fast, int kt_per_split, EpiArgs ep, int upper) {
+                   int K, int tiles_m, int tiles_n, int m_fast, int kt_per_split, EpiArgs ep, int upper, int tri) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -66,8 +66,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   else { tn = bid % tiles_n; tm = bid / tiles_n; }
   const int m0 = tm * BM, n0 = tn * BN;
   const int KT = (K + BK - 1) / BK;
-  const int kt_begin = blockIdx.y * kt_per_split;
-  const int kt_end = min(KT, kt_begin + kt_per_split);
+  // triangular operands: K-tiles that only meet structural zeros are skipped
+  // (tri & 1: P(k, i) = 0 for k < i; tri & 2: Q(k, j) = 0 for k > j)
+  int kt_begin = blockIdx.y * kt_per_split;
+  int kt_end = min(KT, kt_begin + kt_per_split);
+  if (tri & 1) kt_begin = max(kt_begin, m0 / BK);
+  if (tri & 2) kt_end = min(kt_end, (n0 + BN) / BK);
   const int nkt = max(0, kt_end - kt_begin);
 
   if (threadIdx.x == 0) {
@@ -226,7 +230,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
 
 template <int EPI>
 void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, int splits, const EpiArgs& ep,
-            cudaStream_t st, bool upper = false) {
+            cudaStream_t st, bool upper = false, int tri = 0) {
   static bool attr = false;
   if (!attr) {
     LRB_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -237,7 +241,7 @@ void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, i
   const int kt_per_split = (KT + splits - 1) / splits;
   dim3 grid(upper ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n, splits);
   gemm_tn_kernel<EPI><<<grid, THREADS, SMEM_BYTES, st>>>(tp, tq, M, N, K, tiles_m, tiles_n, tiles_m <= tiles_n ? 1 : 0,
-                                                         kt_per_split, ep, upper ? 1 : 0);
+                                                         kt_per_split, ep, upper ? 1 : 0, tri);
   LRB_CHECK_LAUNCH();
 }
 
@@ -246,7 +250,7 @@ void launch(const CUtensorMap& tp, const CUtensorMap& tq, int M, int N, int K, i
 int gemm_tn_grid_ctas(int M, int N) { return ((M + BM - 1) / BM) * ((N + BN - 1) / BN); }
 
 void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper) {
+             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper, int tri) {
   if (upper && M != N) throw CudaError("gemm_tn: upper-tile mode needs a square output");
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {
@@ -269,12 +273,12 @@ void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, c
   }
   splits = std::max(1, std::min(splits, KT));
   if (splits == 1) {
-    launch<kEpiStore>(tp, tq, M, N, K, 1, ep, st, upper);
+    launch<kEpiStore>(tp, tq, M, N, K, 1, ep, st, upper, tri);
     return;
   }
   double* w = ws.get_doubles(WsSlot::kSplitK, (size_t)splits * M * N);
   ep.ws = w;
-  launch<kEpiSplitK>(tp, tq, M, N, K, splits, ep, st, upper);
+  launch<kEpiSplitK>(tp, tq, M, N, K, splits, ep, st, upper, tri);
   const int64_t total = (int64_t)M * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * num_sms());
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(w, splits, M, N, out, ldo, alpha, beta, upper ? 1 : 0);

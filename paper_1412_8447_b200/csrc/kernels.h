@@ -64,7 +64,11 @@ int gemm_tn_grid_ctas(int M, int N);
 // only the output tiles on/above the diagonal (Gram products, M == N; the
 // strictly-lower tiles are left unwritten).
 void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq,
-             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper = false);
+             double* out, int64_t ldo, double alpha, double beta, int splits, cudaStream_t st, bool upper = false,
+             int tri = 0);
+// tri bits for gemm_tn: the K-tiles that only meet structural zeros are skipped
+constexpr int kTriP = 1;  // P(k, i) = 0 for k < i (P = U^T of an upper-triangular U: out = U Q)
+constexpr int kTriQ = 2;  // Q(k, j) = 0 for k > j (Q upper triangular: out = P^T Q)
 // per-CTA partial sums of (R - P^T Q)^2 written to partials_out[0..*num_partials)
 void gemm_tn_resid_sq(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, const double* Q,
                       int64_t ldq, const double* R, int64_t ldr, double* partials_out, int* num_partials,
