@@ -423,3 +423,38 @@ def test_panel_cpqr_tie_after_swap(lr):
     a[:, 0], a[:, 4], a[:, 10] = v, -v, 3.0 * w / np.linalg.norm(w) * np.linalg.norm(v)
     q = lr.cpqr_partial(np.asfortranarray(a), 2)
     assert list(q.pivots[:2]) == [10, 4]
+
+
+@pytest.mark.parametrize("case", ["zero_columns", "rank_deficient", "all_columns", "sparse_like"])
+def test_panel_cpqr_degenerate_inputs(lr, oracle, case):
+    """Panel CPQR (ld 256 / 320 / 512) on degenerate inputs, against the oracle:
+    exact zero columns (norm 0 from the start), a rank-deficient block (norms
+    collapse to roundoff and are recomputed), k = n (every slot pivoted, the
+    final permutation moves all displaced columns), and a mostly-zero matrix
+    like the C^T of the sparse configuration."""
+    rng = np.random.default_rng(len(case))
+    if case == "zero_columns":
+        m, n, k = 300, 900, 300
+        a = oracle.gaussian_matrix(m, n, 5)
+        a[:, rng.choice(n, 200, replace=False)] = 0.0
+    elif case == "rank_deficient":
+        m, n, k = 260, 800, 200
+        a = oracle.gaussian_matrix(m, 150, 6) @ oracle.gaussian_matrix(150, n, 7)
+    elif case == "all_columns":
+        m, n, k = 400, 400, 400
+        a = oracle.gaussian_matrix(m, n, 8)
+    else:
+        m, n, k = 300, 3000, 300
+        a = np.zeros((m, n))
+        for j in range(n):
+            rows = rng.choice(m, 3, replace=False)
+            a[rows, j] = rng.standard_normal(3)
+    a = np.asfortranarray(a)
+    q = lr.cpqr_partial(a, k)
+    o = oracle.cpqr(a, k)
+    if case == "rank_deficient":  # beyond the numerical rank only roundoff is left to pivot on
+        assert np.array_equal(q.pivots[:150], o["pivots"][:150])
+        assert rel(q.s[:150, :150], o["s"][:150, :150]) <= 1e-10
+    else:
+        assert np.array_equal(q.pivots, o["pivots"])
+        assert rel(q.s, o["s"]) <= 1e-12
