@@ -84,6 +84,7 @@ struct PanelArgs {
   unsigned int* bar;          // grid barrier counter (zeroed before each launch)
   int64_t maxcols;            // columns per CTA bound (shared-memory norm arrays)
   int* posof;                 // [n] logical position of each column slot (between launches)
+  unsigned int* ctag;         // [G] step + 1 of the candidate each CTA last staged (release-published)
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
@@ -96,6 +97,22 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& ta
   if (threadIdx.x == 0) {
     // release: the CTA's writes (ordered before this thread by the barrier) become visible gpu-wide
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// the two halves of grid_barrier: publish (after the CTA's partial is
+// written) and wait -- the candidate staging runs in between
+__device__ __forceinline__ void grid_arrive(unsigned int* bar, unsigned int& target) {
+  target += gridDim.x;
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+__device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int target) {
+  if (threadIdx.x == 0) {
     unsigned int v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
@@ -483,6 +500,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     }
     __syncthreads();
     stage(a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0] & 0xffffffffll, 0, false);
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ctag + cta), "r"(1u) : "memory");
     grid_barrier(a.bar, bar_target);
     if (__ldcg(a.flags) != 0) return;
   }
@@ -531,7 +549,15 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
         const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
         if (better(ov, op, bv, bp)) { bv = ov; bp = op; bc = oc; }
       }
-      if (lane == 0) { sh_piv[0] = bp; sh_piv[1] = bc; }
+      if (lane == 0) {
+        sh_piv[0] = bp;
+        sh_piv[1] = bc;
+        // the winner stages its reflector after arriving at the barrier: wait for its tag
+        unsigned int t;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.ctag + bc) : "memory");
+        } while (t != (unsigned int)(s + 1));
+      }
     }
     __syncthreads();
     const int64_t p = sh_piv[0] >> 32;            // logical position of the pivot
@@ -601,11 +627,18 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
     __syncthreads();
     stamp(3);  // CTA argmax, pivot write-back
-    if (s + 1 < a.k)
+    // publish the partial, then stage the next candidate while the other CTAs
+    // finish (the candidate is published by its own tag, not by the barrier)
+    grid_arrive(a.bar, bar_target);
+    if (s + 1 < a.k) {
       stage(a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0] & 0xffffffffll, c + 1, s + 1 < a.t1);
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ctag + cta), "r"((unsigned int)(s + 2))
+                     : "memory");
+    }
     stamp(4);  // stage
     if (tr && a.tstep) a.tstep[(s * G + cta) * 4 + 3] = (gtimer() & ~3ull) | (owner ? 1 : 0);
-    grid_barrier(a.bar, bar_target);
+    grid_wait(a.bar, bar_target);
     if (tr && a.tstep && s + 1 < a.k) a.tstep[((s + 1) * G + cta) * 4] = gtimer();
     stamp(5);  // grid barrier
   }
@@ -784,7 +817,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   const size_t nd = 2 * (size_t)n + 2 * (size_t)G + 2 * (size_t)G * cand_sz + (size_t)n * NB + (size_t)ld * NB;
   const size_t ndisp = 2 * (size_t)k + 2;  // slots away from their final position: <= 2 per step
   const size_t bytes = sizeof(double) * (nd + ndisp * (size_t)ld) + sizeof(long long) * 2 * (size_t)G + 256 +
-                       sizeof(int) * ((size_t)n + ndisp + 2);
+                       sizeof(int) * ((size_t)n + ndisp + 2) + sizeof(unsigned int) * (size_t)G;
   uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
   PanelArgs a{};
   a.W = W;
@@ -807,6 +840,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   a.posof = reinterpret_cast<int*>(disp_cols + ndisp * (size_t)ld);
   int* disp_list = a.posof + n;
   int* disp_count = disp_list + ndisp;
+  a.ctag = reinterpret_cast<unsigned int*>(disp_count + 2);
+  LRB_CUDA(cudaMemsetAsync(a.ctag, 0xFF, sizeof(unsigned int) * (size_t)G, st));  // no candidate staged yet
   a.maxcols = maxcols;
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
