@@ -60,7 +60,8 @@ constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
 // norms and a logical position; the opt-in ceiling (227 KB) also holds the static arrays
 constexpr int kSmemLimit = 216 * 1024;
 inline size_t panel_smem_bytes(int64_t ld, int64_t maxcols) {
-  return sizeof(double) * ((size_t)(NB + 2) * ld + 2 * (size_t)maxcols) + sizeof(int) * (size_t)maxcols;
+  // + logical positions, active list, zero list (ints)
+  return sizeof(double) * ((size_t)(NB + 2) * ld + 2 * (size_t)maxcols) + sizeof(int) * 3 * (size_t)maxcols;
 }
 
 struct PanelArgs {
@@ -85,6 +86,7 @@ struct PanelArgs {
   int64_t maxcols;            // columns per CTA bound (shared-memory norm arrays)
   int* posof;                 // [n] logical position of each column slot (between launches)
   unsigned int* ctag;         // [G] step + 1 of the candidate each CTA last staged (release-published)
+  int* nzero;                 // identically-zero columns found by the first launch
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
@@ -156,7 +158,7 @@ struct PassCtx {
   int64_t p;             // logical position of this step's pivot (the column at position s moves there)
   bool apply;
   double tau, vr_c;
-  int64_t c0, cnt;
+  int64_t c0, cnt;       // cnt: active slots of the CTA (alist)
   int warp, lane;
   const double* vv;
   const double* Vs;
@@ -165,6 +167,7 @@ struct PassCtx {
   double* snr;           // this CTA's running / last exact squared norms (shared memory, index j - c0)
   double* snx;
   int* spos;             // logical positions of the owned slots (shared memory, index j - c0)
+  const int* alist;      // the CTA's slots that are not identically zero, ascending; null: all of them
   unsigned long long recomputes;
 };
 
@@ -195,7 +198,7 @@ __device__ __forceinline__ double group_recompute(const double* col, const doubl
 // norm), so several columns per instruction buy memory-level parallelism:
 // 16 lanes instead of 32 on the early panels took the CPQR of Y from 19.4 to
 // 16.9 ms.
-template <int TC0, int NLD>
+template <int TC0, int NLD, bool LIST>
 __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp) {
   constexpr bool SPEC = TC0 >= 0;
   constexpr int NA = SPEC ? NLD - TC0 : CH;
@@ -226,11 +229,11 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     vl[t] = x.vrow[l * S + t];
   }
   const int lc = c / S, tcs = c % S;  // owner lane / slot of F(j, c)
-  // the warp's slots c0 + warp + PW*q, visited as j = jstart + dj * q
-  // (alternating direction: the previous step's last columns are L2-hot;
-  // 32-bit indices, n < 2^31)
+  // the warp's slots c0 + warp + PW q (or, with identically-zero slots
+  // present, alist[warp + PW q]), visited in alternating direction (the
+  // previous step's last columns are L2-hot; 32-bit indices, n < 2^31)
   const int first = (int)(x.c0 + x.warp);
-  const int n_valid = (int)x.cnt;
+  const int n_valid = ((int)x.cnt - x.warp + PW - 1) / PW;
   const int jstart = (s & 1) ? first + PW * (n_valid - 1) : first;
   const int dj = (s & 1) ? -PW : PW;
   const double* Wb = a.W + base + 2 * l;
@@ -245,7 +248,9 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
   auto fetch = [&](Slot& cb, int qi) {
     const int q = qi * GPW + g;
     cb.ok = q < n_valid;
-    cb.j = jstart + dj * (cb.ok ? q : 0);  // an owned column for the (unused) loads
+    // an owned column for the (unused) loads of an idle lane group
+    cb.j = jstart + dj * (cb.ok ? q : 0);
+    if constexpr (LIST) cb.j = cb.ok ? x.alist[cb.j - (int)x.c0] : (int)x.c0;
     const double* src = Wb + (size_t)cb.j * (size_t)ld;
 #pragma unroll
     for (int k = 0; k < KP; ++k)
@@ -343,7 +348,9 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
 
 // TC0 / NLD: the panel's first active 64-row chunk (t0 / 64; a 32-step panel
 // never crosses a chunk) and ld / 64, or -1 for the generic runtime version
-template <int TC0, int NLD>
+// LIST: identically-zero slots may exist (they leave the pass; one launch with
+// LIST = true finds out, see cpqr_panel)
+template <int TC0, int NLD, bool LIST>
 __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   unsigned int bar_target = 0;
   extern __shared__ double dyn[];
@@ -356,6 +363,9 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   __shared__ double vrow[NB];   // V(s, 0:NB)
   __shared__ double fb[NB];     // F row of the staged candidate column
   __shared__ double sh_alpha;
+  __shared__ int sh_cnt[2 * PT];
+  __shared__ int sh_nact, sh_nzero;
+  __shared__ unsigned long long sh_zkey;
 
   const int G = gridDim.x, cta = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -369,8 +379,9 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
   double* snr = scr + ld;        // [maxcols] norms of the owned slots for this launch
   double* snx = snr + a.maxcols;
   int* spos = reinterpret_cast<int*>(snx + a.maxcols);  // [maxcols] their logical positions
+  int* alist = spos + a.maxcols;  // active slots of this launch
+  int* zlist = alist + a.maxcols;  // identically-zero slots (skipped by the pass)
   for (int64_t i = threadIdx.x; i < (NB + 2) * ld; i += PT) dyn[i] = 0.0;
-  const int64_t cnt = (c1 - c0 - warp + PW - 1) / PW;
   unsigned long long my_recomputes = 0;
   __syncthreads();
 
@@ -480,8 +491,12 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       acc = warp_sum(acc);
       if (lane == 0) {
         a.nrm[j] = acc;
-        a.nrmx[j] = acc;
+        a.nrmx[j] = acc == 0.0 ? -0.0 : acc;  // -0: identically zero, stays zero for the whole CPQR
         a.posof[j] = (int)j;
+      }
+      if (acc == 0.0) {
+        a.F[j * NB + lane] = 0.0;  // its panel updates are no-ops
+        if (lane == 0) atomicAdd(a.nzero, 1);
       }
       const long long key = (j << 32) | j;
       if (better(acc, key, bv, bp)) { bv = acc; bp = key; }
@@ -511,6 +526,43 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     spos[j - c0] = __ldcg(a.posof + j);
   }
   __syncthreads();
+  if constexpr (!LIST) {
+    if (threadIdx.x == 0) {
+      sh_nact = (int)(c1 - c0);
+      sh_nzero = 0;
+    }
+    __syncthreads();
+  } else {  // ordered compaction of the owned slots into the active and zero lists
+    const int64_t nloc = c1 - c0, chunk = (nloc + PT - 1) / PT;
+    const int64_t b0 = min(nloc, chunk * threadIdx.x), b1 = min(nloc, b0 + chunk);
+    int na = 0, nz = 0;
+    for (int64_t t = b0; t < b1; ++t) {
+      if (snx[t] == 0.0 && signbit(snx[t])) ++nz;
+      else ++na;
+    }
+    sh_cnt[threadIdx.x] = na;
+    sh_cnt[PT + threadIdx.x] = nz;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int sa = 0, sz = 0;
+      for (int t = 0; t < PT; ++t) {
+        const int ta = sh_cnt[t], tz = sh_cnt[PT + t];
+        sh_cnt[t] = sa;
+        sh_cnt[PT + t] = sz;
+        sa += ta;
+        sz += tz;
+      }
+      sh_nact = sa;
+      sh_nzero = sz;
+    }
+    __syncthreads();
+    int oa = sh_cnt[threadIdx.x], oz = sh_cnt[PT + threadIdx.x];
+    for (int64_t t = b0; t < b1; ++t) {
+      if (snx[t] == 0.0 && signbit(snx[t])) zlist[oz++] = (int)(c0 + t);
+      else alist[oa++] = (int)(c0 + t);
+    }
+    __syncthreads();
+  }
 
   // ------------------------------------------------------------ steps of this panel
   const bool tr = a.trace != nullptr && threadIdx.x == 0;
@@ -598,12 +650,29 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     double bv = -INFINITY;
     long long bp = INT64_MAX;
     {
-      PassCtx x{a, s, c, p, apply, tau, vr_c, c0, cnt, warp, lane, vv, Vs, wsh, vrow, snr, snx, spos, 0ull};
-      pass_cols<TC0, NLD>(x, bv, bp);
+      PassCtx x{a,    s,    c,     p,    apply, tau,  vr_c, c0,   sh_nact, warp, lane,
+                vv,   Vs,   wsh,   vrow, snr,   snx,  spos, alist, 0ull};
+      pass_cols<TC0, NLD, LIST>(x, bv, bp);
       my_recomputes += x.recomputes;
     }
 
     if (tr && a.tstep) a.tstep[(s * G + cta) * 4 + 2] = gtimer();
+    // identically-zero slots: the one at logical position s takes p; the lowest
+    // logical position among them is this CTA's candidate at norm 0
+    if (LIST && sh_nzero > 0) {
+      if (threadIdx.x == 0) sh_zkey = ~0ull;
+      __syncthreads();
+      unsigned long long zk = ~0ull;
+      for (int t = threadIdx.x; t < sh_nzero; t += PT) {
+        const int z = zlist[t] - (int)c0;
+        if (snr[z] == -INFINITY) continue;  // pivoted (only once every other column is exhausted)
+        int lp = spos[z];
+        if (lp == (int)s) spos[z] = lp = (int)p;
+        const unsigned long long key = ((unsigned long long)lp << 32) | (unsigned long long)(c0 + z);
+        zk = key < zk ? key : zk;
+      }
+      if (zk != ~0ull) atomicMin(&sh_zkey, zk);
+    }
     stamp(2);  // pass
     // (5) CTA argmax, pivot column write-back, V row-major copy for the panel GEMM
     if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
@@ -613,6 +682,10 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
       long long cp = sh_bp[0];
       for (int w = 1; w < PW; ++w)
         if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      if (LIST && sh_nzero > 0 && sh_zkey != ~0ull && better(0.0, (long long)sh_zkey, cv, cp)) {
+        cv = 0.0;
+        cp = (long long)sh_zkey;
+      }
       a.pval[(int64_t)nxt * G + cta] = cv;
       a.ppos[(int64_t)nxt * G + cta] = cp;
       sh_piv[0] = cp;
@@ -774,20 +847,28 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     LRB_CUDA(cudaEventRecord(ev_begin, st));
   }
   // specialised kernels per (ld / 64, first active chunk); ld in {256, 320, 512}
-  static const KernT k4[] = {cpqr_panel_kernel<0, 4>, cpqr_panel_kernel<1, 4>, cpqr_panel_kernel<2, 4>,
-                             cpqr_panel_kernel<3, 4>};
-  static const KernT k5[] = {cpqr_panel_kernel<0, 5>, cpqr_panel_kernel<1, 5>, cpqr_panel_kernel<2, 5>,
-                             cpqr_panel_kernel<3, 5>, cpqr_panel_kernel<4, 5>};
-  static const KernT k8[] = {cpqr_panel_kernel<0, 8>, cpqr_panel_kernel<1, 8>, cpqr_panel_kernel<2, 8>,
-                             cpqr_panel_kernel<3, 8>, cpqr_panel_kernel<4, 8>, cpqr_panel_kernel<5, 8>,
-                             cpqr_panel_kernel<6, 8>, cpqr_panel_kernel<7, 8>};
+#define LRB_PANEL_K(L)                                                                                        \
+  {cpqr_panel_kernel<0, 4, L>, cpqr_panel_kernel<1, 4, L>, cpqr_panel_kernel<2, 4, L>, cpqr_panel_kernel<3, 4, L>}, \
+      {cpqr_panel_kernel<0, 5, L>, cpqr_panel_kernel<1, 5, L>, cpqr_panel_kernel<2, 5, L>,                        \
+       cpqr_panel_kernel<3, 5, L>, cpqr_panel_kernel<4, 5, L>},                                                   \
+      {cpqr_panel_kernel<0, 8, L>, cpqr_panel_kernel<1, 8, L>, cpqr_panel_kernel<2, 8, L>,                        \
+       cpqr_panel_kernel<3, 8, L>, cpqr_panel_kernel<4, 8, L>, cpqr_panel_kernel<5, 8, L>,                        \
+       cpqr_panel_kernel<6, 8, L>, cpqr_panel_kernel<7, 8, L>},                                                   \
+      cpqr_panel_kernel<-1, -1, L>
+  struct KernSet {
+    KernT k4[4], k5[5], k8[8], gen;
+  };
+  // [0]: dense (no identically-zero columns), [1]: with the zero-slot lists
+  static const KernSet ks[2] = {{LRB_PANEL_K(false)}, {LRB_PANEL_K(true)}};
+#undef LRB_PANEL_K
   const int nld = (int)(ld / 64);
-  auto kern_for = [&](int64_t t0) -> KernT {
+  auto kern_for = [&](int64_t t0, bool list) -> KernT {
+    const KernSet& k = ks[list ? 1 : 0];
     const int tc = (int)(t0 / 64);
-    if (nld == 8) return k8[tc];
-    if (nld == 5) return k5[tc];
-    if (nld == 4) return k4[tc];
-    return cpqr_panel_kernel<-1, -1>;
+    if (nld == 8) return k.k8[tc];
+    if (nld == 5) return k.k5[tc];
+    if (nld == 4) return k.k4[tc];
+    return k.gen;
   };
   static bool attr = false;
   if (!attr) {
@@ -798,10 +879,12 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
                                     (int)(fa.maxDynamicSharedSizeBytes > 0 ? 227 * 1024 - fa.sharedSizeBytes
                                                                            : kSmemLimit)));
     };
-    for (KernT kf : k4) set(kf);
-    for (KernT kf : k5) set(kf);
-    for (KernT kf : k8) set(kf);
-    set(cpqr_panel_kernel<-1, -1>);
+    for (const KernSet& k : ks) {
+      for (KernT kf : k.k4) set(kf);
+      for (KernT kf : k.k5) set(kf);
+      for (KernT kf : k.k8) set(kf);
+      set(k.gen);
+    }
     LRB_CUDA(cudaFuncSetAttribute(panel_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 256 * 64)));
     attr = true;
@@ -841,6 +924,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   int* disp_list = a.posof + n;
   int* disp_count = disp_list + ndisp;
   a.ctag = reinterpret_cast<unsigned int*>(disp_count + 2);
+  a.nzero = disp_count + 1;
+  LRB_CUDA(cudaMemsetAsync(a.nzero, 0, sizeof(int), st));
   LRB_CUDA(cudaMemsetAsync(a.ctag, 0xFF, sizeof(unsigned int) * (size_t)G, st));  // no candidate staged yet
   a.maxcols = maxcols;
   a.flags = d_flags;
@@ -867,16 +952,26 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     ev.push_back(e);
   };
   evrec();
+  // the first launch runs the list variant and counts identically-zero
+  // columns; later launches take the dense variant when there are none
+  bool list = true;
+  thread_local int* h_nzero = nullptr;  // mapped pinned word (no copy-engine queueing)
+  if (!h_nzero) LRB_CUDA(cudaMallocHost(&h_nzero, sizeof(int)));
   for (int64_t t0 = 0; t0 < k; t0 += NB) {
     const int64_t t1 = std::min<int64_t>(k, t0 + NB);
+    if (t0 == NB) {
+      LRB_CUDA(cudaStreamSynchronize(st));
+      list = *h_nzero > 0;
+    }
     a.t0 = t0;
     a.t1 = t1;
     a.init = t0 == 0 ? 1 : 0;
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
     evrec();
     void* params[] = {&a};
-    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0), dim3(G), dim3(PT), params, smem, st));
+    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
+    if (t0 == 0) copy_bytes_mapped(h_nzero, a.nzero, sizeof(int), st);
     evrec();
     if (trace && trace_panels) {  // per-panel phase means / maxima over CTAs (diagnostic)
       std::vector<unsigned long long> h(8 * (size_t)G);
