@@ -425,7 +425,7 @@ def test_panel_cpqr_tie_after_swap(lr):
     assert list(q.pivots[:2]) == [10, 4]
 
 
-@pytest.mark.parametrize("case", ["zero_columns", "rank_deficient", "all_columns", "sparse_like"])
+@pytest.mark.parametrize("case", ["zero_columns", "rank_deficient", "all_columns", "sparse_like", "mostly_zero"])
 def test_panel_cpqr_degenerate_inputs(lr, oracle, case):
     """Panel CPQR (ld 256 / 320 / 512) on degenerate inputs, against the oracle:
     exact zero columns (norm 0 from the start), a rank-deficient block (norms
@@ -443,12 +443,16 @@ def test_panel_cpqr_degenerate_inputs(lr, oracle, case):
     elif case == "all_columns":
         m, n, k = 400, 400, 400
         a = oracle.gaussian_matrix(m, n, 8)
-    else:
+    elif case == "sparse_like":
         m, n, k = 300, 3000, 300
         a = np.zeros((m, n))
         for j in range(n):
             rows = rng.choice(m, 3, replace=False)
             a[rows, j] = rng.standard_normal(3)
+    else:  # 60 non-zero columns among 2000, k = 150: the last 90 pivots are zero columns, lowest position first
+        m, n, k = 300, 2000, 150
+        a = np.zeros((m, n))
+        a[:, rng.choice(n, 60, replace=False)] = oracle.gaussian_matrix(m, 60, 9)
     a = np.asfortranarray(a)
     q = lr.cpqr_partial(a, k)
     o = oracle.cpqr(a, k)
