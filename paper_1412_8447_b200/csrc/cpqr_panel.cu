@@ -757,6 +757,11 @@ __global__ void __launch_bounds__(PUW * 32, 1)
       const int kc = 4 * ks + (lane & 3);
       b[ks] = (jb < n && kc < nc) ? __ldg(F + jb * NB + kc) : 0.0;
     }
+    // F rows all zero (pivoted or identically-zero columns): the update is a no-op
+    bool nz = false;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) nz |= b[ks] != 0.0;
+    if (!__any_sync(0xffffffffu, nz)) continue;
     const int64_t jc = j0 + 2 * (lane & 3);
     const bool v0 = jc < n, v1 = jc + 1 < n;
     double* w0 = W + jc * ld + r0 + (lane >> 2);
