@@ -266,10 +266,13 @@ void gemm_tn(Workspace& ws, int M, int N, int K, const double* P, int64_t ldp, c
   ep.beta = beta;
   const int KT = (K + BK - 1) / BK;
   if (splits <= 0) {
-    // auto: fill ~2 waves when the output tile count is small
+    // auto: when the output tiles are fewer than two waves of CTAs (one CTA
+    // per SM), split K so that tiles x splits fills two waves as exactly as
+    // possible (e.g. 10 upper Gram tiles -> 29 splits, 290 CTAs; powers of two
+    // gave 320 = 2.2 waves), each split keeping >= 8 K-tiles
     const int tiles = upper ? ((N + BN - 1) / BN) * ((N + BN - 1) / BN + 1) / 2 : gemm_tn_grid_ctas(M, N);
     splits = 1;
-    while (tiles * splits < 2 * num_sms() && KT / (splits * 2) >= 8) splits *= 2;
+    if (tiles < 2 * num_sms()) splits = std::max(1, std::min(KT / 8, (2 * num_sms()) / tiles));
   }
   splits = std::max(1, std::min(splits, KT));
   if (splits == 1) {
