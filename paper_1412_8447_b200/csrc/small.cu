@@ -494,14 +494,30 @@ __global__ void tri_inv_leaf_kernel(int64_t k, const double* __restrict__ r, int
   }
 }
 
-// C = alpha A B (column-major, small): 32x32 tiles, 256 threads x 4 outputs
-__global__ void gemm_nn_small_kernel(int m, int n, int kk, double alpha, const double* __restrict__ A, int64_t lda,
-                                     const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
-                                     int64_t ldc) {
+// One level of the blocked triangular inverse for every diagonal pair at once
+// (blockIdx.z = pair at p0 = 2 h z; sizes h x hc, hc = min(h, k - p0 - h)):
+// step 0: T_z = R(p0:p0+h, p0+h:p0+h+hc) Rinv(p0+h.., p0+h..)   (h x hc, K = hc)
+// step 1: Rinv(p0:p0+h, p0+h..) = -Rinv(p0.., p0..) T_z          (h x hc, K = h)
+// 32x32 output tiles, 256 threads x 4 outputs, K in 32-deep shared-memory slices.
+__global__ void tri_inv_level_kernel(int step, int64_t h, int64_t k, const double* __restrict__ r, int64_t ldr,
+                                     double* __restrict__ ri, int64_t ldi, double* __restrict__ T) {
   __shared__ double As[32][33];
   __shared__ double Bs[32][33];
+  const int64_t p0 = 2 * h * blockIdx.z;
+  const int64_t hc = min(h, k - p0 - h);
+  if (hc <= 0) return;
+  const int m = (int)h, n = (int)hc, kk = step == 0 ? (int)hc : (int)h;
+  const double* A = step == 0 ? r + p0 + (p0 + h) * ldr : ri + p0 + p0 * ldi;
+  const int64_t lda = step == 0 ? ldr : ldi;
+  double* Tz = T + (size_t)blockIdx.z * (size_t)(h * h);
+  const double* B = step == 0 ? ri + (p0 + h) + (p0 + h) * ldi : Tz;
+  const int64_t ldb = step == 0 ? ldi : h;
+  double* C = step == 0 ? Tz : ri + p0 + (p0 + h) * ldi;
+  const int64_t ldc = step == 0 ? h : ldi;
+  const double alpha = step == 0 ? 1.0 : -1.0;
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
-  const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;  // rows ti, columns tj + 8q
+  if (i0 >= m || j0 >= n) return;
+  const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int l0 = 0; l0 < kk; l0 += 32) {
     for (int t = threadIdx.x; t < 32 * 32; t += blockDim.x) {
@@ -523,12 +539,6 @@ __global__ void gemm_nn_small_kernel(int m, int n, int kk, double alpha, const d
     const int i = i0 + ti, j = j0 + tj + 8 * q;
     if (i < m && j < n) C[i + (int64_t)j * ldc] = alpha * acc[q];
   }
-}
-
-void gemm_nn_small(int m, int n, int kk, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
-                   double* C, int64_t ldc, cudaStream_t st) {
-  gemm_nn_small_kernel<<<dim3((m + 31) / 32, (n + 31) / 32), 256, 0, st>>>(m, n, kk, alpha, A, lda, B, ldb, C, ldc);
-  LRB_CHECK_LAUNCH();
 }
 }  // namespace
 
@@ -591,15 +601,15 @@ void tri_upper_inverse_blocked(int64_t k, const double* r, int64_t ldr, double* 
   if (k <= kInvB) return;
   double* T = nullptr;
   LRB_CUDA(cudaMallocAsync(&T, sizeof(double) * k * k, st));
-  for (int64_t h = kInvB; h < k; h *= 2)
-    for (int64_t p0 = 0; p0 + h < k; p0 += 2 * h) {
-      const int64_t hc = std::min<int64_t>(h, k - p0 - h);
-      // T = B C^-1, then the block = -A^-1 T
-      gemm_nn_small((int)h, (int)hc, (int)hc, 1.0, r + p0 + (p0 + h) * ldr, ldr, rinv + (p0 + h) + (p0 + h) * ldi,
-                    ldi, T, h, st);
-      gemm_nn_small((int)h, (int)hc, (int)h, -1.0, rinv + p0 + p0 * ldi, ldi, T, h, rinv + p0 + (p0 + h) * ldi, ldi,
-                    st);
+  for (int64_t h = kInvB; h < k; h *= 2) {
+    // every pair [A B; 0 C] of this level: T = B C^-1, then the block = -A^-1 T
+    const unsigned pairs = (unsigned)((k - h + 2 * h - 1) / (2 * h));
+    const dim3 grid((unsigned)((h + 31) / 32), (unsigned)((h + 31) / 32), pairs);
+    for (int step = 0; step < 2; ++step) {
+      tri_inv_level_kernel<<<grid, 256, 0, st>>>(step, h, k, r, ldr, rinv, ldi, T);
+      LRB_CHECK_LAUNCH();
     }
+  }
   LRB_CUDA(cudaFreeAsync(T, st));
 }
 
