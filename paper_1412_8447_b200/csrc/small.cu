@@ -212,58 +212,86 @@ __global__ void max_reduce_kernel(const double* __restrict__ p, int n, double* o
 constexpr int kCholB = 64;
 
 __global__ void chol_diag_kernel(int64_t j0, int jb, double* __restrict__ g, int64_t ldg, int* info) {
-  // 256 threads own fixed 4x4 element sets (rows tr + 16u, columns tc + 16v):
-  // per column j, threads 0..jb-1 scale row j (one division each), then every
-  // thread applies the rank-1 update to its own elements
-  __shared__ double a[kCholB][kCholB + 1];
+  // 256 threads own fixed 4x4 element sets (rows tr + 16u, columns tc + 16v)
+  // in registers; per column j the owners of row j scale it and publish it in
+  // shared memory (with one rsqrt per thread), then every thread applies the
+  // rank-1 update to its registers and the owner of the next diagonal entry
+  // publishes it.  Same arithmetic as scaling the row first.
   __shared__ double srow[kCholB];
+  __shared__ double sd;
   __shared__ int fail;
   if (info[0] != 0) return;
-  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
-    const int i = t % jb, j = t / jb;
-    a[i][j] = g[(j0 + i) + (j0 + j) * ldg];
-  }
-  if (threadIdx.x == 0) fail = 0;
-  __syncthreads();
   const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
-  for (int j = 0; j < jb; ++j) {
-    const double d = a[j][j];
-    if (!(d > 0.0) || !isfinite(d)) {  // uniform
-      if (threadIdx.x == 0) fail = j + 1;
-      break;
-    }
-    const double ri = rsqrt(d);  // 1/sqrt(d): multiplications instead of a division chain
-    const int x = threadIdx.x;
-    if (x > j && x < jb) {
-      const double v = a[j][x] * ri;
-      srow[x] = v;
-      a[j][x] = v;
-    }
-    __syncthreads();
-    if (x == j) a[j][j] = sqrt(d);
+  double reg[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int c = tc + 16 * v;
-      if (c > j && c < jb) {
-        const double sc = srow[c];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int r = tr + 16 * u;
-          if (r > j && r <= c) a[r][c] = fma(-srow[r], sc, a[r][c]);
-        }
-      }
+      const int r = tr + 16 * u, c = tc + 16 * v;
+      reg[u][v] = (r <= c && c < jb) ? g[(j0 + r) + (j0 + c) * ldg] : 0.0;
     }
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    fail = 0;
+    sd = g[j0 + j0 * ldg];
   }
   __syncthreads();
+  bool stop = false;
+#pragma unroll
+  for (int U = 0; U < 4; ++U) {
+    for (int jj = 0; jj < 16 && !stop; ++jj) {
+      const int j = 16 * U + jj;
+      if (j >= jb) {
+        stop = true;
+        break;
+      }
+      const double d = sd;
+      if (!(d > 0.0) || !isfinite(d)) {  // uniform
+        if (threadIdx.x == 0) fail = j + 1;
+        stop = true;
+        break;
+      }
+      const double ri = rsqrt(d);
+      if (tr == jj) {  // row j = tr + 16 U
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = tc + 16 * v;
+          if (c > j && c < jb) {
+            reg[U][v] *= ri;
+            srow[c] = reg[U][v];
+          } else if (c == j) {
+            reg[U][v] = sqrt(d);
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = tr + 16 * u;
+        if (r <= j) continue;
+        const double sr = srow[r];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = tc + 16 * v;
+          if (r <= c && c < jb) reg[u][v] = fma(-sr, srow[c], reg[u][v]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (tr == tc && tr + 16 * u == j + 1) sd = reg[u][u];
+      __syncthreads();
+    }
+  }
   if (fail) {
     if (threadIdx.x == 0) info[0] = (int)(j0 + fail);
     return;
   }
-  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
-    const int i = t % jb, j = t / jb;
-    g[(j0 + i) + (j0 + j) * ldg] = i <= j ? a[i][j] : 0.0;
-  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = tr + 16 * u, c = tc + 16 * v;
+      if (r < jb && c < jb) g[(j0 + r) + (j0 + c) * ldg] = r <= c ? reg[u][v] : 0.0;
+    }
 }
 
 // C = beta C + alpha A^T B (column-major, small K): the Cholesky trailing update
