@@ -156,13 +156,27 @@ __global__ void gather_columns_kernel(int64_t m, int64_t k, const double* __rest
   }
 }
 
+// R = A(idx, :): a thread keeps one row index and walks columns (no index
+// division per element; 4 independent column loads in flight).  Each load
+// touches its own 32-byte sector of A (the gather is sector-bound), stores are
+// coalesced along the k rows of a column.
 __global__ void gather_rows_kernel(int64_t k, int64_t n, const double* __restrict__ a, int64_t lda,
                                    const int64_t* __restrict__ idx, double* __restrict__ out, int64_t ldo) {
-  const int64_t total = k * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % k, j = t / k;
-    out[i + j * ldo] = a[idx[i] + j * lda];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const double* src = a + idx[i];
+  double* dst = out + i;
+  const int64_t step = gridDim.y;
+  int64_t j = blockIdx.y;
+  for (; j + 3 * step < n; j += 4 * step) {
+    const double v0 = __ldcs(src + j * lda), v1 = __ldcs(src + (j + step) * lda);
+    const double v2 = __ldcs(src + (j + 2 * step) * lda), v3 = __ldcs(src + (j + 3 * step) * lda);
+    dst[j * ldo] = v0;
+    dst[(j + step) * ldo] = v1;
+    dst[(j + 2 * step) * ldo] = v2;
+    dst[(j + 3 * step) * ldo] = v3;
   }
+  for (; j < n; j += step) dst[j * ldo] = __ldcs(src + j * lda);
 }
 
 __global__ void gather_rows_t_kernel(int64_t k, int64_t n, const double* __restrict__ a, int64_t lda,
@@ -292,7 +306,9 @@ void gather_columns(int64_t m, int64_t k, const double* a, int64_t lda, const in
 void gather_rows(int64_t k, int64_t n, const double* a, int64_t lda, const int64_t* idx, double* out, int64_t ldo,
                  cudaStream_t st) {
   if (k <= 0 || n <= 0) return;
-  gather_rows_kernel<<<grid_for(k * n), 256, 0, st>>>(k, n, a, lda, idx, out, ldo);
+  const unsigned gx = (unsigned)((k + 255) / 256);
+  const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (8 * num_sms() + gx - 1) / gx * 4));
+  gather_rows_kernel<<<dim3(gx, gy), 256, 0, st>>>(k, n, a, lda, idx, out, ldo);
   LRB_CHECK_LAUNCH();
 }
 
