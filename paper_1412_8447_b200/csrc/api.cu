@@ -381,7 +381,17 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
   if (kind == LR_SOLVE_BACKSUB) {
     DBuf<double> Mt((size_t)k * k, c->st);
     DBuf<int> zr(k, c->st);
-    backsub_operator_t(k, s11, ld11, strat.threshold, Mt, zr, c->st);
+    // no diagonal at or below the zeroing tolerance (known from the escalation
+    // check): M = S11^-1 exactly, by the blocked inverse; otherwise the
+    // back-substitution operator with its zeroed rows (solve.hpp:62-89)
+    const bool no_zero_rows = strat.escalate && k > 64 && c->h_scal[1] > strat.threshold * c->h_scal[0];
+    if (no_zero_rows) {
+      DBuf<double> M((size_t)k * k, c->st);
+      tri_upper_inverse_blocked(k, s11, ld11, M, k, c->st);
+      transpose_matrix(k, k, M, k, Mt, k, c->st);
+    } else {
+      backsub_operator_t(k, s11, ld11, strat.threshold, Mt, zr, c->st);
+    }
     gemm(c, k, nc, k, Mt, k, s12, ld12, t, ldt, 1.0, 0.0, -1, false, kTriP);  // M upper triangular
     if (!strat.escalate) {  // allow_singularity_error (solve.hpp:75-83)
       std::vector<int> hz(k);
