@@ -462,3 +462,29 @@ def test_panel_cpqr_degenerate_inputs(lr, oracle, case):
     else:
         assert np.array_equal(q.pivots, o["pivots"])
         assert rel(q.s, o["s"]) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_panel_cpqr_random_sweep(lr, oracle, seed):
+    """Seeded random shapes on the panel path (193 < m <= 512 -> ld 256/320/512,
+    ragged n and k, a random share of identically-zero and duplicated columns)
+    against the oracle: identical pivots, S to 1e-12."""
+    rng = np.random.default_rng(1000 + seed)
+    m = int(rng.integers(193, 513))
+    n = int(rng.integers(m // 2 + 1, 4 * m))
+    a = oracle.gaussian_matrix(m, n, seed) * (2.0 ** rng.uniform(-4, 4, size=n))[None, :]
+    nz = int(rng.integers(0, n // 3))
+    if nz:
+        a[:, rng.choice(n, nz, replace=False)] = 0.0
+    nd = int(rng.integers(0, n // 5))
+    if nd:
+        src = rng.choice(n, nd)
+        dst = rng.choice(n, nd)
+        a[:, dst] = -a[:, src]
+    rank = int(np.linalg.matrix_rank(a))
+    k = int(rng.integers(1, max(2, min(m, rank) + 1)))
+    a = np.asfortranarray(a)
+    q = lr.cpqr_partial(a, k)
+    o = oracle.cpqr(a, k)
+    assert np.array_equal(q.pivots, o["pivots"])
+    assert rel(q.s, o["s"]) <= 1e-12
