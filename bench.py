@@ -476,6 +476,8 @@ def run_sharded(args, rank, world, local_rank):
             dist.barrier()
 
     launches0 = ctx.kernel_launches()
+    ctx.reset_stats()
+    ctx.enable_timing(True)
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -487,12 +489,56 @@ def run_sharded(args, rank, world, local_rank):
         torch.cuda.synchronize()
     barrier()
     launches = ctx.kernel_launches() - launches0
+    stages = ctx.stage_report()
+    ctx.enable_timing(False)
+    # roofline of this rank's sketch contraction (its column shard)
+    shard_cfg = inputs.Config(cfg.name, cfg.m, n_g, cfg.width, cfg.spectrum, cfg.k, OVERSAMPLE, cfg.pipeline)
+    st_avg = {kk: v["ms"] / max(1, v["count"]) for kk, v in stages.items()}
+    roof = kernel_rooflines(shard_cfg, st_avg, stages, args.engine).get("sketch_gemm")
+    if roof:
+        roof = dict(roof, note=f"rank 0's column shard ({n_g} of {cfg.n} columns); the CPQRs are replicated")
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+
+    # e2e: each step copies the rank's column shard from pinned host memory
+    # into the device buffer, runs the sharded CUR and reads the replicated
+    # factors back into pinned host buffers (wall clock, max over ranks)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((n_g, cfg.m), dtype=torch.float64, pin_memory=True).T
+        host.copy_(a)
+        torch.cuda.synchronize()
+        keys = ("c", "u", "r", "col_pivots", "row_pivots")
+        hb = {kk: torch.empty(tuple(res[kk].shape), dtype=res[kk].dtype, pin_memory=True) for kk in keys}
+        d2h = sum(hb[kk].numel() * hb[kk].element_size() for kk in keys)
+
+        def e2e_step():
+            a.copy_(host, non_blocking=True)
+            out = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+            for kk in keys:
+                hb[kk].copy_(out[kk], non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        e2e_step()  # warm-up
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * cfg.m * cfg.n,
+               "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
+               "host_buffer": "pinned column shard per rank (1/N of A) and pinned result buffers",
+               "pipeline": "shard H2D on the compute stream, then the sharded CUR; bytes summed over ranks"}
     if rank != 0:
         return
     fm = flops_model(cfg.m, cfg.n, cfg.k, cfg.k + OVERSAMPLE)
@@ -505,8 +551,8 @@ def run_sharded(args, rank, world, local_rank):
                    "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE, "u_mode": "cpinv_a_rpinv",
                    "parallelism": f"column-sharded x{world}", "l2": "A shard exceeds L2; no flush needed"},
         "fp64_tflops": round(sum(fm.values()) / (ms * 1e-3) / 1e12, 3),
-        "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": None, "cpu_baseline": None,
-        "roofline": None,
+        "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
+        "roofline": roof, "stages_ms": {kk: round(v, 3) for kk, v in st_avg.items()},
     }
     print(json.dumps(line), flush=True)
 
