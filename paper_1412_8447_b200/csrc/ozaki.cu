@@ -520,6 +520,62 @@ __global__ void crt_kernel(int64_t M, int64_t N, const int8_t* __restrict__ res,
   }
 }
 
+// Same reconstruction, four consecutive rows per thread: one 4-byte load per
+// plane instead of four byte loads (the residue planes have ldr % 16 == 0).
+__global__ void __launch_bounds__(256, 3) crt4_kernel(int64_t M, int64_t N, const int8_t* __restrict__ res, int64_t ldr, int64_t plane_stride,
+                            const int* __restrict__ shift_p, const int* __restrict__ shift_q, double* __restrict__ out,
+                            int64_t ldo, double alpha, double beta) {
+  const i128 Mc = (i128)(((u128)c_Mcrt[1] << 64) | (u128)c_Mcrt[0]);
+  const i128 half = Mc >> 1;
+  const u128 K0 = ((u128)c_crt_k0[1] << 64) | (u128)c_crt_k0[0];
+  // flattened (row group, column) work items so short columns keep every lane busy
+  const int64_t G = (M + 3) / 4;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < G * N; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = w / G;
+    const int64_t i0 = 4 * (w - j * G);
+    const int sq = shift_q[j];
+    {
+      const int8_t* r = res + j * ldr + i0;
+      unsigned long long a[4][4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a[e][0] = a[e][1] = a[e][2] = a[e][3] = 0ull;
+#pragma unroll
+      for (int p = 0; p < kOzakiModuli; ++p) {
+        const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(r + p * plane_stride));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t rp = ((w >> (8 * e)) & 0xffu) ^ 0x80u;  // signed residue + 128
+          a[e][0] += (unsigned long long)c_crt_c[p][0] * rp;
+          a[e][1] += (unsigned long long)c_crt_c[p][1] * rp;
+          a[e][2] += (unsigned long long)c_crt_c[p][2] * rp;
+          a[e][3] += (unsigned long long)c_crt_c[p][3] * rp;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + e;
+        if (i >= M) break;
+        const double td = fma(fma(fma((double)a[e][3], 4294967296.0, (double)a[e][2]), 4294967296.0,
+                                  (double)a[e][1]), 4294967296.0, (double)a[e][0]);
+        const long long q = __double2ll_rn(fma(td, c_crt_invM, -c_crt_k0M));
+        const u128 T = (u128)a[e][0] + ((u128)a[e][1] << 32) + ((u128)a[e][2] << 64) + ((u128)a[e][3] << 96);
+        i128 sv = (i128)(T - K0 - (u128)(i128)q * (u128)Mc);
+        if (sv > half) sv -= Mc;
+        else if (sv < -half) sv += Mc;
+        const bool neg = sv < 0;
+        const u128 au = neg ? (u128)(-sv) : (u128)sv;
+        double v = fma((double)(unsigned long long)(au >> 64), 18446744073709551616.0,
+                       (double)(unsigned long long)au);
+        if (neg) v = -v;
+        const int sp = shift_p[i];
+        v = (sp == kOzakiNonFinite || sq == kOzakiNonFinite) ? CUDART_NAN : ldexp(v, -(sp + sq));
+        double* o = out + i + j * ldo;
+        *o = beta == 0.0 ? alpha * v : alpha * v + beta * *o;
+      }
+    }
+  }
+}
+
 CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int64_t ld, int64_t plane_stride,
                                 int box_rows) {
   using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -607,8 +663,8 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
   }
   const CUtensorMap tp = make_tmap_i8_planes(P.planes, P.K, P.cols, P.ld, P.plane_stride, IBM);
   const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, IBN / ICL);
-  const int64_t ldr = M;
-  int8_t* res = static_cast<int8_t*>(ws.get(WsSlot::kTmp7, (size_t)M * N * kOzakiModuli));
+  const int64_t ldr = (M + 15) / 16 * 16;  // 4-byte aligned residue columns for crt4_kernel
+  int8_t* res = static_cast<int8_t*>(ws.get(WsSlot::kTmp7, (size_t)ldr * N * kOzakiModuli));
   const int tiles_m = (int)((M + IBM - 1) / IBM), tiles_n = (int)((N + IBN - 1) / IBN);
   // clusters of ICL CTAs along M: pad the M grid (extra CTAs compute zero rows and store nothing)
   dim3 grid((tiles_m + ICL - 1) / ICL * ICL, tiles_n, kOzakiModuli);
@@ -616,11 +672,11 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
   if ((P.unsigned_res || Q.unsigned_res) && P.K > kOzakiMaxKUnsigned)
     throw CudaError("ozaki_gemm_tn: K too large for an unsigned-residue operand");
   const uint32_t ab_fmt = (P.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
-  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, M * N, ab_fmt);
+  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, ldr * N, ab_fmt);
   LRB_CHECK_LAUNCH();
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((M + 255) / 256, 64));
-  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(N, std::max<int64_t>(1, 16 * num_sms() / gx)));
-  crt_kernel<<<dim3(gx, gy), 256, 0, st>>>(M, N, res, ldr, M * N, P.shift, Q.shift, out, ldo, alpha, beta);
+  const int64_t items = (M + 3) / 4 * N;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 8 * num_sms()));
+  crt4_kernel<<<gx, 256, 0, st>>>(M, N, res, ldr, ldr * N, P.shift, Q.shift, out, ldo, alpha, beta);
   LRB_CHECK_LAUNCH();
 }
 
