@@ -100,7 +100,7 @@ def kernel_rooflines(cfg, st, stages, engine):
             if st.get(name):
                 ops = 16 * 2.0 * cols * cfg.m * cfg.n
                 ach = ops / (st[name] * 1e-3) / 1e12
-                out[name] = {"kernel": f"imma_gemm_kernel + crt_kernel ({what}, 16 INT8 residue GEMMs)",
+                out[name] = {"kernel": f"imma_gemm_kernel + crt4_kernel ({what}, 16 INT8 residue GEMMs)",
                              "bound": "tensor", "achieved": round(ach, 1), "peak": round(i8, 1), "unit": "TOP/s",
                              "frac": round(ach / i8, 4), "traffic": traffic.get(name),
                              "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (INT8 = 2x bf16 rate)",

@@ -62,7 +62,7 @@ def test_launch_step_and_traffic_json(tmp_path, capsys):
     one_cur += [("void lrb::cpqr_panel_kernel<0, 8, 0>(PanelArgs)", 1.5), ("panel_update_dmma_kernel(x)", 0.1)] * 2
     one_cur += [("gemm_tn_kernel<0>(x)", 1.0)]
     one_cur += [("void lrb::cpqr_panel_kernel<0, 8, 0>(PanelArgs)", 1.4)] * 2
-    one_cur += [("split_kernel<0>(long)", 0.2), ("imma_gemm_kernel(x)", 25.0), ("crt_kernel(x)", 0.8)]
+    one_cur += [("split_kernel<0>(long)", 0.2), ("imma_gemm_kernel(x)", 25.0), ("<unnamed>::crt4_kernel(x)", 0.6)]
     names = one_cur * 4 + [("void gemm_tn_kernel<2>(x)", 170.0)]
     path = tmp_path / "launches.csv"
     _write_launch_csv(path, names)

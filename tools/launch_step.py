@@ -38,7 +38,7 @@ def main(path):
     err = [i for i, n in enumerate(names) if n.startswith("gemm_tn_kernel<2>")]
     lo = imma[5] + 1
     hi = min(i for i in err if i > imma[7])
-    while lo < hi and names[lo].startswith("crt_kernel"):
+    while lo < hi and names[lo].startswith(("crt_kernel", "crt4_kernel")):
         lo += 1
     tab = OrderedDict()
     for k, n in zip(ks[lo:hi], names[lo:hi]):

@@ -17,7 +17,7 @@ def main(path, out):
     imma = [i for i, n in enumerate(names) if n.startswith("imma_gemm_kernel")]
     err = [i for i, n in enumerate(names) if n.startswith("gemm_tn_kernel<2>")]
     lo, hi = imma[5] + 1, min(i for i in err if i > imma[7])
-    while names[lo].startswith("crt_kernel"):
+    while names[lo].startswith(("crt_kernel", "crt4_kernel")):
         lo += 1
     seg = list(range(lo, hi))
 
@@ -34,7 +34,7 @@ def main(path, out):
     cut = max(gaps)[1] + 1
     cpqr_y, cpqr_ct = cp[:cut], cp[cut:]
     im = [i for i in seg if names[i].startswith("imma_gemm_kernel")]
-    crt = [i for i in seg if names[i].startswith("crt_kernel")]
+    crt = [i for i in seg if names[i].startswith(("crt_kernel", "crt4_kernel"))]
     split = [i for i in seg if names[i].startswith(("split_kernel", "colmax_kernel"))]
     res = {
         "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control "
