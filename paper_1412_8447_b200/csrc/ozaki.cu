@@ -19,6 +19,7 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -190,6 +191,51 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
+// One tile of kSplitRows consecutive K entries of a column: scale, reduce mod
+// the pairs, then the 16 residues (see above), stored 8 bytes per plane.
+template <bool UNS>
+__device__ __forceinline__ void split_tile(const double (&v)[kSplitRows], double sc1, double sc2,
+                                           int8_t* __restrict__ out, int64_t plane_stride) {
+  constexpr double M52 = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr float M23 = 12582912.0f;          // 1.5 * 2^23
+  double xp[kSplitRows];
+#pragma unroll
+  for (int q = 0; q < kSplitRows; ++q) xp[q] = rint((v[q] * sc1) * sc2);  // exact, |xp| <= 2^beta
+#pragma unroll
+  for (int g = 0; g < kOzakiModuli / 2; ++g) {
+    const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
+    const double invP = 1.0 / P;
+    uint32_t b0[kSplitRows], b1[kSplitRows];
+#pragma unroll
+    for (int q = 0; q < kSplitRows; ++q) {
+      const double qg = fma(xp[q], invP, M52) - M52;
+      const double r = fma(-qg, P, xp[q]);  // exact, |r| < 2^17
+      if constexpr (UNS) {
+        const int iP = kmod(2 * g) * kmod(2 * g + 1);
+        const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
+        const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
+        const uint32_t m0 = (uint32_t)kmod(2 * g), m1 = (uint32_t)kmod(2 * g + 1);
+        b0[q] = u - m0 * __umulhi(u, (uint32_t)((0x100000000ull + m0 - 1) / m0));  // u mod m
+        b1[q] = u - m1 * __umulhi(u, (uint32_t)((0x100000000ull + m1 - 1) / m1));
+      } else {
+        const int lo = __double2loint(r + M52);
+        const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
+        const float rf = fb - M23;                           // r
+        const float m0 = (float)kmod(2 * g), m1 = (float)kmod(2 * g + 1);
+        const float q0 = fmaf(rf, 1.0f / m0, M23) - M23;
+        const float q1 = fmaf(rf, 1.0f / m1, M23) - M23;
+        b0[q] = (uint32_t)__float_as_int(fmaf(-q0, m0, fb));  // 1.5*2^23 + residue, exact
+        b1[q] = (uint32_t)__float_as_int(fmaf(-q1, m1, fb));
+      }
+    }
+    static_assert(kSplitRows == 8, "two packed words per plane");
+    __stcs(reinterpret_cast<uint2*>(out + (2 * g) * plane_stride),
+           make_uint2(pack4(b0[0], b0[1], b0[2], b0[3]), pack4(b0[4], b0[5], b0[6], b0[7])));
+    __stcs(reinterpret_cast<uint2*>(out + (2 * g + 1) * plane_stride),
+           make_uint2(pack4(b1[0], b1[1], b1[2], b1[3]), pack4(b1[4], b1[5], b1[6], b1[7])));
+  }
+}
+
 // UNS: residues t = x' mod m in [0, m) for the u8 operand: the pair remainder
 // comes out of the FP64 stage already biased positive (u = r + B_P, B_P a
 // multiple of P >= 2^17, folded into the low-word constant) and t = u - m
@@ -201,8 +247,6 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
                                                     const unsigned long long* __restrict__ cmax,
                                                     int8_t* __restrict__ planes, int64_t ldp, int64_t plane_stride,
                                                     int* __restrict__ shift) {
-  constexpr double M52 = 6755399441055744.0;  // 1.5 * 2^52
-  constexpr float M23 = 12582912.0f;          // 1.5 * 2^23
   // a CTA walks whole columns (j += gridDim.x) tile by tile: no index
   // division, one scale per column, and a software pipeline: the next tile's
   // 4 values are in flight while this tile's 64 residues are computed and stored
@@ -243,47 +287,7 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
       const int tkn = last ? 0 : tk + 1;
       if (jn < cols) load(jn, tkn, vn);
       const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
-      if (i0 < K) {
-        // modulus pair outer, element inner: the 4 elements' bytes of a plane
-        // are packed and stored as soon as they exist (few live registers)
-        double xp[kSplitRows];
-#pragma unroll
-        for (int q = 0; q < kSplitRows; ++q) xp[q] = rint((v[q] * sc1) * sc2);  // exact, |xp| <= 2^beta
-        int8_t* out = colp + i0;
-#pragma unroll
-        for (int g = 0; g < kOzakiModuli / 2; ++g) {
-          const double P = (double)(kmod(2 * g) * kmod(2 * g + 1));
-          const double invP = 1.0 / P;
-          uint32_t b0[kSplitRows], b1[kSplitRows];
-#pragma unroll
-          for (int q = 0; q < kSplitRows; ++q) {
-            const double qg = fma(xp[q], invP, M52) - M52;
-            const double r = fma(-qg, P, xp[q]);  // exact, |r| < 2^17
-            if constexpr (UNS) {
-              const int iP = kmod(2 * g) * kmod(2 * g + 1);
-              const double bias = M52 + (double)(iP * ((131072 + iP - 1) / iP));  // M52 + B_P
-              const uint32_t u = (uint32_t)__double2loint(r + bias);             // r + B_P in [0, 2^18)
-              const uint32_t m0 = (uint32_t)kmod(2 * g), m1 = (uint32_t)kmod(2 * g + 1);
-              b0[q] = u - m0 * __umulhi(u, (uint32_t)((0x100000000ull + m0 - 1) / m0));  // u mod m
-              b1[q] = u - m1 * __umulhi(u, (uint32_t)((0x100000000ull + m1 - 1) / m1));
-            } else {
-              const int lo = __double2loint(r + M52);
-              const float fb = __int_as_float(0x4B400000 + lo);  // 1.5*2^23 + r
-              const float rf = fb - M23;                           // r
-              const float m0 = (float)kmod(2 * g), m1 = (float)kmod(2 * g + 1);
-              const float q0 = fmaf(rf, 1.0f / m0, M23) - M23;
-              const float q1 = fmaf(rf, 1.0f / m1, M23) - M23;
-              b0[q] = (uint32_t)__float_as_int(fmaf(-q0, m0, fb));  // 1.5*2^23 + residue, exact
-              b1[q] = (uint32_t)__float_as_int(fmaf(-q1, m1, fb));
-            }
-          }
-          static_assert(kSplitRows == 8, "two packed words per plane");
-          __stcs(reinterpret_cast<uint2*>(out + (2 * g) * plane_stride),
-                 make_uint2(pack4(b0[0], b0[1], b0[2], b0[3]), pack4(b0[4], b0[5], b0[6], b0[7])));
-          __stcs(reinterpret_cast<uint2*>(out + (2 * g + 1) * plane_stride),
-                 make_uint2(pack4(b1[0], b1[1], b1[2], b1[3]), pack4(b1[4], b1[5], b1[6], b1[7])));
-        }
-      }
+      if (i0 < K) split_tile<UNS>(v, sc1, sc2, colp + i0, plane_stride);
 #pragma unroll
       for (int q = 0; q < kSplitRows; ++q) v[q] = vn[q];
     }
@@ -599,6 +603,82 @@ CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int
   return map;
 }
 
+// Opt-in (LRB_SPLIT_FUSED=1), slower than the two passes on B200 -- see ozaki_split_into.
+// Column max and split in one pass over X (kSplitCluster CTAs per column):
+// each CTA keeps its kSplitTilesPerCta tiles of the column in registers,
+// the column's max|x| is reduced across the cluster through distributed
+// shared memory, then the tiles are split from registers.  X is read once
+// instead of twice (colmax_kernel + split_kernel); K <= 65536, vec2 layout.
+constexpr int kSplitCluster = 8;
+constexpr int kSplitTilesPerCta = 4;
+template <bool UNS>
+__global__ void __cluster_dims__(kSplitCluster, 1, 1) __launch_bounds__(kSplitThreads, 2)
+split_fused_kernel(int64_t K, int64_t cols, const double* __restrict__ X, int64_t ldx, int beta,
+                   int8_t* __restrict__ planes, int64_t ldp, int64_t plane_stride, int* __restrict__ shift) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ unsigned long long sh[kSplitThreads / 32];
+  __shared__ unsigned long long slot[2];
+  const int rank = (int)cluster.block_rank();
+  const int64_t nclusters = gridDim.x / kSplitCluster;
+  const int tiles_k = (int)((K + kSplitTile - 1) / kSplitTile);
+  const int64_t r_off = (int64_t)kSplitRows * threadIdx.x;
+  int it = 0;
+  for (int64_t j = blockIdx.x / kSplitCluster; j < cols; j += nclusters, ++it) {
+    const double* xc = X + j * ldx;
+    double v[kSplitTilesPerCta][kSplitRows];
+    unsigned long long mx = 0;
+#pragma unroll
+    for (int u = 0; u < kSplitTilesPerCta; ++u) {
+      const int tk = rank * kSplitTilesPerCta + u;
+      const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
+      if (tk < tiles_k && i0 + kSplitRows <= K) {
+#pragma unroll
+        for (int h = 0; h < kSplitRows / 2; ++h) {
+          const double2 a = __ldcs(reinterpret_cast<const double2*>(xc + i0 + 2 * h));
+          v[u][2 * h] = a.x;
+          v[u][2 * h + 1] = a.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kSplitRows; ++q) v[u][q] = (tk < tiles_k && i0 + q < K) ? xc[i0 + q] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q)
+        mx = max(mx, (unsigned long long)__double_as_longlong(fabs(v[u][q])));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = sh[0];
+      for (int w = 1; w < kSplitThreads / 32; ++w) m = max(m, sh[w]);
+      slot[it & 1] = m;
+    }
+    // slot[it & 1] is rewritten two columns later, after the next cluster
+    // barrier, which every CTA reaches only once it has read this column's slots
+    cluster.sync();
+    unsigned long long cm = 0;
+#pragma unroll
+    for (int r = 0; r < kSplitCluster; ++r) cm = max(cm, *cluster.map_shared_rank(&slot[it & 1], r));
+    const double mxd = __longlong_as_double((long long)cm);
+    int e = 0;
+    if (mxd > 0.0 && isfinite(mxd)) frexp(mxd, &e);
+    const int sft = (mxd > 0.0 && isfinite(mxd)) ? beta - e : 0;
+    if (rank == 0 && threadIdx.x == 0) shift[j] = isfinite(mxd) ? sft : kOzakiNonFinite;
+    const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
+    int8_t* colp = planes + j * ldp;
+#pragma unroll
+    for (int u = 0; u < kSplitTilesPerCta; ++u) {
+      const int tk = rank * kSplitTilesPerCta + u;
+      const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
+      if (tk < tiles_k && i0 < K) split_tile<UNS>(v[u], sc1, sc2, colp + i0, plane_stride);
+    }
+  }
+  cluster.sync();  // no CTA leaves while a peer may still read its slots
+}
+
 }  // namespace
 
 int ozaki_beta(int64_t K) {
@@ -617,16 +697,30 @@ void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cuda
   upload_constants();
   const int64_t K = op.K, cols = op.cols;
   if (K < 1 || cols < 1) return;
+  if (op.unsigned_res && K > kOzakiMaxKUnsigned) throw CudaError("ozaki_split: unsigned residues need K <= 65536");
+  const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
+  // "1": cluster-fused split (reads X once, but measured slower: 22-25 ms vs
+  // 14 ms for the two passes at C4 -- the register-resident column leaves 16
+  // warps per SM and no load/compute overlap; kept for A/B and tests)
+  const char* fe = std::getenv("LRB_SPLIT_FUSED");
+  const bool fused_off = !(fe && fe[0] == '1');
+  if (!fused_off && vec2 && K >= (int64_t)kSplitCluster * kSplitTile &&
+      K <= (int64_t)kSplitCluster * kSplitTilesPerCta * kSplitTile) {
+    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(cols, 2 * num_sms() / kSplitCluster));
+    auto kern = op.unsigned_res ? split_fused_kernel<true> : split_fused_kernel<false>;
+    kern<<<(int)(ncl * kSplitCluster), kSplitThreads, 0, st>>>(K, cols, X, ldx, op.beta, op.planes, op.ld,
+                                                                 op.plane_stride, op.shift);
+    LRB_CHECK_LAUNCH();
+    return;
+  }
   unsigned long long* cmax = nullptr;
   LRB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cmax), sizeof(unsigned long long) * cols, st));
   LRB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * cols, st));
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cols, 8 * num_sms()));  // split: whole columns per CTA
-  const bool vec2 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0);
   const int64_t mtiles = (K + kMaxRowsPerThread * kSplitThreads - 1) / (kMaxRowsPerThread * kSplitThreads) * cols;
   const int gm = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, 8 * num_sms()));
   colmax_kernel<<<gm, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, cmax);
   LRB_CHECK_LAUNCH();
-  if (op.unsigned_res && K > kOzakiMaxKUnsigned) throw CudaError("ozaki_split: unsigned residues need K <= 65536");
   auto kern = op.unsigned_res ? split_kernel<true> : split_kernel<false>;
   kern<<<g, kSplitThreads, 0, st>>>(K, cols, X, ldx, vec2, op.beta, cmax, op.planes, op.ld, op.plane_stride,
                                             op.shift);

@@ -71,7 +71,8 @@ def test_gemm_mode_switch(lr):
 
 
 @pytest.mark.parametrize("M,N,K", [(510, 1000, 777), (128, 256, 128), (5, 7, 3), (300, 260, 4100),
-                                   (129, 257, 129), (1, 1, 1), (64, 300, 65536)])
+                                   (129, 257, 129), (1, 1, 1), (64, 300, 65536), (33, 70, 20002),
+                                   (20, 40, 16384)])
 def test_ozaki_gemm_error_bound(lr, ozaki, M, N, K):
     rng = np.random.default_rng(M * 7 + N * 3 + K)
     P = rng.standard_normal((K, M))
@@ -86,9 +87,10 @@ def test_ozaki_gemm_error_bound(lr, ozaki, M, N, K):
     assert np.linalg.norm(err) <= 2 * np.linalg.norm((dm - ex).astype(np.float64)) + 1e-300
 
 
-def test_ozaki_gemm_scaling_and_special_columns(lr, ozaki):
+@pytest.mark.parametrize("K", [1000, 16390])
+def test_ozaki_gemm_scaling_and_special_columns(lr, ozaki, K):
     rng = np.random.default_rng(5)
-    K, M, N = 1000, 40, 70
+    M, N = 40, 70
     P = rng.standard_normal((K, M))
     Q = rng.standard_normal((K, N))
     P[:, 3] = 0.0                       # zero column
@@ -107,6 +109,28 @@ def test_ozaki_gemm_scaling_and_special_columns(lr, ozaki):
     assert np.all(err <= bound)
     assert np.all(out[3, :] == 0.0) and np.all(out[:, 5] == 0.0)
     assert out[13, 12] == float(P[:, 13] @ Q[:, 12])  # integer data: exact
+
+
+@pytest.mark.parametrize("K", [16384, 30002, 65536])
+def test_ozaki_fused_split_equals_two_pass(lr, ozaki, K, monkeypatch):
+    """The cluster-fused column max + split (one read of X) and the two-pass
+    colmax_kernel + split_kernel give bit-identical products, NaN / Inf /
+    zero columns included."""
+    rng = np.random.default_rng(K)
+    P = rng.standard_normal((K, 24))
+    Q = rng.standard_normal((K, 37))
+    P[:, 2] = 0.0
+    P[K // 2, 3] = np.nan
+    Q[K - 1, 4] = np.inf
+    Q[:, 5] *= 2.0 ** -600
+    P[::5, 6] *= 1e8
+    monkeypatch.setenv("LRB_SPLIT_FUSED", "1")
+    fused = _gemm(lr, ozaki, P, Q)
+    monkeypatch.setenv("LRB_SPLIT_FUSED", "0")
+    two = _gemm(lr, ozaki, P, Q)
+    assert np.array_equal(np.isnan(fused), np.isnan(two))
+    assert np.array_equal(np.nan_to_num(fused), np.nan_to_num(two))
+    assert np.all(np.isnan(fused[3, :])) and np.all(np.isnan(fused[:, 4]))
 
 
 def test_ozaki_gemm_deterministic(lr, ozaki):
