@@ -612,40 +612,62 @@ CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int
 constexpr int kSplitCluster = 8;
 constexpr int kSplitTilesPerCta = 4;
 template <bool UNS>
-__global__ void __cluster_dims__(kSplitCluster, 1, 1) __launch_bounds__(kSplitThreads, 2)
+__global__ void __cluster_dims__(kSplitCluster, 1, 1) __launch_bounds__(kSplitThreads, 3)
 split_fused_kernel(int64_t K, int64_t cols, const double* __restrict__ X, int64_t ldx, int beta,
                    int8_t* __restrict__ planes, int64_t ldp, int64_t plane_stride, int* __restrict__ shift) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
+  // this CTA's rows of the column, staged by cp.async: thread t's 8 rows of a
+  // tile at 64t bytes, its four 16-byte pieces XOR-swizzled by (t >> 1) & 3 so
+  // the per-thread 16-byte shared loads are conflict-free
+  extern __shared__ __align__(16) double xs[];
   __shared__ unsigned long long sh[kSplitThreads / 32];
   __shared__ unsigned long long slot[2];
   const int rank = (int)cluster.block_rank();
   const int64_t nclusters = gridDim.x / kSplitCluster;
   const int tiles_k = (int)((K + kSplitTile - 1) / kSplitTile);
   const int64_t r_off = (int64_t)kSplitRows * threadIdx.x;
+  const int swz = (threadIdx.x >> 1) & 3;
   int it = 0;
   for (int64_t j = blockIdx.x / kSplitCluster; j < cols; j += nclusters, ++it) {
     const double* xc = X + j * ldx;
-    double v[kSplitTilesPerCta][kSplitRows];
-    unsigned long long mx = 0;
 #pragma unroll
     for (int u = 0; u < kSplitTilesPerCta; ++u) {
       const int tk = rank * kSplitTilesPerCta + u;
       const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
+      double* d = xs + u * kSplitTile + r_off;
       if (tk < tiles_k && i0 + kSplitRows <= K) {
 #pragma unroll
         for (int h = 0; h < kSplitRows / 2; ++h) {
-          const double2 a = __ldcs(reinterpret_cast<const double2*>(xc + i0 + 2 * h));
-          v[u][2 * h] = a.x;
-          v[u][2 * h + 1] = a.y;
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(d + 2 * (h ^ swz));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(xc + i0 + 2 * h) : "memory");
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < kSplitRows; ++q) v[u][q] = (tk < tiles_k && i0 + q < K) ? xc[i0 + q] : 0.0;
+        for (int h = 0; h < kSplitRows / 2; ++h) {
+          const int64_t i = i0 + 2 * h;
+          d[2 * (h ^ swz)] = (tk < tiles_k && i < K) ? xc[i] : 0.0;
+          d[2 * (h ^ swz) + 1] = (tk < tiles_k && i + 1 < K) ? xc[i + 1] : 0.0;
+        }
       }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    auto tile = [&](int u, double (&v)[kSplitRows]) {
+      const double* d = xs + u * kSplitTile + r_off;
 #pragma unroll
-      for (int q = 0; q < kSplitRows; ++q)
-        mx = max(mx, (unsigned long long)__double_as_longlong(fabs(v[u][q])));
+      for (int h = 0; h < kSplitRows / 2; ++h) {
+        const double2 a = *reinterpret_cast<const double2*>(d + 2 * (h ^ swz));
+        v[2 * h] = a.x;
+        v[2 * h + 1] = a.y;
+      }
+    };
+    unsigned long long mx = 0;
+#pragma unroll
+    for (int u = 0; u < kSplitTilesPerCta; ++u) {
+      double v[kSplitRows];
+      tile(u, v);
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q) mx = max(mx, (unsigned long long)__double_as_longlong(fabs(v[q])));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -669,11 +691,15 @@ split_fused_kernel(int64_t K, int64_t cols, const double* __restrict__ X, int64_
     if (rank == 0 && threadIdx.x == 0) shift[j] = isfinite(mxd) ? sft : kOzakiNonFinite;
     const double sc1 = ldexp(1.0, sft / 2), sc2 = ldexp(1.0, sft - sft / 2);
     int8_t* colp = planes + j * ldp;
-#pragma unroll
+#pragma unroll 1
     for (int u = 0; u < kSplitTilesPerCta; ++u) {
       const int tk = rank * kSplitTilesPerCta + u;
       const int64_t i0 = (int64_t)tk * kSplitTile + r_off;
-      if (tk < tiles_k && i0 < K) split_tile<UNS>(v[u], sc1, sc2, colp + i0, plane_stride);
+      if (tk < tiles_k && i0 < K) {
+        double v[kSplitRows];
+        tile(u, v);
+        split_tile<UNS>(v, sc1, sc2, colp + i0, plane_stride);
+      }
     }
   }
   cluster.sync();  // no CTA leaves while a peer may still read its slots
@@ -706,9 +732,36 @@ void ozaki_split_into(const double* X, int64_t ldx, const OzakiOperand& op, cuda
   const bool fused_off = !(fe && fe[0] == '1');
   if (!fused_off && vec2 && K >= (int64_t)kSplitCluster * kSplitTile &&
       K <= (int64_t)kSplitCluster * kSplitTilesPerCta * kSplitTile) {
-    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(cols, 2 * num_sms() / kSplitCluster));
     auto kern = op.unsigned_res ? split_fused_kernel<true> : split_fused_kernel<false>;
-    kern<<<(int)(ncl * kSplitCluster), kSplitThreads, 0, st>>>(K, cols, X, ldx, op.beta, op.planes, op.ld,
+    constexpr int kFusedSmem = kSplitTilesPerCta * kSplitTile * (int)sizeof(double);  // 64 KB
+    static thread_local bool attr = false;
+    if (!attr) {
+      LRB_CUDA(cudaFuncSetAttribute(split_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+      LRB_CUDA(cudaFuncSetAttribute(split_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+      attr = true;
+    }
+    // persistent clusters: only as many as are co-resident (GPC packing of
+    // 8-CTA clusters leaves fewer than 3 * SMs / 8), or the excess run as a tail
+    static thread_local int max_cl = 0;
+    if (!max_cl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kSplitCluster * 64);
+      cfg.blockDim = dim3(kSplitThreads);
+      cfg.dynamicSmemBytes = kFusedSmem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kSplitCluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      LRB_CUDA(cudaOccupancyMaxActiveClusters(&max_cl, split_fused_kernel<false>, &cfg));
+      max_cl = std::max(1, max_cl);
+      if (std::getenv("LRB_WS_DEBUG")) std::fprintf(stderr, "[lrb] split_fused: %d co-resident clusters\n", max_cl);
+    }
+    const int budget_cl = g_sm_budget > 0 ? std::max(1, max_cl * g_sm_budget / kNumSMsB200) : max_cl;
+    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(cols, std::min(max_cl, budget_cl)));
+    kern<<<(int)(ncl * kSplitCluster), kSplitThreads, kFusedSmem, st>>>(K, cols, X, ldx, op.beta, op.planes, op.ld,
                                                                  op.plane_stride, op.shift);
     LRB_CHECK_LAUNCH();
     return;
