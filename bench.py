@@ -4,6 +4,7 @@
 k = 500, p = 10, U = C^+ A R^+).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c1|c2|c3|c5]
 
 One "step" = one full randomized CUR (sketch -> CPQR(Y) -> T solve -> row ID
 on C -> U = C^+ A R^+ and the tsID skeleton) with A resident in HBM
@@ -13,15 +14,24 @@ no flush is needed between steps.  Device time = CUDA events on the stream
 the library launches on, max over ranks.
 
 The two A-sized contractions run on the Ozaki-II engine by default
-(--engine ozaki: FP64 products emulated exactly on the INT8 tensor cores,
-DESIGN.md section 4); --engine dmma uses the FP64 DMMA GEMM.
+(--engine ozaki: FP64 products of inputs rounded to 54 bits per column,
+computed exactly on the INT8 tensor cores); --engine
+dmma uses the FP64 DMMA GEMM.
 
-N > 1 (torchrun): the column-sharded path by default (--mode sharded, strong
-scaling, distributed.py); --mode replicas factors one copy of A per rank.
+--gpus N without torchrun: bench.py re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous).  N > 1: the
+column-sharded path by default (--mode sharded, strong scaling,
+distributed.py); --mode replicas factors one copy of A per rank.
 
 --impl reference: the reference's CPU algorithm (the C restatement in
-oracle/, see DESIGN.md for why not oracle/_ref) on this host's cores, on a
-bounded C4-shaped sample, extrapolated stage by stage to 65536^2.
+oracle/, see DESIGN.md for why not oracle/_ref) on ALL host cores, run ONCE
+at the full configuration (C4: about 6-10 min on a 16-core host; the line
+reports steps = 1 whatever --steps asked).  C1-C3: median of 5 full runs.
+
+--workload c1|c2|c3: BASELINE configs[0..2] (deterministic column ID
+1000x800 k=50; deterministic CUR 4000x3000 k=100; randomized column ID
+20000^2 k=200 p=10), device-resident, with the measured full-size CPU
+oracle run next to them.
 """
 import argparse
 import json
@@ -83,7 +93,7 @@ def measured_traffic(cfg):
         return {}
 
 
-def kernel_rooflines(cfg, st, stages, engine):
+def kernel_rooflines(cfg, st, per_step, engine):
     """Roofline entries of the step's big kernels from their CUDA-event stage
     times (average per launch).  `traffic`: DRAM bytes per launch measured by
     ncu (profiles/r01_traffic.json) where captured."""
@@ -93,9 +103,7 @@ def kernel_rooflines(cfg, st, stages, engine):
     ell = cfg.k + OVERSAMPLE
     out = {}
     if engine == "ozaki":
-        # INT8 tensor peak: not in MEASURED_PEAKS.json; the B200 INT8/FP8 dense rate is
-        # 2x bf16, so 2 x the measured sustained cuBLAS bf16 figure (kernel timed in a long step)
-        i8 = 2.0 * peaks.get("bf16_tflops_sustained", 1393.6)
+        i8, i8_src = int8_peak(peaks)
         for name, cols, what in (("sketch_gemm", ell, "Y = Omega A"), ("ctA_gemm", cfg.k, "X^T = A^T Q_c")):
             if st.get(name):
                 ops = 16 * 2.0 * cols * cfg.m * cfg.n
@@ -103,12 +111,13 @@ def kernel_rooflines(cfg, st, stages, engine):
                 out[name] = {"kernel": f"imma_gemm_kernel + crt4_kernel ({what}, 16 INT8 residue GEMMs)",
                              "bound": "tensor", "achieved": round(ach, 1), "peak": round(i8, 1), "unit": "TOP/s",
                              "frac": round(ach / i8, 4), "traffic": traffic.get(name),
-                             "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (INT8 = 2x bf16 rate)",
+                             "peak_source": i8_src,
                              "algorithmic": f"16 moduli x 2*{cols}*m*n = {ops:.4e} int8 op per launch"}
         if st.get("ozaki_split"):
-            calls = stages["ozaki_split"]["count"]
+            # the split stage closes twice per CUR (A + Omega before the sketch, Q_c before
+            # A^T Q_c): its per-step total covers every split of the step
             b = (ozaki_split_bytes(cfg.m, cfg.n) + ozaki_split_bytes(cfg.m, ell) + ozaki_split_bytes(cfg.m, cfg.k))
-            ach = b / (stages["ozaki_split"]["ms"] / calls * 2 * 1e-3) / 1e9
+            ach = b / (per_step["ozaki_split"] * 1e-3) / 1e9
             out["ozaki_split"] = {"kernel": "colmax_kernel + split_kernel (A, Omega^T, Q_c residue planes)",
                                   "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                                   "frac": round(ach / hbm, 4), "traffic": traffic.get("ozaki_split"),
@@ -126,10 +135,18 @@ def kernel_rooflines(cfg, st, stages, engine):
         if st.get(name):
             b = cpqr_bytes(rows, cols, steps)
             ach = b / (st[name] * 1e-3) / 1e9
+            tb = traffic.get(name)
+            meas = tb / (st[name] * 1e-3) / 1e9 if tb else None
             out[name] = {"kernel": "cpqr_panel_kernel x16 + panel_update_dmma_kernel x15 (delayed-update CPQR, one "
                                    "cooperative launch per 32 steps, logical column swaps)",
                          "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(ach / hbm, 4), "traffic": traffic.get(name),
+                         "frac": round(ach / hbm, 4), "traffic": tb,
+                         "measured_bytes_gbs": round(meas, 1) if meas else None,
+                         "measured_bytes_frac": round(meas / hbm, 4) if meas else None,
+                         "measured_bytes_note": "ncu DRAM bytes of the panel form (traffic) / this stage's time: "
+                                                "the fraction of HBM the kernel actually moves; `frac` divides the "
+                                                "right-looking algorithmic count (SURVEY 8d), which the panel form "
+                                                "does not move",
                          "algorithmic": f"SURVEY 8d right-looking count sum_s 16 (rows-s)(cols-s) + 32 (cols-s) "
                                         f"= {b:.4e} B per launch (the panel form moves less: see traffic)",
                          "note": "per step ~7 us of fixed latency (argmax -> reflector broadcast -> candidate "
@@ -145,6 +162,25 @@ def read_peaks():
             return json.load(f)
     except Exception:
         return {}
+
+
+INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_int8_peak.json")
+
+
+def int8_peak(peaks):
+    """Dense INT8 tensor peak (TOP/s) for a kernel timed inside the long,
+    power-capped step: the sustained cuBLASLt IMMA figure measured on this
+    pool's B200 by tools/microbench/int8_peak.py (committed under profiles/),
+    else 2 x the driver's sustained bf16 figure (the B200 INT8 rate is 2x bf16)."""
+    try:
+        with open(INT8_PEAK_FILE) as f:
+            rec = json.load(f)
+        return float(rec["int8_tops_sustained"]), (
+            "profiles/r02_int8_peak.json: torch._int_mm (cuBLASLt IMMA) 8192^3 back to back, sustained "
+            f"(burst {rec.get('int8_tops')} TOP/s)")
+    except Exception:
+        return 2.0 * peaks.get("bf16_tflops_sustained", 1393.6), \
+            "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (INT8 = 2x bf16 rate; no measured INT8 file)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -251,38 +287,139 @@ def cpu_reference_estimate(sample=2048, threads=0, repeats=1):
                  "scale": scale, "sample": f"{m}x{n} C4-shaped (width {cfg.width}), k={k}, p={OVERSAMPLE}"}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_c4(cfg):
+    """The C4 matrix in host memory: built on the GPU with plain torch when one
+    is present (inputs.synthetic_torch: no product kernels involved), else
+    with numpy.  Input plumbing, untimed."""
+    from paper_1412_8447_b200 import inputs
+    try:
+        import torch
+        if torch.cuda.is_available():
+            a_dev = inputs.synthetic_torch(cfg, device="cuda", col_block=8192)
+            host = np.empty((cfg.m, cfg.n), order="F")
+            ht = torch.from_numpy(host)
+            for j0 in range(0, cfg.n, 4096):
+                ht[:, j0:j0 + 4096].copy_(a_dev[:, j0:j0 + 4096])
+            del a_dev, ht
+            torch.cuda.empty_cache()
+            return host, "GPU (plain torch), copied to host"
+    except Exception:
+        pass
+    return inputs.synthetic_np(cfg), "numpy"
+
+
+def oracle_workload(o, cfg, a, workload):
+    """One full CPU run of a BASELINE configuration on the oracle; returns
+    (stage seconds, outputs).  C4 goes stage by stage (tools/c4_full_oracle.py)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    if workload == "c4":
+        from c4_full_oracle import run_oracle_cur
+        out, t = run_oracle_cur(o, a, cfg.k, cfg.oversample, cfg.sketch_seed, log=lambda *_: None)
+        return t, out
+    t0 = time.perf_counter()
+    if workload == "c1":
+        piv, coeff = o.id_column(a, cfg.k)
+        out = dict(col_pivots=piv, col_coeff=coeff)
+    elif workload == "c2":
+        out = o.cur_id(a, cfg.k, u_mode=1)
+    else:
+        piv, coeff = o.randomized_id(a, cfg.k, cfg.oversample, cfg.sketch_seed)
+        out = dict(col_pivots=piv, col_coeff=coeff)
+    return {"total": time.perf_counter() - t0}, out
+
+
+WORKLOAD_TEXT = {
+    "c1": "deterministic column ID, BASELINE configs[0] (1000x800, s_j = e^-j/20, k=50)",
+    "c2": "deterministic CUR, BASELINE configs[1] (4000x3000, s_j = (j+1)^-2, k=100, U = C^+ A R^+)",
+    "c3": "randomized column ID, BASELINE configs[2] (20000^2, width 2000, s_j = e^-j/40, k=200, p=10)",
+    "c4": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, U = C^+ A R^+)",
+}
+METRIC = {
+    "c1": "time-to-ID (s), deterministic column ID 1000x800 k=50",
+    "c2": "time-to-CUR (s), deterministic CUR 4000x3000 k=100",
+    "c3": "time-to-ID (s), randomized column ID 20000^2 k=200",
+    "c4": "time-to-CUR (s), randomized CUR 65536^2 k=500",
+}
+
+
 def run_reference(args, rank, world):
+    """The reference's CPU path (oracle port) on this host, at the FULL
+    configuration.  C4 runs once (minutes); C1-C3 five times (median).  Only
+    rank 0 works under torchrun."""
     if rank != 0:
         return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+    from paper_1412_8447_b200 import inputs
+    wl = args.workload if args.workload in ("c1", "c2", "c3") else "c4"
+    cfg = inputs.CONFIGS[wl]
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_reference_estimate(args.cpu_sample, threads)
-    vals = []
-    det = None
-    for _ in range(args.steps):
-        v, det = cpu_reference_estimate(args.cpu_sample, threads)
-        vals.append(v)
-    value = float(np.median(vals))
+    o = Oracle()
+    o.set_threads(threads)
+    t0 = time.time()
+    if wl == "c4":
+        a, where = host_c4(cfg)
+    else:
+        a, where = inputs.synthetic_np(cfg), "numpy"
+    gen_s = time.time() - t0
+    runs = 1 if wl == "c4" else 5
+    totals, stages, out = [], None, None
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        stages, out = oracle_workload(o, cfg, a, wl)
+        totals.append(time.perf_counter() - t0)
+    value = float(np.median(totals))
+    det = {"stage_seconds": {s_: round(v, 3) for s_, v in stages.items()}, "run_seconds": [round(v, 3) for v in totals],
+           "cpu_model": cpu_model(), "nproc": os.cpu_count(), "threads": threads, "input": where,
+           "input_gen_s": round(gen_s, 1), "requested": {"steps": args.steps, "warmup": args.warmup}}
+    if wl == "c4":
+        from paper_1412_8447_b200 import inputs as _in
+        gold = os.path.join(ROOT, "tests", "golden", "c4_full.npz")
+        if os.path.exists(gold):
+            g = np.load(gold)
+            same_input = str(g["a_sha256"]) == _in.sha256_colblocks(a)
+            det["golden_check"] = {"same_input_sha256": same_input,
+                                   "col_pivots_equal": bool(np.array_equal(out["col_pivots"], g["col_pivots"])),
+                                   "row_pivots_equal": bool(np.array_equal(out["row_pivots"], g["row_pivots"]))}
+        # single-thread figure of the sketch (exactly linear in the column count: 1024 of the
+        # 65536 columns, x64), the reference's own build being single-threaded Eigen
+        o.set_threads(1)
+        t0 = time.perf_counter()
+        o.sketch_gaussian(np.asfortranarray(a[:, :1024]), cfg.k + cfg.oversample, cfg.sketch_seed)
+        ts = time.perf_counter() - t0
+        o.set_threads(threads)
+        det["single_thread_sketch_s"] = round(ts * cfg.n / 1024, 1)
     line = {
-        "metric": "time-to-CUR (s), randomized CUR 65536^2 k=500",
+        "metric": METRIC[wl],
         "impl": "reference",
         "value": value,
         "unit": "s",
         "n_gpus": args.gpus,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": runs,
+        "warmup": 0,
         "ms_per_step": value * 1e3,
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded U diag(s) V^T, C4 spectrum)",
-        "config": {"workload": "randomized CUR + tsID, BASELINE configs[3] (65536^2, width 1024, k=500, p=10, "
-                               "U = C^+ A R^+)", "m": M, "n": N, "k": K_RANK, "oversample": OVERSAMPLE,
-                   "u_mode": "cpinv_a_rpinv"},
+        "data": "synthetic (seeded U diag(s) V^T, BASELINE spectrum)",
+        "config": {"workload": WORKLOAD_TEXT[wl], "m": cfg.m, "n": cfg.n, "k": cfg.k,
+                   "oversample": cfg.oversample, "u_mode": "cpinv_a_rpinv" if wl in ("c2", "c4") else None},
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": det["sample"] + "; stage times extrapolated to 65536^2 "
-                                                   "(GEMM stages x(M/m)(N/n), n-linear x N/n, m-linear x M/m)"},
+                         "sample": f"the full {cfg.m}x{cfg.n} configuration, no sampling ("
+                                   f"{'one run' if runs == 1 else 'median of 5 runs'}); oracle/lowrank_oracle.c on "
+                                   f"{threads} threads of {cpu_model()}"},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "details": det,
     }
@@ -357,7 +494,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         ha = host.numpy()
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        e2e_steps = args.e2e_steps or args.steps
         hout = lr.pinned_cur_outputs(cfg.m, cfg.n, cfg.k)  # reused page-locked result buffers
         cur = lr.randomized_cur(ha, cfg.k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=hout)  # warm-up
         barrier()
@@ -393,7 +530,7 @@ def run_ours(args, rank, world, local_rank):
     total_flops = sum(fm.values())
     st = {k: v["ms"] / max(1, v["count"]) for k, v in stages.items()}
     per_step = {k: v["ms"] / args.steps for k, v in stages.items()}
-    kern = kernel_rooflines(cfg, st, stages, args.engine)
+    kern = kernel_rooflines(cfg, st, per_step, args.engine)
     # the headline roofline is the dominant kernel: the single stage launch with
     # the longest duration (the ozaki_split entry sums several split launches
     # of different operands, so its per-step share is not one kernel's)
@@ -430,7 +567,10 @@ def run_ours(args, rank, world, local_rank):
         "rel_error_fro": err / na,
         "roofline": roof,
         "roofline_secondary": secondary,
-        "stages_ms": {k: round(v, 3) for k, v in st.items()},
+        "stages_ms": {k: round(v, 3) for k, v in per_step.items()},
+        "stages_note": "per-step totals of the library's CUDA-event stage marks (each interval closes at the named "
+                       "mark); they sum to ms_per_step up to the gaps between calls",
+        "stages_ms_sum": round(sum(per_step.values()), 3),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
@@ -494,7 +634,8 @@ def run_sharded(args, rank, world, local_rank):
     # roofline of this rank's sketch contraction (its column shard)
     shard_cfg = inputs.Config(cfg.name, cfg.m, n_g, cfg.width, cfg.spectrum, cfg.k, OVERSAMPLE, cfg.pipeline)
     st_avg = {kk: v["ms"] / max(1, v["count"]) for kk, v in stages.items()}
-    roof = kernel_rooflines(shard_cfg, st_avg, stages, args.engine).get("sketch_gemm")
+    st_step = {kk: v["ms"] / args.steps for kk, v in stages.items()}
+    roof = kernel_rooflines(shard_cfg, st_avg, st_step, args.engine).get("sketch_gemm")
     if roof:
         roof = dict(roof, note=f"rank 0's column shard ({n_g} of {cfg.n} columns); the CPQRs are replicated")
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -524,7 +665,7 @@ def run_sharded(args, rank, world, local_rank):
             torch.cuda.current_stream(dev).synchronize()
 
         e2e_step()  # warm-up
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        e2e_steps = args.e2e_steps or args.steps
         barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
@@ -552,9 +693,151 @@ def run_sharded(args, rank, world, local_rank):
                    "parallelism": f"column-sharded x{world}", "l2": "A shard exceeds L2; no flush needed"},
         "fp64_tflops": round(sum(fm.values()) / (ms * 1e-3) / 1e12, 3),
         "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
-        "roofline": roof, "stages_ms": {kk: round(v, 3) for kk, v in st_avg.items()},
+        "roofline": roof, "stages_ms": {kk: round(v, 3) for kk, v in st_step.items()},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_config(args, rank, world, local_rank):
+    """BASELINE configs[0..2] on one GPU (N > 1: independent replicas), A
+    resident in HBM.  C1 (6.4 MB) and C2 (96 MB) fit in the 126 MB L2, so L2
+    is flushed (a 256 MB write) before every timed step and each step is timed
+    on its own; C3's A (3.2 GB) exceeds L2.  The CPU figure is the oracle's
+    full-size run of the same configuration (single thread, the reference's
+    own build being single-threaded Eigen; all threads in details)."""
+    import torch
+
+    import paper_1412_8447_b200 as lr
+    from paper_1412_8447_b200 import inputs
+
+    wl = args.workload
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = inputs.CONFIGS[wl]
+    ctx = lr.Context(local_rank)
+    lr.lowrank._default = ctx
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8 if args.engine == "ozaki" else ctx.GEMM_DMMA)
+    a_host = inputs.synthetic_np(cfg)
+    a = lr.empty_colmajor(cfg.m, cfg.n, dev)
+    a.copy_(torch.from_numpy(a_host))
+    sk = lr.SketchConfig(oversample=cfg.oversample, seed=cfg.sketch_seed)
+
+    def step(out=None):
+        if wl == "c1":
+            return lr.id_column_device(a, cfg.k, ctx=ctx, out=out)
+        if wl == "c2":
+            return lr.cur_id_device(a, cfg.k, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx, out=out)
+        return lr.randomized_id_device(a, cfg.k, sk, ctx=ctx, out=out)
+
+    out = None
+    for _ in range(args.warmup):
+        out = step(out)
+    torch.cuda.synchronize()
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev) if wl in ("c1", "c2") else None
+    ctx.reset_stats()
+    ctx.enable_timing(True)
+    launches0 = ctx.kernel_launches()
+    times = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1.0)  # 256 MB > L2: the step starts cold
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = step(out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = ctx.kernel_launches() - launches0
+    stages = ctx.stage_report()
+    ctx.enable_timing(False)
+    ms = float(np.mean(times))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    per_step = {kk: v["ms"] / args.steps for kk, v in stages.items()}
+    # e2e through the host API (numpy A in, factors out)
+    ts = []
+    if not args.no_e2e:
+        for _ in range(max(1, args.warmup)):
+            host_call(lr, wl, a_host, cfg, sk, ctx)
+        for _ in range(args.e2e_steps or args.steps):
+            t0 = time.perf_counter()
+            host_call(lr, wl, a_host, cfg, sk, ctx)
+            ts.append(time.perf_counter() - t0)
+    if rank != 0:
+        return
+    roof = None
+    ell = cfg.k + cfg.oversample
+    if wl == "c3" and per_step.get("sketch_gemm"):
+        if args.engine == "ozaki":
+            i8, src = int8_peak(read_peaks())
+            ops = 16 * 2.0 * ell * cfg.m * cfg.n
+            ach = ops / (per_step["sketch_gemm"] * 1e-3) / 1e12
+            roof = {"kernel": "imma_gemm_kernel + crt4_kernel (Y = Omega A, 16 INT8 residue GEMMs)", "bound": "tensor",
+                    "achieved": round(ach, 1), "peak": i8, "unit": "TOP/s", "frac": round(ach / i8, 4),
+                    "traffic": None, "peak_source": src,
+                    "algorithmic": f"16 moduli x 2*{ell}*m*n = {ops:.4e} int8 op"}
+        else:
+            fl = 2.0 * ell * cfg.m * cfg.n
+            ach = fl / (per_step["sketch_gemm"] * 1e-3) / 1e12
+            roof = {"kernel": "gemm_tn_kernel (Y = Omega A, FP64 DMMA)", "bound": "tensor", "achieved": round(ach, 2),
+                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+                    "traffic": None, "peak_source": FP64_PEAK_SOURCE, "algorithmic": f"{fl:.4e} flop"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_lib import Oracle
+        o = Oracle()
+        res = {}
+        for thr in (1, os.cpu_count() or 1):
+            o.set_threads(thr)
+            vals = []
+            for _ in range(3 if wl == "c3" else 5):
+                t0 = time.perf_counter()
+                oracle_workload(o, cfg, a_host, wl)
+                vals.append(time.perf_counter() - t0)
+            res[thr] = float(np.median(vals))
+        cpu = {"value": res[1], "unit": "s", "cores": 1, "kind": "port",
+               "sample": f"the full {cfg.m}x{cfg.n} configuration (median of {3 if wl == 'c3' else 5} runs), "
+                         f"single thread of {cpu_model()}",
+               "all_threads": {"value": res[os.cpu_count() or 1], "cores": os.cpu_count()}}
+    line = {
+        "metric": METRIC[wl], "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U diag(s) V^T, BASELINE spectrum)",
+        "config": {"workload": WORKLOAD_TEXT[wl], "m": cfg.m, "n": cfg.n, "k": cfg.k, "oversample": cfg.oversample,
+                   "l2": "flushed (256 MB write) before every step" if flush is not None else "A exceeds L2",
+                   "gemm_engine": args.engine, "parallelism": "replicas" if world > 1 else "single"},
+        "step_ms": [round(t, 4) for t in times],
+        "roofline": roof,
+        "stages_ms": {kk: round(v, 4) for kk, v in per_step.items()},
+        "e2e": {"value": float(np.mean(ts)), "unit": "s", "h2d_bytes_per_step": 8 * cfg.m * cfg.n,
+                "d2h_bytes_per_step": e2e_d2h(wl, cfg), "steps": len(ts),
+                "host_buffer": "pageable numpy A and results (host API)"} if ts else None,
+        "cpu_baseline": cpu, "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(), "lib_stats": ctx.stats(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def host_call(lr, wl, a_host, cfg, sk, ctx):
+    if wl == "c1":
+        return lr.id_column(a_host, cfg.k, ctx=ctx)
+    if wl == "c2":
+        return lr.cur_id(a_host, cfg.k, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx)
+    return lr.randomized_id(a_host, cfg.k, sk, ctx=ctx)
+
+
+def e2e_d2h(wl, cfg):
+    m, n, k = cfg.m, cfg.n, cfg.k
+    if wl in ("c1", "c3"):
+        return 8 * n + 8 * k * (n - k)
+    return 8 * (m + n) + 8 * (m * k + k * k + k * n + k * (n - k) + k * (m - k) + k * k)
 
 
 def run_sparse(args, rank, world, local_rank):
@@ -620,6 +903,36 @@ def run_sparse(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """--gpus N > 1 without torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank launch and timing plumbing only (gloo, CPU):
+    barrier, max-over-ranks timing, rank 0 prints the line.  No factorization."""
+    import torch
+    import torch.distributed as dist
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": "launcher self-test", "dry_run": True, "value": float(t.item()), "unit": "s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ranks_seen": world}),
+              flush=True)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -630,21 +943,33 @@ def main():
     p.add_argument("--n", type=int, default=N)
     p.add_argument("--k", type=int, default=K_RANK)
     p.add_argument("--cpu-sample", type=int, default=2048)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=0, help="e2e calls timed (0 = --steps)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--workload", default="c4", choices=["c4", "c5"],
-                   help="c4: dense randomized CUR 65536^2 (headline); c5: sparse CSR 200000x100000")
+    p.add_argument("--workload", default="c4", choices=["c4", "c1", "c2", "c3", "c5"],
+                   help="c4: dense randomized CUR 65536^2 (headline); c1-c3: BASELINE configs[0..2]; "
+                        "c5: sparse CSR 200000x100000")
     p.add_argument("--power", type=int, default=0,
                    help="power iterations q (sketch.hpp:148-164; BASELINE configs use q = 0)")
     p.add_argument("--engine", default="ozaki", choices=["ozaki", "dmma"],
                    help="contraction engine of the two A-sized GEMMs (lr_ctx_set_gemm_mode)")
     p.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "sharded"],
                    help="N>1: 'sharded' (column blocks of A, strong scaling) or 'replicas'")
+    p.add_argument("--dry-run", action="store_true", help="launcher self-test on CPU (gloo), no factorization")
     args = p.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_dry(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -656,6 +981,8 @@ def main():
     mode = args.mode if args.mode != "auto" else ("sharded" if world > 1 else "single")
     if args.workload == "c5":
         run_sparse(args, rank, world, local_rank)
+    elif args.workload in ("c1", "c2", "c3"):
+        run_config(args, rank, world, local_rank)
     elif mode == "sharded":
         run_sharded(args, rank, world, local_rank)
     else:

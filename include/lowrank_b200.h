@@ -3,7 +3,7 @@
  *
  * Drop-in boundary for the reference library `lowrank` (header-only C++ on
  * Eigen, /root/reference/proj/include/lowrank).  Each entry point replaces
- * the reference template cited next to it; include/lowrank/lowrank_b200.hpp
+ * the reference template cited next to it; include/lowrank_b200/lowrank.hpp
  * re-declares the reference's C++ names (namespace lowrank) on top of this
  * ABI, and INTEGRATION.md shows the bindings.
  *
@@ -172,6 +172,8 @@ int lr_pinv(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, dou
 /* id.hpp:91-105 id_column(a, k, strategy): pivots n, coeff k x (n-k) */
 int lr_id_column(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
                  lr_solve_strategy strategy, int64_t* pivots, double* coeff);
+int lr_id_column_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                   lr_solve_strategy strategy, int64_t* pivots, double* coeff);
 /* id.hpp:108-119 id_row(a, k, strategy): pivots m, coeff k x (m-k) */
 int lr_id_row(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
               lr_solve_strategy strategy, int64_t* pivots, double* coeff);

@@ -116,30 +116,98 @@ static int require_rank_in_range(int64_t k, int64_t rows, int64_t cols, const ch
   return LRO_OK;
 }
 
-/* C = A * B.  Blocked over (j, k) with OpenMP over column blocks of C; each
- * output element is summed over k in ascending order, so the result does not
- * depend on the thread count. */
-void lro_gemm_nn(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-                 const double* B, int64_t ldb, double* C, int64_t ldc) {
-  const int64_t NB = 16;
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t j0 = 0; j0 < N; j0 += NB) {
-    const int64_t j1 = j0 + NB < N ? j0 + NB : N;
-    for (int64_t j = j0; j < j1; ++j)
-      for (int64_t i = 0; i < M; ++i) C[IDX(i, j, ldc)] = 0.0;
-    const int64_t KB = 256;
-    for (int64_t k0 = 0; k0 < K; k0 += KB) {
-      const int64_t k1 = k0 + KB < K ? k0 + KB : K;
-      for (int64_t j = j0; j < j1; ++j) {
-        double* c = C + (size_t)j * ldc;
-        for (int64_t k = k0; k < k1; ++k) {
-          const double b = B[IDX(k, j, ldb)];
-          const double* a = A + (size_t)k * lda;
-          for (int64_t i = 0; i < M; ++i) c[i] += a[i] * b;
-        }
+/* C(i0.., j0..) += A(:, k0..k0+kc) B(k0..k0+kc, j0..) on an mc x nc block.
+ * Every output element is updated as c = c + a_k b_k for k ascending, one
+ * rounded product and one rounded sum per term (no FMA contraction: the
+ * file is built with -ffp-contract=off), so the result is bitwise the plain
+ * triple loop's.  Four columns x four k are kept per pass so each c value is
+ * loaded and stored once per four terms and each a value feeds four
+ * columns; the i loop vectorises (elementwise, no reordering). */
+#if defined(__x86_64__) && defined(__GNUC__) && !defined(__clang__)
+__attribute__((target_clones("avx512f", "avx2", "default")))
+#endif
+static void gemm_block(int64_t mc, int64_t nc, int64_t kc, const double* restrict A, int64_t lda,
+                       const double* restrict B, int64_t ldb, double* restrict C, int64_t ldc) {
+  int64_t j = 0;
+  for (; j + 4 <= nc; j += 4) {
+    double* restrict c0 = C + (size_t)j * ldc;
+    double* restrict c1 = c0 + ldc;
+    double* restrict c2 = c1 + ldc;
+    double* restrict c3 = c2 + ldc;
+    const double* b0 = B + (size_t)j * ldb;
+    const double* b1 = b0 + ldb;
+    const double* b2 = b1 + ldb;
+    const double* b3 = b2 + ldb;
+    int64_t k = 0;
+    for (; k + 4 <= kc; k += 4) {
+      const double* a0 = A + (size_t)k * lda;
+      const double* a1 = a0 + lda;
+      const double* a2 = a1 + lda;
+      const double* a3 = a2 + lda;
+      const double x00 = b0[k], x01 = b0[k + 1], x02 = b0[k + 2], x03 = b0[k + 3];
+      const double x10 = b1[k], x11 = b1[k + 1], x12 = b1[k + 2], x13 = b1[k + 3];
+      const double x20 = b2[k], x21 = b2[k + 1], x22 = b2[k + 2], x23 = b2[k + 3];
+      const double x30 = b3[k], x31 = b3[k + 1], x32 = b3[k + 2], x33 = b3[k + 3];
+      for (int64_t i = 0; i < mc; ++i) {
+        const double p0 = a0[i], p1 = a1[i], p2 = a2[i], p3 = a3[i];
+        c0[i] = (((c0[i] + p0 * x00) + p1 * x01) + p2 * x02) + p3 * x03;
+        c1[i] = (((c1[i] + p0 * x10) + p1 * x11) + p2 * x12) + p3 * x13;
+        c2[i] = (((c2[i] + p0 * x20) + p1 * x21) + p2 * x22) + p3 * x23;
+        c3[i] = (((c3[i] + p0 * x30) + p1 * x31) + p2 * x32) + p3 * x33;
+      }
+    }
+    for (; k < kc; ++k) {
+      const double* a0 = A + (size_t)k * lda;
+      const double x0 = b0[k], x1 = b1[k], x2 = b2[k], x3 = b3[k];
+      for (int64_t i = 0; i < mc; ++i) {
+        const double p = a0[i];
+        c0[i] += p * x0;
+        c1[i] += p * x1;
+        c2[i] += p * x2;
+        c3[i] += p * x3;
       }
     }
   }
+  for (; j < nc; ++j) {
+    double* restrict c = C + (size_t)j * ldc;
+    const double* b = B + (size_t)j * ldb;
+    int64_t k = 0;
+    for (; k + 4 <= kc; k += 4) {
+      const double* a0 = A + (size_t)k * lda;
+      const double* a1 = a0 + lda;
+      const double* a2 = a1 + lda;
+      const double* a3 = a2 + lda;
+      const double x0 = b[k], x1 = b[k + 1], x2 = b[k + 2], x3 = b[k + 3];
+      for (int64_t i = 0; i < mc; ++i) c[i] = (((c[i] + a0[i] * x0) + a1[i] * x1) + a2[i] * x2) + a3[i] * x3;
+    }
+    for (; k < kc; ++k) {
+      const double* a0 = A + (size_t)k * lda;
+      const double x = b[k];
+      for (int64_t i = 0; i < mc; ++i) c[i] += a0[i] * x;
+    }
+  }
+}
+
+/* C = A * B.  OpenMP over (row block, column block) tiles of C; each output
+ * element is summed over k in ascending order from zero (gemm_block), so the
+ * result does not depend on the thread count or the blocking. */
+void lro_gemm_nn(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int64_t NB = 16, MB = 512, KB = 256;
+  const int64_t nj = (N + NB - 1) / NB, ni = (M + MB - 1) / MB;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t jb = 0; jb < nj; ++jb)
+    for (int64_t ib = 0; ib < ni; ++ib) {
+      const int64_t j0 = jb * NB, j1 = j0 + NB < N ? j0 + NB : N;
+      const int64_t i0 = ib * MB, i1 = i0 + MB < M ? i0 + MB : M;
+      for (int64_t j = j0; j < j1; ++j)
+        for (int64_t i = i0; i < i1; ++i) C[IDX(i, j, ldc)] = 0.0;
+      for (int64_t k0 = 0; k0 < K; k0 += KB) {
+        const int64_t k1 = k0 + KB < K ? k0 + KB : K;
+        gemm_block(i1 - i0, j1 - j0, k1 - k0, A + IDX(i0, k0, lda), lda, B + IDX(k0, j0, ldb), ldb,
+                   C + IDX(i0, j0, ldc), ldc);
+      }
+    }
 }
 
 /* C = A^T * B  (A is K x M) */
@@ -1042,20 +1110,45 @@ int lro_cur_error_fro(int64_t m, int64_t n, const double* a, int64_t lda, int64_
                       const double* u, const double* r, double* out) {
   double* cu = NEW(double, m * k);
   lro_gemm_nn(m, k, k, c, m, u, k, cu, m);
-  double err2 = 0.0, a2 = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : err2, a2)
-  for (int64_t j = 0; j < n; ++j) {
-    for (int64_t i = 0; i < m; ++i) {
-      double acc = 0.0;
-      for (int64_t l = 0; l < k; ++l) acc += cu[IDX(i, l, m)] * r[IDX(l, j, k)];
-      const double x = a[IDX(i, j, lda)];
-      const double d = x - acc;
-      err2 += d * d;
-      a2 += x * x;
+  /* (C U) R one 16-column block at a time (each entry summed over l
+   * ascending, as gemm_block does); per-block partial sums are added in
+   * block order, so the result does not depend on the thread count */
+  const int64_t NB = 16, MB = 512, KB = 256;
+  const int64_t nb = (n + NB - 1) / NB;
+  double* part = NEW(double, 2 * nb);
+#pragma omp parallel
+  {
+    double* p = NEW(double, MB * NB);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t j0 = b * NB, nc = j0 + NB < n ? NB : n - j0;
+      double e2 = 0.0, x2 = 0.0;
+      for (int64_t i0 = 0; i0 < m; i0 += MB) {
+        const int64_t mc = i0 + MB < m ? MB : m - i0;
+        for (int64_t t = 0; t < MB * NB; ++t) p[t] = 0.0;
+        for (int64_t l0 = 0; l0 < k; l0 += KB)
+          gemm_block(mc, nc, l0 + KB < k ? KB : k - l0, cu + IDX(i0, l0, m), m, r + IDX(l0, j0, k), k, p, MB);
+        for (int64_t j = 0; j < nc; ++j)
+          for (int64_t i = 0; i < mc; ++i) {
+            const double x = a[IDX(i0 + i, j0 + j, lda)];
+            const double d = x - p[IDX(i, j, MB)];
+            e2 += d * d;
+            x2 += x * x;
+          }
+      }
+      part[2 * b] = e2;
+      part[2 * b + 1] = x2;
     }
+    free(p);
+  }
+  double err2 = 0.0, a2 = 0.0;
+  for (int64_t b = 0; b < nb; ++b) {
+    err2 += part[2 * b];
+    a2 += part[2 * b + 1];
   }
   out[0] = sqrt(err2);
   out[1] = sqrt(a2);
+  free(part);
   free(cu);
   return LRO_OK;
 }

@@ -82,6 +82,8 @@ SIGNATURES = {
     "lr_pinv": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, ctypes.c_double, c_dp], ctypes.c_int),
     "lr_id_column": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
                      ctypes.c_int),
+    "lr_id_column_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
+                       ctypes.c_int),
     "lr_id_row": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_solve_strategy, c_ip, c_dp],
                   ctypes.c_int),
     "lr_randomized_id": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, lr_sketch_config,

@@ -317,7 +317,12 @@ struct OzakiScope {
   lr_ctx* c;
   explicit OzakiScope(lr_ctx* cc) : c(cc) { c->oz_cache_on = true; }
   ~OzakiScope() {
-    if (c->oz_pinned) return;  // a pinned operand's planes stay valid across calls
+    if (c->oz_pinned) {  // a pinned operand's planes stay valid across calls; any other
+      // matrix split during this call (e.g. a CUR input that is not the pinned one,
+      // or upload_sketch's call-local copy) must not be matched by address later
+      if (c->oz_src != c->pin_src) c->oz_src = nullptr;
+      return;
+    }
     c->oz_cache_on = false;
     c->oz_src = nullptr;  // the planes stay allocated in the workspace for the next call
   }
@@ -429,25 +434,52 @@ void solve_core(lr_ctx* c, int64_t k, int64_t nc, const double* s11, int64_t ld1
     return;
   }
   // Tikhonov (solve.hpp:133-142): (S11^T S11 + ridge^2 I) T = S11^T S12, solved
-  // by Cholesky on the GPU (the reference runs CG to 1e-28 relative residual).
+  // by Cholesky on the GPU; when the normal matrix is singular (ridge = 0 and a
+  // rank-deficient S11) the Cholesky breaks down and the reference's own
+  // method runs instead: conjugate gradients per column to 1e-28 relative
+  // residual, leaving on a non-positive curvature (solve.hpp:37-57).
   DBuf<double> s((size_t)k * k, c->st), rhs((size_t)k * nc, c->st);
   copy_upper(k, s11, ld11, s, k, c->st);
-  DBuf<double> eye((size_t)k * k, c->st);
+  DBuf<double> nm((size_t)k * k, c->st), eye((size_t)k * k, c->st);
   {
     std::vector<double> he((size_t)k * k, 0.0);
     for (int64_t i = 0; i < k; ++i) he[i + i * k] = strat.ridge * strat.ridge;
-    LRB_CUDA(cudaMemcpyAsync(eye.p, he.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, c->st));
+    LRB_CUDA(cudaMemcpyAsync(nm.p, he.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, c->st));
     sync(c);
   }
-  gemm(c, k, k, k, s, k, s, k, eye, k, 1.0, 1.0);  // eye = S^T S + ridge^2 I
-  gemm(c, k, nc, k, s, k, s12, ld12, rhs, k);      // rhs = S^T S12
+  gemm(c, k, k, k, s, k, s, k, nm, k, 1.0, 1.0);  // nm = S^T S + ridge^2 I
+  gemm(c, k, nc, k, s, k, s12, ld12, rhs, k);     // rhs = S^T S12
+  copy_matrix(k, k, nm, k, eye, k, c->st);
   DBuf<int> info(1, c->st);
   cholesky_upper(c->ws, k, eye, k, info, c->st);
-  DBuf<double> ri((size_t)k * k, c->st), rit((size_t)k * k, c->st), y((size_t)k * nc, c->st);
-  tri_upper_inverse(k, eye, k, ri, k, c->st);
-  transpose_matrix(k, k, ri, k, rit, k, c->st);
-  gemm(c, k, nc, k, ri, k, rhs, k, y, k);     // y = R^-T rhs
-  gemm(c, k, nc, k, rit, k, y, k, t, ldt);    // t = R^-1 y
+  d2h_mapped(c, c->h_flags, info.p, sizeof(int));
+  sync(c);
+  if (c->h_flags[0] == 0) {
+    DBuf<double> ri((size_t)k * k, c->st), rit((size_t)k * k, c->st), y((size_t)k * nc, c->st);
+    tri_upper_inverse(k, eye, k, ri, k, c->st);
+    transpose_matrix(k, k, ri, k, rit, k, c->st);
+    gemm(c, k, nc, k, ri, k, rhs, k, y, k);     // y = R^-T rhs
+    gemm(c, k, nc, k, rit, k, y, k, t, ldt);    // t = R^-1 y
+    return;
+  }
+  const int64_t ldk = even(k);
+  DBuf<double> nme((size_t)ldk * k, c->st), x((size_t)ldk * nc, c->st), r((size_t)ldk * nc, c->st),
+      d((size_t)ldk * nc, c->st), nd((size_t)ldk * nc, c->st), state((size_t)3 * nc, c->st);
+  DBuf<int> act(1, c->st);
+  copy_matrix(k, k, nm, k, nme, ldk, c->st);
+  cg_init(k, nc, ldk, rhs, k, x, r, d, state, c->st);
+  const int64_t max_iters = 8 * k + 16;
+  for (int64_t it = 0; it < max_iters; ++it) {
+    gemm(c, k, nc, k, nme, ldk, d, ldk, nd, ldk);  // nd = normal d (normal symmetric)
+    LRB_CUDA(cudaMemsetAsync(act.p, 0, sizeof(int), c->st));
+    cg_step(k, nc, ldk, nd, x, r, d, state, act, c->st);
+    if ((it & 7) == 7 || it + 1 == max_iters) {
+      d2h_mapped(c, c->h_flags, act.p, sizeof(int));
+      sync(c);
+      if (c->h_flags[0] == 0) break;
+    }
+  }
+  copy_matrix(k, nc, x, ldk, t, ldt, c->st);
 }
 
 // ---------------------------------------------------------------- SVD / pinv
@@ -494,11 +526,18 @@ void pinv_svd_path(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda
   gemm(c, n, m, rank, P, even(rank), Q, even(rank), out, ldo);
 }
 
+// Largest ||R||_F ||R^-1||_F for which a pseudoinverse with relative cutoff
+// thr (svd.hpp:193-207: keep sigma_i >= thr sigma_1) provably truncates
+// nothing: ||R||_F >= sigma_1 and ||R^-1||_F >= 1/sigma_min, so a bound below
+// 1/thr gives sigma_min > thr sigma_1.  1e7 caps it for the CholeskyQR2
+// accuracy argument (cond^2 eps of the first Gram matrix well below 1).
+double fast_cond_limit(double thr) { return std::min(1e7, 1.0 / thr); }
+
 // CholeskyQR2 of a tall X (rows x k, ld) given also X^T (k x rows, ldt):
 // R (k x k upper) with X = Q R, Rinv = R^-1.  Returns false when the Gram
-// factorisation breaks down or cond bound ||R||_F ||R^-1||_F > 1e7.
+// factorisation breaks down or cond bound ||R||_F ||R^-1||_F >= max_cond.
 bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, const double* Xt, int64_t ldxt,
-             double* R, double* Rinv) {
+             double* R, double* Rinv, double max_cond = 1e7) {
   DBuf<double> G((size_t)k * k, c->st), R1inv((size_t)k * k, c->st), Q1((size_t)even(rows) * k, c->st);
   DBuf<int> info(2, c->st);
   gemm(c, k, k, rows, X, ldx, X, ldx, G, k, 1.0, 0.0, -1, true);  // G1 = X^T X (upper tiles)
@@ -524,7 +563,7 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   d2h_mapped(c, c->h_scal, f.p, 2 * sizeof(double));
   sync(c);
   const double cond_bound = std::sqrt(c->h_scal[0]) * std::sqrt(c->h_scal[1]);
-  return std::isfinite(cond_bound) && cond_bound < 1e7;
+  return std::isfinite(cond_bound) && cond_bound < max_cond;
 }
 
 void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out, int64_t ldo) {
@@ -544,7 +583,7 @@ void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, do
       copy_matrix(m, n, a, lda, Xt, even(k), c->st);
     }
     DBuf<double> R((size_t)k * k, c->st), Ri((size_t)k * k, c->st);
-    if (cholqr2(c, rows, k, X, even(rows), Xt, even(k), R, Ri)) {
+    if (cholqr2(c, rows, k, X, even(rows), Xt, even(k), R, Ri, fast_cond_limit(thr))) {
       // X^+ = R^-1 R^-T X^T (k x rows).  Qt = R^-T X^T: Qt(l,j) = sum_t Ri(t,l) Xt(t,j)
       DBuf<double> Qt((size_t)even(k) * rows, c->st), Rit((size_t)k * k, c->st);
       gemm(c, k, rows, k, Ri, k, Xt, even(k), Qt, even(k));
@@ -825,7 +864,7 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
   copy_matrix(k, n, R, k, Rk, ldk, c->st);  // R with an even leading dimension for TMA
   DBuf<double> Sr((size_t)k * k, c->st), Sri((size_t)k * k, c->st);
   mark(c, "gather_r");
-  const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
+  const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
   mark(c, "cholqr2_r");
   c->stats.pinv_fast_path = 0;
   c->stats.concurrent_tail = 0;
@@ -833,7 +872,7 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
     DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st);
     DBuf<double> Cm((size_t)even(m) * k, c->st);
     copy_matrix(m, k, C, m, Cm, even(m), c->st);
-    const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci);
+    const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci, fast_cond_limit(thr));
     mark(c, "cholqr2_c");
     if (c_ok && r_ok) {
       c->stats.pinv_fast_path = 1;
@@ -1042,7 +1081,7 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
   mark(c, "gather_c");
   DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st), Cm((size_t)even(m) * k, c->st);
   copy_matrix(m, k, C, m, Cm, even(m), c->st);
-  const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci);
+  const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci, fast_cond_limit(thr));
   mark(c, "cholqr2_c");
   DBuf<double> Qc((size_t)even(m) * k, c->st), Xt((size_t)even(n) * k, c->st);
   DBuf<double> tau(k, c->st), Rt((size_t)even(n) * k, c->st), Rk((size_t)ldk * n, c->st);
@@ -1050,6 +1089,28 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
   cudaEvent_t fork = record_event(c->st);
   cudaEvent_t done2 = nullptr, done1 = nullptr;
   const auto& sp = c->split;
+  // Declared after the buffers, so it runs first when chain 1 throws (e.g. a
+  // SingularityError from its coefficient solve): the main stream waits for
+  // both partition streams before any buffer above is released in its order.
+  struct JoinChains {
+    cudaStream_t main, s1, s2;
+    cudaEvent_t* ev[3];
+    ~JoinChains() {
+      for (cudaStream_t s : {s1, s2}) {
+        if (!s || s == main) continue;
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) continue;
+        cudaEventRecord(e, s);
+        cudaStreamWaitEvent(main, e, 0);
+        cudaEventDestroy(e);
+      }
+      for (cudaEvent_t* e : ev)
+        if (*e) {
+          cudaEventDestroy(*e);
+          *e = nullptr;
+        }
+    }
+  } join{c->st, sp.s1, sp.s2, {&fork, &done1, &done2}};
   if (c_ok) {  // chain 2 first: it has no host synchronisation, so it is fully enqueued before chain 1 blocks
     OnPartition on(c, sp.s2, sp.n2, fork);
     gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m), 1.0, 0.0, -1, false, kTriQ);         // Qc = C Rc^-1
@@ -1067,14 +1128,12 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
     on_r();
     transpose_matrix(k, n, R, k, Rt, even(n), c->st);
     copy_matrix(k, n, R, k, Rk, ldk, c->st);
-    r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri);
+    r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
     if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n), 1.0, 0.0, -1, false, kTriQ);  // Qr = R^T Sr^-1
     done1 = record_event(c->st);
   }
   LRB_CUDA(cudaStreamWaitEvent(c->st, done1, 0));
   if (done2) LRB_CUDA(cudaStreamWaitEvent(c->st, done2, 0));
-  for (cudaEvent_t e : {fork, done1, done2})
-    if (e) cudaEventDestroy(e);
   mark(c, "tsid_ctA_split");
   if (!(c_ok && r_ok)) {  // rare: the general U path, sequentially
     u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, LR_U_CPINV_A_RPINV, U, Ct,
@@ -1714,6 +1773,14 @@ int lr_id_column(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, 
     sync(c);
   });
 }
+int lr_id_column_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                   lr_solve_strategy strat, int64_t* pivots, double* coeff) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "id_column");
+    id_column_core(c, m, n, a, lda, k, strat, pivots, coeff, k);
+  });
+}
 int lr_id_row(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, lr_solve_strategy strat,
               int64_t* pivots, double* coeff) {
   return guard([&] {
@@ -2138,8 +2205,11 @@ int lr_id_from_sample_d(lr_ctx* c, int64_t ell, int64_t n, const double* y, int6
     DBuf<double> W((size_t)lw * n, c->st), tau(steps, c->st);
     zero_pad_rows(c, W, ell, lw, n);
     copy_matrix(ell, n, y, ldy, W, lw, c->st);
+    mark(c, "sample_exchange");  // since the previous stage: the caller's all-gather of Y (sharded protocol)
     cpqr_core(c, ell, n, W, lw, steps, pivots, tau, "cpqr_partial", work_padded(ell, lw));
+    mark(c, "cpqr_sample");
     solve_core(c, k, n - k, W, lw, W.p + k * lw, lw, strat, coeff, k, false);
+    mark(c, "coeff_solve_col");
   });
 }
 

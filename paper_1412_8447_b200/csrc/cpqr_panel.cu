@@ -308,7 +308,7 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
       if (need) {
         nr = qq;
         nx = qq;
-        ++x.recomputes;
+        if (l == 0) ++x.recomputes;  // one count per column (its group leader)
       }
     }
     if (cb.ok) {
@@ -725,7 +725,9 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     a.trace[cta * 8 + 6] += clock64() - ck0;
     a.trace[cta * 8 + 7] += gtimer() - tk0;
   }
-  if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
+  // every group leader of the warp holds its columns' count
+  const unsigned int wcount = __reduce_add_sync(0xffffffffu, (unsigned int)my_recomputes);
+  if (lane == 0 && wcount) atomicAdd(a.recomputes, (unsigned long long)wcount);
 }
 
 // Panel update on the DMMA pipe: W(r0:r1, :) -= V(r0:r1, 0:nc) F(:, 0:nc)^T as

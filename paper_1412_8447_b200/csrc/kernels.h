@@ -150,6 +150,12 @@ void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld1
                            cudaStream_t st);
 // Cholesky G = R^T R (upper R, k x k, in place on a copy); info[0] = first failing column+1 or 0
 void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st);
+// batched conjugate gradients (solve.hpp:37-57), one column per warp; x, r, d
+// k x nc with leading dimension ld, state 3 doubles per column (rho, stop, active)
+void cg_init(int64_t k, int64_t nc, int64_t ld, const double* rhs, int64_t ldr, double* x, double* r, double* d, double* state,
+             cudaStream_t st);
+void cg_step(int64_t k, int64_t nc, int64_t ld, const double* nd, double* x, double* r, double* d, double* state, int* n_active,
+             cudaStream_t st);
 // inverse of an upper-triangular R (k x k) -> Rinv (upper)
 void tri_upper_inverse(int64_t k, const double* r, int64_t ldr, double* rinv, int64_t ldi, cudaStream_t st);
 // same for a nonzero diagonal (no singular-row handling), blocked: CholeskyQR factors

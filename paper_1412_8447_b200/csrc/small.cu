@@ -468,6 +468,87 @@ void backsub_residual_rows(int64_t k, int64_t nc, const double* s11, int64_t ld1
   LRB_CUDA(cudaFreeAsync(partial, st));
 }
 
+// ---------------------------------------------------------------- batched CG
+// solve.hpp:37-57 (detail::conjugate_gradient) for every column j of the
+// right-hand side at once: one warp per column keeps its x, r, d (k entries,
+// ld k) and (rho, stop, active); the k x k products normal * D of all
+// columns are one GEMM between iterations.  Column semantics as the
+// reference: x = 0, r = d = rhs, stop = 1e-28 ||rhs||^2, iterate while
+// it < max_iters and rho > stop, leave on denom = d.(normal d) <= 0.
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void cg_init_kernel(int64_t k, int64_t nc, int64_t ld, const double* __restrict__ rhs, int64_t ldr,
+                               double* __restrict__ x, double* __restrict__ r, double* __restrict__ d,
+                               double* __restrict__ st) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= nc) return;
+  double acc = 0.0;
+  for (int64_t i = lane; i < k; i += 32) {
+    const double b = rhs[j * ldr + i];
+    x[j * ld + i] = 0.0;
+    r[j * ld + i] = b;
+    d[j * ld + i] = b;
+    acc += b * b;
+  }
+  acc = warp_sum_d(acc);
+  if (lane == 0) {
+    st[3 * j] = acc;              // rho
+    st[3 * j + 1] = 1e-28 * acc;  // stop
+    st[3 * j + 2] = acc > 1e-28 * acc ? 1.0 : 0.0;
+  }
+}
+
+__global__ void cg_step_kernel(int64_t k, int64_t nc, int64_t ld, const double* __restrict__ nd, double* __restrict__ x,
+                               double* __restrict__ r, double* __restrict__ d, double* __restrict__ st,
+                               int* __restrict__ n_active) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= nc || st[3 * j + 2] == 0.0) return;
+  double den = 0.0;
+  for (int64_t i = lane; i < k; i += 32) den += d[j * ld + i] * nd[j * ld + i];
+  den = warp_sum_d(den);
+  if (den <= 0.0) {
+    if (lane == 0) st[3 * j + 2] = 0.0;
+    return;
+  }
+  const double rho = st[3 * j], alpha = rho / den;
+  double rn = 0.0;
+  for (int64_t i = lane; i < k; i += 32) {
+    x[j * ld + i] += alpha * d[j * ld + i];
+    const double ri = r[j * ld + i] - alpha * nd[j * ld + i];
+    r[j * ld + i] = ri;
+    rn += ri * ri;
+  }
+  rn = warp_sum_d(rn);
+  const double beta = rn / rho;
+  for (int64_t i = lane; i < k; i += 32) d[j * ld + i] = r[j * ld + i] + beta * d[j * ld + i];
+  if (lane == 0) {
+    st[3 * j] = rn;
+    const bool act = rn > st[3 * j + 1];
+    st[3 * j + 2] = act ? 1.0 : 0.0;
+    if (act) atomicAdd(n_active, 1);
+  }
+}
+
+void cg_init(int64_t k, int64_t nc, int64_t ld, const double* rhs, int64_t ldr, double* x, double* r, double* d, double* state,
+             cudaStream_t st) {
+  const int64_t g = (nc * 32 + 255) / 256;
+  cg_init_kernel<<<(unsigned)g, 256, 0, st>>>(k, nc, ld, rhs, ldr, x, r, d, state);
+  LRB_CHECK_LAUNCH();
+}
+
+void cg_step(int64_t k, int64_t nc, int64_t ld, const double* nd, double* x, double* r, double* d, double* state, int* n_active,
+             cudaStream_t st) {
+  const int64_t g = (nc * 32 + 255) / 256;
+  cg_step_kernel<<<(unsigned)g, 256, 0, st>>>(k, nc, ld, nd, x, r, d, state, n_active);
+  LRB_CHECK_LAUNCH();
+}
+
 void cholesky_upper(Workspace& ws, int64_t k, double* g, int64_t ldg, int* info, cudaStream_t st) {
   if (k <= 2 * kCholB || (ldg & 1) || (reinterpret_cast<uintptr_t>(g) & 15)) {
     cholesky_upper_kernel<<<1, 1024, 0, st>>>(k, g, ldg, info);

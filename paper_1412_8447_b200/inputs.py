@@ -100,27 +100,55 @@ def synthetic_np(cfg: Config) -> np.ndarray:
     return np.asfortranarray((u * cfg.singular_values()) @ v.T)
 
 
+def _i64(c: int) -> int:
+    """uint64 constant -> the int64 with the same bits (torch has no uint64 math)."""
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def gaussian_torch(rows: int, cols: int, seed: int, device="cuda", chunk: int = 1 << 24):
+    """rng.hpp:74-94 in plain torch int64 arithmetic (wrapping multiply,
+    logical shifts by masking), column-major rows x cols.  INPUT plumbing
+    only: it does not call the product library, so the reference arm of
+    bench.py can build the same A without touching our kernels.  The integer
+    stream is exact; torch's log/cos/sin may differ from glibc by an ulp."""
+    import torch
+    g, m1, m2 = _i64(int(GOLDEN)), _i64(int(M1)), _i64(int(M2))
+
+    def lsr(z, s):
+        return (z >> s) & ((1 << (64 - s)) - 1)
+
+    def stream(idx):
+        z = (idx + 1) * g + _i64(seed & 0xFFFFFFFFFFFFFFFF)
+        z = (z ^ lsr(z, 30)) * m1
+        z = (z ^ lsr(z, 27)) * m2
+        return z ^ lsr(z, 31)
+
+    total = rows * cols
+    flat = torch.empty(total + (total & 1), dtype=torch.float64, device=device)
+    for p0 in range(0, total, 2 * chunk):
+        pairs = torch.arange(p0, min(total, p0 + 2 * chunk), 2, dtype=torch.int64, device=device)
+        u1 = (lsr(stream(pairs), 11) + 1).to(torch.float64) * 2.0 ** -53
+        u2 = lsr(stream(pairs + 1), 11).to(torch.float64) * 2.0 ** -53
+        r = torch.sqrt(-2.0 * torch.log(u1))
+        ang = (2.0 * math.pi) * u2
+        flat[p0:p0 + 2 * pairs.numel():2] = r * torch.cos(ang)
+        flat[p0 + 1:p0 + 2 * pairs.numel():2] = r * torch.sin(ang)
+    # stream index i*cols + j is entry (i, j): row-major stream, column-major storage
+    return flat[:total].view(rows, cols).t().contiguous().t()
+
+
 def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None, col_range=None):
     """A = U diag(s) V^T generated on the GPU, column-major (input plumbing:
-    torch QR / matmul build the input, the product path never uses them).
-    col_range=(lo, width) builds only the column block A(:, lo:lo+width)."""
+    plain torch -- the counter-stream Gaussian above, QR and matmul; the
+    product library is not involved).  col_range=(lo, width) builds only the
+    column block A(:, lo:lo+width)."""
     import torch
 
-    from .lowrank import default_context, empty_colmajor, on_torch_stream
-
-    ctx = default_context()
-    lib = ctx.lib
-
-    def gauss(rows, cols, seed):
-        g = empty_colmajor(rows, cols, device)
-        with on_torch_stream(ctx):  # g may reuse memory torch's stream is still reading
-            rc = lib.lr_gaussian_matrix_d(ctx.h, rows, cols, seed, g.data_ptr(), rows)
-        if rc != 0:
-            raise RuntimeError(lib.lr_last_error().decode())
-        return g
+    def empty_colmajor(rows, cols, dev):
+        return torch.empty((cols, rows), dtype=torch.float64, device=dev).t()
 
     def haar(rows, cols, seed):
-        q, r = torch.linalg.qr(gauss(rows, cols, seed))
+        q, r = torch.linalg.qr(gaussian_torch(rows, cols, seed, device))
         return q * torch.sign(torch.diagonal(r))
 
     u = haar(cfg.m, cfg.width, derive_seed(cfg.seed, 1))
@@ -133,12 +161,30 @@ def synthetic_torch(cfg: Config, device="cuda", col_block: int | None = None, co
     for j0 in range(0, width, step):
         j1 = min(width, j0 + step)
         a[:, j0:j1] = us @ v[lo + j0:lo + j1].T
-    torch.cuda.synchronize()
+    if a.is_cuda:
+        torch.cuda.synchronize()
     return a
 
 
 def sha256(a: np.ndarray) -> str:
     return hashlib.sha256(np.asfortranarray(a).tobytes(order="F")).hexdigest()
+
+
+def sha256_colblocks(a: np.ndarray, block: int = 1024, threads: int = 16) -> str:
+    """SHA-256 over the SHA-256 digests of consecutive column blocks of a
+    column-major array (blocks hashed in parallel threads: hashlib releases
+    the GIL), so a 34 GB matrix hashes in seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+    if not a.flags.f_contiguous:
+        raise ValueError("sha256_colblocks: column-major (Fortran-ordered) array expected")
+    n = a.shape[1]
+
+    def one(j0):
+        return hashlib.sha256(memoryview(a[:, j0:min(n, j0 + block)].T.reshape(-1))).digest()
+
+    with ThreadPoolExecutor(threads) as ex:
+        digests = list(ex.map(one, range(0, n, block)))
+    return hashlib.sha256(b"".join(digests)).hexdigest()
 
 
 def synthetic_csr_torch(m: int, n: int, nnz_per_col: int, seed: int = 1412, device="cuda"):

@@ -28,6 +28,7 @@ __all__ = [
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
     "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
+    "id_column_device", "randomized_id_device", "cur_id_device",
 ]
 
 LowrankCudaError = L.LowrankCudaError
@@ -721,6 +722,63 @@ def randomized_cur_device(a, k: int, cfg: Optional[SketchConfig] = None, strateg
     with on_torch_stream(c):
         _raise(c.lib.lr_randomized_cur_d(
             c.h, m, n, _dptr(a), lda, k, (cfg or SketchConfig())._c(), (strategy or SolveStrategy.automatic())._c(),
+            float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]), _dptr(out["row_pivots"]), _dptr(out["c"]),
+            _dptr(out["u"]), _dptr(out["r"]), _dptr(out["col_coeff"]), _dptr(out["row_coeff"]),
+            _dptr(out["skeleton"])))
+    return out
+
+
+def id_column_device(a, k: int, strategy: Optional[SolveStrategy] = None, ctx: Optional[Context] = None,
+                     out: Optional[dict] = None) -> dict:
+    """lr_id_column_d (id.hpp:91-105) on a device-resident column-major tensor."""
+    import torch
+    c = _ctx(ctx)
+    m, n = a.shape
+    if out is None:
+        out = {"pivots": torch.empty(n, dtype=torch.int64, device=a.device),
+               "coeff": empty_colmajor(k, max(n - k, 1), a.device)}
+    with on_torch_stream(c):
+        _raise(c.lib.lr_id_column_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k,
+                                    (strategy or SolveStrategy.automatic())._c(), _dptr(out["pivots"]),
+                                    _dptr(out["coeff"])))
+    return out
+
+
+def randomized_id_device(a, k: int, cfg: Optional[SketchConfig] = None, strategy: Optional[SolveStrategy] = None,
+                         ctx: Optional[Context] = None, out: Optional[dict] = None) -> dict:
+    """lr_randomized_id_d (sketch.hpp:200-223) on a device-resident column-major tensor."""
+    import torch
+    c = _ctx(ctx)
+    m, n = a.shape
+    if out is None:
+        out = {"pivots": torch.empty(n, dtype=torch.int64, device=a.device),
+               "coeff": empty_colmajor(k, max(n - k, 1), a.device)}
+    with on_torch_stream(c):
+        _raise(c.lib.lr_randomized_id_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, (cfg or SketchConfig())._c(),
+                                        (strategy or SolveStrategy.automatic())._c(), _dptr(out["pivots"]),
+                                        _dptr(out["coeff"])))
+    return out
+
+
+def cur_id_device(a, k: int, strategy: Optional[SolveStrategy] = None, pinv_threshold: float = 1e-12,
+                  u_mode: int = U_VT_RPINV, ctx: Optional[Context] = None, out: Optional[dict] = None) -> dict:
+    """lr_cur_id_d (cur.hpp:36-42; U = C^+ A R^+ with U_CPINV_A_RPINV) on a
+    device-resident column-major tensor."""
+    import torch
+    c = _ctx(ctx)
+    m, n = a.shape
+    dev = a.device
+    if out is None:
+        out = {
+            "col_pivots": torch.empty(n, dtype=torch.int64, device=dev),
+            "row_pivots": torch.empty(m, dtype=torch.int64, device=dev),
+            "c": empty_colmajor(m, k, dev), "u": empty_colmajor(k, k, dev), "r": empty_colmajor(k, n, dev),
+            "col_coeff": empty_colmajor(k, max(n - k, 1), dev), "row_coeff": empty_colmajor(k, max(m - k, 1), dev),
+            "skeleton": empty_colmajor(k, k, dev),
+        }
+    with on_torch_stream(c):
+        _raise(c.lib.lr_cur_id_d(
+            c.h, m, n, _dptr(a), _colmajor_ld(a), k, (strategy or SolveStrategy.automatic())._c(),
             float(pinv_threshold), int(u_mode), _dptr(out["col_pivots"]), _dptr(out["row_pivots"]), _dptr(out["c"]),
             _dptr(out["u"]), _dptr(out["r"]), _dptr(out["col_coeff"]), _dptr(out["row_coeff"]),
             _dptr(out["skeleton"])))

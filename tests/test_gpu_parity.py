@@ -120,12 +120,16 @@ def test_cpqr_rank_deficient_and_det(lr, oracle):
                                      ((4000, 300), 100), ((64, 64), 64), ((3, 1000), 3), ((777, 5), 5)])
 def test_cpqr_matches_oracle(lr, oracle, shape, k):
     a = inputs.synthetic_np(inputs.scaled(inputs.CONFIGS["c4"], shape[0], shape[1], width=min(shape), k=k))
+    ctx = lr.default_context()
+    ctx.reset_stats()
     g = lr.cpqr_partial(a, k)
     o = oracle.cpqr(a, k)
     assert np.array_equal(g.pivots, o["pivots"])
     assert rel(g.s, o["s"]) <= TOL and rel(g.q, o["q"]) <= TOL
-    st = lr.default_context().stats()
-    assert st["cpqr_steps"] >= k
+    st = ctx.stats()
+    assert st["cpqr_steps"] == k
+    # cpqr.hpp:78-84: the exact-norm recomputes happen at the same (step, column) pairs
+    assert st["norm_recomputes"] == o["recomputes"], (st["norm_recomputes"], o["recomputes"])
 
 
 def test_cpqr_validation(lr, oracle):

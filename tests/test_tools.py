@@ -25,12 +25,20 @@ def test_rooflines_from_stage_report():
               "cpqr_sample": {"ms": 20.8, "count": 1}, "cpqr_ct": {"ms": 20.1, "count": 1},
               "ctA_gemm": {"ms": 26.1, "count": 1}}
     st = {k: v["ms"] / v["count"] for k, v in stages.items()}
-    kern = bench.kernel_rooflines(_cfg(), st, stages, "ozaki")
+    per_step = {k: v["ms"] for k, v in stages.items()}  # one step
+    kern = bench.kernel_rooflines(_cfg(), st, per_step, "ozaki")
     sk = kern["sketch_gemm"]
     ops = 16 * 2.0 * bench.ELL * bench.M * bench.N
     assert abs(sk["achieved"] - round(ops / (27.5e-3) / 1e12, 1)) < 0.2
     assert sk["bound"] == "tensor" and 0 < sk["frac"] < 1.5 and sk["unit"] == "TOP/s"
     assert kern["cpqr_sample"]["bound"] == "hbm" and kern["cpqr_sample"]["unit"] == "GB/s"
+    # the split's achieved bandwidth uses its per-step total (both split marks of the step)
+    sp = kern["ozaki_split"]
+    b = (bench.ozaki_split_bytes(bench.M, bench.N) + bench.ozaki_split_bytes(bench.M, bench.ELL)
+         + bench.ozaki_split_bytes(bench.M, bench.K_RANK))
+    assert abs(sp["achieved"] - round(b / 28.0e-3 / 1e9, 1)) < 0.2
+    if kern["cpqr_sample"]["traffic"]:
+        assert kern["cpqr_sample"]["measured_bytes_frac"] < kern["cpqr_sample"]["frac"]
     # the headline is the longest single stage launch: the sketch GEMM, not the
     # split entry that sums the A, Omega and Q_c splits (14 ms per call)
     dom = max(kern, key=lambda n: st.get(n, 0.0))
