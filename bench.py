@@ -583,8 +583,10 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_sharded(args, rank, world, local_rank):
-    """Column-sharded randomized CUR (paper_1412_8447_b200/distributed.py):
-    strong scaling, the whole 65536^2 problem split over the ranks."""
+    """Column-sharded randomized CUR (lr_randomized_cur_sharded_d over an NCCL
+    communicator the library binds, csrc/shard.cu): strong scaling, the whole
+    65536^2 problem split over the ranks; both CPQRs sharded (one all-gather of
+    pivot candidates per step), no all-gather of the sample."""
     import torch
 
     import paper_1412_8447_b200 as lr
@@ -601,13 +603,17 @@ def run_sharded(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8 if args.engine == "ozaki" else ctx.GEMM_DMMA)
+    D.attach_nccl(ctx, world=world, rank=rank)
     off, n_g = D.shard_bounds(cfg.n, world, rank)
     a = inputs.synthetic_torch(cfg, device=dev, col_block=8192, col_range=(off, n_g))
-    be = D.DeviceBackend(ctx, dev)
-    comm = D.TorchComm(lambda x: x, lambda t: t)
+    sk = lr.SketchConfig(oversample=OVERSAMPLE, seed=cfg.sketch_seed)
+
+    def step(out=None):
+        return D.randomized_cur_sharded_device(ctx, a, off, cfg.n, cfg.k, sk, out=out)
+
     res = None
     for _ in range(args.warmup):
-        res = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+        res = step(res)
     torch.cuda.synchronize()
 
     def barrier():
@@ -624,7 +630,7 @@ def run_sharded(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            res = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+            res = step(res)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -637,7 +643,7 @@ def run_sharded(args, rank, world, local_rank):
     st_step = {kk: v["ms"] / args.steps for kk, v in stages.items()}
     roof = kernel_rooflines(shard_cfg, st_avg, st_step, args.engine).get("sketch_gemm")
     if roof:
-        roof = dict(roof, note=f"rank 0's column shard ({n_g} of {cfg.n} columns); the CPQRs are replicated")
+        roof = dict(roof, note=f"rank 0's column shard ({n_g} of {cfg.n} columns)")
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         import torch.distributed as dist
@@ -647,19 +653,19 @@ def run_sharded(args, rank, world, local_rank):
 
     # e2e: each step copies the rank's column shard from pinned host memory
     # into the device buffer, runs the sharded CUR and reads the replicated
-    # factors back into pinned host buffers (wall clock, max over ranks)
+    # factors (and the rank's R block) back into pinned host buffers
     e2e = None
     if not args.no_e2e:
         host = torch.empty((n_g, cfg.m), dtype=torch.float64, pin_memory=True).T
         host.copy_(a)
         torch.cuda.synchronize()
-        keys = ("c", "u", "r", "col_pivots", "row_pivots")
+        keys = ("c", "u", "r_local", "col_pivots", "row_pivots", "col_coeff", "row_coeff", "skeleton")
         hb = {kk: torch.empty(tuple(res[kk].shape), dtype=res[kk].dtype, pin_memory=True) for kk in keys}
         d2h = sum(hb[kk].numel() * hb[kk].element_size() for kk in keys)
 
         def e2e_step():
             a.copy_(host, non_blocking=True)
-            out = D.randomized_cur_sharded(be, comm, a, off, cfg.n, cfg.k, OVERSAMPLE, cfg.sketch_seed)
+            out = step(res)
             for kk in keys:
                 hb[kk].copy_(out[kk], non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
@@ -680,6 +686,8 @@ def run_sharded(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                "host_buffer": "pinned column shard per rank (1/N of A) and pinned result buffers",
                "pipeline": "shard H2D on the compute stream, then the sharded CUR; bytes summed over ranks"}
+    stats = ctx.stats()
+    D.detach_nccl(ctx)
     if rank != 0:
         return
     fm = flops_model(cfg.m, cfg.n, cfg.k, cfg.k + OVERSAMPLE)
@@ -690,10 +698,11 @@ def run_sharded(args, rank, world, local_rank):
         "data": "synthetic (seeded U diag(s) V^T, C4 spectrum, generated on device per column shard)",
         "config": {"workload": "randomized CUR + tsID, BASELINE configs[3], column-sharded", "m": cfg.m,
                    "n": cfg.n, "k": cfg.k, "oversample": OVERSAMPLE, "u_mode": "cpinv_a_rpinv",
-                   "parallelism": f"column-sharded x{world}", "l2": "A shard exceeds L2; no flush needed"},
+                   "parallelism": f"column-sharded x{world} (sharded CPQRs, NCCL)",
+                   "l2": "A shard exceeds L2; no flush needed"},
         "fp64_tflops": round(sum(fm.values()) / (ms * 1e-3) / 1e12, 3),
         "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
-        "roofline": roof, "stages_ms": {kk: round(v, 3) for kk, v in st_step.items()},
+        "roofline": roof, "stages_ms": {kk: round(v, 3) for kk, v in st_step.items()}, "lib_stats": stats,
     }
     print(json.dumps(line), flush=True)
 

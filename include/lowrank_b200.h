@@ -43,6 +43,7 @@ extern "C" {
 #define LR_ERUNTIME 4    /* std::runtime_error                             */
 #define LR_ECUDA 5       /* device / driver failure                        */
 #define LR_EUNSUPPORTED 6 /* reference feature not on the B200 path yet    */
+#define LR_ENCCL 7        /* NCCL failure (column-sharded entry points)    */
 
 /* SolveKind, solve.hpp:9 */
 #define LR_SOLVE_BACKSUB 0
@@ -264,6 +265,41 @@ int lr_cholqr2_d(lr_ctx* ctx, int64_t rows, int64_t k, const double* x, int64_t 
 /* Y (M x N) = P^T Q on the context's contraction engine (benchmark / test access) */
 int lr_gemm_tn_d(lr_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo);
+
+/* ---- column-sharded multi-GPU entry points (one process per GPU; SURVEY.md
+   section 8e).  Rank g passes its column block A(:, col_offset : col_offset +
+   n_local) of the m x n_total matrix (device pointer).  The CPQRs run sharded:
+   per step one ncclAllGather carries every rank's pivot candidate (norm^2,
+   logical position, the column), every rank applies the winner's reflector to
+   its own columns (cpqr.hpp:48-85) -- no rank holds the whole sample.  Outputs
+   are replicated on every rank except R, of which each rank gets its column
+   block (k x n_local).  Without an attached communicator the same code runs
+   for one unsharded rank (col_offset 0, n_local = n_total).  The reference's
+   interface has no multi-process form; these extend lr_randomized_cur_d
+   (sketch.hpp:227-234, lowrank_main.cpp:215) and lr_cpqr_partial_d
+   (cpqr.hpp:32-114). ---- */
+/* NCCL unique id (128 bytes) made on one rank and shared with the others */
+int lr_nccl_get_unique_id(unsigned char* id);
+/* bind an NCCL communicator (ncclCommInitRank over the process's libnccl.so.2) */
+int lr_ctx_attach_comm(lr_ctx* ctx, const unsigned char* id, int nranks, int rank);
+int lr_ctx_detach_comm(lr_ctx* ctx);
+int lr_ctx_comm_info(lr_ctx* ctx, int* nranks, int* rank);
+/* test vehicle: without a communicator, run the sharded CPQRs as `nshards`
+   column blocks inside this process (each step: the blocks' candidates are
+   gathered by device copies, then every block's step kernel runs; no kernel
+   waits on another).  0 = off. */
+int lr_ctx_set_shard_emulation(lr_ctx* ctx, int nshards);
+/* pivots (n_total) and the sign-fixed top k rows of R in logical column order
+   (s, k x n_total, ld k), replicated */
+int lr_cpqr_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                      const double* a_local, int64_t lda, int64_t k, int64_t* pivots, double* s);
+/* randomized CUR (Gaussian sketch, q = 0) of the column-sharded A; u_mode as
+   lr_randomized_cur_d; r_local is this rank's k x n_local block of R */
+int lr_randomized_cur_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                                const double* a_local, int64_t lda, int64_t k, lr_sketch_config cfg,
+                                lr_solve_strategy strategy, double pinv_threshold, int u_mode,
+                                int64_t* col_pivots, int64_t* row_pivots, double* c, double* u, double* r_local,
+                                double* col_coeff, double* row_coeff, double* skeleton);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblowrank_b200.so")
 
-LR_OK, LR_EINVAL, LR_ESINGULAR, LR_ECONVERGE, LR_ERUNTIME, LR_ECUDA, LR_EUNSUPPORTED = range(7)
+LR_OK, LR_EINVAL, LR_ESINGULAR, LR_ECONVERGE, LR_ERUNTIME, LR_ECUDA, LR_EUNSUPPORTED, LR_ENCCL = range(8)
 LR_SOLVE_BACKSUB, LR_SOLVE_PINV, LR_SOLVE_TIKHONOV = range(3)
 LR_SKETCH_GAUSSIAN, LR_SKETCH_SRFT = range(2)
 LR_U_VT_RPINV, LR_U_CPINV_A_RPINV = range(2)
@@ -126,6 +126,17 @@ SIGNATURES = {
     "lr_tri_upper_inverse_d": ([ctypes.c_void_p, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_cholqr2_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp, ctypes.POINTER(ctypes.c_int)],
                      ctypes.c_int),
+    "lr_nccl_get_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+    "lr_ctx_attach_comm": ([ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "lr_ctx_detach_comm": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_set_shard_emulation": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "lr_ctx_comm_info": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
+                         ctypes.c_int),
+    "lr_cpqr_sharded_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp],
+                          ctypes.c_int),
+    "lr_randomized_cur_sharded_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64,
+                                     lr_sketch_config, lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip,
+                                     c_dp, c_dp, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),
 }
 
 _lib = None

@@ -49,6 +49,9 @@ int guard(F&& f) {
   } catch (const CudaError& e) {
     g_err = e.what();
     return LR_ECUDA;
+  } catch (const NcclError& e) {
+    g_err = e.what();
+    return LR_ENCCL;
   } catch (const std::bad_alloc&) {
     g_err = "host allocation failed";
     return LR_ERUNTIME;
@@ -152,6 +155,11 @@ struct lr_ctx {
     CUgreenCtx g1 = nullptr, g2 = nullptr;
     CUstream s1 = nullptr, s2 = nullptr;
   } split;
+  // communicator of the column-sharded entry points (lr_ctx_attach_comm)
+  lrb::ShardComm comm;
+  // > 0 (no communicator): the sharded CPQRs run as that many column blocks in
+  // this process (lr_ctx_set_shard_emulation, a single-GPU test vehicle)
+  int emu_shards = 0;
 };
 
 namespace {
@@ -1393,6 +1401,228 @@ void arena_close() {
   tl_arena = nullptr;
 }
 
+// ---------------------------------------------------------------- column-sharded pipeline (multi-GPU)
+// One process per GPU, rank g owning the column block A(:, off_g : off_g + n_g)
+// (SURVEY.md section 8e).  Every decision that ends a call (non-finite input,
+// escalation, CholeskyQR2 acceptance, singularity) is taken on replicated,
+// all-reduced data, so all ranks take it together and no rank is left waiting
+// in a collective.
+// all ranks agree on a flag (max over ranks)
+bool any_rank(lr_ctx* c, bool local) {
+  if (!c->comm.comm) return local;
+  DBuf<double> f(1, c->st);
+  const double v = local ? 1.0 : 0.0;
+  LRB_CUDA(cudaMemcpyAsync(f.p, &v, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  c->comm.all_reduce_max(f, 1, c->st);
+  d2h_mapped(c, c->h_scal, f.p, sizeof(double));
+  sync(c);
+  return c->h_scal[0] != 0.0;
+}
+
+// cpqr.hpp:32-114 on the column-sharded short-wide matrix a (m x n_loc, this
+// rank's columns [off, off + n_loc) of m x n_total), `steps` steps; replicated
+// perm (n_total) and the sign-fixed top `krows` rows of R in logical order
+// (S, krows x n_total, ld krows).
+void cpqr_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t off, int64_t n_total, const double* a,
+                       int64_t lda, int64_t steps, int64_t krows, int64_t* perm, double* S, const char* who,
+                       int emulate_shards = 0) {
+  require_nonempty(m, n_total, who);
+  require_rank_in_range(steps, m, n_total, who);
+  const int64_t ldw = even(m);
+  DBuf<double> W((size_t)ldw * std::max<int64_t>(n_loc, 1), c->st);
+  if (n_loc > 0) copy_matrix(m, n_loc, a, lda, W, ldw, c->st);
+  DBuf<int> flags(1, c->st);
+  DBuf<long long> rec(1, c->st);
+  LRB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), c->st));
+  LRB_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(long long), c->st));
+  if (emulate_shards > 0)
+    cpqr_sharded_emulated(c->ws, emulate_shards, m, n_total, W, ldw, steps, krows, perm, S, krows, flags, rec, c->st);
+  else
+    cpqr_sharded(c->ws, c->comm, m, n_loc, off, n_total, W, ldw, steps, krows, perm, S, krows, flags, rec, c->st);
+  c->comm.all_reduce_sum(reinterpret_cast<int64_t*>(rec.p), 1, c->st);
+  d2h_mapped(c, c->h_flags, flags.p, sizeof(int));
+  d2h_mapped(c, c->h_ll, rec.p, sizeof(long long));
+  sync(c);
+  if (any_rank(c, c->h_flags[0] != 0)) fail(LR_EINVAL, std::string(who) + ": matrix has non-finite entries");
+  c->stats.cpqr_steps += steps;
+  c->stats.norm_recomputes += c->h_ll[0];
+}
+
+// sketch.hpp:227-234 (+ lowrank_main.cpp:215 for u_mode LR_U_CPINV_A_RPINV)
+// on the column-sharded A.  Replicated outputs: col_pivots (n), row_pivots
+// (m), C (m x k), U, col_coeff (k x (n-k)), row_coeff (k x (m-k)), skeleton;
+// R_loc (k x n_loc) is this rank's block of R.
+void randomized_cur_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t off, int64_t n, const double* a,
+                                 int64_t lda, int64_t k, const lr_sketch_config& cfg, const lr_solve_strategy& strat,
+                                 double thr, int u_mode, int64_t* col_piv, int64_t* row_piv, double* C, double* U,
+                                 double* R_loc, double* col_coeff, double* row_coeff, double* skeleton) {
+  const ShardComm& cm = c->comm;
+  if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
+  if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
+    fail(LR_EUNSUPPORTED, "randomized_cur (column-sharded): Gaussian sketch with q = 0 only");
+  if (u_mode != LR_U_VT_RPINV && u_mode != LR_U_CPINV_A_RPINV) fail(LR_EINVAL, "randomized_cur: unknown u_mode");
+  if (off < 0 || n_loc < 0 || off + n_loc > n) fail(LR_EINVAL, "randomized_cur (column-sharded): bad column block");
+  const int64_t ell = check_randomized_id(m, n, k, cfg);
+  if (any_rank(c, n_loc > 0 && !device_all_finite(c, m, n_loc, a, lda)))
+    fail(LR_EINVAL, "sketch_gaussian: matrix has non-finite entries");
+  mark(c, "begin");
+  OzakiScope scope(c);  // the shard's residue planes serve the sketch and A^T Q_c
+  const int64_t ldk = even(k);
+  // (1) Y_g = Omega A_g (Omega from the counter stream: identical on every rank)
+  const int64_t ldy = even(ell);
+  DBuf<double> Y((size_t)ldy * std::max<int64_t>(n_loc, 1), c->st);
+  if (n_loc > 0) sketch_core(c, m, n_loc, a, lda, ell, cfg.seed, Y, ldy);
+  // (2) CPQR(Y), ell steps, sharded; T = S11^-1 S12 on the replicated top k rows
+  DBuf<double> S1((size_t)k * n, c->st);
+  const int emu = c->comm.comm ? 0 : c->emu_shards;
+  cpqr_sharded_core(c, ell, n_loc, off, n, Y, ldy, std::min(ell, n), k, col_piv, S1, "cpqr_partial", emu);
+  mark(c, "cpqr_sample");
+  solve_core(c, k, n - k, S1, k, S1.p + k * k, k, strat, col_coeff, k, false);
+  mark(c, "coeff_solve_col");
+  // (3) C = A(:, J): owners gather, all-reduce-sum (one non-zero term per entry)
+  {
+    DBuf<int64_t> idx(k, c->st);
+    owned_index(col_piv, k, off, n_loc, idx, c->st);
+    gather_columns(m, k, a, lda, idx, C, m, c->st);
+    cm.all_reduce_sum(C, (size_t)m * k, c->st);
+  }
+  mark(c, "gather_c");
+  // (4) row ID: CPQR of C^T sharded by row blocks of C, k steps
+  const int64_t r0 = m * cm.rank / cm.nranks, m_loc = m * (cm.rank + 1) / cm.nranks - r0;
+  {
+    DBuf<double> Ct_loc((size_t)ldk * std::max<int64_t>(m_loc, 1), c->st), S1r((size_t)k * m, c->st);
+    if (m_loc > 0) transpose_matrix(m_loc, k, C + r0, m, Ct_loc, ldk, c->st);
+    cpqr_sharded_core(c, k, m_loc, r0, m, Ct_loc, ldk, k, k, row_piv, S1r, "cpqr_partial", emu);
+    mark(c, "cpqr_ct");
+    solve_core(c, k, m - k, S1r, k, S1r.p + k * k, k, strat, row_coeff, k, false);
+    if (skeleton) gather_rows(k, k, C, m, row_piv, skeleton, k, c->st);
+    mark(c, "coeff_solve_row");
+  }
+  // (5) R_g = A_g(I, :)
+  if (n_loc > 0) gather_rows(k, n_loc, a, lda, row_piv, R_loc, k, c->st);
+  mark(c, "gather_r");
+  // (6) U.  C = Qc Rc (replicated CholeskyQR2); R^T = Qr Sr by CholeskyQR2 with
+  // all-reduced Gram matrices over the column blocks
+  const int64_t nl = std::max<int64_t>(n_loc, 1), ldn = even(nl);
+  DBuf<double> Rt((size_t)ldn * k, c->st), Rk((size_t)ldk * nl, c->st);
+  LRB_CUDA(cudaMemsetAsync(Rt.p, 0, sizeof(double) * ldn * k, c->st));
+  LRB_CUDA(cudaMemsetAsync(Rk.p, 0, sizeof(double) * ldk * nl, c->st));
+  if (n_loc > 0) {
+    transpose_matrix(k, n_loc, R_loc, k, Rt, ldn, c->st);
+    copy_matrix(k, n_loc, R_loc, k, Rk, ldk, c->st);
+  }
+  DBuf<double> G((size_t)k * k, c->st), S1i((size_t)k * k, c->st), Q1((size_t)ldn * k, c->st);
+  DBuf<double> G2((size_t)k * k, c->st), S2t((size_t)k * k, c->st), Sr((size_t)k * k, c->st),
+      Sri((size_t)k * k, c->st);
+  DBuf<int> info(2, c->st);
+  bool r_ok = true;
+  gemm(c, k, k, nl, Rt, ldn, Rt, ldn, G, k);  // R_g R_g^T
+  cm.all_reduce_sum(G, (size_t)k * k, c->st);
+  cholesky_upper(c->ws, k, G, k, info, c->st);
+  d2h_mapped(c, c->h_flags, info.p, sizeof(int));
+  sync(c);
+  r_ok = c->h_flags[0] == 0;
+  if (r_ok) {
+    tri_upper_inverse_blocked(k, G, k, S1i, k, c->st);
+    gemm(c, nl, k, k, Rk, ldk, S1i, k, Q1, ldn, 1.0, 0.0, -1, false, kTriQ);  // Q1_g = R_g^T S1^-1
+    gemm(c, k, k, nl, Q1, ldn, Q1, ldn, G2, k);
+    cm.all_reduce_sum(G2, (size_t)k * k, c->st);
+    cholesky_upper(c->ws, k, G2, k, info.p + 1, c->st);
+    d2h_mapped(c, c->h_flags + 1, info.p + 1, sizeof(int));
+    sync(c);
+    r_ok = c->h_flags[1] == 0;
+  }
+  if (r_ok) {
+    transpose_matrix(k, k, G2, k, S2t, k, c->st);
+    gemm(c, k, k, k, S2t, k, G, k, Sr, k);  // Sr = S2 S1
+    tri_upper_inverse_blocked(k, Sr, k, Sri, k, c->st);
+    DBuf<double> part(4 * num_sms() + 4, c->st), f(2, c->st);
+    frob2(k, k, Sr, k, part, f, c->st);
+    frob2(k, k, Sri, k, part, f.p + 1, c->st);
+    d2h_mapped(c, c->h_scal, f.p, 2 * sizeof(double));
+    sync(c);
+    const double cb = std::sqrt(c->h_scal[0]) * std::sqrt(c->h_scal[1]);
+    r_ok = std::isfinite(cb) && cb < fast_cond_limit(thr);
+  }
+  mark(c, "cholqr2_r");
+  // local rows of R^+ (n_loc x k, ld ldn): Qr_g Sr^-T on the fast path
+  // (R^T = Qr Sr => R^+ = Qr Sr^-T), else rows of the truncated pseudoinverse of
+  // the all-gathered R (svd.hpp:193-207, Jacobi route)
+  DBuf<double> Rp_loc((size_t)ldn * k, c->st);
+  LRB_CUDA(cudaMemsetAsync(Rp_loc.p, 0, sizeof(double) * ldn * k, c->st));
+  DBuf<double> Qr;
+  if (r_ok) {
+    Qr = DBuf<double>((size_t)ldn * k, c->st);
+    gemm(c, nl, k, k, Rk, ldk, Sri, k, Qr, ldn, 1.0, 0.0, -1, false, kTriQ);  // Qr_g = R_g^T Sr^-1
+  } else {
+    DBuf<double> Rfull((size_t)k * n, c->st), Rp((size_t)n * k, c->st);
+    LRB_CUDA(cudaMemsetAsync(Rfull.p, 0, sizeof(double) * k * n, c->st));
+    if (n_loc > 0) copy_matrix(k, n_loc, R_loc, k, Rfull.p + off * k, k, c->st);
+    cm.all_reduce_sum(Rfull, (size_t)k * n, c->st);
+    pinv_core(c, k, n, Rfull, k, thr, Rp, n);
+    if (n_loc > 0) copy_matrix(n_loc, k, Rp.p + off, n, Rp_loc, ldn, c->st);
+  }
+  auto rp_from_qr = [&] {
+    DBuf<double> srt((size_t)k * k, c->st), Qrt((size_t)ldk * nl, c->st);
+    transpose_matrix(k, k, Sri, k, srt, k, c->st);
+    transpose_matrix(nl, k, Qr, ldn, Qrt, ldk, c->st);
+    gemm(c, nl, k, k, Qrt, ldk, srt, k, Rp_loc, ldn);  // R^+_g = Qr_g Sr^-T
+  };
+  if (u_mode == LR_U_CPINV_A_RPINV) {
+    DBuf<double> Ct((size_t)ldk * m, c->st), Cm((size_t)even(m) * k, c->st), Rc((size_t)k * k, c->st),
+        Rci((size_t)k * k, c->st);
+    transpose_matrix(m, k, C, m, Ct, ldk, c->st);
+    copy_matrix(m, k, C, m, Cm, even(m), c->st);
+    const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci, fast_cond_limit(thr));
+    mark(c, "cholqr2_c");
+    DBuf<double> Xt((size_t)ldn * k, c->st), W((size_t)k * k, c->st);
+    LRB_CUDA(cudaMemsetAsync(Xt.p, 0, sizeof(double) * ldn * k, c->st));
+    if (c_ok && r_ok) {
+      c->stats.pinv_fast_path = 1;
+      // U = Rc^-1 (Qc^T A Qr) Sr^-T with W = sum_g (A_g^T Qc)^T Qr_g
+      DBuf<double> Qc((size_t)even(m) * k, c->st);
+      gemm(c, m, k, k, Ct, ldk, Rci, k, Qc, even(m), 1.0, 0.0, -1, false, kTriQ);  // Qc = C Rc^-1
+      mark(c, "form_q");
+      if (n_loc > 0) gemm_a(c, nl, k, m, a, lda, Qc, even(m), Xt, ldn, 0);       // X_g^T = A_g^T Qc
+      mark(c, "ctA_gemm");
+      gemm(c, k, k, nl, Xt, ldn, Qr, ldn, W, k);
+      cm.all_reduce_sum(W, (size_t)k * k, c->st);
+      DBuf<double> t1((size_t)k * k, c->st), tt((size_t)k * k, c->st), st2((size_t)k * k, c->st);
+      transpose_matrix(k, k, Rci, k, tt, k, c->st);
+      gemm(c, k, k, k, tt, k, W, k, t1, k);  // Rc^-1 W
+      transpose_matrix(k, k, t1, k, tt, k, c->st);
+      transpose_matrix(k, k, Sri, k, st2, k, c->st);
+      gemm(c, k, k, k, tt, k, st2, k, U, k);  // (Rc^-1 W) Sr^-T
+    } else {
+      // U = sum_g (C^+ A_g) R^+_g with the replicated truncated C^+ (Jacobi route)
+      c->stats.pinv_fast_path = 0;
+      if (r_ok) rp_from_qr();
+      DBuf<double> Cp((size_t)k * m, c->st), Cpt((size_t)even(m) * k, c->st);
+      pinv_core(c, m, k, C, m, thr, Cp, k);
+      transpose_matrix(k, m, Cp, k, Cpt, even(m), c->st);
+      if (n_loc > 0) gemm_a(c, nl, k, m, a, lda, Cpt, even(m), Xt, ldn, 0);  // X_g^T = A_g^T C^+T
+      mark(c, "ctA_gemm");
+      gemm(c, k, k, nl, Xt, ldn, Rp_loc, ldn, U, k);
+      cm.all_reduce_sum(U, (size_t)k * k, c->st);
+    }
+  } else {
+    // u = basis()^T R^+ (cur.hpp:30) = sum_g B_g R^+_g, B_g = the basis rows of the owned columns
+    if (r_ok) rp_from_qr();
+    c->stats.pinv_fast_path = r_ok ? 1 : 0;
+    DBuf<int64_t> inv(n, c->st);
+    inverse_perm(col_piv, n, inv, c->st);
+    DBuf<double> B((size_t)k * nl, c->st), Bt((size_t)ldn * k, c->st);
+    LRB_CUDA(cudaMemsetAsync(Bt.p, 0, sizeof(double) * ldn * k, c->st));
+    if (n_loc > 0) {
+      basis_rows(inv, off, n_loc, k, col_coeff, k, B, c->st);
+      transpose_matrix(k, n_loc, B, k, Bt, ldn, c->st);
+    }
+    gemm(c, k, k, nl, Bt, ldn, Rp_loc, ldn, U, k);  // U = B_g R^+_g
+    cm.all_reduce_sum(U, (size_t)k * k, c->st);
+  }
+  mark(c, "u_small");
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1443,6 +1673,7 @@ int lr_ctx_destroy(lr_ctx* c) {
     if (c->up_st) cudaStreamDestroy(c->up_st);
     if (c->down_st) cudaStreamDestroy(c->down_st);
     release_sm_split(c);
+    nccl_comm_destroy(c->comm.comm);
     cudaStreamDestroy(c->own);
     delete c;
   });
@@ -2276,6 +2507,82 @@ int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, in
     if (M < 1 || N < 1 || K < 1) fail(LR_EINVAL, "gemm_tn: dimensions must be positive");
     // in the Ozaki mode both operands are split (no A cache outside a CUR call)
     gemm_a(c, M, N, K, P, ldp, Q, ldq, out, ldo, -1);
+  });
+}
+
+
+// ---- column-sharded entry points (one process per GPU)
+int lr_nccl_get_unique_id(unsigned char* id) {
+  return guard([&] {
+    if (!id) fail(LR_EINVAL, "nccl_get_unique_id: null buffer");
+    nccl_unique_id(id);
+  });
+}
+int lr_ctx_attach_comm(lr_ctx* c, const unsigned char* id, int nranks, int rank) {
+  return guard([&] {
+    checked(c);
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) fail(LR_EINVAL, "attach_comm: bad unique id, size or rank");
+    if (c->comm.comm) nccl_comm_destroy(c->comm.comm);
+    c->comm = ShardComm{};
+    ShardComm sc;
+    sc.comm = nccl_comm_init(id, nranks, rank);
+    sc.nranks = nranks;
+    sc.rank = rank;
+    c->comm = sc;
+  });
+}
+int lr_ctx_detach_comm(lr_ctx* c) {
+  return guard([&] {
+    checked(c);
+    LRB_CUDA(cudaStreamSynchronize(c->st));
+    nccl_comm_destroy(c->comm.comm);
+    c->comm = ShardComm{};
+  });
+}
+int lr_ctx_comm_info(lr_ctx* c, int* nranks, int* rank) {
+  return guard([&] {
+    checked(c);
+    if (nranks) *nranks = c->comm.nranks;
+    if (rank) *rank = c->comm.rank;
+  });
+}
+int lr_cpqr_sharded_d(lr_ctx* c, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                      const double* a_local, int64_t lda, int64_t k, int64_t* pivots, double* s) {
+  return guard([&] {
+    checked(c);
+    if (n_local > 0) require_ld(m, lda, "cpqr_partial");
+    if (col_offset < 0 || n_local < 0 || col_offset + n_local > n_total)
+      fail(LR_EINVAL, "cpqr_partial (column-sharded): bad column block");
+    cpqr_sharded_core(c, m, n_local, col_offset, n_total, a_local, lda, k, k, pivots, s, "cpqr_partial",
+                      c->comm.comm ? 0 : c->emu_shards);
+  });
+}
+int lr_ctx_set_shard_emulation(lr_ctx* c, int nshards) {
+  return guard([&] {
+    checked(c);
+    if (nshards < 0 || nshards > 64) fail(LR_EINVAL, "set_shard_emulation: 0..64 shards");
+    c->emu_shards = nshards;
+  });
+}
+int lr_randomized_cur_sharded_d(lr_ctx* c, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                                const double* a_local, int64_t lda, int64_t k, lr_sketch_config cfg,
+                                lr_solve_strategy strat, double thr, int u_mode, int64_t* col_pivots,
+                                int64_t* row_pivots, double* C, double* U, double* r_local, double* col_coeff,
+                                double* row_coeff, double* skeleton) {
+  return guard([&] {
+    checked(c);
+    if (n_local > 0) require_ld(m, lda, "randomized_cur");
+    DBuf<double> cc, rc;
+    if (!col_coeff) {
+      cc = DBuf<double>((size_t)k * std::max<int64_t>(n_total - k, 1), c->st);
+      col_coeff = cc;
+    }
+    if (!row_coeff) {
+      rc = DBuf<double>((size_t)k * std::max<int64_t>(m - k, 1), c->st);
+      row_coeff = rc;
+    }
+    randomized_cur_sharded_core(c, m, n_local, col_offset, n_total, a_local, lda, k, cfg, strat, thr, u_mode,
+                                col_pivots, row_pivots, C, U, r_local, col_coeff, row_coeff, skeleton);
   });
 }
 

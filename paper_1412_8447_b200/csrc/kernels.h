@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <cstddef>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace lrb {
@@ -39,6 +41,7 @@ enum class WsSlot : int {
   kOzPShift,
   kOzQ,
   kOzQShift,
+  kShard,      // sharded CPQR state (shard.cu)
   kCount
 };
 
@@ -220,5 +223,45 @@ void copy_bytes_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st
 // SRFT fallback, reproduced bit for bit
 void gemm_tn_ordered(int M, int N, int K, const double* P, int64_t ldp, const double* Q, int64_t ldq, double* out,
                      int64_t ldo, cudaStream_t st);
+
+// ---------------------------------------------------------------- multi-GPU (shard.cu)
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void nccl_unique_id(unsigned char out[128]);
+void* nccl_comm_init(const unsigned char id[128], int nranks, int rank);
+void nccl_comm_destroy(void* comm);
+
+// The collectives of the column-sharded entry points, on the caller's stream.
+// Without a communicator (one unsharded rank) they are local no-ops / copies.
+struct ShardComm {
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0;
+  void all_gather_bytes(const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st) const;
+  void all_reduce_sum(double* buf, size_t count, cudaStream_t st) const;
+  void all_reduce_sum(int64_t* buf, size_t count, cudaStream_t st) const;
+  void all_reduce_max(double* buf, size_t count, cudaStream_t st) const;
+};
+
+// cpqr.hpp:32-114 on a column-sharded short-wide matrix (shard.cu header):
+// W (m x n_loc, ld) is this rank's block of columns [off, off + n_loc) of an
+// m x n_total matrix, overwritten; `steps` steps.  Replicated outputs: perm
+// (n_total) and the sign-fixed top `krows` rows of R in logical column order
+// S (krows x n_total, ld lds).
+void cpqr_sharded(Workspace& ws, const ShardComm& comm, int64_t m, int64_t n_loc, int64_t off, int64_t n_total,
+                  double* W, int64_t ld, int64_t steps, int64_t krows, int64_t* perm, double* S, int64_t lds,
+                  int* d_flags, long long* d_recomputes, cudaStream_t st);
+// the same protocol over `nshards` column blocks of one matrix in one process
+// (test vehicle for the multi-rank logic on one GPU; kernels run in sequence)
+void cpqr_sharded_emulated(Workspace& ws, int nshards, int64_t m, int64_t n, double* W, int64_t ld, int64_t steps,
+                           int64_t krows, int64_t* perm, double* S, int64_t lds, int* d_flags,
+                           long long* d_recomputes, cudaStream_t st);
+
+// helpers of the sharded pipeline: owned slot of each global pivot (-1 when
+// another rank owns it), inverse permutation, basis() rows of owned columns
+void owned_index(const int64_t* perm, int64_t k, int64_t off, int64_t n_loc, int64_t* idx, cudaStream_t st);
+void inverse_perm(const int64_t* perm, int64_t n, int64_t* inv, cudaStream_t st);
+void basis_rows(const int64_t* inv, int64_t off, int64_t n_loc, int64_t k, const double* coeff, int64_t ldc,
+                double* B, cudaStream_t st);
 
 }  // namespace lrb

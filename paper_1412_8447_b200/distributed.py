@@ -4,34 +4,59 @@ Rank g owns a contiguous column block A_g = A(:, off_g : off_g + n_g).  The
 pipeline of sketch.hpp:227-234 (+ the lowrank_main.cpp:215 middle factor)
 becomes
 
-  stage                        work on rank g                 exchange
-  Y_g = Omega A_g              sketch GEMM (no comm)          all-gather Y (l x n)
-  CPQR(Y) -> pivots, T         replicated (identical bits)    -
-  C = A(:, J)                  masked gather of owned cols    all-reduce-sum (exact: one term/col)
-  row ID of C, skeleton        replicated                     -
-  R_g = A_g(I, :)              local gather                   -
-  C = Qc Rc (CholeskyQR2)      replicated                     -
-  R^T = Qr Sr                  Gram of R_g^T                  2 x all-reduce (k x k)
-  W = Qc^T A Qr                A_g^T Qc, then (.)^T Qr_g       all-reduce (k x k)
-  U = Rc^-1 W Sr^-T            replicated                     -
-  R = [R_g]                    -                              all-gather (k x n)
+  stage                        work on rank g                     exchange
+  Y_g = Omega A_g              sketch GEMM (Omega from the        -
+                               counter stream, identical bits)
+  CPQR(Y), l steps             norms, argmax, reflector apply     per step: all-gather of the
+                               on the owned columns of Y          N pivot candidates (16 B header
+                                                                  + one column each)
+  S1 (top k rows of R)         scatter by logical position        all-reduce-sum (exact)
+  T = S11^-1 S12               replicated solve                   -
+  C = A(:, J)                  masked gather of owned columns     all-reduce-sum (exact)
+  CPQR(C^T), k steps           sharded by row blocks of C         as CPQR(Y)
+  R_g = A_g(I, :)              local gather                       -
+  C = Qc Rc (CholeskyQR2)      replicated                         -
+  R^T = Qr Sr                  Gram of R_g^T                      2 x all-reduce (k x k)
+  W = Qc^T A Qr                A_g^T Qc, then (.)^T Qr_g           all-reduce (k x k)
+  U = Rc^-1 W Sr^-T            replicated                         -
 
-The two big contractions (the sketch and A^T Qc) shard perfectly; the CPQRs
-are replicated this round (a per-step exchange of the staged reflector is the
-next step).  Every exchange is a plain collective, so the protocol is
-exercised on CPU with gloo (tests/test_distributed.py, numpy backend) and on
-GPUs with NCCL (DeviceBackend over the C ABI shard primitives).
+No rank ever holds the whole sample Y: the per-step candidate exchange is
+north_star's "NCCL selects the global pivot, the Householder reflector is
+broadcast" fused into one all-gather (every rank sends its best column; all
+ranks pick the same winner from the same bytes and build the same reflector).
+
+Two implementations of the one protocol:
+
+* the PRODUCT path is native: ``randomized_cur_sharded_device`` is a single
+  C-ABI call per rank (``lr_randomized_cur_sharded_d``, csrc/shard.cu +
+  csrc/api.cu) over an NCCL communicator the library binds with
+  ``attach_nccl`` (unique id shared through torch.distributed);
+* ``randomized_cur_sharded`` / ``cpqr_sharded`` below are the same protocol
+  step by step on the host over any collective backend -- the executable
+  specification the multi-process tests run over gloo on CPU
+  (tests/test_distributed.py supplies the shard primitives there; this module
+  has no CPU compute of its own).
 """
 from __future__ import annotations
 
 import ctypes
-from typing import Any, Dict
+from typing import Any, Dict, Optional
 
 import numpy as np
 
 
+def shard_bounds(n: int, world: int, rank: int):
+    """Contiguous column block of rank `rank` (sizes differ by at most one)."""
+    lo = n * rank // world
+    hi = n * (rank + 1) // world
+    return lo, hi - lo
+
+
+# ---------------------------------------------------------------- collectives
 class TorchComm:
-    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo on CPU)."""
+    """Collectives over torch.distributed (gloo on CPU, NCCL for CUDA tensors),
+    counting the bytes each rank contributes (tests assert the sample Y is
+    never gathered)."""
 
     def __init__(self, to_tensor, from_tensor):
         import torch.distributed as dist
@@ -40,211 +65,166 @@ class TorchComm:
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self._t = to_tensor
         self._f = from_tensor
+        self.bytes_sent = 0      # every collective
+        self.bytes_gathered = 0  # all-gathers only (the per-step pivot candidates)
 
-    def all_gather_cols(self, x):
-        if self.world == 1:
-            return x
+    def all_gather_flat(self, x):
+        """(L,) on every rank -> (world, L)"""
         import torch
-        t = self._t(x)
-        # column-major (m x n_g) == row-major (n_g x m): gather along dim 0 of the
-        # transpose; blocks are padded to a common height (collectives need equal sizes)
-        tt = t.T.contiguous()
-        sizes = [torch.zeros(1, dtype=torch.int64, device=tt.device) for _ in range(self.world)]
-        self.dist.all_gather(sizes, torch.tensor([tt.shape[0]], dtype=torch.int64, device=tt.device))
-        hs = [int(s.item()) for s in sizes]
-        hmax = max(hs)
-        if tt.shape[0] < hmax:
-            tt = torch.cat([tt, torch.zeros((hmax - tt.shape[0], tt.shape[1]), dtype=tt.dtype, device=tt.device)])
-        parts = [torch.empty((hmax, tt.shape[1]), dtype=tt.dtype, device=tt.device) for _ in hs]
-        self.dist.all_gather(parts, tt)
-        return self._f(torch.cat([p[:h] for p, h in zip(parts, hs)], dim=0).T)
+        t = self._t(np.ascontiguousarray(x)).reshape(-1)
+        self.bytes_sent += t.numel() * t.element_size()
+        self.bytes_gathered += t.numel() * t.element_size()
+        if self.world == 1:
+            return self._f(t.reshape(1, -1))
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t)
+        return self._f(torch.stack(parts))
 
     def all_reduce_sum(self, x):
+        t = self._t(x)
+        self.bytes_sent += t.numel() * t.element_size()
         if self.world == 1:
             return x
-        t = self._t(x)
-        tc = t.T.contiguous()
+        tc = t.T.contiguous() if t.dim() == 2 else t.contiguous()
         self.dist.all_reduce(tc)
-        return self._f(tc.T)
+        return self._f(tc.T if t.dim() == 2 else tc)
 
 
-class DeviceBackend:
-    """Shard primitives on the B200 (liblowrank_b200.so, device pointers)."""
-
-    def __init__(self, ctx, device):
-        import torch
-        from .lowrank import _raise, empty_colmajor
-        self.torch = torch
-        self.ctx = ctx
-        self.lib = ctx.lib
-        self.dev = device
-        self._raise = _raise
-        self._empty = empty_colmajor
-        # library kernels and torch plumbing (copies, collectives) share one stream
-        ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
-
-    # --- helpers
-    def empty(self, m, n):
-        return self._empty(m, n, self.dev)
-
-    @staticmethod
-    def ld(t):
-        return int(t.stride(1)) if t.dim() == 2 and t.shape[1] > 1 else max(1, int(t.shape[0]))
-
-    def cm(self, t):
-        """column-major copy if needed"""
-        if t.dim() == 2 and t.stride(0) == 1 and (t.shape[1] <= 1 or t.stride(1) >= max(1, t.shape[0])):
-            return t
-        out = self.empty(t.shape[0], t.shape[1])
-        out.copy_(t)
-        return out
-
-    def cache_operand(self, a):
-        m, n = a.shape
-        self._raise(self.lib.lr_ctx_cache_operand(self.ctx.h, a.data_ptr(), m, n, self.ld(a)))
-
-    def clear_operand_cache(self):
-        self._raise(self.lib.lr_ctx_clear_operand_cache(self.ctx.h))
-
-    def sketch(self, a, ell, seed):
-        m, n = a.shape
-        y = self.empty(ell, n)
-        self._raise(self.lib.lr_sketch_gaussian_d(self.ctx.h, m, n, a.data_ptr(), self.ld(a), ell, seed,
-                                                  y.data_ptr(), self.ld(y)))
-        return y
-
-    def id_from_sample(self, y, k, strategy):
-        ell, n = y.shape
-        y = self.cm(y)
-        piv = self.torch.empty(n, dtype=self.torch.int64, device=self.dev)
-        coeff = self.empty(k, max(n - k, 1))
-        self._raise(self.lib.lr_id_from_sample_d(self.ctx.h, ell, n, y.data_ptr(), self.ld(y), k, strategy._c(),
-                                                 piv.data_ptr(), coeff.data_ptr()))
-        return piv, coeff[:, : n - k]
-
-    def owned_index(self, j, off, n_g):
-        jj = j.clone()
-        mask = (jj >= off) & (jj < off + n_g)
-        return self.torch.where(mask, jj - off, self.torch.full_like(jj, -1))
-
-    def gather_columns(self, a, idx):
-        m = a.shape[0]
-        idx = idx.contiguous()
-        out = self.empty(m, idx.numel())
-        self._raise(self.lib.lr_gather_columns_d(self.ctx.h, m, idx.numel(), a.data_ptr(), self.ld(a),
-                                                 idx.data_ptr(), out.data_ptr(), self.ld(out)))
-        return out
-
-    def gather_rows(self, a, idx):
-        n = a.shape[1]
-        idx = idx.contiguous()
-        out = self.empty(idx.numel(), n)
-        self._raise(self.lib.lr_gather_rows_d(self.ctx.h, idx.numel(), n, a.data_ptr(), self.ld(a), idx.data_ptr(),
-                                              out.data_ptr(), self.ld(out)))
-        return out
-
-    def tsid_from_c(self, c, k, strategy):
-        m = c.shape[0]
-        c = self.cm(c)
-        rp = self.torch.empty(m, dtype=self.torch.int64, device=self.dev)
-        rc = self.empty(k, max(m - k, 1))
-        sk = self.empty(k, k)
-        self._raise(self.lib.lr_tsid_from_skeleton_columns_d(self.ctx.h, m, k, c.data_ptr(), self.ld(c),
-                                                             strategy._c(), rp.data_ptr(), rc.data_ptr(),
-                                                             sk.data_ptr()))
-        return rp, rc[:, : m - k], sk
-
-    def transpose(self, x):
-        m, n = x.shape
-        x = self.cm(x)
-        out = self.empty(n, m)
-        self._raise(self.lib.lr_transpose_d(self.ctx.h, m, n, x.data_ptr(), self.ld(x), out.data_ptr(),
-                                            self.ld(out)))
-        return out
-
-    def gemm_tn(self, p, q):
-        K, M = p.shape
-        K2, N = q.shape
-        assert K == K2
-        p, q = self.cm(p), self.cm(q)
-        out = self.empty(M, N)
-        self._raise(self.lib.lr_gemm_tn_d(self.ctx.h, M, N, K, p.data_ptr(), self.ld(p), q.data_ptr(), self.ld(q),
-                                          out.data_ptr(), self.ld(out)))
-        return out
-
-    def cholesky(self, g):
-        out = self._contig_copy(g)
-        self._raise(self.lib.lr_cholesky_upper_d(self.ctx.h, out.shape[0], out.data_ptr(), self.ld(out)))
-        return out
-
-    def _contig_copy(self, g):
-        out = self.empty(g.shape[0], g.shape[1])
-        out.copy_(g)
-        return out
-
-    def tri_inv(self, r):
-        r = self.cm(r)
-        out = self.empty(r.shape[0], r.shape[1])
-        self._raise(self.lib.lr_tri_upper_inverse_d(self.ctx.h, r.shape[0], r.data_ptr(), self.ld(r), out.data_ptr(),
-                                                    self.ld(out)))
-        return out
-
-    def cholqr2(self, x):
-        rows, k = x.shape
-        x = self.cm(x)
-        r, ri = self.empty(k, k), self.empty(k, k)
-        ok = ctypes.c_int(0)
-        self._raise(self.lib.lr_cholqr2_d(self.ctx.h, rows, k, x.data_ptr(), self.ld(x), r.data_ptr(), ri.data_ptr(),
-                                          ctypes.byref(ok)))
-        return r, ri, bool(ok.value)
+# ---------------------------------------------------------------- host protocol
+def cpqr_sharded(be, comm, w_local, off: int, n_total: int, steps: int, krows: int):
+    """cpqr.hpp:32-114 on the column-sharded short-wide matrix: per step one
+    all-gather of the ranks' pivot candidates; the backend applies the
+    winner's reflector to the owned columns.  Returns the replicated
+    permutation (n_total) and the sign-fixed top `krows` rows of R in logical
+    column order (krows x n_total)."""
+    st = be.shard_begin(w_local, off)
+    for s in range(steps):
+        cands = comm.all_gather_flat(be.shard_candidate(st))
+        be.shard_step(st, s, cands)
+    perm_part, s_part = be.shard_scatter(st, n_total, steps, krows)
+    return comm.all_reduce_sum(perm_part), comm.all_reduce_sum(s_part)
 
 
 def randomized_cur_sharded(be, comm, a_local, col_offset: int, n_total: int, k: int, oversample: int = 10,
                            seed: int = 0, strategy=None) -> Dict[str, Any]:
-    """Column-sharded randomized CUR with U = C^+ A R^+ (see module docstring).
-    Returns the replicated factors (C, U, full R, both index sets, both
-    coefficient blocks, skeleton)."""
-    from .lowrank import SolveStrategy
-    strategy = strategy or SolveStrategy.automatic()
+    """Column-sharded randomized CUR with U = C^+ A R^+ (module docstring), the
+    host form of lr_randomized_cur_sharded_d.  Returns the replicated factors
+    (C, U, both index sets, both coefficient blocks, skeleton) and this
+    rank's block of R."""
     m, n_g = a_local.shape
     ell = k + oversample
-    be.cache_operand(a_local)  # the shard enters the sketch and A^T Q_c: split it once (Ozaki engine)
-    try:
-        y_local = be.sketch(a_local, ell, seed)
-        y = comm.all_gather_cols(y_local)
-        assert y.shape[1] == n_total
-        piv, coeff = be.id_from_sample(y, k, strategy)
-        own = be.owned_index(piv[:k], col_offset, n_g)
-        c = comm.all_reduce_sum(be.gather_columns(a_local, own))
-        row_piv, row_coeff, skeleton = be.tsid_from_c(c, k, strategy)
-        r_local = be.gather_rows(a_local, row_piv[:k])
-        # C = Qc Rc (replicated)
-        rc, rci, ok_c = be.cholqr2(c)
-        # R^T = Qr Sr over the column blocks (CholeskyQR2 with all-reduced Gram matrices)
-        rt_local = be.transpose(r_local)
-        s1 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(rt_local, rt_local)))
-        s1i = be.tri_inv(s1)
-        q1_local = be.gemm_tn(r_local, s1i)
-        s2 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(q1_local, q1_local)))
-        s = be.gemm_tn(be.transpose(s2), s1)
-        si = be.tri_inv(s)
-        if not ok_c:
-            raise NotImplementedError("sharded CUR: C is too ill-conditioned for CholeskyQR2 (use the 1-GPU path)")
-        qr_local = be.gemm_tn(r_local, si)
-        qc = be.gemm_tn(be.transpose(c), rci)
-        xt_local = be.gemm_tn(a_local, qc)
-        w = comm.all_reduce_sum(be.gemm_tn(xt_local, qr_local))
-        t1 = be.gemm_tn(be.transpose(rci), w)
-        u = be.gemm_tn(be.transpose(t1), be.transpose(si))
-        r = comm.all_gather_cols(r_local)
-    finally:
-        be.clear_operand_cache()
-    return dict(col_pivots=piv, row_pivots=row_piv, c=c, u=u, r=r, col_coeff=coeff, row_coeff=row_coeff,
-                skeleton=skeleton)
+    y_local = be.sketch(a_local, ell, seed)
+    perm, s1 = cpqr_sharded(be, comm, y_local, col_offset, n_total, min(ell, n_total), k)
+    coeff = be.coeff_solve(s1[:, :k], s1[:, k:], strategy)
+    own = be.owned_index(perm[:k], col_offset, n_g)
+    c = comm.all_reduce_sum(be.gather_columns(a_local, own))
+    r0, m_g = shard_bounds(m, comm.world, comm.rank)
+    row_perm, s1r = cpqr_sharded(be, comm, be.transpose(c[r0:r0 + m_g, :]), r0, m, k, k)
+    row_coeff = be.coeff_solve(s1r[:, :k], s1r[:, k:], strategy)
+    skeleton = be.gather_rows(c, row_perm[:k])
+    r_local = be.gather_rows(a_local, row_perm[:k])
+    # C = Qc Rc (replicated); R^T = Qr Sr by CholeskyQR2 with all-reduced Gram matrices
+    rc, rci, ok_c = be.cholqr2(c)
+    rt_local = be.transpose(r_local)
+    s1g = be.cholesky(comm.all_reduce_sum(be.gemm_tn(rt_local, rt_local)))
+    q1_local = be.gemm_tn(r_local, be.tri_inv(s1g))
+    s2 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(q1_local, q1_local)))
+    sr = be.gemm_tn(be.transpose(s2), s1g)
+    sri = be.tri_inv(sr)
+    if not ok_c:
+        raise RuntimeError("host protocol: C is too ill-conditioned for CholeskyQR2 "
+                           "(the device path takes the truncated pseudoinverse route)")
+    qr_local = be.gemm_tn(r_local, sri)
+    qc = be.gemm_tn(be.transpose(c), rci)
+    xt_local = be.gemm_tn(a_local, qc)
+    w = comm.all_reduce_sum(be.gemm_tn(xt_local, qr_local))
+    t1 = be.gemm_tn(be.transpose(rci), w)
+    u = be.gemm_tn(be.transpose(t1), be.transpose(sri))
+    return dict(col_pivots=perm, row_pivots=row_perm, c=c, u=u, r_local=r_local, col_coeff=coeff,
+                row_coeff=row_coeff, skeleton=skeleton)
 
 
-def shard_bounds(n: int, world: int, rank: int):
-    """Contiguous column block of rank `rank` (sizes differ by at most one)."""
-    lo = n * rank // world
-    hi = n * (rank + 1) // world
-    return lo, hi - lo
+# ---------------------------------------------------------------- device (product) path
+def attach_nccl(ctx, world: Optional[int] = None, rank: Optional[int] = None) -> None:
+    """Bind an NCCL communicator to the library context: rank 0 makes the
+    unique id (lr_nccl_get_unique_id), torch.distributed carries it to the
+    other ranks, every rank calls lr_ctx_attach_comm.  Without an initialised
+    process group (one process) a 1-rank communicator is made."""
+    from .lowrank import _raise
+    lib = ctx.lib
+    if world is None or rank is None:
+        try:
+            import torch.distributed as dist
+            inited = dist.is_initialized()
+        except Exception:
+            inited = False
+        world = dist.get_world_size() if inited else 1
+        rank = dist.get_rank() if inited else 0
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _raise(lib.lr_nccl_get_unique_id(uid))
+    if world > 1:
+        import torch.distributed as dist
+        obj = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+    _raise(lib.lr_ctx_attach_comm(ctx.h, uid, int(world), int(rank)))
+
+
+def detach_nccl(ctx) -> None:
+    from .lowrank import _raise
+    _raise(ctx.lib.lr_ctx_detach_comm(ctx.h))
+
+
+def randomized_cur_sharded_device(ctx, a_local, col_offset: int, n_total: int, k: int, cfg=None, strategy=None,
+                                  pinv_threshold: float = 1e-12, u_mode: Optional[int] = None,
+                                  out: Optional[dict] = None) -> dict:
+    """lr_randomized_cur_sharded_d: this rank's column block a_local (m x n_g,
+    column-major CUDA tensor) of the m x n_total matrix.  Replicated outputs
+    (col_pivots, row_pivots, c, u, col_coeff, row_coeff, skeleton) plus r_local
+    (k x n_g).  Needs attach_nccl(ctx) on every rank when n_g < n_total."""
+    import torch
+
+    from .lowrank import (U_CPINV_A_RPINV, SketchConfig, SolveStrategy, _colmajor_ld, _dptr, _raise,
+                          empty_colmajor, on_torch_stream)
+    m, n_g = a_local.shape
+    dev = a_local.device
+    if out is None:
+        out = {
+            "col_pivots": torch.empty(n_total, dtype=torch.int64, device=dev),
+            "row_pivots": torch.empty(m, dtype=torch.int64, device=dev),
+            "c": empty_colmajor(m, k, dev), "u": empty_colmajor(k, k, dev),
+            "r_local": empty_colmajor(k, max(n_g, 1), dev),
+            "col_coeff": empty_colmajor(k, max(n_total - k, 1), dev),
+            "row_coeff": empty_colmajor(k, max(m - k, 1), dev), "skeleton": empty_colmajor(k, k, dev),
+        }
+    with on_torch_stream(ctx):
+        _raise(ctx.lib.lr_randomized_cur_sharded_d(
+            ctx.h, m, n_g, int(col_offset), int(n_total), _dptr(a_local), _colmajor_ld(a_local), k,
+            (cfg or SketchConfig())._c(), (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold),
+            int(U_CPINV_A_RPINV if u_mode is None else u_mode), _dptr(out["col_pivots"]), _dptr(out["row_pivots"]),
+            _dptr(out["c"]), _dptr(out["u"]), _dptr(out["r_local"]), _dptr(out["col_coeff"]),
+            _dptr(out["row_coeff"]), _dptr(out["skeleton"])))
+    return out
+
+
+def cpqr_sharded_device(ctx, w_local, col_offset: int, n_total: int, k: int):
+    """lr_cpqr_sharded_d: pivots (n_total) and the sign-fixed top k rows of R in
+    logical order (k x n_total), replicated."""
+    import torch
+
+    from .lowrank import _colmajor_ld, _dptr, _raise, empty_colmajor, on_torch_stream
+    m, n_g = w_local.shape
+    piv = torch.empty(n_total, dtype=torch.int64, device=w_local.device)
+    s = empty_colmajor(k, n_total, w_local.device)
+    with on_torch_stream(ctx):
+        _raise(ctx.lib.lr_cpqr_sharded_d(ctx.h, m, n_g, int(col_offset), int(n_total), _dptr(w_local),
+                                         _colmajor_ld(w_local), k, _dptr(piv), _dptr(s)))
+    return piv, s
+
+
+def set_shard_emulation(ctx, nshards: int) -> None:
+    """Single-GPU test vehicle: without a communicator, run the sharded CPQRs as
+    `nshards` column blocks in this process (lr_ctx_set_shard_emulation)."""
+    from .lowrank import _raise
+    _raise(ctx.lib.lr_ctx_set_shard_emulation(ctx.h, int(nshards)))

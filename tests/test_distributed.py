@@ -65,20 +65,88 @@ def backsub_np(s11, s12):
     return t
 
 
-class NumpyBackend:
-    def cache_operand(self, a):
-        pass
+class NumpyShard:
+    """State of one rank's block in the sharded CPQR (the numpy mirror of
+    csrc/shard.cu: running / exact norms, logical positions, pivoted flags)."""
 
-    def clear_operand_cache(self):
-        pass
+    def __init__(self, w, off):
+        self.w = np.array(w, dtype=float, order="F")
+        self.off = off
+        self.nrm = (self.w * self.w).sum(axis=0)
+        self.nx = self.nrm.copy()
+        self.pos = off + np.arange(self.w.shape[1])
+        self.done = np.zeros(self.w.shape[1], dtype=bool)
+        self.rdiag = []
+        self.recomputes = 0
+
+
+class NumpyBackend:
+    """Shard primitives in numpy (test infrastructure: the protocol under test
+    is distributed.py's; the checker is the oracle)."""
 
     def sketch(self, a, ell, seed):
         return np.asfortranarray(inputs.gaussian_np(ell, a.shape[0], seed) @ a)
 
-    def id_from_sample(self, y, k, strategy):
-        piv, s = cpqr_np(y, min(y.shape))
-        s1 = s[:k]
-        return piv, backsub_np(s1[:, :k], s1[:, k:])
+    # --- sharded CPQR (cpqr.hpp:48-85 per owned column)
+    def shard_begin(self, w, off):
+        return NumpyShard(w, off)
+
+    def shard_candidate(self, st):
+        m = st.w.shape[0]
+        act = np.flatnonzero(~st.done)
+        if act.size == 0:
+            return np.concatenate([[-np.inf, 0.0, -1.0, 0.0], np.zeros(m)])
+        best = max(act, key=lambda j: (st.nrm[j], -st.pos[j]))  # largest norm, then lowest position
+        return np.concatenate([[st.nrm[best], st.pos[best], st.off + best, 1.0], st.w[:, best]])
+
+    def shard_step(self, st, s, cands):
+        valid = [r for r in range(cands.shape[0]) if cands[r, 3] != 0.0]
+        win = max(valid, key=lambda r: (cands[r, 0], -cands[r, 1]))
+        wpos, wcol = int(cands[win, 1]), int(cands[win, 2])
+        x = cands[win, 4 + s:].copy()
+        cn = np.sqrt(x @ x)
+        alpha = x[0]
+        apply = cn > 0.0
+        beta = (-cn if alpha >= 0 else cn) if apply else alpha
+        tau = (beta - alpha) / beta if apply else 0.0
+        v = np.concatenate([[1.0], x[1:] / (alpha - beta)]) if apply else None
+        st.rdiag.append(beta)
+        for j in range(st.w.shape[1]):
+            if st.done[j]:
+                continue
+            if st.off + j == wcol:
+                if apply:
+                    st.w[s, j] = beta
+                    st.w[s + 1:, j] = v[1:]
+                st.done[j] = True
+                st.pos[j] = s
+                continue
+            if st.pos[j] == s:
+                st.pos[j] = wpos
+            col = st.w[s:, j]
+            if apply:
+                col -= (tau * v) * (v @ col)
+            st.nrm[j] -= st.w[s, j] ** 2
+            if st.nrm[j] < 1e-6 * st.nx[j]:
+                st.nrm[j] = (st.w[s + 1:, j] ** 2).sum()
+                st.nx[j] = st.nrm[j]
+                st.recomputes += 1
+
+    def shard_scatter(self, st, n_total, steps, krows):
+        perm = np.zeros(n_total, dtype=np.int64)
+        s_out = np.zeros((krows, n_total), order="F")
+        sign = np.where(np.asarray(st.rdiag[:krows]) < 0.0, -1.0, 1.0)
+        for j in range(st.w.shape[1]):
+            p = st.pos[j]
+            perm[p] = st.off + j
+            col = st.w[:krows, j].copy()
+            if p < steps:
+                col[np.arange(krows) > p] = 0.0
+            s_out[:, p] = sign * col
+        return perm, s_out
+
+    def coeff_solve(self, s11, s12, strategy):
+        return backsub_np(s11, s12)
 
     def owned_index(self, j, off, n_g):
         return np.where((j >= off) & (j < off + n_g), j - off, -1)
@@ -92,10 +160,6 @@ class NumpyBackend:
 
     def gather_rows(self, a, idx):
         return np.asfortranarray(a[idx, :])
-
-    def tsid_from_c(self, c, k, strategy):
-        piv, s = cpqr_np(c.T, k)
-        return piv, backsub_np(s[:, :k], s[:, k:]), np.asfortranarray(c[piv[:k], :])
 
     def transpose(self, x):
         return np.asfortranarray(x.T)
@@ -133,8 +197,12 @@ def _worker(rank, world, port, out_path):
                            lambda t: np.asfortranarray(t.numpy()))
         res = D.randomized_cur_sharded(NumpyBackend(), comm, np.asfortranarray(a[:, off:off + n_g]), off,
                                        a.shape[1], k, oversample=5, seed=3)
-        if rank == 0:
-            np.savez(out_path, **{kk: np.asarray(v) for kk, v in res.items()})
+        # R is returned by column block: gather it here for the comparison only
+        r = comm.all_reduce_sum(np.asfortranarray(
+            np.pad(res.pop("r_local"), ((0, 0), (off, a.shape[1] - off - n_g)))))
+        res["r"] = r
+        res["bytes_gathered"] = np.array(comm.bytes_gathered)
+        np.savez(out_path + f".{rank}.npz", **{kk: np.asarray(v) for kk, v in res.items()})
     finally:
         dist.destroy_process_group()
 
@@ -145,34 +213,61 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2])
+class One:
+    world, rank = 1, 0
+    bytes_sent = 0
+
+    def all_gather_flat(self, x):
+        return np.asarray(x).reshape(1, -1)
+
+    def all_reduce_sum(self, x):
+        return x
+
+
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_protocol_matches_single_process(tmp_path, world, oracle):
-    out = str(tmp_path / "dist.npz")
+    out = str(tmp_path / "dist")
     mp.spawn(_worker, args=(world, free_port(), out), nprocs=world, join=True)
-    got = np.load(out)
     a, k = make_problem()
-
-    class One:
-        world, rank = 1, 0
-
-        def all_gather_cols(self, x):
-            return x
-
-        def all_reduce_sum(self, x):
-            return x
-
     ref = D.randomized_cur_sharded(NumpyBackend(), One(), a, 0, a.shape[1], k, oversample=5, seed=3)
-    assert np.array_equal(got["col_pivots"], ref["col_pivots"])
-    assert np.array_equal(got["row_pivots"], ref["row_pivots"])
-    assert np.array_equal(got["c"], ref["c"]) and np.array_equal(got["r"], ref["r"])
-    assert np.array_equal(got["skeleton"], ref["skeleton"])
-    assert np.linalg.norm(got["u"] - ref["u"]) <= 1e-12 * np.linalg.norm(ref["u"])
-    # and against the CPU oracle of the reference algorithm
     o = oracle.randomized_cur(a, k, 5, 3, u_mode=1)
-    assert np.array_equal(got["col_pivots"], o["col_pivots"])
-    assert np.array_equal(got["row_pivots"], o["row_pivots"])
-    assert np.linalg.norm(got["u"] - o["u"]) <= 1e-10 * np.linalg.norm(o["u"])
-    assert np.linalg.norm(got["col_coeff"] - o["col_coeff"]) <= 1e-10 * np.linalg.norm(o["col_coeff"])
+    ell = k + 5
+    for rank in range(world):
+        got = np.load(out + f".{rank}.npz")
+        # every rank holds the same replicated factors, bitwise equal to one process
+        for key in ("col_pivots", "row_pivots", "c", "skeleton", "col_coeff", "row_coeff"):
+            assert np.array_equal(got[key], ref[key]), key
+        assert np.array_equal(got["r"], ref["r_local"])
+        assert np.linalg.norm(got["u"] - ref["u"]) <= 1e-12 * np.linalg.norm(ref["u"])
+        # and against the CPU oracle of the reference algorithm
+        assert np.array_equal(got["col_pivots"], o["col_pivots"])
+        assert np.array_equal(got["row_pivots"], o["row_pivots"])
+        assert np.linalg.norm(got["u"] - o["u"]) <= 1e-10 * np.linalg.norm(o["u"])
+        assert np.linalg.norm(got["col_coeff"] - o["col_coeff"]) <= 1e-10 * np.linalg.norm(o["col_coeff"])
+        assert np.linalg.norm(got["row_coeff"] - o["row_coeff"]) <= 1e-10 * np.linalg.norm(o["row_coeff"])
+        # the sample Y (ell x n) is never gathered: the only all-gathers are the
+        # per-step pivot candidates, one header + one column per rank and step
+        assert int(got["bytes_gathered"]) == 8 * ((4 + ell) * ell + (4 + k) * k)
+
+
+def test_sharded_cpqr_recompute_and_pivots_match_oracle(oracle):
+    """The sharded CPQR protocol on uneven blocks (including an empty one)
+    reproduces the oracle's pivots, R rows and exact-norm recompute count."""
+    a = inputs.synthetic_np(inputs.scaled(inputs.CONFIGS["c4"], 40, 300, width=40, k=30))
+    k = 30
+    o = oracle.cpqr(a, k, want_q=False)
+    be = NumpyBackend()
+    for bounds in ([(0, 300)], [(0, 0), (0, 170), (170, 130)], [(0, 100), (100, 100), (200, 100)]):
+        states = [be.shard_begin(a[:, lo:lo + w], lo) for lo, w in bounds]
+        for s in range(k):
+            cands = np.stack([be.shard_candidate(st) for st in states])
+            for st in states:
+                be.shard_step(st, s, cands)
+        perm = sum(be.shard_scatter(st, 300, k, k)[0] for st in states)
+        s_rows = sum(be.shard_scatter(st, 300, k, k)[1] for st in states)
+        assert np.array_equal(perm, o["pivots"])
+        assert np.linalg.norm(s_rows - o["s"]) <= 1e-12 * np.linalg.norm(o["s"])
+        assert sum(st.recomputes for st in states) == o["recomputes"]
 
 
 def test_shard_bounds_cover_columns():
