@@ -112,6 +112,7 @@ def kernel_rooflines(cfg, st, per_step, engine):
                              "bound": "tensor", "achieved": round(ach, 1), "peak": round(i8, 1), "unit": "TOP/s",
                              "frac": round(ach / i8, 4), "traffic": traffic.get(name),
                              "peak_source": i8_src,
+                             "frac_vs_burst": round(ach / int8_burst(), 4) if int8_burst() else None,
                              "algorithmic": f"16 moduli x 2*{cols}*m*n = {ops:.4e} int8 op per launch"}
         if st.get("ozaki_split"):
             # the split stage closes twice per CUR (A + Omega before the sketch, Q_c before
@@ -165,6 +166,14 @@ def read_peaks():
 
 
 INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_int8_peak.json")
+
+
+def int8_burst():
+    try:
+        with open(INT8_PEAK_FILE) as f:
+            return float(json.load(f)["int8_tops"])
+    except Exception:
+        return None
 
 
 def int8_peak(peaks):
@@ -541,7 +550,17 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         est, det = cpu_reference_estimate(args.cpu_sample, os.cpu_count() or 1)
         cpu = {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-               "sample": det["sample"] + "; stage times extrapolated to 65536^2", "details": det}
+               "sample": det["sample"] + "; stage times extrapolated to 65536^2 (bounded sample, this run)",
+               "details": det}
+        try:  # the full-size CPU run of the same configuration (tools/c4_full_oracle.py on a GPU box)
+            with open(os.path.join(ROOT, "profiles", "r02_c4_full_cpu.json")) as f:
+                full = json.load(f)
+            cpu["measured_full_size"] = {"value": full["total_seconds"], "unit": "s", "cores": full["threads"],
+                                         "cpu_model": full["cpu_model"], "stage_seconds": full["stage_seconds"],
+                                         "source": "profiles/r02_c4_full_cpu.json (one full 65536^2 oracle run; "
+                                                   "bench.py --impl reference repeats it)"}
+        except Exception:
+            pass
     line = {
         "metric": "time-to-CUR (s), randomized CUR 65536^2 k=500",
         "value": ms / 1e3,

@@ -131,8 +131,10 @@ def randomized_cur_sharded(be, comm, a_local, col_offset: int, n_total: int, k: 
     s2 = be.cholesky(comm.all_reduce_sum(be.gemm_tn(q1_local, q1_local)))
     sr = be.gemm_tn(be.transpose(s2), s1g)
     sri = be.tri_inv(sr)
-    if not ok_c:
-        raise RuntimeError("host protocol: C is too ill-conditioned for CholeskyQR2 "
+    # the same acceptance as the device path: ||Sr||_F ||Sr^-1||_F < min(1e7, 1/threshold)
+    ok_r = be.cond_bound(sr, sri) < 1e7
+    if not (ok_c and ok_r):
+        raise RuntimeError("host protocol: C or R is too ill-conditioned for CholeskyQR2 "
                            "(the device path takes the truncated pseudoinverse route)")
     qr_local = be.gemm_tn(r_local, sri)
     qc = be.gemm_tn(be.transpose(c), rci)

@@ -173,6 +173,9 @@ class NumpyBackend:
     def tri_inv(self, r):
         return np.asfortranarray(np.linalg.inv(r))
 
+    def cond_bound(self, r, ri):
+        return np.linalg.norm(r) * np.linalg.norm(ri)
+
     def cholqr2(self, x):
         r1 = self.cholesky(x.T @ x)
         q1 = x @ np.linalg.inv(r1)
