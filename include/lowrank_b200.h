@@ -301,6 +301,48 @@ int lr_randomized_cur_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t
                                 int64_t* col_pivots, int64_t* row_pivots, double* c, double* u, double* r_local,
                                 double* col_coeff, double* row_coeff, double* skeleton);
 
+/* ---- verifiers at scale (verify.hpp:14-166).  The reference takes every
+   spectral norm as sigma_1 of a full SVD of the materialised m x n residual
+   (svd.hpp:185-189); here the residual A - X Y stays an operator and sigma_1
+   comes from a seeded block Krylov iteration on E^T E (converged to 1e-14
+   relative, from below); Frobenius norms by the fused residual GEMM. ---- */
+typedef struct lr_error_report { /* verify.hpp:22-28 */
+  double abs_spectral, rel_spectral, abs_frob, rel_frob;
+  int rel_is_absolute;
+} lr_error_report;
+typedef struct lr_lemma1_report { /* verify.hpp:60-66 */
+  double lhs, rhs, e_norm, etilde_norm;
+  int holds;
+} lr_lemma1_report;
+typedef struct lr_lemma2_report { /* verify.hpp:86-95 */
+  double etilde_norm, fe_norm, entry_diff, e_norm, t_norm, bound_rhs;
+  int holds, bound_holds;
+} lr_lemma2_report;
+typedef struct lr_corollary_report { /* verify.hpp:136-143 */
+  double lhs, bound, t_norm, e_norm, ceiling;
+  int holds;
+} lr_corollary_report;
+/* ||A - X Y||_2 and ||A - X Y||_F (X m x k, Y k x n; k = 0: of A); either output may be NULL */
+int lr_residual_norms_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                        const double* x, int64_t ldx, const double* y, int64_t ldy, double* spectral,
+                        double* frobenius);
+/* verify.hpp:31-56 error_report(a, approx) for approx = X Y */
+int lr_error_report_lowrank_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                              const double* x, int64_t ldx, const double* y, int64_t ldy, lr_error_report* out);
+/* verify.hpp:70-80 verify_lemma1(a, cur, col_id, row_basis): the CUR given by its
+   index sets, coefficient blocks and U (C, R, W rebuilt from A) */
+int lr_verify_lemma1_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots,
+                       const double* row_coeff, const double* u, lr_lemma1_report* out);
+/* verify.hpp:97-130 verify_lemma2(a, col_id, row_id) */
+int lr_verify_lemma2_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots,
+                       const double* row_coeff, lr_lemma2_report* out);
+/* verify.hpp:144-160 verify_corollary(a, cur, col_id, strategy) */
+int lr_verify_corollary_d(lr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                          const int64_t* col_pivots, const double* col_coeff, const double* u,
+                          lr_solve_strategy strategy, lr_corollary_report* out);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -41,6 +41,27 @@ class lr_stats(ctypes.Structure):
                 ("concurrent_tail", ctypes.c_int)]
 
 
+class lr_error_report(ctypes.Structure):
+    _fields_ = [("abs_spectral", ctypes.c_double), ("rel_spectral", ctypes.c_double),
+                ("abs_frob", ctypes.c_double), ("rel_frob", ctypes.c_double), ("rel_is_absolute", ctypes.c_int)]
+
+
+class lr_lemma1_report(ctypes.Structure):
+    _fields_ = [("lhs", ctypes.c_double), ("rhs", ctypes.c_double), ("e_norm", ctypes.c_double),
+                ("etilde_norm", ctypes.c_double), ("holds", ctypes.c_int)]
+
+
+class lr_lemma2_report(ctypes.Structure):
+    _fields_ = [("etilde_norm", ctypes.c_double), ("fe_norm", ctypes.c_double), ("entry_diff", ctypes.c_double),
+                ("e_norm", ctypes.c_double), ("t_norm", ctypes.c_double), ("bound_rhs", ctypes.c_double),
+                ("holds", ctypes.c_int), ("bound_holds", ctypes.c_int)]
+
+
+class lr_corollary_report(ctypes.Structure):
+    _fields_ = [("lhs", ctypes.c_double), ("bound", ctypes.c_double), ("t_norm", ctypes.c_double),
+                ("e_norm", ctypes.c_double), ("ceiling", ctypes.c_double), ("holds", ctypes.c_int)]
+
+
 # every exported symbol of include/lowrank_b200.h with its argument types
 SIGNATURES = {
     "lr_last_error": ([], ctypes.c_char_p),
@@ -126,6 +147,16 @@ SIGNATURES = {
     "lr_tri_upper_inverse_d": ([ctypes.c_void_p, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_cholqr2_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_dp, c_dp, ctypes.POINTER(ctypes.c_int)],
                      ctypes.c_int),
+    "lr_residual_norms_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64,
+                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "lr_error_report_lowrank_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64,
+                                   ctypes.POINTER(lr_error_report)], ctypes.c_int),
+    "lr_verify_lemma1_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp, c_ip, c_dp, c_dp,
+                            ctypes.POINTER(lr_lemma1_report)], ctypes.c_int),
+    "lr_verify_lemma2_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp, c_ip, c_dp,
+                            ctypes.POINTER(lr_lemma2_report)], ctypes.c_int),
+    "lr_verify_corollary_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp, c_dp,
+                               lr_solve_strategy, ctypes.POINTER(lr_corollary_report)], ctypes.c_int),
     "lr_nccl_get_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lr_ctx_attach_comm": ([ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "lr_ctx_detach_comm": ([ctypes.c_void_p], ctypes.c_int),

@@ -1623,6 +1623,163 @@ void randomized_cur_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t of
   mark(c, "u_small");
 }
 
+// ---------------------------------------------------------------- verifiers (verify.hpp:14-166) at scale
+// The reference evaluates every spectral norm as sigma_1 of a full Jacobi SVD
+// of the materialised m x n residual (svd.hpp:185-189, verify.hpp:39-124).
+// Here the residuals stay operators (E = A - X Y applied to blocks of
+// vectors through A, A^T, X, Y) and sigma_1 comes from a block Krylov
+// iteration on E^T E: a seeded Gaussian start block, every Krylov block made
+// orthonormal against the basis (block Gram-Schmidt twice, then CholeskyQR2 /
+// Householder), Ritz value sigma_1 = sqrt(lambda_max(Z^T Z)) with Z = E K over
+// the whole basis (Jacobi SVD of the small Gram matrix).  It increases
+// monotonically to sigma_1(E) and stops when two consecutive values agree to
+// 1e-14 relative or the basis is exhausted.
+using BlockOp = std::function<void(int64_t r, const double* in, int64_t ldi, double* out, int64_t ldo)>;
+
+double krylov_sigma1(lr_ctx* c, int64_t rows, int64_t cols, const BlockOp& E, const BlockOp& Et, uint64_t seed,
+                     int64_t b = 32, int qmax = 12) {
+  const int64_t cap = std::min<int64_t>((int64_t)(qmax + 1) * b, std::min(rows, cols));
+  if (cap < 1) return 0.0;
+  b = std::min(b, cap);
+  const int64_t ldk = even(cols), ldz = even(rows), ldkt = even(cap);
+  DBuf<double> K((size_t)ldk * cap, c->st), Kt((size_t)ldkt * cols, c->st), Z((size_t)ldz * cap, c->st);
+  DBuf<double> blk((size_t)ldk * b, c->st), H((size_t)ldkt * b, c->st), part(4 * num_sms() + 4, c->st),
+      nrm(2, c->st);
+  gaussian_matrix(cols, b, seed, blk, ldk, false, c->st);
+  int64_t nb = 0;
+  double prev = -1.0, est = 0.0;
+  for (int it = 0; it <= qmax && nb < cap; ++it) {
+    const int64_t r0 = std::min(b, cap - nb);
+    // block Gram-Schmidt (twice) against the basis; a block that vanishes
+    // against it means the Krylov space is exhausted
+    frob2(cols, r0, blk, ldk, part, nrm, c->st);
+    for (int pass = 0; pass < 2 && nb > 0; ++pass) {
+      gemm(c, nb, r0, cols, K, ldk, blk, ldk, H, ldkt);                  // H = K^T blk
+      gemm(c, cols, r0, nb, Kt, ldkt, H, ldkt, blk, ldk, -1.0, 1.0);      // blk -= K H
+    }
+    frob2(cols, r0, blk, ldk, part, nrm.p + 1, c->st);
+    d2h_mapped(c, c->h_scal, nrm.p, 2 * sizeof(double));
+    sync(c);
+    if (!(c->h_scal[1] > 1e-24 * c->h_scal[0]) || c->h_scal[1] == 0.0) break;
+    const int64_t r = orth_cols_core(c, cols, r0, blk, ldk, K.p + nb * ldk, ldk);
+    if (r < 1) break;
+    transpose_matrix(cols, r, K.p + nb * ldk, ldk, Kt.p + nb, ldkt, c->st);
+    E(r, K.p + nb * ldk, ldk, Z.p + nb * ldz, ldz);  // Z(:, new) = E K(:, new)
+    const int64_t nb_new = nb + r;
+    DBuf<double> G((size_t)nb_new * nb_new, c->st), u((size_t)nb_new * nb_new, c->st), s(nb_new, c->st),
+        v((size_t)nb_new * nb_new, c->st);
+    gemm(c, nb_new, nb_new, rows, Z, ldz, Z, ldz, G, nb_new);  // Z^T Z
+    svd_core(c, nb_new, nb_new, G, nb_new, u, s, v);
+    d2h_mapped(c, c->h_scal, s.p, sizeof(double));
+    sync(c);
+    est = std::sqrt(std::max(0.0, c->h_scal[0]));
+    if (prev >= 0.0 && std::abs(est - prev) <= 1e-14 * est) break;
+    prev = est;
+    // next block: E^T E applied to the newest block
+    Et(r, Z.p + nb * ldz, ldz, blk, ldk);
+    nb = nb_new;
+    if (r < b) break;
+  }
+  return est;
+}
+
+// E = A - X Y (X m x k, Y k x n; k = 0: E = A) as a block operator.  At is A^T
+// (n x m, ld ldat): the column-major A serves E^T U = A^T U - Y^T (X^T U)
+// directly and At serves E V = A V - X (Y V) on the same GEMM.
+struct ResidualOp {
+  lr_ctx* c;
+  int64_t m, n, k;
+  const double *A, *At, *X, *Xt, *Y, *Yt;
+  int64_t lda, ldat, ldx, ldxt, ldy, ldyt;
+  void apply(int64_t r, const double* V, int64_t ldv, double* out, int64_t ldo) const {
+    gemm(c, m, r, n, At, ldat, V, ldv, out, ldo);  // A V
+    if (k > 0) {
+      DBuf<double> t((size_t)k * r, c->st);
+      gemm(c, k, r, n, Yt, ldyt, V, ldv, t, k);            // Y V
+      gemm(c, m, r, k, Xt, ldxt, t, k, out, ldo, -1.0, 1.0);  // -= X (Y V)
+    }
+  }
+  void apply_t(int64_t r, const double* U, int64_t ldu, double* out, int64_t ldo) const {
+    gemm(c, n, r, m, A, lda, U, ldu, out, ldo);  // A^T U
+    if (k > 0) {
+      DBuf<double> t((size_t)k * r, c->st);
+      gemm(c, k, r, m, X, ldx, U, ldu, t, k);               // X^T U
+      gemm(c, n, r, k, Y, ldy, t, k, out, ldo, -1.0, 1.0);  // -= Y^T (X^T U)
+    }
+  }
+};
+
+// the transposes a ResidualOp needs, owned
+struct ResidualBufs {
+  DBuf<double> Xt, Yt;
+};
+ResidualOp residual_op(lr_ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, const double* At,
+                       int64_t ldat, int64_t k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                       ResidualBufs& bufs) {
+  ResidualOp op{c, m, n, k, A, At, X, nullptr, Y, nullptr, lda, ldat, ldx, even(k), ldy, even(n)};
+  if (k > 0) {
+    bufs.Xt = DBuf<double>((size_t)even(k) * m, c->st);
+    bufs.Yt = DBuf<double>((size_t)even(n) * k, c->st);
+    transpose_matrix(m, k, X, ldx, bufs.Xt, even(k), c->st);
+    transpose_matrix(k, n, Y, ldy, bufs.Yt, even(n), c->st);
+    op.Xt = bufs.Xt;
+    op.Yt = bufs.Yt;
+  }
+  return op;
+}
+
+double op_sigma1(lr_ctx* c, const ResidualOp& op, uint64_t seed) {
+  return krylov_sigma1(
+      c, op.m, op.n, [&](int64_t r, const double* i, int64_t li, double* o, int64_t lo) { op.apply(r, i, li, o, lo); },
+      [&](int64_t r, const double* i, int64_t li, double* o, int64_t lo) { op.apply_t(r, i, li, o, lo); }, seed);
+}
+
+// ||A - X Y||_F by the fused residual GEMM (never forms X Y)
+double residual_frob(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* X,
+                     int64_t ldx, const double* Y, int64_t ldy) {
+  DBuf<double> part(4 * num_sms() + 4, c->st), res(2, c->st);
+  if (k == 0) {
+    frob2(m, n, a, lda, part, res, c->st);
+  } else {
+    const int64_t ldk = even(k);
+    DBuf<double> Xt((size_t)ldk * m, c->st), Yk((size_t)ldk * n, c->st);
+    transpose_matrix(m, k, X, ldx, Xt, ldk, c->st);
+    copy_matrix(k, n, Y, ldy, Yk, ldk, c->st);
+    const int tiles = gemm_tn_grid_ctas((int)m, (int)n);
+    DBuf<double> parts(std::max(tiles, 4 * num_sms()) + 4, c->st);
+    int np = 0;
+    gemm_tn_resid_sq(c->ws, (int)m, (int)n, (int)k, Xt, ldk, Yk, ldk, a, lda, parts, &np, c->st);
+    sum_partials(parts, np, res, c->st);
+  }
+  d2h_mapped(c, c->h_scal, res.p, sizeof(double));
+  sync(c);
+  return std::sqrt(c->h_scal[0]);
+}
+
+// the pieces of the verifiers: A^T, C = A(:, J), V^T = basis()^T (k x n), R = A(I, :), W^T (k x m)
+struct VerifyParts {
+  DBuf<double> At, C, Vt, R, Wt, W;
+};
+void basis_t(lr_ctx* c, int64_t n, int64_t k, const int64_t* piv, const double* coeff, int64_t ldc, double* out) {
+  DBuf<int64_t> inv(n, c->st);
+  inverse_perm(piv, n, inv, c->st);
+  basis_rows(inv, 0, n, k, coeff, ldc, out, c->st);  // out (k x n): column j = basis() row j
+}
+// ||T||_2 of a k x nc coefficient block (ld ldt): sqrt(lambda_max(T T^T)) (Jacobi SVD of the k x k Gram)
+double coeff_norm2(lr_ctx* c, int64_t k, int64_t nc, const double* t, int64_t ldt) {
+  if (nc == 0) return 0.0;
+  DBuf<double> Tt((size_t)even(nc) * k, c->st), G((size_t)k * k, c->st), u((size_t)k * k, c->st), s(k, c->st),
+      v((size_t)k * k, c->st);
+  transpose_matrix(k, nc, t, ldt, Tt, even(nc), c->st);
+  gemm(c, k, k, nc, Tt, even(nc), Tt, even(nc), G, k);
+  svd_core(c, k, k, G, k, u, s, v);
+  d2h_mapped(c, c->h_scal, s.p, sizeof(double));
+  sync(c);
+  return std::sqrt(std::max(0.0, c->h_scal[0]));
+}
+
+constexpr uint64_t kVerifySeed = 0x5eed1412ull;
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -2583,6 +2740,221 @@ int lr_randomized_cur_sharded_d(lr_ctx* c, int64_t m, int64_t n_local, int64_t c
     }
     randomized_cur_sharded_core(c, m, n_local, col_offset, n_total, a_local, lda, k, cfg, strat, thr, u_mode,
                                 col_pivots, row_pivots, C, U, r_local, col_coeff, row_coeff, skeleton);
+  });
+}
+
+
+// ---- verifiers at scale (verify.hpp:14-166; spectral norms by block Krylov on the residual operators)
+int lr_residual_norms_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const double* x,
+                        int64_t ldx, const double* y, int64_t ldy, double* spectral, double* frobenius) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "spectral_norm");
+    require_ld(m, lda, "spectral_norm");
+    if (k < 0 || k > std::min(m, n)) fail(LR_EINVAL, "residual_norms: rank out of range");
+    if (spectral) {
+      DBuf<double> At((size_t)even(n) * m, c->st);
+      transpose_matrix(m, n, a, lda, At, even(n), c->st);
+      ResidualBufs rb;
+      const ResidualOp op = residual_op(c, m, n, a, lda, At, even(n), k, x, ldx, y, ldy, rb);
+      *spectral = op_sigma1(c, op, kVerifySeed);
+    }
+    if (frobenius) *frobenius = residual_frob(c, m, n, a, lda, k, x, ldx, y, ldy);
+  });
+}
+
+int lr_error_report_lowrank_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                              const double* x, int64_t ldx, const double* y, int64_t ldy, lr_error_report* out) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "error_report");
+    require_ld(m, lda, "error_report");
+    if (!out) fail(LR_EINVAL, "error_report: null report");
+    DBuf<double> At((size_t)even(n) * m, c->st);
+    transpose_matrix(m, n, a, lda, At, even(n), c->st);
+    ResidualBufs r0, r1;
+    const double a2 = op_sigma1(c, residual_op(c, m, n, a, lda, At, even(n), 0, nullptr, 1, nullptr, 1, r0),
+                                kVerifySeed);
+    const double af = residual_frob(c, m, n, a, lda, 0, nullptr, 1, nullptr, 1);
+    lr_error_report rep{};
+    rep.abs_spectral = op_sigma1(c, residual_op(c, m, n, a, lda, At, even(n), k, x, ldx, y, ldy, r1), kVerifySeed);
+    rep.abs_frob = residual_frob(c, m, n, a, lda, k, x, ldx, y, ldy);
+    if (af == 0.0) {  // verify.hpp:41-44
+      rep.rel_is_absolute = 1;
+      rep.rel_spectral = rep.abs_spectral;
+      rep.rel_frob = rep.abs_frob;
+    } else {
+      rep.rel_spectral = rep.abs_spectral / a2;
+      rep.rel_frob = rep.abs_frob / af;
+    }
+    *out = rep;
+  });
+}
+
+namespace {
+// C = A(:, J), V^T, R = A(I, :), W, (C U) and A^T for the verifiers
+struct VerifyInputs {
+  DBuf<double> At, C, Ct, Vt, R, Wt, W, CU;
+};
+void verify_inputs(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k, const int64_t* col_piv,
+                   const double* col_coeff, const int64_t* row_piv, const double* row_coeff, const double* u,
+                   VerifyInputs& v) {
+  v.At = DBuf<double>((size_t)even(n) * m, c->st);
+  transpose_matrix(m, n, a, lda, v.At, even(n), c->st);
+  v.C = DBuf<double>((size_t)m * k, c->st);
+  gather_columns(m, k, a, lda, col_piv, v.C, m, c->st);
+  v.Vt = DBuf<double>((size_t)k * n, c->st);
+  basis_t(c, n, k, col_piv, col_coeff, k, v.Vt);
+  if (row_piv) {
+    v.R = DBuf<double>((size_t)k * n, c->st);
+    gather_rows(k, n, a, lda, row_piv, v.R, k, c->st);
+  }
+  if (row_piv && row_coeff) {
+    v.Wt = DBuf<double>((size_t)k * m, c->st);
+    basis_t(c, m, k, row_piv, row_coeff, k, v.Wt);
+    v.W = DBuf<double>((size_t)m * k, c->st);
+    transpose_matrix(k, m, v.Wt, k, v.W, m, c->st);
+  }
+  if (u) {  // reconstruct(cur) = (C U) R  (cur.hpp:77-80)
+    v.Ct = DBuf<double>((size_t)even(k) * m, c->st);
+    transpose_matrix(m, k, v.C, m, v.Ct, even(k), c->st);
+    v.CU = DBuf<double>((size_t)m * k, c->st);
+    gemm(c, m, k, k, v.Ct, even(k), u, k, v.CU, m);
+  }
+}
+}  // namespace
+
+int lr_verify_lemma1_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots,
+                       const double* row_coeff, const double* u, lr_lemma1_report* out) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "verify_lemma1");
+    require_rank_in_range(k, m, n, "verify_lemma1");
+    if (!out) fail(LR_EINVAL, "verify_lemma1: null report");
+    VerifyInputs v;
+    verify_inputs(c, m, n, a, lda, k, col_pivots, col_coeff, row_pivots, row_coeff, u, v);
+    ResidualBufs b0, b1, b2;
+    lr_lemma1_report rep{};
+    rep.e_norm = op_sigma1(c, residual_op(c, m, n, a, lda, v.At, even(n), k, v.C, m, v.Vt, k, b0), kVerifySeed);
+    rep.etilde_norm = op_sigma1(c, residual_op(c, m, n, a, lda, v.At, even(n), k, v.W, m, v.R, k, b1), kVerifySeed);
+    rep.lhs = op_sigma1(c, residual_op(c, m, n, a, lda, v.At, even(n), k, v.CU, m, v.R, k, b2), kVerifySeed);
+    rep.rhs = rep.e_norm + rep.etilde_norm;
+    rep.holds = rep.lhs <= rep.rhs * (1.0 + 1e-8);  // verify.hpp:77-78
+    *out = rep;
+  });
+}
+
+int lr_verify_lemma2_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                       const int64_t* col_pivots, const double* col_coeff, const int64_t* row_pivots,
+                       const double* row_coeff, lr_lemma2_report* out) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "verify_lemma2");
+    require_rank_in_range(k, m, n, "verify_lemma2");
+    if (!out) fail(LR_EINVAL, "verify_lemma2: null report");
+    VerifyInputs v;
+    verify_inputs(c, m, n, a, lda, k, col_pivots, col_coeff, row_pivots, row_coeff, nullptr, v);
+    const int64_t mr = m - k, ldr = even(std::max<int64_t>(mr, 1));
+    ResidualBufs be, bw;
+    const ResidualOp e = residual_op(c, m, n, a, lda, v.At, even(n), k, v.C, m, v.Vt, k, be);
+    const ResidualOp w = residual_op(c, m, n, a, lda, v.At, even(n), k, v.W, m, v.R, k, bw);
+    lr_lemma2_report rep{};
+    rep.e_norm = op_sigma1(c, e, kVerifySeed);
+    rep.etilde_norm = op_sigma1(c, w, kVerifySeed);
+    // the permuted stack [0; F E] (verify.hpp:108-117) as an operator: rows I(l), l >= k,
+    // take E(I(l), :) - T(:, l-k)^T E(I_skel, :); the skeleton rows are zero
+    DBuf<double> Tt((size_t)ldr * k, c->st);
+    if (mr > 0) transpose_matrix(k, mr, row_coeff, k, Tt, ldr, c->st);
+    auto stack = [&](int64_t r, double* x, int64_t ldx, double* o, int64_t ldo) {  // o = S x (m x r)
+      DBuf<double> sk((size_t)k * r, c->st), rs((size_t)ldr * r, c->st);
+      gather_rows(k, r, x, ldx, row_pivots, sk, k, c->st);
+      if (mr > 0) {
+        gather_rows(mr, r, x, ldx, row_pivots + k, rs, ldr, c->st);
+        gemm(c, mr, r, k, row_coeff, k, sk, k, rs, ldr, -1.0, 1.0);
+      }
+      scatter_stack(m, r, k, row_pivots, nullptr, 0, rs, ldr, o, ldo, c->st);
+    };
+    auto stack_t = [&](int64_t r, const double* x, int64_t ldx, double* o, int64_t ldo) {  // o = S^T x
+      DBuf<double> rs((size_t)ldr * r, c->st), top((size_t)k * r, c->st);
+      LRB_CUDA(cudaMemsetAsync(top.p, 0, sizeof(double) * k * r, c->st));
+      if (mr > 0) {
+        gather_rows(mr, r, x, ldx, row_pivots + k, rs, ldr, c->st);
+        gemm(c, k, r, mr, Tt, ldr, rs, ldr, top, k, -1.0, 0.0);
+      }
+      scatter_stack(m, r, k, row_pivots, top, k, rs, ldr, o, ldo, c->st);
+    };
+    const int64_t ldm = even(m);
+    rep.fe_norm = krylov_sigma1(
+        c, m, n,
+        [&](int64_t r, const double* in, int64_t li, double* o, int64_t lo) {
+          DBuf<double> t((size_t)ldm * r, c->st);
+          e.apply(r, in, li, t, ldm);
+          stack(r, t, ldm, o, lo);
+        },
+        [&](int64_t r, const double* in, int64_t li, double* o, int64_t lo) {
+          DBuf<double> t((size_t)ldm * r, c->st);
+          stack_t(r, in, li, t, ldm);
+          e.apply_t(r, t, ldm, o, lo);
+        },
+        kVerifySeed);
+    // entrywise gap of the two paths: direct - stack = -(C(I_res,:) - T^T C(I_skel,:)) V^T on
+    // the residual rows and 0 on the skeleton rows; its largest entry, by column blocks
+    rep.entry_diff = 0.0;
+    if (mr > 0) {
+      DBuf<double> Csk((size_t)k * k, c->st), D((size_t)ldr * k, c->st), Dt((size_t)even(k) * mr, c->st);
+      gather_rows(k, k, v.C, m, row_pivots, Csk, k, c->st);
+      gather_rows(mr, k, v.C, m, row_pivots + k, D, ldr, c->st);
+      gemm(c, mr, k, k, row_coeff, k, Csk, k, D, ldr, -1.0, 1.0);
+      transpose_matrix(mr, k, D, ldr, Dt, even(k), c->st);
+      DBuf<double> Vk((size_t)even(k) * n, c->st);
+      copy_matrix(k, n, v.Vt, k, Vk, even(k), c->st);
+      const int64_t nb = 2048;
+      DBuf<double> blk((size_t)ldr * nb, c->st), part(4 * num_sms() + 4, c->st), mx(1, c->st);
+      double emax = 0.0;
+      for (int64_t j0 = 0; j0 < n; j0 += nb) {
+        const int64_t w2 = std::min(nb, n - j0);
+        gemm(c, mr, w2, k, Dt, even(k), Vk.p + j0 * even(k), even(k), blk, ldr);
+        max_abs(mr, w2, blk, ldr, part, mx, c->st);
+        d2h_mapped(c, c->h_scal, mx.p, sizeof(double));
+        sync(c);
+        emax = std::max(emax, c->h_scal[0]);
+      }
+      rep.entry_diff = emax;
+    }
+    rep.t_norm = mr > 0 ? coeff_norm2(c, k, mr, row_coeff, k) : 0.0;
+    rep.bound_rhs = (1.0 + rep.t_norm) * rep.e_norm;
+    const double scale = std::max(rep.etilde_norm, rep.fe_norm);
+    const double af = residual_frob(c, m, n, a, lda, 0, nullptr, 1, nullptr, 1);
+    rep.holds = std::abs(rep.etilde_norm - rep.fe_norm) <= 1e-8 * scale || scale <= 1e-12 * af;  // verify.hpp:126-127
+    rep.bound_holds = rep.etilde_norm <= rep.bound_rhs * (1.0 + 1e-8);
+    *out = rep;
+  });
+}
+
+int lr_verify_corollary_d(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t k,
+                          const int64_t* col_pivots, const double* col_coeff, const double* u, lr_solve_strategy strat,
+                          lr_corollary_report* out) {
+  return guard([&] {
+    checked(c);
+    require_ld(m, lda, "verify_corollary");
+    require_rank_in_range(k, m, n, "verify_corollary");
+    if (!out) fail(LR_EINVAL, "verify_corollary: null report");
+    // the row skeletonization of C recomputed (verify.hpp:148: id_row(skeleton_columns(a, col_id), k))
+    DBuf<int64_t> rp(m, c->st);
+    DBuf<double> rcf((size_t)k * std::max<int64_t>(m - k, 1), c->st), Cb((size_t)m * k, c->st);
+    tsid_core(c, m, n, a, lda, k, col_pivots, strat, rp, rcf, k, nullptr, Cb, nullptr);
+    VerifyInputs v;
+    verify_inputs(c, m, n, a, lda, k, col_pivots, col_coeff, rp, nullptr, u, v);
+    ResidualBufs b0, b1;
+    lr_corollary_report rep{};
+    rep.t_norm = m > k ? coeff_norm2(c, k, m - k, rcf, k) : 0.0;
+    rep.e_norm = op_sigma1(c, residual_op(c, m, n, a, lda, v.At, even(n), k, v.C, m, v.Vt, k, b0), kVerifySeed);
+    rep.lhs = op_sigma1(c, residual_op(c, m, n, a, lda, v.At, even(n), k, v.CU, m, v.R, k, b1), kVerifySeed);
+    rep.bound = (2.0 + rep.t_norm) * rep.e_norm;
+    rep.ceiling = 2.0 * std::sqrt((double)k * (double)(m - k));
+    rep.holds = rep.lhs <= rep.bound * (1.0 + 1e-8);
+    *out = rep;
   });
 }
 

@@ -58,6 +58,8 @@ struct CpqrArgs {
   int nopivot;  // unpivoted Householder QR (orth_rows fallback): position s is always the pivot
 };
 
+constexpr int kSU = 4;  // streamed 64-row chunks in flight per lane (tall matrices)
+
 __device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
 }
@@ -313,10 +315,25 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
           if (i + 1 >= s && i + 1 < m) dot = fma(cb.c[t][1], vv[i + 1], dot);
         }
       }
-      for (int t = CH; t < nchunks; ++t) {  // streamed rows (tall matrices)
-        const int64_t i = 64 * t + 2 * lane;
-        if (i < m && i >= s) dot = fma(src[i], vv[i], dot);
-        if (i + 1 < m && i + 1 >= s) dot = fma(src[i + 1], vv[i + 1], dot);
+      // streamed rows (tall matrices): kSU chunks' loads issued before their FMAs
+      // (the FMA order, hence the result, is that of the one-chunk loop)
+      for (int t = CH; t < nchunks; t += kSU) {
+        double xv[kSU][2];
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int64_t i = 64 * (t + u) + 2 * lane;
+          const bool in = t + u < nchunks;
+          xv[u][0] = (in && i < m && i >= s) ? src[i] : 0.0;
+          xv[u][1] = (in && i + 1 < m && i + 1 >= s) ? src[i + 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int64_t i = 64 * (t + u) + 2 * lane;
+          if (t + u < nchunks) {
+            if (i < m && i >= s) dot = fma(xv[u][0], vv[i], dot);
+            if (i + 1 < m && i + 1 >= s) dot = fma(xv[u][1], vv[i + 1], dot);
+          }
+        }
       }
       dot = warp_sum(dot);
       double xs = 0.0, tail2 = 0.0;
@@ -339,20 +356,30 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
           else dst[i] = cb.c[t][0];
         }
       }
-      for (int t = CH; t < nchunks; ++t) {
+      for (int t = CH; t < nchunks; t += kSU) {
+        double xv[kSU][2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = 64 * t + 2 * lane + e;
-          if (r < m) {
-            double c = src[r];
-            if (r >= s) {
-              if (apply) c = fma(-tv[r], dot, c);
-              if (r == s) xs = c;
-              else tail2 = fma(c, c, tail2);
-            }
-            dst[r] = c;  // rows < s copied through unchanged (needed when from_s)
+        for (int u = 0; u < kSU; ++u)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t r = 64 * (t + u) + 2 * lane + e;
+            xv[u][e] = (t + u < nchunks && r < m) ? src[r] : 0.0;
           }
-        }
+#pragma unroll
+        for (int u = 0; u < kSU; ++u)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t r = 64 * (t + u) + 2 * lane + e;
+            if (t + u < nchunks && r < m) {
+              double c = xv[u][e];
+              if (r >= s) {
+                if (apply) c = fma(-tv[r], dot, c);
+                if (r == s) xs = c;
+                else tail2 = fma(c, c, tail2);
+              }
+              dst[r] = c;  // rows < s copied through unchanged (needed when from_s)
+            }
+          }
       }
       if (from_s)  // rows < s of the swapped-in column that sit in skipped cached chunks
         for (int64_t r = lane; r < s && r < 64 * (int64_t)CH; r += 32) dst[r] = olds[r];

@@ -264,4 +264,8 @@ void inverse_perm(const int64_t* perm, int64_t n, int64_t* inv, cudaStream_t st)
 void basis_rows(const int64_t* inv, int64_t off, int64_t n_loc, int64_t k, const double* coeff, int64_t ldc,
                 double* B, cudaStream_t st);
 
+// verify.cu: out(piv[l], :) = l < k ? (top ? top(l, :) : 0) : res(l - k, :) for an m x b block
+void scatter_stack(int64_t m, int64_t b, int64_t k, const int64_t* piv, const double* top, int64_t ldt,
+                   const double* res, int64_t ldr, double* out, int64_t ldo, cudaStream_t st);
+
 }  // namespace lrb

@@ -28,7 +28,8 @@ __all__ = [
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
     "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
-    "id_column_device", "randomized_id_device", "cur_id_device",
+    "id_column_device", "randomized_id_device", "cur_id_device", "residual_norms_device", "error_report_device",
+    "verify_lemma1_device", "verify_lemma2_device", "verify_corollary_device",
 ]
 
 LowrankCudaError = L.LowrankCudaError
@@ -794,6 +795,75 @@ def cur_error_fro_device(a, cur: dict, ctx: Optional[Context] = None):
         _raise(c.lib.lr_cur_error_fro_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(cur["c"]), _dptr(cur["u"]),
                                         _dptr(cur["r"]), _ptr(res)))
     return float(res[0]), float(res[1])
+
+
+# ------------------------------------------------------------------ verifiers at scale (verify.hpp)
+def _rep(st) -> dict:
+    return {f: (bool(getattr(st, f)) if t is ctypes.c_int else float(getattr(st, f))) for f, t in st._fields_}
+
+
+def residual_norms_device(a, x=None, y=None, spectral: bool = True, ctx: Optional[Context] = None):
+    """(||A - X Y||_2, ||A - X Y||_F) for device tensors (x m x k, y k x n; None: norms of A).
+    The residual is never formed (block Krylov / fused residual GEMM)."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    k = 0 if x is None else int(x.shape[1])
+    sp, fr = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    with on_torch_stream(c):
+        _raise(c.lib.lr_residual_norms_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(x) if k else None,
+                                         _colmajor_ld(x) if k else 1, _dptr(y) if k else None,
+                                         _colmajor_ld(y) if k else 1, ctypes.byref(sp) if spectral else None,
+                                         ctypes.byref(fr)))
+    return (float(sp.value) if spectral else None), float(fr.value)
+
+
+def error_report_device(a, x, y, ctx: Optional[Context] = None) -> dict:
+    """verify.hpp:31-56 error_report(a, approx) with approx = X Y (device tensors)."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    rep = L.lr_error_report()
+    with on_torch_stream(c):
+        _raise(c.lib.lr_error_report_lowrank_d(c.h, m, n, _dptr(a), _colmajor_ld(a), int(x.shape[1]), _dptr(x),
+                                               _colmajor_ld(x), _dptr(y), _colmajor_ld(y), ctypes.byref(rep)))
+    return _rep(rep)
+
+
+def verify_lemma1_device(a, k: int, col_pivots, col_coeff, row_pivots, row_coeff, u,
+                         ctx: Optional[Context] = None) -> dict:
+    """verify.hpp:70-80: ||A - CUR||_2 <= ||A - C V^T||_2 + ||A - W R||_2 for the CUR given
+    by its index sets, coefficient blocks and U (device tensors)."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    rep = L.lr_lemma1_report()
+    with on_torch_stream(c):
+        _raise(c.lib.lr_verify_lemma1_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(col_pivots), _dptr(col_coeff),
+                                        _dptr(row_pivots), _dptr(row_coeff), _dptr(u), ctypes.byref(rep)))
+    return _rep(rep)
+
+
+def verify_lemma2_device(a, k: int, col_pivots, col_coeff, row_pivots, row_coeff,
+                         ctx: Optional[Context] = None) -> dict:
+    """verify.hpp:97-130: the row-ID error directly and through the permuted stack [0; F E]."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    rep = L.lr_lemma2_report()
+    with on_torch_stream(c):
+        _raise(c.lib.lr_verify_lemma2_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(col_pivots), _dptr(col_coeff),
+                                        _dptr(row_pivots), _dptr(row_coeff), ctypes.byref(rep)))
+    return _rep(rep)
+
+
+def verify_corollary_device(a, k: int, col_pivots, col_coeff, u, strategy: Optional[SolveStrategy] = None,
+                            ctx: Optional[Context] = None) -> dict:
+    """verify.hpp:144-160: ||A - CUR||_2 <= (2 + ||T||_2) ||A - C V^T||_2."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    rep = L.lr_corollary_report()
+    with on_torch_stream(c):
+        _raise(c.lib.lr_verify_corollary_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(col_pivots),
+                                           _dptr(col_coeff), _dptr(u), (strategy or SolveStrategy.automatic())._c(),
+                                           ctypes.byref(rep)))
+    return _rep(rep)
 
 
 # ------------------------------------------------------------------ sparse (BASELINE config 5)

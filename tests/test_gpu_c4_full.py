@@ -100,3 +100,25 @@ def test_c4_full_size_vs_oracle(lr, gold, c4_matrix, engine):
     assert e / na == pytest.approx(float(gold["err"]) / float(gold["na"]), rel=TOL)
     assert stats["norm_recomputes"] == int(gold["recomputes_y"]) + int(gold["recomputes_ct"]), \
         (stats["norm_recomputes"], int(gold["recomputes_y"]), int(gold["recomputes_ct"]))
+
+
+def test_c4_full_size_verifiers(lr, gold, c4_matrix):
+    """verify.hpp's Lemma 1 and Corollary at 65536^2 on the GPU (block Krylov
+    spectral norms of the never-formed 34 GB residuals): the bounds hold, and
+    each spectral norm sits below the matching Frobenius norm."""
+    import torch
+    a = c4_matrix
+    k = int(gold["k"])
+    ctx = lr.default_context()
+    sk = lr.SketchConfig(oversample=int(gold["oversample"]), seed=int(gold["sketch_seed"]))
+    out = lr.randomized_cur_device(a, k, sk, u_mode=lr.U_CPINV_A_RPINV, ctx=ctx)
+    torch.cuda.synchronize()
+    l1 = lr.verify_lemma1_device(a, k, out["col_pivots"], out["col_coeff"], out["row_pivots"], out["row_coeff"],
+                                 out["u"])
+    assert l1["holds"] and 0.0 < l1["lhs"] <= l1["rhs"] * (1 + 1e-8)
+    e, na = lr.cur_error_fro_device(a, out, ctx=ctx)
+    assert l1["lhs"] <= e * (1 + 1e-12)  # ||.||_2 <= ||.||_F
+    co = lr.verify_corollary_device(a, k, out["col_pivots"], out["col_coeff"], out["u"])
+    assert co["holds"] and co["e_norm"] == pytest.approx(l1["e_norm"], rel=1e-10)
+    assert co["lhs"] == pytest.approx(l1["lhs"], rel=1e-10)
+    print(f"C4 lemma1 {l1}  corollary {co}")
