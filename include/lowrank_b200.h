@@ -262,6 +262,12 @@ int lr_tri_upper_inverse_d(lr_ctx* ctx, int64_t k, const double* r, int64_t ldr,
 int lr_cholqr2_d(lr_ctx* ctx, int64_t rows, int64_t k, const double* x, int64_t ldx, double* r, double* rinv,
                  int* ok);
 
+/* C (m x n) = A (m x k) B (k x n) on the GPU (FP64 DMMA): the products of the
+   reconstructions id.hpp:143-159 / cur.hpp:77-80; host and device pointers */
+int lr_gemm(lr_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
+            int64_t ldb, double* c, int64_t ldc);
+int lr_gemm_d(lr_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
+              int64_t ldb, double* c, int64_t ldc);
 /* Y (M x N) = P^T Q on the context's contraction engine (benchmark / test access) */
 int lr_gemm_tn_d(lr_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp, const double* Q,
                  int64_t ldq, double* out, int64_t ldo);

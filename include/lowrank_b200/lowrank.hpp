@@ -101,6 +101,19 @@ inline std::vector<int64_t> from_index(const IndexVector& p) {
 }
 inline Index ld(const MatrixX<double>& a) { return std::max<Index>(1, a.rows()); }
 
+/// a * b on the GPU (lr_gemm): the reconstruction products stay off the host
+inline MatrixX<double> matmul(const MatrixX<double>& a, const MatrixX<double>& b) {
+  if (a.cols() != b.rows()) throw std::invalid_argument("matmul: inner dimensions differ");
+  MatrixX<double> c(a.rows(), b.cols());
+  if (c.rows() == 0 || c.cols() == 0) return c;
+  if (a.cols() == 0) {
+    c.setZero();
+    return c;
+  }
+  check(lr_gemm(context(), a.rows(), b.cols(), a.cols(), a.data(), ld(a), b.data(), ld(b), c.data(), ld(c)));
+  return c;
+}
+
 }  // namespace b200
 
 // ---------------------------------------------------------------- core.hpp
@@ -414,15 +427,15 @@ TwoSidedId<typename Derived::Scalar> id_two_sided(const Eigen::MatrixBase<Derive
 
 template <typename Derived, typename Scalar = typename Derived::Scalar>
 MatrixX<Scalar> reconstruct(const Eigen::MatrixBase<Derived>& a, const ColumnId<Scalar>& id) {
-  return skeleton_columns(a, id) * id.basis().transpose();
+  return b200::matmul(skeleton_columns(a, id), MatrixX<Scalar>(id.basis().transpose()));
 }
 template <typename Derived, typename Scalar = typename Derived::Scalar>
 MatrixX<Scalar> reconstruct(const Eigen::MatrixBase<Derived>& a, const RowId<Scalar>& id) {
-  return id.basis() * skeleton_rows(a, id);
+  return b200::matmul(id.basis(), skeleton_rows(a, id));
 }
 template <typename Scalar>
 MatrixX<Scalar> reconstruct(const TwoSidedId<Scalar>& tsid) {
-  return tsid.row_basis() * tsid.skeleton * tsid.col_basis().transpose();
+  return b200::matmul(b200::matmul(tsid.row_basis(), tsid.skeleton), MatrixX<Scalar>(tsid.col_basis().transpose()));
 }
 
 // ---------------------------------------------------------------- cur.hpp
@@ -467,7 +480,7 @@ CurDecomposition<typename Derived::Scalar> cur_id(const Eigen::MatrixBase<Derive
 
 template <typename Scalar>
 MatrixX<Scalar> reconstruct(const CurDecomposition<Scalar>& cur) {
-  return cur.c * cur.u * cur.r;
+  return b200::matmul(b200::matmul(cur.c, cur.u), cur.r);
 }
 
 /// cur.hpp:52-74 (Eq. 31 variant; not on the hot path): the same
@@ -483,10 +496,11 @@ MatrixX<Scalar> cur_refined_u(const Eigen::MatrixBase<Derived>& a, const CurDeco
   for (Index j = 0; j < a.cols(); ++j)
     if (col_id.pivots(j) != qr.pivots(j)) throw std::invalid_argument("cur_refined_u: pivot sequences disagree");
   MatrixX<Scalar> residual = a;
-  const MatrixX<Scalar> qs = qr.q * qr.s;
+  const MatrixX<Scalar> qs = b200::matmul(qr.q, qr.s);
   for (Index j = 0; j < a.cols(); ++j) residual.col(qr.pivots(j)) -= qs.col(j);
-  const MatrixX<Scalar> rhs = col_id.basis().transpose() + pinv(cur.c, pinv_threshold) * residual;
-  return rhs * pinv(cur.r, pinv_threshold);
+  const MatrixX<Scalar> rhs =
+      MatrixX<Scalar>(col_id.basis().transpose()) + b200::matmul(pinv(cur.c, pinv_threshold), residual);
+  return b200::matmul(rhs, pinv(cur.r, pinv_threshold));
 }
 
 // ---------------------------------------------------------------- sketch.hpp

@@ -129,6 +129,8 @@ SIGNATURES = {
                          ctypes.c_int),
     "lr_cur_error_fro_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp],
                            ctypes.c_int),
+    "lr_gemm": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
+    "lr_gemm_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_gemm_tn_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64],
                      ctypes.c_int),
     "lr_randomized_cur_csr_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_ip, c_ip, c_dp, c_i64, lr_sketch_config,

@@ -2667,6 +2667,36 @@ int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, in
   });
 }
 
+// C (m x n) = A (m x k) B (k x n), column-major: the reconstructions of
+// id.hpp:143-159 / cur.hpp:77-80 on the GPU (the drop-in header and the Python
+// mirror route their products here instead of a host GEMM)
+int lr_gemm_d(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b, int64_t ldb,
+              double* out, int64_t ldo) {
+  return guard([&] {
+    checked(c);
+    if (m < 1 || n < 1 || k < 1) fail(LR_EINVAL, "gemm: dimensions must be positive");
+    require_ld(m, lda, "gemm");
+    require_ld(k, ldb, "gemm");
+    require_ld(m, ldo, "gemm");
+    DBuf<double> at((size_t)even(k) * m, c->st);
+    transpose_matrix(m, k, a, lda, at, even(k), c->st);
+    gemm(c, m, n, k, at, even(k), b, ldb, out, ldo);
+  });
+}
+int lr_gemm(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b, int64_t ldb,
+            double* out, int64_t ldo) {
+  return guard([&] {
+    checked(c);
+    if (m < 1 || n < 1 || k < 1) fail(LR_EINVAL, "gemm: dimensions must be positive");
+    int64_t la, lb;
+    DBuf<double> da = to_dev(c, m, k, a, lda, &la), db = to_dev(c, k, n, b, ldb, &lb);
+    DBuf<double> at((size_t)even(k) * m, c->st), dc((size_t)m * n, c->st);
+    transpose_matrix(m, k, da, la, at, even(k), c->st);
+    gemm(c, m, n, k, at, even(k), db, lb, dc, m);
+    to_host(c, m, n, dc, m, out, ldo);
+    sync(c);
+  });
+}
 
 // ---- column-sharded entry points (one process per GPU)
 int lr_nccl_get_unique_id(unsigned char* id) {

@@ -28,7 +28,7 @@ __all__ = [
     "skeleton_columns", "skeleton_rows", "reconstruct", "frobenius_norm", "cur_error_fro",
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
     "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
-    "id_column_device", "randomized_id_device", "cur_id_device", "residual_norms_device", "error_report_device",
+    "id_column_device", "randomized_id_device", "cur_id_device", "residual_norms_device", "matmul", "error_report_device",
     "verify_lemma1_device", "verify_lemma2_device", "verify_corollary_device",
 ]
 
@@ -667,18 +667,36 @@ def skeleton_rows(a, rid: RowId) -> np.ndarray:
     return select_rows(a, rid.pivots, rid.rank)
 
 
+def matmul(a, b, ctx: Optional[Context] = None) -> np.ndarray:
+    """C = A B on the GPU (lr_gemm, FP64 DMMA): the products of the reconstructions."""
+    c = _ctx(ctx)
+    a, b = _f64(a), _f64(b)
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2:
+        raise ValueError("matmul: inner dimensions differ")
+    out = np.empty((m, n), order="F")
+    if m == 0 or n == 0:
+        return out
+    if k == 0:
+        out[:] = 0.0
+        return out
+    _raise(c.lib.lr_gemm(c.h, m, n, k, _ptr(a), _ld(a), _ptr(b), _ld(b), _ptr(out), max(1, m)))
+    return out
+
+
 def reconstruct(*args):
-    """id.hpp:144-159 / cur.hpp:77-80 (small-size verification helper)."""
+    """id.hpp:144-159 / cur.hpp:77-80, the products on the GPU (lr_gemm)."""
     if len(args) == 1 and isinstance(args[0], CurDecomposition):
         cur = args[0]
-        return cur.c @ cur.u @ cur.r
+        return matmul(matmul(cur.c, cur.u), cur.r)
     if len(args) == 1 and isinstance(args[0], TwoSidedId):
         t = args[0]
-        return t.row_basis() @ t.skeleton @ t.col_basis().T
+        return matmul(matmul(t.row_basis(), t.skeleton), np.asfortranarray(t.col_basis().T))
     a, idobj = args
     if isinstance(idobj, ColumnId):
-        return skeleton_columns(a, idobj) @ idobj.basis().T
-    return idobj.basis() @ skeleton_rows(a, idobj)
+        return matmul(skeleton_columns(a, idobj), np.asfortranarray(idobj.basis().T))
+    return matmul(idobj.basis(), skeleton_rows(a, idobj))
 
 
 def frobenius_norm(a) -> float:
