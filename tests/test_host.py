@@ -1,5 +1,6 @@
 """Host-side mirror of the reference interface (no GPU needed)."""
 import numpy as np
+import pytest
 
 from paper_1412_8447_b200 import lowrank as lr
 
@@ -37,6 +38,7 @@ def test_column_id_basis_has_identity_block():  # id.hpp:21-30, test_id.cpp:24-3
     assert np.array_equal(rid.basis(), v)
 
 
+@pytest.mark.gpu  # the reconstruction products run on the GPU (lr_gemm)
 def test_reconstruct_two_sided():
     a = np.arange(12.0).reshape(4, 3)
     cid = lr.ColumnId(3, 3, np.array([0, 1, 2]), np.zeros((3, 0)))
