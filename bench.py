@@ -678,16 +678,23 @@ def run_sharded(args, rank, world, local_rank):
         host = torch.empty((n_g, cfg.m), dtype=torch.float64, pin_memory=True).T
         host.copy_(a)
         torch.cuda.synchronize()
-        keys = ("c", "u", "r_local", "col_pivots", "row_pivots", "col_coeff", "row_coeff", "skeleton")
-        hb = {kk: torch.empty(tuple(res[kk].shape), dtype=res[kk].dtype, pin_memory=True) for kk in keys}
-        d2h = sum(hb[kk].numel() * hb[kk].element_size() for kk in keys)
+        del a, res
+        torch.cuda.empty_cache()
+        host_np = host.numpy()  # column-major view of the pinned shard
+
+        def pinned(shape, dtype):
+            t = torch.empty(tuple(reversed(shape)), dtype=dtype, pin_memory=True)
+            return t.numpy().T if len(shape) == 2 else t.numpy()
+
+        k = cfg.k
+        hout = {"col_pivots": pinned((cfg.n,), torch.int64), "row_pivots": pinned((cfg.m,), torch.int64),
+                "c": pinned((cfg.m, k), torch.float64), "u": pinned((k, k), torch.float64),
+                "r_local": pinned((k, n_g), torch.float64), "col_coeff": pinned((k, cfg.n - k), torch.float64),
+                "row_coeff": pinned((k, cfg.m - k), torch.float64), "skeleton": pinned((k, k), torch.float64)}
+        d2h = sum(v.nbytes for v in hout.values())
 
         def e2e_step():
-            a.copy_(host, non_blocking=True)
-            out = step(res)
-            for kk in keys:
-                hb[kk].copy_(out[kk], non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
+            D.randomized_cur_sharded_host(ctx, host_np, off, cfg.n, cfg.k, sk, out=hout)
 
         e2e_step()  # warm-up
         e2e_steps = args.e2e_steps or args.steps
@@ -704,7 +711,8 @@ def run_sharded(args, rank, world, local_rank):
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * cfg.m * cfg.n,
                "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                "host_buffer": "pinned column shard per rank (1/N of A) and pinned result buffers",
-               "pipeline": "shard H2D on the compute stream, then the sharded CUR; bytes summed over ranks"}
+               "pipeline": "lr_randomized_cur_sharded: the shard uploaded in column chunks, each chunk sketched "
+                           "as it lands, then the sharded CUR; bytes summed over ranks"}
     stats = ctx.stats()
     D.detach_nccl(ctx)
     if rank != 0:

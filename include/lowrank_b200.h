@@ -111,6 +111,9 @@ int lr_ctx_set_gemm_mode(lr_ctx* ctx, int mode);
    lr_ctx_clear_operand_cache.  The caller must not modify a in between. */
 int lr_ctx_cache_operand(lr_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda);
 int lr_ctx_clear_operand_cache(lr_ctx* ctx);
+/* free the context's grow-only device workspace (Ozaki residue planes of A:
+   2 bytes of HBM per byte of A, CPQR state, the call arena) */
+int lr_ctx_release_workspace(lr_ctx* ctx);
 int lr_ctx_get_gemm_mode(lr_ctx* ctx);
 /* back to the context's own (non-blocking) stream, the default after creation */
 int lr_ctx_use_own_stream(lr_ctx* ctx);
@@ -299,6 +302,13 @@ int lr_ctx_set_shard_emulation(lr_ctx* ctx, int nshards);
    (s, k x n_total, ld k), replicated */
 int lr_cpqr_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
                       const double* a_local, int64_t lda, int64_t k, int64_t* pivots, double* s);
+/* host pointers: the rank's block is uploaded in column chunks with the sketch
+   of each chunk overlapped with the transfer; outputs back in host memory */
+int lr_randomized_cur_sharded(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                              const double* a_local, int64_t lda, int64_t k, lr_sketch_config cfg,
+                              lr_solve_strategy strategy, double pinv_threshold, int u_mode, int64_t* col_pivots,
+                              int64_t* row_pivots, double* c, double* u, double* r_local, double* col_coeff,
+                              double* row_coeff, double* skeleton);
 /* randomized CUR (Gaussian sketch, q = 0) of the column-sharded A; u_mode as
    lr_randomized_cur_d; r_local is this rank's k x n_local block of R */
 int lr_randomized_cur_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,

@@ -76,6 +76,7 @@ SIGNATURES = {
     "lr_ctx_get_gemm_mode": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_cache_operand": ([ctypes.c_void_p, c_dp, c_i64, c_i64, c_i64], ctypes.c_int),
     "lr_ctx_clear_operand_cache": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_release_workspace": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_get_stats": ([ctypes.c_void_p, ctypes.POINTER(lr_stats)], ctypes.c_int),
     "lr_ctx_synchronize": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_enable_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
@@ -167,6 +168,9 @@ SIGNATURES = {
                          ctypes.c_int),
     "lr_cpqr_sharded_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64, c_ip, c_dp],
                           ctypes.c_int),
+    "lr_randomized_cur_sharded": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64,
+                                   lr_sketch_config, lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip,
+                                   c_dp, c_dp, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),
     "lr_randomized_cur_sharded_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_i64, c_dp, c_i64, c_i64,
                                      lr_sketch_config, lr_solve_strategy, ctypes.c_double, ctypes.c_int, c_ip, c_ip,
                                      c_dp, c_dp, c_dp, c_dp, c_dp, c_dp], ctypes.c_int),

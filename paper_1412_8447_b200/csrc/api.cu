@@ -1455,7 +1455,8 @@ void cpqr_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t off, int64_t
 void randomized_cur_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t off, int64_t n, const double* a,
                                  int64_t lda, int64_t k, const lr_sketch_config& cfg, const lr_solve_strategy& strat,
                                  double thr, int u_mode, int64_t* col_piv, int64_t* row_piv, double* C, double* U,
-                                 double* R_loc, double* col_coeff, double* row_coeff, double* skeleton) {
+                                 double* R_loc, double* col_coeff, double* row_coeff, double* skeleton,
+                                 const double* Ypre = nullptr, int64_t ldy_pre = 0) {
   const ShardComm& cm = c->comm;
   if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
   if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
@@ -1468,10 +1469,18 @@ void randomized_cur_sharded_core(lr_ctx* c, int64_t m, int64_t n_loc, int64_t of
   mark(c, "begin");
   OzakiScope scope(c);  // the shard's residue planes serve the sketch and A^T Q_c
   const int64_t ldk = even(k);
-  // (1) Y_g = Omega A_g (Omega from the counter stream: identical on every rank)
-  const int64_t ldy = even(ell);
-  DBuf<double> Y((size_t)ldy * std::max<int64_t>(n_loc, 1), c->st);
-  if (n_loc > 0) sketch_core(c, m, n_loc, a, lda, ell, cfg.seed, Y, ldy);
+  // (1) Y_g = Omega A_g (Omega from the counter stream: identical on every rank);
+  // Ypre: already formed by the caller (the pipelined host upload)
+  int64_t ldy = even(ell);
+  DBuf<double> Yb;
+  const double* Y = Ypre;
+  if (Ypre) {
+    ldy = ldy_pre;
+  } else {
+    Yb = DBuf<double>((size_t)ldy * std::max<int64_t>(n_loc, 1), c->st);
+    if (n_loc > 0) sketch_core(c, m, n_loc, a, lda, ell, cfg.seed, Yb, ldy);
+    Y = Yb;
+  }
   // (2) CPQR(Y), ell steps, sharded; T = S11^-1 S12 on the replicated top k rows
   DBuf<double> S1((size_t)k * n, c->st);
   const int emu = c->comm.comm ? 0 : c->emu_shards;
@@ -1865,6 +1874,24 @@ int lr_ctx_cache_operand(lr_ctx* c, const double* a, int64_t m, int64_t n, int64
     c->pin_K = m;
     c->pin_cols = n;
     c->pin_ld = lda;
+  });
+}
+// frees the grow-only workspace (Ozaki residue planes, CPQR state, ...) and the
+// call arena; the next call grows them again
+int lr_ctx_release_workspace(lr_ctx* c) {
+  return guard([&] {
+    checked(c);
+    LRB_CUDA(cudaStreamSynchronize(c->st));
+    c->ws.release_all();
+    c->oz_src = nullptr;
+    c->oz_pinned = false;
+    c->oz_cache_on = false;
+    c->pin_src = nullptr;
+    if (c->arena.base) {
+      LRB_CUDA(cudaFree(c->arena.base));
+      c->arena.base = nullptr;
+      c->arena.cap = c->arena.used = c->arena.overflow = c->arena.want = 0;
+    }
   });
 }
 int lr_ctx_clear_operand_cache(lr_ctx* c) {
@@ -2731,6 +2758,42 @@ int lr_ctx_comm_info(lr_ctx* c, int* nranks, int* rank) {
     checked(c);
     if (nranks) *nranks = c->comm.nranks;
     if (rank) *rank = c->comm.rank;
+  });
+}
+// host pointers: this rank's block uploads in column chunks with the sketch of
+// each chunk issued as it lands (upload_sketch), then the sharded pipeline;
+// the replicated factors and the rank's R block come back to host memory
+int lr_randomized_cur_sharded(lr_ctx* c, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,
+                              const double* a_local, int64_t lda, int64_t k, lr_sketch_config cfg,
+                              lr_solve_strategy strat, double thr, int u_mode, int64_t* col_pivots,
+                              int64_t* row_pivots, double* C, double* U, double* r_local, double* col_coeff,
+                              double* row_coeff, double* skeleton) {
+  return guard([&] {
+    checked(c);
+    if (n_local < 1) fail(LR_EINVAL, "randomized_cur (column-sharded, host): empty column block");
+    require_ld(m, lda, "randomized_cur");
+    const int64_t ell = check_randomized_id(m, n_total, k, cfg);
+    if (cfg.kind != LR_SKETCH_GAUSSIAN || cfg.power != 0)
+      fail(LR_EUNSUPPORTED, "randomized_cur (column-sharded): Gaussian sketch with q = 0 only");
+    const int64_t l = even(m), ldy = even(ell);
+    DBuf<double> d((size_t)l * n_local, c->st), Y((size_t)ldy * n_local, c->st);
+    DBuf<int64_t> cp(n_total, c->st), rp(m, c->st);
+    DBuf<double> Cd((size_t)m * k, c->st), Ud((size_t)k * k, c->st), Rd((size_t)k * n_local, c->st),
+        ccd((size_t)k * std::max<int64_t>(n_total - k, 1), c->st),
+        rcd((size_t)k * std::max<int64_t>(m - k, 1), c->st), skd((size_t)k * k, c->st);
+    OzakiScope scope(c);
+    upload_sketch(c, m, n_local, a_local, lda, d, l, ell, cfg.seed, Y, ldy, cfg.kind);
+    randomized_cur_sharded_core(c, m, n_local, col_offset, n_total, d, l, k, cfg, strat, thr, u_mode, cp, rp, Cd,
+                                Ud, Rd, ccd, rcd, skd, Y, ldy);
+    idx_to_host(c, n_total, cp, col_pivots);
+    idx_to_host(c, m, rp, row_pivots);
+    to_host(c, m, k, Cd, m, C, m);
+    to_host(c, k, k, Ud, k, U, k);
+    to_host(c, k, n_local, Rd, k, r_local, k);
+    if (col_coeff) to_host(c, k, n_total - k, ccd, k, col_coeff, k);
+    if (row_coeff) to_host(c, k, m - k, rcd, k, row_coeff, k);
+    if (skeleton) to_host(c, k, k, skd, k, skeleton, k);
+    sync(c);
   });
 }
 int lr_cpqr_sharded_d(lr_ctx* c, int64_t m, int64_t n_local, int64_t col_offset, int64_t n_total,

@@ -210,6 +210,30 @@ def randomized_cur_sharded_device(ctx, a_local, col_offset: int, n_total: int, k
     return out
 
 
+def randomized_cur_sharded_host(ctx, a_local, col_offset: int, n_total: int, k: int, cfg=None, strategy=None,
+                                pinv_threshold: float = 1e-12, u_mode: Optional[int] = None,
+                                out: Optional[dict] = None) -> dict:
+    """lr_randomized_cur_sharded: this rank's column block in HOST memory (a
+    column-major float64 array, ideally page-locked); the upload runs in column
+    chunks with each chunk's sketch issued as it lands.  Outputs in host arrays
+    (reused from `out`)."""
+    from .lowrank import (U_CPINV_A_RPINV, SketchConfig, SolveStrategy, _f64, _ld, _ptr, _raise)
+    a_local = _f64(a_local)
+    m, n_g = a_local.shape
+    if out is None:
+        out = {"col_pivots": np.empty(n_total, dtype=np.int64), "row_pivots": np.empty(m, dtype=np.int64),
+               "c": np.empty((m, k), order="F"), "u": np.empty((k, k), order="F"),
+               "r_local": np.empty((k, n_g), order="F"), "col_coeff": np.empty((k, max(n_total - k, 1)), order="F"),
+               "row_coeff": np.empty((k, max(m - k, 1)), order="F"), "skeleton": np.empty((k, k), order="F")}
+    _raise(ctx.lib.lr_randomized_cur_sharded(
+        ctx.h, m, n_g, int(col_offset), int(n_total), _ptr(a_local), _ld(a_local), k, (cfg or SketchConfig())._c(),
+        (strategy or SolveStrategy.automatic())._c(), float(pinv_threshold),
+        int(U_CPINV_A_RPINV if u_mode is None else u_mode), _ptr(out["col_pivots"]), _ptr(out["row_pivots"]),
+        _ptr(out["c"]), _ptr(out["u"]), _ptr(out["r_local"]), _ptr(out["col_coeff"]), _ptr(out["row_coeff"]),
+        _ptr(out["skeleton"])))
+    return out
+
+
 def cpqr_sharded_device(ctx, w_local, col_offset: int, n_total: int, k: int):
     """lr_cpqr_sharded_d: pivots (n_total) and the sign-fixed top k rows of R in
     logical order (k x n_total), replicated."""

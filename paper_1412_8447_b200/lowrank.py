@@ -282,6 +282,10 @@ class Context:
         _raise(self.lib.lr_ctx_stage_report(self.h, buf, len(buf)))
         return json.loads(buf.value.decode())
 
+    def release_workspace(self) -> None:
+        """Free the grow-only device workspace (Ozaki residue planes, CPQR state, call arena)."""
+        _raise(self.lib.lr_ctx_release_workspace(self.h))
+
     def reset_stats(self) -> None:
         _raise(self.lib.lr_ctx_reset_stats(self.h))
 

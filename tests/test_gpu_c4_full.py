@@ -52,7 +52,12 @@ def c4_matrix(gold):
     digest = inputs.sha256_colblocks(host)
     del ht, host
     assert digest == str(gold["a_sha256"]), "the regenerated C4 matrix differs from the golden run's input"
-    return a
+    yield a
+    # hand the ~100 GB (A, its residue planes) back for the later full-size tests
+    del a
+    import paper_1412_8447_b200 as lr
+    lr.default_context().release_workspace()
+    torch.cuda.empty_cache()
 
 
 def _checks(t, gold, prefix):

@@ -130,3 +130,26 @@ def test_sharded_cur_validation(lr):
     with pytest.raises(NotImplementedError):
         D.randomized_cur_sharded_device(lr.default_context(), a, 0, cfg.n, cfg.k, lr.SketchConfig(power=1))
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+def test_sharded_host_entry_matches_device_entry(lr, engine):
+    """lr_randomized_cur_sharded (host block, chunked upload overlapped with the
+    sketch) gives the device entry's factors: bitwise on the Ozaki engine
+    (exact integer products), to roundoff on DMMA (the chunked sketch GEMM may
+    pick another split-K)."""
+    from paper_1412_8447_b200 import distributed as D
+    cfg, a_np, a = _problem(lr, 1536, 1280, 768, 120)
+    ref, _ = _run(lr, D, a, cfg, engine=engine)
+    ctx = lr.default_context()
+    ctx.set_gemm_mode(engine)
+    try:
+        got = D.randomized_cur_sharded_host(ctx, a_np, 0, cfg.n, cfg.k, lr.SketchConfig(oversample=10, seed=5))
+    finally:
+        ctx.set_gemm_mode(0)
+    for kk in KEYS:
+        g = got[kk][:, :ref[kk].shape[1]] if got[kk].ndim == 2 else got[kk]
+        if engine == 1 or kk in ("col_pivots", "row_pivots", "c", "r_local", "skeleton"):
+            assert np.array_equal(ref[kk], g), kk
+        else:
+            assert rel(g, ref[kk]) <= 1e-12, kk
