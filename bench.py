@@ -82,12 +82,14 @@ def ozaki_split_bytes(rows, cols):
 
 
 def measured_traffic(cfg):
-    """DRAM bytes per stage launch from the committed ncu capture
-    (profiles/r01_traffic.json, C4 shapes only), else None."""
+    """DRAM bytes per stage launch from the newest committed ncu capture
+    (profiles/rNN_traffic.json, C4 shapes only), else None."""
     if (cfg.m, cfg.n, cfg.k) != (M, N, K_RANK):
         return {}
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))  # the newest round's capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(files[-1]) as f:
             return json.load(f).get("per_launch", {})
     except Exception:
         return {}
@@ -96,7 +98,7 @@ def measured_traffic(cfg):
 def kernel_rooflines(cfg, st, per_step, engine):
     """Roofline entries of the step's big kernels from their CUDA-event stage
     times (average per launch).  `traffic`: DRAM bytes per launch measured by
-    ncu (profiles/r01_traffic.json) where captured."""
+    ncu (the newest profiles/rNN_traffic.json) where captured."""
     peaks = read_peaks()
     traffic = measured_traffic(cfg) if engine == "ozaki" else {}
     hbm = peaks.get("hbm_gbs", 6548.5)

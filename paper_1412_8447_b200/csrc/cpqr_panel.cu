@@ -87,6 +87,7 @@ struct PanelArgs {
   int* posof;                 // [n] logical position of each column slot (between launches)
   unsigned int* ctag;         // [G] step + 1 of the candidate each CTA last staged (release-published)
   int* nzero;                 // identically-zero columns found by the first launch
+  int keep1024;               // the last keep1024/1024 of each warp's sweep is loaded L2::evict_last
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
@@ -131,6 +132,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
+}
+
+// column loads with an L2 eviction priority: the columns a warp visits last in
+// step s are the ones it visits first in step s + 1 (the sweep alternates
+// direction), so they are kept (evict_last) and the rest streamed (evict_first)
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_l2hint(const double2* ptr, uint64_t pol) {
+  double2 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(ptr), "l"(pol));
+  return r;
 }
 
 __device__ double cta_sum(double x, double* sh) {
@@ -245,6 +265,8 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     int j, lp;
     bool ok;
   };
+  const int keep_from = n_valid - (int)(((long long)n_valid * a.keep1024) >> 10);
+  const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
   auto fetch = [&](Slot& cb, int qi) {
     const int q = qi * GPW + g;
     cb.ok = q < n_valid;
@@ -252,10 +274,11 @@ __device__ __forceinline__ void pass_cols(PassCtx& x, double& bv, long long& bp)
     cb.j = jstart + dj * (cb.ok ? q : 0);
     if constexpr (LIST) cb.j = cb.ok ? x.alist[cb.j - (int)x.c0] : (int)x.c0;
     const double* src = Wb + (size_t)cb.j * (size_t)ld;
+    const uint64_t pol = q >= keep_from ? pol_keep : pol_stream;
 #pragma unroll
     for (int k = 0; k < KP; ++k)
       if (active(k)) {
-        const double2 xx = __ldcs(reinterpret_cast<const double2*>(src + 2 * L * k));
+        const double2 xx = ld_l2hint(reinterpret_cast<const double2*>(src + 2 * L * k), pol);
         cb.c[k][0] = xx.x;
         cb.c[k][1] = xx.y;
       }
@@ -973,6 +996,14 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     a.t0 = t0;
     a.t1 = t1;
     a.init = t0 == 0 ? 1 : 0;
+    {  // L2 keep share of the sweep (measured, profiles/r02_cpqr_profile.md): sweeps that fit
+      // in ~110 MB are kept whole; larger ones keep their last ~40 MB (more evicts the
+      // lines the streaming part still reuses).  LRB_CPQR_L2KEEP=<MB> overrides.
+      static const double keep_env = getenv("LRB_CPQR_L2KEEP") ? atof(getenv("LRB_CPQR_L2KEEP")) : -1.0;
+      const double sweep = 8.0 * (double)(ld - 64 * (t0 / 64)) * (double)std::max<int64_t>(1, n - t0);
+      const double keep_mb = keep_env >= 0.0 ? keep_env : (sweep <= 110e6 ? 1e9 : 40.0);
+      a.keep1024 = (int)std::min(1024.0, 1024.0 * keep_mb * 1e6 / sweep);
+    }
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
     evrec();
     void* params[] = {&a};
