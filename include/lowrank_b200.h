@@ -44,6 +44,7 @@ extern "C" {
 #define LR_ECUDA 5       /* device / driver failure                        */
 #define LR_EUNSUPPORTED 6 /* reference feature not on the B200 path yet    */
 #define LR_ENCCL 7        /* NCCL failure (column-sharded entry points)    */
+#define LR_EPARSE 8       /* lowrank::ParseError (io.hpp readers)          */
 
 /* SolveKind, solve.hpp:9 */
 #define LR_SOLVE_BACKSUB 0
@@ -316,6 +317,17 @@ int lr_randomized_cur_sharded_d(lr_ctx* ctx, int64_t m, int64_t n_local, int64_t
                                 lr_solve_strategy strategy, double pinv_threshold, int u_mode,
                                 int64_t* col_pivots, int64_t* row_pivots, double* c, double* u, double* r_local,
                                 double* col_coeff, double* row_coeff, double* skeleton);
+
+/* ---- the reference's binary matrix format (io.hpp:197-233: two little-endian
+   int64 dimensions, then row-major doubles) straight to / from device memory:
+   the file streams through page-locked buffers in row blocks, each block is
+   copied to the GPU while the next is read, and transposed there into the
+   column-major layout every entry point takes.  Errors follow io.hpp
+   (LR_EPARSE + the reference's messages). ---- */
+/* out == NULL: only *rows / *cols are read (size the buffer); else out is
+   rows x cols column-major with leading dimension ldo */
+int lr_read_matrix_binary_d(lr_ctx* ctx, const char* path, int64_t* rows, int64_t* cols, double* out, int64_t ldo);
+int lr_write_matrix_binary_d(lr_ctx* ctx, const char* path, int64_t m, int64_t n, const double* a, int64_t lda);
 
 /* ---- verifiers at scale (verify.hpp:14-166).  The reference takes every
    spectral norm as sigma_1 of a full SVD of the materialised m x n residual

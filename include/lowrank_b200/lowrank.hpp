@@ -68,6 +68,7 @@ inline void check(int rc) {
     case LR_ESINGULAR: throw SingularityError(msg, static_cast<Index>(lr_last_singular_index()));
     case LR_ECONVERGE: throw ConvergenceError(msg);
     case LR_ECUDA: throw DeviceError(msg);
+    case LR_EPARSE: throw ParseError(msg);
     default: throw std::runtime_error(msg);
   }
 }

@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblowrank_b200.so")
 
-LR_OK, LR_EINVAL, LR_ESINGULAR, LR_ECONVERGE, LR_ERUNTIME, LR_ECUDA, LR_EUNSUPPORTED, LR_ENCCL = range(8)
+LR_OK, LR_EINVAL, LR_ESINGULAR, LR_ECONVERGE, LR_ERUNTIME, LR_ECUDA, LR_EUNSUPPORTED, LR_ENCCL, LR_EPARSE = range(9)
 LR_SOLVE_BACKSUB, LR_SOLVE_PINV, LR_SOLVE_TIKHONOV = range(3)
 LR_SKETCH_GAUSSIAN, LR_SKETCH_SRFT = range(2)
 LR_U_VT_RPINV, LR_U_CPINV_A_RPINV = range(2)
@@ -130,6 +130,9 @@ SIGNATURES = {
                          ctypes.c_int),
     "lr_cur_error_fro_d": ([ctypes.c_void_p, c_i64, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_dp, c_dp],
                            ctypes.c_int),
+    "lr_read_matrix_binary_d": ([ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_dp,
+                                 c_i64], ctypes.c_int),
+    "lr_write_matrix_binary_d": ([ctypes.c_void_p, ctypes.c_char_p, c_i64, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_gemm": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_gemm_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64], ctypes.c_int),
     "lr_gemm_tn_d": ([ctypes.c_void_p, c_i64, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_i64],

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -2691,6 +2692,98 @@ int lr_gemm_tn_d(lr_ctx* c, int64_t M, int64_t N, int64_t K, const double* P, in
     if (M < 1 || N < 1 || K < 1) fail(LR_EINVAL, "gemm_tn: dimensions must be positive");
     // in the Ozaki mode both operands are split (no A cache outside a CUR call)
     gemm_a(c, M, N, K, P, ldp, Q, ldq, out, ldo, -1);
+  });
+}
+
+// ---- io.hpp:197-233 binary matrices straight to / from device memory
+namespace {
+constexpr int64_t kIoBlockBytes = 64ll << 20;  // row block per transfer (page-locked, double-buffered)
+struct PinnedPair {
+  double* h[2] = {nullptr, nullptr};
+  ~PinnedPair() {
+    for (double* p : h)
+      if (p) cudaFreeHost(p);
+  }
+};
+}  // namespace
+
+int lr_read_matrix_binary_d(lr_ctx* c, const char* path, int64_t* rows, int64_t* cols, double* out, int64_t ldo) {
+  return guard([&] {
+    checked(c);
+    const std::string p = path ? path : "";
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(p.c_str(), "rb"), std::fclose);
+    if (!f) fail(LR_EPARSE, p + ":0: cannot open file");
+    int64_t dims[2] = {0, 0};
+    if (std::fread(dims, sizeof(int64_t), 2, f.get()) != 2 || dims[0] < 1 || dims[1] < 1)
+      fail(LR_EPARSE, p + ":0: invalid binary matrix header");
+    const int64_t m = dims[0], n = dims[1];
+    if (rows) *rows = m;
+    if (cols) *cols = n;
+    if (!out) return;
+    require_ld(m, ldo, "read_matrix_binary");
+    // row blocks of rb rows (row-major rb x n = column-major n x rb, ld n)
+    const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(m, kIoBlockBytes / (8 * n)));
+    PinnedPair hb;
+    for (auto& h : hb.h) LRB_CUDA(cudaMallocHost(&h, sizeof(double) * (size_t)rb * n));
+    DBuf<double> db0((size_t)rb * n, c->st), db1((size_t)rb * n, c->st);
+    double* db[2] = {db0.p, db1.p};
+    cudaStream_t up = aux_stream(c->up_st);
+    cudaEvent_t copied[2], used[2];
+    for (int b = 0; b < 2; ++b) {
+      LRB_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+      LRB_CUDA(cudaEventCreateWithFlags(&used[b], cudaEventDisableTiming));
+      LRB_CUDA(cudaEventRecord(used[b], c->st));
+    }
+    struct Ev {
+      cudaEvent_t* e;
+      ~Ev() {
+        for (int b = 0; b < 4; ++b) cudaEventDestroy(e[b]);
+      }
+    };
+    cudaEvent_t all[4] = {copied[0], copied[1], used[0], used[1]};
+    Ev ev{all};
+    int64_t blk = 0;
+    for (int64_t i0 = 0; i0 < m; i0 += rb, ++blk) {
+      const int b = (int)(blk & 1);
+      const int64_t r = std::min(rb, m - i0);
+      LRB_CUDA(cudaEventSynchronize(copied[b]));  // the host buffer's previous upload is done
+      if (std::fread(hb.h[b], sizeof(double), (size_t)(r * n), f.get()) != (size_t)(r * n))
+        fail(LR_EPARSE, p + ":0: truncated binary matrix payload");
+      LRB_CUDA(cudaStreamWaitEvent(up, used[b], 0));  // the device buffer's previous transpose is done
+      LRB_CUDA(cudaMemcpyAsync(db[b], hb.h[b], sizeof(double) * (size_t)(r * n), cudaMemcpyHostToDevice, up));
+      LRB_CUDA(cudaEventRecord(copied[b], up));
+      LRB_CUDA(cudaStreamWaitEvent(c->st, copied[b], 0));
+      transpose_matrix(n, r, db[b], n, out + i0, ldo, c->st);  // rows i0 .. i0 + r - 1, column-major
+      LRB_CUDA(cudaEventRecord(used[b], c->st));
+    }
+    sync(c);
+  });
+}
+
+int lr_write_matrix_binary_d(lr_ctx* c, const char* path, int64_t m, int64_t n, const double* a, int64_t lda) {
+  return guard([&] {
+    checked(c);
+    require_nonempty(m, n, "write_matrix_binary");
+    require_ld(m, lda, "write_matrix_binary");
+    const std::string p = path ? path : "";
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(p.c_str(), "wb"), std::fclose);
+    if (!f) fail(LR_ERUNTIME, "write_matrix_binary: cannot open " + p);
+    const int64_t dims[2] = {m, n};
+    if (std::fwrite(dims, sizeof(int64_t), 2, f.get()) != 2) fail(LR_ERUNTIME, "write_matrix_binary: write failed for " + p);
+    const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(m, kIoBlockBytes / (8 * n)));
+    PinnedPair hb;
+    for (auto& h : hb.h) LRB_CUDA(cudaMallocHost(&h, sizeof(double) * (size_t)rb * n));
+    DBuf<double> db((size_t)rb * n, c->st);
+    int64_t blk = 0;
+    for (int64_t i0 = 0; i0 < m; i0 += rb, ++blk) {
+      const int b = (int)(blk & 1);
+      const int64_t r = std::min(rb, m - i0);
+      transpose_matrix(r, n, a + i0, lda, db, n, c->st);  // rows i0.. -> row-major block
+      LRB_CUDA(cudaMemcpyAsync(hb.h[b], db.p, sizeof(double) * (size_t)(r * n), cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      if (std::fwrite(hb.h[b], sizeof(double), (size_t)(r * n), f.get()) != (size_t)(r * n))
+        fail(LR_ERUNTIME, "write_matrix_binary: write failed for " + p);
+    }
   });
 }
 

@@ -29,12 +29,17 @@ __all__ = [
     "randomized_cur_device", "cur_error_fro_device", "empty_colmajor", "U_VT_RPINV", "U_CPINV_A_RPINV",
     "randomized_cur_csr_device", "cur_error_fro_csr_device", "pinned_cur_outputs", "CUR_OUTPUT_KEYS",
     "id_column_device", "randomized_id_device", "cur_id_device", "residual_norms_device", "matmul", "error_report_device",
-    "verify_lemma1_device", "verify_lemma2_device", "verify_corollary_device",
+    "verify_lemma1_device", "verify_lemma2_device", "verify_corollary_device", "ParseError",
+    "read_matrix_binary_device", "write_matrix_binary_device",
 ]
 
 LowrankCudaError = L.LowrankCudaError
 U_VT_RPINV = L.LR_U_VT_RPINV          # cur.hpp:30
 U_CPINV_A_RPINV = L.LR_U_CPINV_A_RPINV  # lowrank_main.cpp:215
+
+
+class ParseError(RuntimeError):
+    """core.hpp:40-42: malformed input file (io.hpp readers)."""
 
 
 class SingularityError(RuntimeError):
@@ -67,6 +72,8 @@ def _raise(rc: int) -> None:
         raise LowrankCudaError(msg)
     if rc == L.LR_EUNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == L.LR_EPARSE:
+        raise ParseError(msg)
     raise RuntimeError(msg)
 
 
@@ -817,6 +824,28 @@ def cur_error_fro_device(a, cur: dict, ctx: Optional[Context] = None):
         _raise(c.lib.lr_cur_error_fro_d(c.h, m, n, _dptr(a), _colmajor_ld(a), k, _dptr(cur["c"]), _dptr(cur["u"]),
                                         _dptr(cur["r"]), _ptr(res)))
     return float(res[0]), float(res[1])
+
+
+# ------------------------------------------------------------------ io.hpp binary matrices <-> device
+def read_matrix_binary_device(path: str, device="cuda", ctx: Optional[Context] = None):
+    """io.hpp:215-233 read_matrix_binary straight into a column-major CUDA tensor
+    (row blocks streamed through page-locked buffers, transposed on the GPU)."""
+    c = _ctx(ctx)
+    rows, cols = ctypes.c_int64(0), ctypes.c_int64(0)
+    _raise(c.lib.lr_read_matrix_binary_d(c.h, str(path).encode(), ctypes.byref(rows), ctypes.byref(cols), None, 1))
+    out = empty_colmajor(rows.value, cols.value, device)
+    with on_torch_stream(c):
+        _raise(c.lib.lr_read_matrix_binary_d(c.h, str(path).encode(), ctypes.byref(rows), ctypes.byref(cols),
+                                             _dptr(out), _colmajor_ld(out)))
+    return out
+
+
+def write_matrix_binary_device(path: str, a, ctx: Optional[Context] = None) -> None:
+    """io.hpp:199-213 write_matrix_binary from a column-major CUDA tensor."""
+    c = _ctx(ctx)
+    m, n = a.shape
+    with on_torch_stream(c):
+        _raise(c.lib.lr_write_matrix_binary_d(c.h, str(path).encode(), m, n, _dptr(a), _colmajor_ld(a)))
 
 
 # ------------------------------------------------------------------ verifiers at scale (verify.hpp)

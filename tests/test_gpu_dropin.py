@@ -1,4 +1,4 @@
-"""The reference's OWN unit suites (proj/tests/test_{core,cpqr,solve,svd,id,cur,sketch}.cpp),
+"""The reference's OWN unit suites (proj/tests/test_{core,cpqr,solve,svd,id,cur,sketch,io,matgen}.cpp),
 unmodified, compiled against the B200 drop-in header (tests/dropin ->
 include/lowrank_b200/lowrank.hpp) and run on the GPU: every lowrank:: call in
 them goes through the C ABI."""
