@@ -56,7 +56,25 @@ struct CpqrArgs {
   int* flags;
   unsigned long long* recomputes;
   int nopivot;  // unpivoted Householder QR (orth_rows fallback): position s is always the pivot
+  unsigned int* bar;  // grid barrier counter (zeroed before the launch)
 };
+
+// Grid barrier of the co-resident (cooperative) grid: one release reduction
+// per CTA on a monotonic counter, an acquire spin (cooperative groups'
+// grid.sync measured ~9 us per barrier on this part; this is one L2 round
+// trip after the last arrival).
+__device__ __forceinline__ void cpqr_grid_barrier(unsigned int* bar, unsigned int& target) {
+  target += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 constexpr int kSU = 4;  // streamed 64-row chunks in flight per lane (tall matrices)
 
@@ -136,7 +154,7 @@ __device__ __forceinline__ void load_col(Col<CH>& col, const double* src, bool c
 
 template <int CH, bool PF, bool FAST, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned int bar_target = 0;
   extern __shared__ double dyn[];
   __shared__ double sh_red[kMaxWarps];
   __shared__ double sh_bv[kMaxWarps];
@@ -218,7 +236,7 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
     __syncthreads();
     stage_candidate(a, a.cand + (int64_t)cta * cand_sz, 0, sh_piv[0], sh_red);
   }
-  grid.sync();
+  cpqr_grid_barrier(a.bar, bar_target);
   if (__ldcg(a.flags) != 0) return;
 
   // ------------------------------------------------------------ steps
@@ -541,7 +559,7 @@ __global__ void __launch_bounds__(NT, MINB) cpqr_kernel(CpqrArgs a) {
     }
     __syncthreads();
     stage_candidate(a, a.cand + ((int64_t)nxt * G + cta) * cand_sz, s + 1, sh_piv[0], sh_red);
-    grid.sync();
+    cpqr_grid_barrier(a.bar, bar_target);
   }
   if (lane == 0 && my_recomputes) atomicAdd(a.recomputes, (unsigned long long)my_recomputes);
 }
@@ -643,6 +661,8 @@ void cpqr_inplace(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, in
   a.flags = d_flags;
   a.recomputes = reinterpret_cast<unsigned long long*>(d_recomputes);
   a.nopivot = nopivot ? 1 : 0;
+  a.bar = reinterpret_cast<unsigned int*>(a.ppos + 2 * (size_t)Gmax);  // in the 256 B tail of the state
+  LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
   const size_t smem = ld <= kMaxSmemRows ? 2 * sizeof(double) * (size_t)ld : 0;
   const bool fast = padded && ld % 64 == 0 && ld <= 512;
   if (fast) {
