@@ -148,6 +148,8 @@ struct lr_ctx {
   // auxiliary streams of the host-pointer entry points: host->device upload
   // of A (overlapped with the sketch) and device->host of finished factors
   cudaStream_t up_st = nullptr, down_st = nullptr;
+  cudaStream_t side_st = nullptr;  // second chain of independent small factorizations (cholqr2_pair)
+  Workspace ws_side;               // its scratch (split-K partials, Cholesky panels)
   Arena arena;
   // two disjoint SM partitions (green contexts) for the concurrent CUR tail
   struct SmSplit {
@@ -575,6 +577,114 @@ bool cholqr2(lr_ctx* c, int64_t rows, int64_t k, const double* X, int64_t ldx, c
   return std::isfinite(cond_bound) && cond_bound < max_cond;
 }
 
+cudaStream_t aux_stream(cudaStream_t& s);
+
+// Two independent CholeskyQR2 factorizations (cholqr2 above) interleaved on
+// two streams: each is a chain of latency-bound small kernels (Gram GEMM,
+// blocked Cholesky, triangular inverse) with host reads of the Cholesky info
+// and the condition bound; phase by phase the two chains run concurrently and
+// share those synchronisation points (three instead of six).
+struct Chol2Job {
+  int64_t rows, k;
+  const double* X;
+  int64_t ldx;
+  const double* Xt;
+  int64_t ldxt;
+  double* R;
+  double* Rinv;
+  double max_cond;
+  bool ok;
+};
+void cholqr2_pair(lr_ctx* c, Chol2Job& j0, Chol2Job& j1) {
+  cudaStream_t S[2] = {c->st, aux_stream(c->side_st)};
+  Chol2Job* J[2] = {&j0, &j1};
+  DBuf<double> G[2], R1inv[2], Q1[2], G2[2], R2t[2], part[2], f[2];
+  DBuf<int> info(4, c->st);
+  for (int i = 0; i < 2; ++i) {
+    const int64_t k = J[i]->k, rows = J[i]->rows;
+    G[i] = DBuf<double>((size_t)k * k, c->st);
+    R1inv[i] = DBuf<double>((size_t)k * k, c->st);
+    Q1[i] = DBuf<double>((size_t)even(rows) * k, c->st);
+    G2[i] = DBuf<double>((size_t)k * k, c->st);
+    R2t[i] = DBuf<double>((size_t)k * k, c->st);
+    part[i] = DBuf<double>(4 * num_sms() + 4, c->st);
+    f[i] = DBuf<double>(2, c->st);
+    J[i]->ok = false;
+  }
+  cudaEvent_t fork = nullptr, join = nullptr;
+  LRB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventRecord(fork, S[0]));  // the buffers above (and the jobs' inputs) are ordered on S[0]
+  LRB_CUDA(cudaStreamWaitEvent(S[1], fork, 0));
+  cudaStream_t main_st = c->st;
+  // the side chain runs with its own stream AND its own workspace (the GEMM's
+  // split-K partials and the Cholesky panels live in workspace slots)
+  auto on = [&](int i, const std::function<void()>& fn) {
+    c->st = S[i];
+    if (i == 1) c->ws.swap(c->ws_side);
+    auto restore = [&] {
+      if (i == 1) c->ws.swap(c->ws_side);
+      c->st = main_st;
+    };
+    try {
+      fn();
+    } catch (...) {
+      restore();
+      throw;
+    }
+    restore();
+  };
+  auto sync_both = [&] {
+    LRB_CUDA(cudaStreamSynchronize(S[0]));
+    LRB_CUDA(cudaStreamSynchronize(S[1]));
+  };
+  // phase 1: G1 = X^T X (upper tiles), R1 = chol(G1)
+  for (int i = 0; i < 2; ++i)
+    on(i, [&] {
+      const Chol2Job& j = *J[i];
+      gemm(c, j.k, j.k, j.rows, j.X, j.ldx, j.X, j.ldx, G[i], j.k, 1.0, 0.0, -1, true);
+      cholesky_upper(c->ws, j.k, G[i], j.k, info.p + i, c->st);
+      copy_bytes_mapped(c->h_flags + i, info.p + i, sizeof(int), c->st);
+    });
+  sync_both();
+  bool ok[2] = {c->h_flags[0] == 0, c->h_flags[1] == 0};
+  // phase 2: Q1 = X R1^-1, G2 = Q1^T Q1, R2 = chol(G2)
+  for (int i = 0; i < 2; ++i)
+    if (ok[i])
+      on(i, [&] {
+        const Chol2Job& j = *J[i];
+        tri_upper_inverse_blocked(j.k, G[i], j.k, R1inv[i], j.k, c->st);
+        gemm(c, j.rows, j.k, j.k, j.Xt, j.ldxt, R1inv[i], j.k, Q1[i], even(j.rows), 1.0, 0.0, -1, false, kTriQ);
+        gemm(c, j.k, j.k, j.rows, Q1[i], even(j.rows), Q1[i], even(j.rows), G2[i], j.k, 1.0, 0.0, -1, true);
+        cholesky_upper(c->ws, j.k, G2[i], j.k, info.p + 2 + i, c->st);
+        copy_bytes_mapped(c->h_flags + 2 + i, info.p + 2 + i, sizeof(int), c->st);
+      });
+  sync_both();
+  for (int i = 0; i < 2; ++i) ok[i] = ok[i] && c->h_flags[2 + i] == 0;
+  // phase 3: R = R2 R1, R^-1, ||R||_F ||R^-1||_F
+  for (int i = 0; i < 2; ++i)
+    if (ok[i])
+      on(i, [&] {
+        const Chol2Job& j = *J[i];
+        transpose_matrix(j.k, j.k, G2[i], j.k, R2t[i], j.k, c->st);
+        gemm(c, j.k, j.k, j.k, R2t[i], j.k, G[i], j.k, j.R, j.k);
+        tri_upper_inverse_blocked(j.k, j.R, j.k, j.Rinv, j.k, c->st);
+        frob2(j.k, j.k, j.R, j.k, part[i], f[i], c->st);
+        frob2(j.k, j.k, j.Rinv, j.k, part[i], f[i].p + 1, c->st);
+        copy_bytes_mapped(c->h_scal + 2 * i, f[i].p, 2 * sizeof(double), c->st);
+      });
+  sync_both();
+  for (int i = 0; i < 2; ++i) {
+    if (!ok[i]) continue;
+    const double cb = std::sqrt(c->h_scal[2 * i]) * std::sqrt(c->h_scal[2 * i + 1]);
+    J[i]->ok = std::isfinite(cb) && cb < J[i]->max_cond;
+  }
+  LRB_CUDA(cudaEventRecord(join, S[1]));
+  LRB_CUDA(cudaStreamWaitEvent(S[0], join, 0));
+  cudaEventDestroy(fork);
+  cudaEventDestroy(join);
+}
+
 void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out, int64_t ldo) {
   if (!(thr > 0.0 && thr < 1.0)) fail(LR_EINVAL, "pinv: threshold must lie in (0,1)");
   require_nonempty(m, n, "svd");
@@ -873,16 +983,18 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
   copy_matrix(k, n, R, k, Rk, ldk, c->st);  // R with an even leading dimension for TMA
   DBuf<double> Sr((size_t)k * k, c->st), Sri((size_t)k * k, c->st);
   mark(c, "gather_r");
-  const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
-  mark(c, "cholqr2_r");
   c->stats.pinv_fast_path = 0;
   c->stats.concurrent_tail = 0;
   if (u_mode == LR_U_CPINV_A_RPINV) {
     DBuf<double> Rc((size_t)k * k, c->st), Rci((size_t)k * k, c->st);
     DBuf<double> Cm((size_t)even(m) * k, c->st);
     copy_matrix(m, k, C, m, Cm, even(m), c->st);
-    const bool c_ok = cholqr2(c, m, k, Cm, even(m), Ct, ldk, Rc, Rci, fast_cond_limit(thr));
-    mark(c, "cholqr2_c");
+    // R^T = Qr Sr and C = Qc Rc are independent: both CholeskyQR2 chains at once
+    Chol2Job jr{n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr), false};
+    Chol2Job jc{m, k, Cm, even(m), Ct, ldk, Rc, Rci, fast_cond_limit(thr), false};
+    cholqr2_pair(c, jr, jc);
+    const bool r_ok = jr.ok, c_ok = jc.ok;
+    mark(c, "cholqr2_rc");
     if (c_ok && r_ok) {
       c->stats.pinv_fast_path = 1;
       // C = Qc Rc, R^T = Qr Sr  =>  U = C^+ A R^+ = Rc^-1 (Qc^T A Qr) Sr^-T.
@@ -919,6 +1031,8 @@ void u_core(lr_ctx* c, int64_t m, int64_t n, int64_t k, const double* C, const d
     return;
   }
   // u = basis()^T pinv(r) (cur.hpp:30) = R+^T(:, J_skel)^T + coeff R+(J_res, :)
+  const bool r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
+  mark(c, "cholqr2_r");
   DBuf<double> Rpt((size_t)ldk * n, c->st);  // R+^T (k x n)
   if (r_ok) {
     c->stats.pinv_fast_path = 1;
@@ -1833,12 +1947,14 @@ int lr_ctx_destroy(lr_ctx* c) {
     cudaStreamSynchronize(c->st);
     cudaDeviceSynchronize();
     c->ws.release_all();
+    c->ws_side.release_all();
     if (c->arena.base) cudaFree(c->arena.base);
     cudaFreeHost(c->h_flags);
     cudaFreeHost(c->h_scal);
     cudaFreeHost(c->h_ll);
     if (c->up_st) cudaStreamDestroy(c->up_st);
     if (c->down_st) cudaStreamDestroy(c->down_st);
+    if (c->side_st) cudaStreamDestroy(c->side_st);
     release_sm_split(c);
     nccl_comm_destroy(c->comm.comm);
     cudaStreamDestroy(c->own);
@@ -1883,7 +1999,9 @@ int lr_ctx_release_workspace(lr_ctx* c) {
   return guard([&] {
     checked(c);
     LRB_CUDA(cudaStreamSynchronize(c->st));
+    if (c->side_st) LRB_CUDA(cudaStreamSynchronize(c->side_st));
     c->ws.release_all();
+    c->ws_side.release_all();
     c->oz_src = nullptr;
     c->oz_pinned = false;
     c->oz_cache_on = false;

@@ -54,6 +54,12 @@ class Workspace {
   void* try_get(WsSlot s, size_t bytes);
   double* get_doubles(WsSlot s, size_t n) { return static_cast<double*>(get(s, n * sizeof(double))); }
   void release_all();
+  void swap(Workspace& o) noexcept {
+    ptr_.swap(o.ptr_);
+    cap_.swap(o.cap_);
+  }
+  Workspace(const Workspace&) = delete;  // owns device allocations
+  Workspace& operator=(const Workspace&) = delete;
 
  private:
   std::vector<void*> ptr_;
