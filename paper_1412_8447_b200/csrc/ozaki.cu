@@ -306,9 +306,9 @@ __global__ void __launch_bounds__(256) split_kernel(int64_t K, int64_t cols, con
 // cluster-wide: every CTA's MMA commit arrives on the stage's empty barrier
 // in all four CTAs (count 4).
 constexpr int IBM = 128, IBN = 512, IBK = 64;  // tile; K in bytes (= int8 elements) per stage
-constexpr int ICL = 4;                         // cluster size along M
+constexpr int ICL = 4;                         // cluster size along M (largest; 2 and 1 for short M)
 constexpr int ISTAGES = 5;
-constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, IB_SLICE = IB_BYTES / ICL;
+constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK;
 constexpr int ISTAGE_BYTES = IA_BYTES + IB_BYTES;
 constexpr int ITHREADS = 6 * 32;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2-5 epilogue
 constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
@@ -348,7 +348,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-__global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
+// CL: CTAs per cluster along M sharing the Q tile by multicast (4 when the M
+// tiles come in fours; 2 / 1 for short M, e.g. C3's l = 210 = 2 tiles, which a
+// 4-cluster would pad to 4 tiles of mostly zero rows)
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(ITHREADS, 1)
     imma_gemm_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
                      int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride, uint32_t ab_fmt) {
   extern __shared__ uint8_t smem_raw[];
@@ -368,7 +372,7 @@ __global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
     if (lane == 0) {
       for (int s = 0; s < ISTAGES; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], ICL);
+        mbar_init(&empty[s], CL);
       }
       mbar_init(tmem_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -394,8 +398,12 @@ __global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
         uint8_t* sp = smem + s * ISTAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], ISTAGE_BYTES);
         tma_load_3d(sp, &tmp, &full[s], i * IBK, m0, plane);
-        tma_load_3d_mc(sp + IA_BYTES + rank * IB_SLICE, &tmq, &full[s], i * IBK, n0 + (int)rank * (IBN / ICL), plane,
-                       (uint16_t)((1u << ICL) - 1));
+        // this CTA's 512 / CL columns of the Q stage, in TMA boxes of at most 256 columns
+        constexpr int kBox = IBN / CL < 256 ? IBN / CL : 256;
+#pragma unroll
+        for (int t = 0; t < IBN / CL / kBox; ++t)
+          tma_load_3d_mc(sp + IA_BYTES + rank * (IB_BYTES / CL) + t * kBox * IBK, &tmq, &full[s], i * IBK,
+                         n0 + (int)rank * (IBN / CL) + t * kBox, plane, (uint16_t)((1u << CL) - 1));
       }
     }
   } else if (warp == 1) {
@@ -427,7 +435,7 @@ __global__ void __cluster_dims__(ICL, 1, 1) __launch_bounds__(ITHREADS, 1)
         asm volatile(
             "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
                 smem_u32(&empty[s])),
-            "h"((uint16_t)((1u << ICL) - 1))
+            "h"((uint16_t)((1u << CL) - 1))
             : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -805,21 +813,27 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
   if (P.K > (int64_t(1) << 17)) throw CudaError("ozaki_gemm_tn: K > 2^17 would overflow the int32 accumulators");
   static bool attr = false;
   if (!attr) {
-    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
     attr = true;
   }
+  const int tiles_m0 = (int)((M + IBM - 1) / IBM);
+  // the cluster size that wastes no M tile (padding 2 tiles to 4 doubled C3's sketch work)
+  const int cl = tiles_m0 % 4 == 0 ? 4 : (tiles_m0 % 2 == 0 ? 2 : (tiles_m0 == 1 ? 1 : 4));
   const CUtensorMap tp = make_tmap_i8_planes(P.planes, P.K, P.cols, P.ld, P.plane_stride, IBM);
-  const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, IBN / ICL);
+  const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, std::min(256, IBN / cl));
   const int64_t ldr = (M + 15) / 16 * 16;  // 4-byte aligned residue columns for crt4_kernel
   int8_t* res = static_cast<int8_t*>(ws.get(WsSlot::kTmp7, (size_t)ldr * N * kOzakiModuli));
   const int tiles_m = (int)((M + IBM - 1) / IBM), tiles_n = (int)((N + IBN - 1) / IBN);
-  // clusters of ICL CTAs along M: pad the M grid (extra CTAs compute zero rows and store nothing)
-  dim3 grid((tiles_m + ICL - 1) / ICL * ICL, tiles_n, kOzakiModuli);
+  // clusters of cl CTAs along M: pad the M grid (extra CTAs compute zero rows and store nothing)
+  dim3 grid((tiles_m + cl - 1) / cl * cl, tiles_n, kOzakiModuli);
   if (P.unsigned_res && Q.unsigned_res) throw CudaError("ozaki_gemm_tn: at most one unsigned-residue operand");
   if ((P.unsigned_res || Q.unsigned_res) && P.K > kOzakiMaxKUnsigned)
     throw CudaError("ozaki_gemm_tn: K too large for an unsigned-residue operand");
   const uint32_t ab_fmt = (P.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
-  imma_gemm_kernel<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, ldr * N, ab_fmt);
+  auto kern = cl == 4 ? imma_gemm_kernel<4> : (cl == 2 ? imma_gemm_kernel<2> : imma_gemm_kernel<1>);
+  kern<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, ldr * N, ab_fmt);
   LRB_CHECK_LAUNCH();
   const int64_t items = (M + 3) / 4 * N;
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 8 * num_sms()));
