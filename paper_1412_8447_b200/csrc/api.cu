@@ -611,11 +611,23 @@ void cholqr2_pair(lr_ctx* c, Chol2Job& j0, Chol2Job& j1) {
     f[i] = DBuf<double>(2, c->st);
     J[i]->ok = false;
   }
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr;
   LRB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-  LRB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
   LRB_CUDA(cudaEventRecord(fork, S[0]));  // the buffers above (and the jobs' inputs) are ordered on S[0]
   LRB_CUDA(cudaStreamWaitEvent(S[1], fork, 0));
+  cudaEventDestroy(fork);
+  // Declared after the buffers, so it runs first on every exit (an exception
+  // included): S[0] waits for the side chain before any buffer is released.
+  struct Join {
+    cudaStream_t main, side;
+    ~Join() {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+      cudaEventRecord(e, side);
+      cudaStreamWaitEvent(main, e, 0);
+      cudaEventDestroy(e);
+    }
+  } join{S[0], S[1]};
   cudaStream_t main_st = c->st;
   // the side chain runs with its own stream AND its own workspace (the GEMM's
   // split-K partials and the Cholesky panels live in workspace slots)
@@ -679,10 +691,6 @@ void cholqr2_pair(lr_ctx* c, Chol2Job& j0, Chol2Job& j1) {
     const double cb = std::sqrt(c->h_scal[2 * i]) * std::sqrt(c->h_scal[2 * i + 1]);
     J[i]->ok = std::isfinite(cb) && cb < J[i]->max_cond;
   }
-  LRB_CUDA(cudaEventRecord(join, S[1]));
-  LRB_CUDA(cudaStreamWaitEvent(S[0], join, 0));
-  cudaEventDestroy(fork);
-  cudaEventDestroy(join);
 }
 
 void pinv_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, double thr, double* out, int64_t ldo) {
@@ -2860,6 +2868,15 @@ int lr_read_matrix_binary_d(lr_ctx* c, const char* path, int64_t* rows, int64_t*
     };
     cudaEvent_t all[4] = {copied[0], copied[1], used[0], used[1]};
     Ev ev{all};
+    // runs before the buffers above are released, on every exit: no copy or
+    // transpose may still touch them
+    struct Drain {
+      cudaStream_t a, b;
+      ~Drain() {
+        cudaStreamSynchronize(a);
+        cudaStreamSynchronize(b);
+      }
+    } drain{up, c->st};
     int64_t blk = 0;
     for (int64_t i0 = 0; i0 < m; i0 += rb, ++blk) {
       const int b = (int)(blk & 1);
