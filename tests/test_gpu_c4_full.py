@@ -127,3 +127,39 @@ def test_c4_full_size_verifiers(lr, gold, c4_matrix):
     assert co["holds"] and co["e_norm"] == pytest.approx(l1["e_norm"], rel=1e-10)
     assert co["lhs"] == pytest.approx(l1["lhs"], rel=1e-10)
     print(f"C4 lemma1 {l1}  corollary {co}")
+
+
+def test_c4_full_size_sharded_protocol_8_shards(lr, gold, c4_matrix):
+    """The column-sharded pipeline (lr_randomized_cur_sharded_d) at full C4 size
+    with its CPQRs run as 8 column blocks (shard emulation: each step the 8
+    blocks' pivot candidates are gathered and every block applies the winner's
+    reflector to its own columns -- the multi-GPU protocol on one GPU, kernels
+    in sequence): the oracle's index sets, U, T checksums and error."""
+    import torch
+
+    from paper_1412_8447_b200 import distributed as D
+    a = c4_matrix
+    k = int(gold["k"])
+    ctx = lr.default_context()
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+    D.set_shard_emulation(ctx, 8)
+    try:
+        ctx.reset_stats()
+        sk = lr.SketchConfig(oversample=int(gold["oversample"]), seed=int(gold["sketch_seed"]))
+        out = D.randomized_cur_sharded_device(ctx, a, 0, a.shape[1], k, sk)
+        torch.cuda.synchronize()
+        stats = ctx.stats()
+    finally:
+        D.set_shard_emulation(ctx, 0)
+        ctx.set_gemm_mode(ctx.GEMM_DMMA)
+    assert np.array_equal(out["col_pivots"].cpu().numpy(), gold["col_pivots"])
+    assert np.array_equal(out["row_pivots"].cpu().numpy(), gold["row_pivots"])
+    assert rel(out["u"].cpu().numpy(), gold["u"]) <= TOL
+    for key, prefix in (("col_coeff", "tcol"), ("row_coeff", "trow")):
+        ck = _checks(out[key].cpu().numpy(), gold, prefix)
+        for name in ("colnorms", "tg", "ht"):
+            assert rel(ck[name], gold[f"{prefix}_{name}"]) <= TOL, (key, name)
+    cur = {"c": out["c"], "u": out["u"], "r": out["r_local"]}
+    e, na = lr.cur_error_fro_device(a, cur, ctx=ctx)
+    assert e / na == pytest.approx(float(gold["err"]) / float(gold["na"]), rel=TOL)
+    assert stats["norm_recomputes"] == int(gold["recomputes_y"]) + int(gold["recomputes_ct"])
