@@ -40,129 +40,14 @@
 #include <vector>
 #include <algorithm>
 
-#include "common.cuh"
-#include "kernels.h"
+#include "cpqr_panel.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace lrb {
 
+namespace cpqr_detail {
 namespace {
-
-constexpr int NB = 32;       // panel width (one F entry per lane)
-constexpr int CH = 8;        // 64-row chunks held in registers: ld <= 512
-constexpr int PT = 256;      // threads per CTA (8 warps, one CTA per SM; up to 255 registers)
-constexpr int kRowsPerThread = (64 * CH + PT - 1) / PT;
-constexpr int PW = PT / 32;
-constexpr int kMaxG = 256;       // per-CTA partials read by one warp (8 per lane)
-constexpr int kHdr = 4;      // candidate header: alpha, beta, tau, apply
-// dynamic shared memory: (NB+2) ld doubles (v, V, scratch) + per owned slot two
-// norms and a logical position; the opt-in ceiling (227 KB) also holds the static arrays
-constexpr int kSmemLimit = 216 * 1024;
-inline size_t panel_smem_bytes(int64_t ld, int64_t maxcols) {
-  // + logical positions, active list, zero list (ints)
-  return sizeof(double) * ((size_t)(NB + 2) * ld + 2 * (size_t)maxcols) + sizeof(int) * 3 * (size_t)maxcols;
-}
-
-struct PanelArgs {
-  double* W;
-  int64_t m, n, ld, k;
-  int64_t t0, t1;            // steps [t0, t1) of this launch (t1 - t0 <= NB)
-  int init;                  // first launch: norms, pivots, first candidate
-  int64_t* piv;
-  double* nrm;
-  double* nrmx;
-  double* tau;
-  double* pval;              // [2][G]
-  long long* ppos;           // [2][G]
-  double* cand;              // [2][G][kHdr + ld + NB]: reflector + w of each CTA's best column
-  double* F;                 // [n][NB] row-major
-  double* Vg;                // [ld][NB] row-major copy of the panel's V (GEMM operand)
-  int* flags;
-  unsigned long long* recomputes;
-  unsigned long long* trace;  // optional per-phase ns of CTA 0 (LRB_CPQR_TRACE), 8 slots
-  unsigned long long* tstep;  // optional per-step barrier arrival / departure times [k][G][2]
-  unsigned int* bar;          // grid barrier counter (zeroed before each launch)
-  int64_t maxcols;            // columns per CTA bound (shared-memory norm arrays)
-  int* posof;                 // [n] logical position of each column slot (between launches)
-  unsigned int* ctag;         // [G] step + 1 of the candidate each CTA last staged (release-published)
-  int* nzero;                 // identically-zero columns found by the first launch
-  int keep1024;               // the last keep1024/1024 of each warp's sweep is loaded L2::evict_last
-};
-
-// Grid barrier for the co-resident (cooperative) grid: one release atomic per
-// CTA on a monotonic counter and an acquire spin without back-off.  (The
-// cooperative-groups grid.sync measured ~9 us per barrier here; this one is
-// the latency of an L2 atomic round trip plus the last arrival.)
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& target) {
-  target += gridDim.x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // release: the CTA's writes (ordered before this thread by the barrier) become visible gpu-wide
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
-// the two halves of grid_barrier: publish (after the CTA's partial is
-// written) and wait -- the candidate staging runs in between
-__device__ __forceinline__ void grid_arrive(unsigned int* bar, unsigned int& target) {
-  target += gridDim.x;
-  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-}
-__device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int target) {
-  if (threadIdx.x == 0) {
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ bool better(double v1, long long p1, double v2, long long p2) {
-  return v1 > v2 || (v1 == v2 && p1 < p2);
-}
-
-// column loads with an L2 eviction priority: the columns a warp visits last in
-// step s are the ones it visits first in step s + 1 (the sweep alternates
-// direction), so they are kept (evict_last) and the rest streamed (evict_first)
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-  uint64_t p;
-  if (keep)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double2 ld_l2hint(const double2* ptr, uint64_t pol) {
-  double2 r;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(r.x), "=d"(r.y)
-               : "l"(ptr), "l"(pol));
-  return r;
-}
-
-__device__ double cta_sum(double x, double* sh) {
-  x = warp_sum(x);
-  const int w = threadIdx.x >> 5;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[w] = x;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < PW; ++i) t += sh[i];
-  return t;
-}
 
 struct Col {
   double c[CH][2];
@@ -191,21 +76,7 @@ struct PassCtx {
   unsigned long long recomputes;
 };
 
-// group version of the recompute (L lanes per column): rows s+1..m-1 of the
-// column re-read from W (L2-hot), F(j, 0:c] from global (written by the group)
-template <int L>
-__device__ __forceinline__ double group_recompute(const double* col, const double* Fj, int64_t s, int64_t m,
-                                               int64_t ld, int c, const double* Vs, int l) {
-  double q = 0.0;
-  for (int64_t r = s + 1 + l; r < m; r += L) {
-    double x = col[r];
-    for (int i = 0; i <= c; ++i) x = fma(-Vs[i * ld + r], Fj[i], x);
-    q = fma(x, x, q);
-  }
-#pragma unroll
-  for (int o = L / 2; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  return q;
-}
+
 
 // One step's pass over a warp's column slots (pivoted slots: loads only).
 // TC0 = first active 64-row chunk (s / 64, constant over a 32-step panel),
@@ -850,8 +721,9 @@ __global__ void move_slots_kernel(double* __restrict__ W, int64_t ld, const int*
   }
 }
 
-
 }  // namespace
+}  // namespace cpqr_detail
+using namespace cpqr_detail;
 
 bool cpqr_panel_supported(int64_t m, int64_t n, int64_t ld, bool padded) {
   static const bool off = [] {
@@ -892,7 +764,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   static const KernSet ks[2] = {{LRB_PANEL_K(false)}, {LRB_PANEL_K(true)}};
 #undef LRB_PANEL_K
   const int nld = (int)(ld / 64);
-  auto kern_for = [&](int64_t t0, bool list) -> KernT {
+  auto kern_for = [&](int64_t t0, bool list, bool lazy) -> KernT {
+    if (lazy) return lazy_kernel_for(nld, (int)(t0 / 64), list);
     const KernSet& k = ks[list ? 1 : 0];
     const int tc = (int)(t0 / 64);
     if (nld == 8) return k.k8[tc];
@@ -915,6 +788,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       for (KernT kf : k.k8) set(kf);
       set(k.gen);
     }
+    lazy_set_attributes();
     LRB_CUDA(cudaFuncSetAttribute(panel_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 256 * 64)));
     attr = true;
@@ -924,13 +798,24 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   int G = std::min(grid_cap > 0 ? std::min(grid_cap, num_sms()) : num_sms(), kMaxG);
   G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + PW - 1) / PW));
   const int64_t maxcols = (n + G - 1) / G + 1;
-  const size_t smem = panel_smem_bytes(ld, maxcols);
+  // Bound-pruned (lazy) steps for wide sweeps, where the eager pass streams the
+  // whole trailing block every step; for narrower ones (n < 32768) the eager
+  // pass is cheaper than the lazy panels' end-of-panel catch-up (measured:
+  // 510 x 65536 C4 sample 17.2 -> 14.7 ms, 210 x 20000 2.7 -> 4.3 ms).
+  // LRB_CPQR_LAZY=0 / 1 forces either (read per call: tests switch it in-process).
+  const char* lz_env = getenv("LRB_CPQR_LAZY");
+  const bool lazy_want = lz_env ? atoi(lz_env) != 0 : n >= 32768;
+  static const double lazy_beta = getenv("LRB_CPQR_BETA") ? atof(getenv("LRB_CPQR_BETA")) : 0.0;
+  const bool lazy = lazy_want && lazy_smem_bytes(ld, maxcols) <= (size_t)kSmemLimit;
+  const size_t smem = lazy ? lazy_smem_bytes(ld, maxcols) : panel_smem_bytes(ld, maxcols);
   if (smem > (size_t)kSmemLimit) throw CudaError("cpqr_panel: too many columns per CTA for the shared norms");
   const size_t cand_sz = kHdr + (size_t)ld + NB;
   const size_t nd = 2 * (size_t)n + 2 * (size_t)G + 2 * (size_t)G * cand_sz + (size_t)n * NB + (size_t)ld * NB;
   const size_t ndisp = 2 * (size_t)k + 2;  // slots away from their final position: <= 2 per step
   const size_t bytes = sizeof(double) * (nd + ndisp * (size_t)ld) + sizeof(long long) * 2 * (size_t)G + 256 +
-                       sizeof(int) * ((size_t)n + ndisp + 2) + sizeof(unsigned int) * (size_t)G;
+                       sizeof(int) * ((size_t)n + ndisp + 2) + sizeof(unsigned int) * (size_t)G +
+                       // lazy: wall, stats, epoch, catch-up levels
+                       sizeof(double) * NB * NB + 4 * sizeof(unsigned long long) + sizeof(int) * ((size_t)n + 2) + 8;
   uint8_t* base = static_cast<uint8_t*>(ws.get(WsSlot::kCpqrState, bytes));
   PanelArgs a{};
   a.W = W;
@@ -955,6 +840,16 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   int* disp_count = disp_list + ndisp;
   a.ctag = reinterpret_cast<unsigned int*>(disp_count + 2);
   a.nzero = disp_count + 1;
+  {  // lazy state after the tags (8-byte aligned)
+    uintptr_t pz = reinterpret_cast<uintptr_t>(a.ctag + G);
+    pz = (pz + 7) & ~uintptr_t(7);
+    a.wall = reinterpret_cast<double*>(pz);
+    a.lstats = reinterpret_cast<unsigned long long*>(a.wall + NB * NB);
+    a.epoch = reinterpret_cast<unsigned int*>(a.lstats + 3);
+    a.cjg = reinterpret_cast<int*>(a.lstats + 4);
+    a.beta = lazy_beta;
+    if (lazy) LRB_CUDA(cudaMemsetAsync(a.lstats, 0, 4 * sizeof(unsigned long long), st));
+  }
   LRB_CUDA(cudaMemsetAsync(a.nzero, 0, sizeof(int), st));
   LRB_CUDA(cudaMemsetAsync(a.ctag, 0xFF, sizeof(unsigned int) * (size_t)G, st));  // no candidate staged yet
   a.maxcols = maxcols;
@@ -987,9 +882,10 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   bool list = true;
   thread_local int* h_nzero = nullptr;  // mapped pinned word (no copy-engine queueing)
   if (!h_nzero) LRB_CUDA(cudaMallocHost(&h_nzero, sizeof(int)));
-  for (int64_t t0 = 0; t0 < k; t0 += NB) {
-    const int64_t t1 = std::min<int64_t>(k, t0 + NB);
-    if (t0 == NB) {
+  const int64_t pstep = lazy ? NBL : NB;  // steps per launch
+  for (int64_t t0 = 0; t0 < k; t0 += pstep) {
+    const int64_t t1 = std::min<int64_t>(k, t0 + pstep);
+    if (t0 == pstep) {
       LRB_CUDA(cudaStreamSynchronize(st));
       list = *h_nzero > 0;
     }
@@ -1007,7 +903,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
     evrec();
     void* params[] = {&a};
-    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list), dim3(G), dim3(PT), params, smem, st));
+    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list, lazy), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
     if (t0 == 0) copy_bytes_mapped(h_nzero, a.nzero, sizeof(int), st);
     evrec();
@@ -1029,8 +925,31 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       fprintf(stderr, "\n");
       prev = h;
     }
+    if (lazy) {  // catch every column up on this panel's reflectors, then the rank-NB update
+      FinArgs fa{};
+      fa.W = W;
+      fa.ld = ld;
+      fa.m = m;
+      fa.n = n;
+      fa.t0 = t0;
+      fa.t1 = t1;
+      fa.r1 = std::min<int64_t>(ld, (m + 7) & ~int64_t(7));
+      fa.C = (int)(t1 - t0);
+      fa.upd = (t1 < k && t1 < m && t1 < n && fa.r1 > t1) ? 1 : 0;
+      fa.Vg = a.Vg;
+      fa.F = a.F;
+      fa.tau = tau + t0;
+      fa.wall = a.wall;
+      fa.nrm = a.nrm;
+      fa.nrmx = a.nrmx;
+      fa.cj = a.cjg;
+      fa.recomputes = a.recomputes;
+      const int64_t ngroups = (n + 7) / 8;
+      const int fg = (int)std::min<int64_t>((ngroups + FW - 1) / FW, num_sms());
+      launch_panel_finalize(fa, fg, st);
+    }
     // A_p(t1:m, t1:n) -= V(t1:m, 0:c) F(t1:n, 0:c)^T  (rows/cols of later panels only)
-    if (t1 < k && t1 < m && t1 < n) {
+    if (!lazy && t1 < k && t1 < m && t1 < n) {
       // every slot (pivoted ones have F = 0); rows t1..m rounded up to 8 (padding rows stay 0)
       const int64_t r1 = std::min<int64_t>(ld, (m + 7) & ~int64_t(7));
       const int64_t ngroups = (n + 7) / 8;
@@ -1097,6 +1016,13 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       double cyc = 0, ns = 0;
       for (int g = 0; g < G; ++g) { cyc += (double)h[g * 8 + 6]; ns += (double)h[g * 8 + 7]; }
       fprintf(stderr, "cpqr_panel trace SM clock %.0f MHz over %.3f ms\n", 1e3 * cyc / ns, ns / G / 1e6);
+    }
+    if (lazy) {
+      unsigned long long ls[2];
+      LRB_CUDA(cudaMemcpyAsync(ls, a.lstats, sizeof ls, cudaMemcpyDeviceToHost, st));
+      LRB_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "cpqr_lazy: %llu retry rounds, %.1f columns evaluated per step (%.2f%% of n)\n", ls[0],
+              (double)ls[1] / (double)std::max<int64_t>(1, k), 100.0 * (double)ls[1] / (double)std::max<int64_t>(1, k) / (double)n);
     }
     if (a.tstep) {  // per step: the last-arriving CTA's phases vs the CTA mean (steps 1..k-1)
       std::vector<unsigned long long> t(4 * (size_t)G * k);
