@@ -457,6 +457,54 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
     }
     __syncthreads();
   }
+  if (a.entry) {  // first eager launch after lazy panels: exact norms, no candidate staged yet
+    double bv = -INFINITY;
+    long long bp = INT64_MAX;
+    for (int i = threadIdx.x; i < sh_nact; i += PT) {
+      const int j = LIST ? alist[i] : (int)c0 + i;
+      const int li = j - (int)c0;
+      const long long key = ((long long)spos[li] << 32) | (long long)j;
+      if (snr[li] != -INFINITY && better(snr[li], key, bv, bp)) { bv = snr[li]; bp = key; }
+    }
+    if (threadIdx.x == 0) sh_zkey = ~0ull;
+    __syncthreads();
+    if (LIST) {  // the lowest logical position among the live zero slots competes at norm 0
+      unsigned long long zk = ~0ull;
+      for (int t = threadIdx.x; t < sh_nzero; t += PT) {
+        const int z = zlist[t] - (int)c0;
+        if (snr[z] == -INFINITY) continue;
+        const unsigned long long key = ((unsigned long long)spos[z] << 32) | (unsigned long long)(c0 + z);
+        zk = key < zk ? key : zk;
+      }
+      if (zk != ~0ull) atomicMin(&sh_zkey, zk);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const long long op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
+    }
+    if (lane == 0) { sh_bv[warp] = bv; sh_bp[warp] = bp; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double cv = sh_bv[0];
+      long long cp = sh_bp[0];
+      for (int w = 1; w < PW; ++w)
+        if (better(sh_bv[w], sh_bp[w], cv, cp)) { cv = sh_bv[w]; cp = sh_bp[w]; }
+      if (LIST && sh_zkey != ~0ull && better(0.0, (long long)sh_zkey, cv, cp)) {
+        cv = 0.0;
+        cp = (long long)sh_zkey;
+      }
+      a.pval[(a.t0 & 1) * G + cta] = cv;
+      a.ppos[(a.t0 & 1) * G + cta] = cp;
+      sh_piv[0] = cp;
+    }
+    __syncthreads();
+    stage(a.cand + ((a.t0 & 1) * G + cta) * cand_sz, a.t0, sh_piv[0] & 0xffffffffll, 0, false);
+    if (threadIdx.x == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ctag + cta), "r"((unsigned int)(a.t0 + 1)) : "memory");
+    grid_barrier(a.bar, bar_target);
+  }
 
   // ------------------------------------------------------------ steps of this panel
   const bool tr = a.trace != nullptr && threadIdx.x == 0;
@@ -882,10 +930,20 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
   bool list = true;
   thread_local int* h_nzero = nullptr;  // mapped pinned word (no copy-engine queueing)
   if (!h_nzero) LRB_CUDA(cudaMallocHost(&h_nzero, sizeof(int)));
-  const int64_t pstep = lazy ? NBL : NB;  // steps per launch
-  for (int64_t t0 = 0; t0 < k; t0 += pstep) {
-    const int64_t t1 = std::min<int64_t>(k, t0 + pstep);
-    if (t0 == pstep) {
+  // lazy panels (NBL steps) while the trailing block is tall; the last
+  // LRB_CPQR_EAGER_ROWS (default 0: measured no gain at 128-256) rows of ld run the eager kernel, whose
+  // per-step pass is cheap once the sweep is short (its first launch stages
+  // the entry candidate itself: a.entry)
+  static const int64_t eager_rows = getenv("LRB_CPQR_EAGER_ROWS") ? atoll(getenv("LRB_CPQR_EAGER_ROWS")) : 0;
+  const int64_t lazy_end = lazy ? std::max<int64_t>(0, ((ld - eager_rows) / 64) * 64) : 0;
+  int launches = 0;
+  bool prev_lazy = false;
+  for (int64_t t0 = 0, t1 = 0; t0 < k; t0 = t1) {
+    const bool lz = lazy && t0 < lazy_end;
+    t1 = std::min<int64_t>(k, t0 + (lz ? NBL : NB));
+    a.entry = (!lz && prev_lazy) ? 1 : 0;
+    prev_lazy = lz;
+    if (++launches == 2) {
       LRB_CUDA(cudaStreamSynchronize(st));
       list = *h_nzero > 0;
     }
@@ -903,7 +961,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
     evrec();
     void* params[] = {&a};
-    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list, lazy), dim3(G), dim3(PT), params, smem, st));
+    LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list, lz), dim3(G), dim3(PT), params, smem, st));
     LRB_CHECK_LAUNCH();
     if (t0 == 0) copy_bytes_mapped(h_nzero, a.nzero, sizeof(int), st);
     evrec();
@@ -925,7 +983,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       fprintf(stderr, "\n");
       prev = h;
     }
-    if (lazy) {  // catch every column up on this panel's reflectors, then the rank-NB update
+    if (lz) {  // catch every column up on this panel's reflectors, then the rank-NB update
       FinArgs fa{};
       fa.W = W;
       fa.ld = ld;
@@ -949,7 +1007,7 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       launch_panel_finalize(fa, fg, st);
     }
     // A_p(t1:m, t1:n) -= V(t1:m, 0:c) F(t1:n, 0:c)^T  (rows/cols of later panels only)
-    if (!lazy && t1 < k && t1 < m && t1 < n) {
+    if (!lz && t1 < k && t1 < m && t1 < n) {
       // every slot (pivoted ones have F = 0); rows t1..m rounded up to 8 (padding rows stay 0)
       const int64_t r1 = std::min<int64_t>(ld, (m + 7) & ~int64_t(7));
       const int64_t ngroups = (n + 7) / 8;

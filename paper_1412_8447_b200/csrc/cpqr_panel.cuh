@@ -53,6 +53,7 @@ struct PanelArgs {
   double* wall;               // [NB][NB] w of each panel step (row c: V(:, i)^T v_c, i < c)
   unsigned int* epoch;        // rounds published so far (candidate tags / buffer parity across launches)
   double beta;                // > 0: fixed threshold factor; <= 0: adaptive
+  int entry;                  // eager kernel after lazy panels: stage the step-t0 candidate first
   unsigned long long* lstats; // [0] retry rounds, [1] columns evaluated by the step passes
 };
 
