@@ -140,8 +140,12 @@ def kernel_rooflines(cfg, st, per_step, engine):
             ach = b / (st[name] * 1e-3) / 1e9
             tb = traffic.get(name)
             meas = tb / (st[name] * 1e-3) / 1e9 if tb else None
-            out[name] = {"kernel": "cpqr_panel_kernel x16 + panel_update_dmma_kernel x15 (delayed-update CPQR, one "
-                                   "cooperative launch per 32 steps, logical column swaps)",
+            kern = ("cpqr_lazy_kernel x32 + panel_finalize_kernel x32 (bound-pruned panel CPQR: per step only the "
+                    "columns whose norm bound can reach the maximum are caught up; one cooperative launch per 16 "
+                    "steps, DMMA end-of-panel catch-up + rank-16 update, logical column swaps)") if cols >= 32768 else (
+                    "cpqr_panel_kernel x16 + panel_update_dmma_kernel x15 (delayed-update CPQR, one cooperative "
+                    "launch per 32 steps, logical column swaps)")
+            out[name] = {"kernel": kern,
                          "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "traffic": tb,
                          "measured_bytes_gbs": round(meas, 1) if meas else None,
@@ -152,10 +156,9 @@ def kernel_rooflines(cfg, st, per_step, engine):
                                                 "does not move",
                          "algorithmic": f"SURVEY 8d right-looking count sum_s 16 (rows-s)(cols-s) + 32 (cols-s) "
                                         f"= {b:.4e} B per launch (the panel form moves less: see traffic)",
-                         "note": "per step ~7 us of fixed latency (argmax -> reflector broadcast -> candidate "
-                                 "staging -> grid barrier) on top of the HBM-bound pass; runs at the power-capped "
-                                 "SM clock left by the INT8 GEMMs; tools/bench_cpqr.py with LRB_CPQR_TRACE=1 "
-                                 "breaks it down"}
+                         "note": "latency-bound per step (candidate loads -> catch-up -> CTA argmax -> grid "
+                                 "barrier -> reflector staging); runs at the power-capped SM clock left by the INT8 "
+                                 "GEMMs; tools/bench_cpqr.py with LRB_CPQR_TRACE=1 breaks it down"}
     return out
 
 

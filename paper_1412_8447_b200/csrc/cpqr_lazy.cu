@@ -35,7 +35,7 @@ __device__ __forceinline__ void lazy_tag_wait(const unsigned int* tag, unsigned 
   do {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(tag) : "memory");
     if (clock64() - t0 > (8ll << 30)) lazy_stuck("candidate tag", s, t, want);
-  } while (t != want);
+  } while (!tag_ready(t, want));
 }
 
 // ============================================================ lazy (bound-pruned) variant

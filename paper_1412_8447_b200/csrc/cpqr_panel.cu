@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_panel_kernel(PanelArgs a) {
         unsigned int t;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.ctag + bc) : "memory");
-        } while (t != (unsigned int)(s + 1));
+        } while (!tag_ready(t, (unsigned int)(s + 1)));
       }
     }
     __syncthreads();
@@ -959,6 +959,9 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
       a.keep1024 = (int)std::min(1024.0, 1024.0 * keep_mb * 1e6 / sweep);
     }
     LRB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned int), st));
+    // eager tags count steps, lazy ones rounds (>= steps): waiters accept tags >= the wanted
+    // one, so the lazy panels' tags are cleared before the eager tail
+    if (a.entry) LRB_CUDA(cudaMemsetAsync(a.ctag, 0xFF, sizeof(unsigned int) * (size_t)G, st));
     evrec();
     void* params[] = {&a};
     LRB_CUDA(cudaLaunchCooperativeKernel((void*)kern_for(t0, list, lz), dim3(G), dim3(PT), params, smem, st));

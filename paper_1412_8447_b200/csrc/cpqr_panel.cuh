@@ -91,6 +91,15 @@ __device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int 
   __syncthreads();
 }
 
+// A CTA's candidate tag is monotonic within one CPQR call (reset to ~0u: none
+// staged yet).  A waiter accepts any tag >= the one it needs: the owner may
+// already have staged its next round's candidate (other buffer parity) while a
+// slow CTA is still reading this round's -- waiting for equality would then
+// deadlock the grid.
+__device__ __forceinline__ bool tag_ready(unsigned int t, unsigned int want) {
+  return t != ~0u && (int)(t - want) >= 0;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -28,7 +28,7 @@ def rows(path):
 
 def short(n):
     n = n.split("(")[0].replace("void ", "").replace("lrb::", "").replace("(anonymous namespace)::", "")
-    return n.replace("<unnamed>::", "")
+    return n.replace("<unnamed>::", "").replace("cpqr_detail::", "")
 
 
 def main(path):

@@ -28,7 +28,8 @@ def main(path, out):
         return {"launches": len(ids), "dram_read_bytes": rd, "dram_write_bytes": wr, "traffic_bytes": rd + wr,
                 "ncu_ms": round(ms, 4)}
 
-    cp = [i for i in seg if names[i].startswith(("cpqr_panel_kernel", "panel_update", "perm_scatter", "move_slots"))]
+    cp = [i for i in seg if names[i].startswith(("cpqr_panel_kernel", "cpqr_lazy_kernel", "panel_finalize_kernel",
+                                                 "panel_update", "perm_scatter", "move_slots"))]
     # two CPQRs: split at the largest index gap
     gaps = [(cp[j + 1] - cp[j], j) for j in range(len(cp) - 1)]
     cut = max(gaps)[1] + 1
@@ -45,7 +46,8 @@ def main(path, out):
     }
     res["per_launch"] = {k: v["traffic_bytes"] for k, v in res["per_step"].items()}
     res["per_launch_note"] = ("bytes = dram__bytes_read.sum + dram__bytes_write.sum summed over the launches of one "
-                              "stage (CPQR: 16 panel launches + 15 DMMA panel updates + final permutation; INT8 GEMM: "
+                              "stage (CPQR: every panel launch -- eager or bound-pruned -- with its DMMA update / finalize and "
+                              "the final permutation; INT8 GEMM: "
                               "imma + crt; split: every colmax + split launch of the step)")
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res["per_step"], indent=1))
