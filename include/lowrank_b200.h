@@ -116,6 +116,14 @@ int lr_ctx_clear_operand_cache(lr_ctx* ctx);
    2 bytes of HBM per byte of A, CPQR state, the call arena) */
 int lr_ctx_release_workspace(lr_ctx* ctx);
 int lr_ctx_get_gemm_mode(lr_ctx* ctx);
+/* Schedule of the randomized CUR's tail (u_mode LR_U_CPINV_A_RPINV, large A).
+   After C = A(:, J) two chains are independent: the row ID of C (CPQR of C^T,
+   id.hpp:101-128) and Q_c -> A^T Q_c (lowrank_main.cpp:210-215).  sms > 0 runs
+   them concurrently, the row ID on an SM partition of that size; 0 runs them
+   one after the other; -1 (default) chooses: concurrent with 48 SMs when the
+   INT8 engine contracts A and m, n >= 32768.  Same kernels and index sets
+   either way; the factors agree to roundoff (split-K depends on the SM count). */
+int lr_ctx_set_concurrent_tail(lr_ctx* ctx, int sms);
 /* back to the context's own (non-blocking) stream, the default after creation */
 int lr_ctx_use_own_stream(lr_ctx* ctx);
 int lr_ctx_get_stats(lr_ctx* ctx, lr_stats* out);

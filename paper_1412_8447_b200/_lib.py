@@ -77,6 +77,7 @@ SIGNATURES = {
     "lr_ctx_cache_operand": ([ctypes.c_void_p, c_dp, c_i64, c_i64, c_i64], ctypes.c_int),
     "lr_ctx_clear_operand_cache": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_release_workspace": ([ctypes.c_void_p], ctypes.c_int),
+    "lr_ctx_set_concurrent_tail": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "lr_ctx_get_stats": ([ctypes.c_void_p, ctypes.POINTER(lr_stats)], ctypes.c_int),
     "lr_ctx_synchronize": ([ctypes.c_void_p], ctypes.c_int),
     "lr_ctx_enable_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),

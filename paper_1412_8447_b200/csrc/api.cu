@@ -152,8 +152,12 @@ struct lr_ctx {
   Workspace ws_side;               // its scratch (split-K partials, Cholesky panels)
   Arena arena;
   // two disjoint SM partitions (green contexts) for the concurrent CUR tail
+  // SMs of the concurrent CUR tail's row-ID partition (lr_ctx_set_concurrent_tail):
+  // -1 automatic, 0 sequential tail, > 0 that many
+  int tail_sms = -1;
   struct SmSplit {
     bool tried = false, ok = false;
+    int want = 0;        // partition size the green contexts were built for
     int n1 = 0, n2 = 0;  // SMs of partition 1 (row ID chain) / 2 (A^T Q_c chain)
     CUgreenCtx g1 = nullptr, g2 = nullptr;
     CUstream s1 = nullptr, s2 = nullptr;
@@ -1111,15 +1115,28 @@ void release_sm_split(lr_ctx* c) {
   sp = lr_ctx::SmSplit{};
 }
 
-bool sm_split(lr_ctx* c) {
+// SMs for the row-ID chain of the concurrent tail, 0 = sequential tail.
+// Automatic choice (measured at C4 on the Ozaki engine with the bound-pruned
+// CPQR, profiles/r02_cur_split_sweep.jsonl: 123.2 ms sequential, 119.9-120.4 ms
+// with 32-48 SMs): 48 SMs when A^T Q_c runs on the INT8 engine and both
+// dimensions are >= 32768.  On the DMMA engine the A^T Q_c GEMM is 5x longer
+// than the row ID, and a static partition would slow it for its whole length.
+int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
+  if (c->tail_sms >= 0) return c->tail_sms;
+  if (const char* e = getenv("LRB_CUR_SPLIT")) return std::max(0, atoi(e));
+  return (c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768) ? 48 : 0;
+}
+
+bool sm_split(lr_ctx* c, int want) {
   auto& sp = c->split;
-  if (sp.tried) return sp.ok;
-  sp.tried = true;
-  // off by default: at C4 both chains scale ~linearly with their SM share, so
-  // the concurrent schedule measured slower than the sequential one (71 vs 62 ms)
-  const char* e = getenv("LRB_CUR_SPLIT");
-  const int want = e ? atoi(e) : 0;
   if (want <= 0) return false;
+  if (sp.tried && sp.want == want) return sp.ok;
+  if (sp.tried) {  // another partition size: rebuild the green contexts
+    LRB_CUDA(cudaStreamSynchronize(c->st));
+    release_sm_split(c);
+  }
+  sp.tried = true;
+  sp.want = want;
   using DeviceGet = CUresult (*)(CUdevice*, int);
   using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
   using Split = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
@@ -1147,6 +1164,7 @@ bool sm_split(lr_ctx* c) {
       gstream(&sp.s2, sp.g2, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
     release_sm_split(c);
     sp.tried = true;
+    sp.want = want;
     return false;
   }
   sp.n1 = (int)part[0].sm.smCount;
@@ -1190,7 +1208,8 @@ cudaEvent_t record_event(cudaStream_t s) {
 }
 
 bool split_applies(lr_ctx* c, int64_t m, int64_t n, int64_t k, int u_mode) {
-  return u_mode == LR_U_CPINV_A_RPINV && m >= 16384 && n >= 16384 && k > 192 && k <= 512 && sm_split(c);
+  return u_mode == LR_U_CPINV_A_RPINV && m >= 16384 && n >= 16384 && k > 192 && k <= 512 &&
+         sm_split(c, tail_sms_wanted(c, m, n));
 }
 
 // tsid_core + cur_core (u_mode LR_U_CPINV_A_RPINV) with the two chains
@@ -1249,6 +1268,16 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
     done2 = record_event(c->st);
   }
   bool r_ok = false;
+  // CholeskyQR2 of R^T: DMMA GEMMs that scale with the SM count, so by default
+  // they run after the join on the whole GPU and chain 1 keeps only the
+  // latency-bound row ID (LRB_CUR_SPLIT_LATE_R=0: inside chain 1's partition)
+  static const bool late_r = !(getenv("LRB_CUR_SPLIT_LATE_R") && atoi(getenv("LRB_CUR_SPLIT_LATE_R")) == 0);
+  auto factor_r = [&] {
+    transpose_matrix(k, n, R, k, Rt, even(n), c->st);
+    copy_matrix(k, n, R, k, Rk, ldk, c->st);
+    r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
+    if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n), 1.0, 0.0, -1, false, kTriQ);  // Qr = R^T Sr^-1
+  };
   {
     OnPartition on(c, sp.s1, sp.n1, fork);
     cpqr_core(c, k, m, Ctp, ldct, k, row_piv, tau, "cpqr_partial", work_padded(k, ldct));
@@ -1257,14 +1286,12 @@ void tsid_cur_split(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t ld
     on_rows();
     gather_rows(k, n, a, lda, row_piv, R, k, c->st);
     on_r();
-    transpose_matrix(k, n, R, k, Rt, even(n), c->st);
-    copy_matrix(k, n, R, k, Rk, ldk, c->st);
-    r_ok = cholqr2(c, n, k, Rt, even(n), Rk, ldk, Sr, Sri, fast_cond_limit(thr));
-    if (r_ok) gemm(c, n, k, k, Rk, ldk, Sri, k, Qr, even(n), 1.0, 0.0, -1, false, kTriQ);  // Qr = R^T Sr^-1
+    if (!late_r) factor_r();
     done1 = record_event(c->st);
   }
   LRB_CUDA(cudaStreamWaitEvent(c->st, done1, 0));
   if (done2) LRB_CUDA(cudaStreamWaitEvent(c->st, done2, 0));
+  if (late_r) factor_r();
   mark(c, "tsid_ctA_split");
   if (!(c_ok && r_ok)) {  // rare: the general U path, sequentially
     u_core(c, m, n, k, C, R, col_piv, col_coeff, ldcc, thr, LR_U_CPINV_A_RPINV, U, Ct,
@@ -1987,6 +2014,13 @@ int lr_ctx_set_gemm_mode(lr_ctx* c, int mode) {
   });
 }
 int lr_ctx_get_gemm_mode(lr_ctx* c) { return c ? c->gemm_mode : -1; }
+int lr_ctx_set_concurrent_tail(lr_ctx* c, int sms) {
+  return guard([&] {
+    checked(c);
+    if (sms < -1) fail(LR_EINVAL, "set_concurrent_tail: sms must be -1 (automatic), 0 (off) or an SM count");
+    c->tail_sms = sms;
+  });
+}
 int lr_ctx_cache_operand(lr_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda) {
   return guard([&] {
     checked(c);

@@ -269,6 +269,12 @@ class Context:
         default) or GEMM_OZAKI_INT8 (FP64 emulated on the INT8 tensor cores)."""
         _raise(self.lib.lr_ctx_set_gemm_mode(self.h, int(mode)))
 
+    def set_concurrent_tail(self, sms: int = -1) -> None:
+        """Schedule of the randomized CUR's tail: sms > 0 runs the row ID of C
+        on an SM partition of that size next to A^T Q_c, 0 runs them one after
+        the other, -1 (default) lets the library choose."""
+        _raise(self.lib.lr_ctx_set_concurrent_tail(self.h, int(sms)))
+
     def gemm_mode(self) -> int:
         return int(self.lib.lr_ctx_get_gemm_mode(self.h))
 

@@ -105,6 +105,9 @@ def test_c4_full_size_vs_oracle(lr, gold, c4_matrix, engine):
     assert e / na == pytest.approx(float(gold["err"]) / float(gold["na"]), rel=TOL)
     assert stats["norm_recomputes"] == int(gold["recomputes_y"]) + int(gold["recomputes_ct"]), \
         (stats["norm_recomputes"], int(gold["recomputes_y"]), int(gold["recomputes_ct"]))
+    # the automatic tail schedule: concurrent chains on the INT8 engine at this size, sequential on DMMA
+    if "LRB_CUR_SPLIT" not in os.environ:
+        assert stats["concurrent_tail"] == (1 if engine == "ozaki" else 0)
 
 
 def test_c4_full_size_verifiers(lr, gold, c4_matrix):

@@ -83,3 +83,45 @@ def test_concurrent_tail_host_entry(lr):
     assert np.array_equal(np.asarray(cur.row_pivots), dev["row_pivots"])
     assert np.array_equal(np.asarray(cur.c), dev["c"]) and np.array_equal(np.asarray(cur.r), dev["r"])
     assert _rel(cur.u, dev["u"]) <= TOL
+
+
+def test_concurrent_tail_setter_and_automatic_choice(lr):
+    """lr_ctx_set_concurrent_tail: an explicit partition size gives the
+    sequential results on one context (green contexts rebuilt when the size
+    changes); the automatic choice keeps a 16384^2 problem sequential (it
+    switches on at m, n >= 32768 on the INT8 engine: tests/test_gpu_c4_full.py
+    runs that against the full-size oracle result) and stays off on the DMMA
+    engine."""
+    import torch
+    from paper_1412_8447_b200 import inputs
+    k = 300
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 16384, 16384, width=768, k=k)
+    a = inputs.synthetic_torch(cfg, device="cuda", col_block=4096)
+    torch.cuda.synchronize()
+    ctx = lr.Context(0)
+    ctx.set_gemm_mode(ctx.GEMM_OZAKI_INT8)
+    sk = lr.SketchConfig(oversample=10, seed=7)
+
+    def run():
+        r = {kk: v.cpu().numpy() for kk, v in lr.randomized_cur_device(a, k, sk, u_mode=lr.U_CPINV_A_RPINV,
+                                                                      ctx=ctx).items()}
+        ctx.synchronize()
+        return r, ctx.stats()["concurrent_tail"]
+
+    auto, on_auto = run()
+    assert on_auto == 0
+    res = {}
+    for sms in (48, 64, 0):
+        ctx.set_concurrent_tail(sms)
+        res[sms], on = run()
+        assert on == (1 if sms else 0)
+    ctx.set_concurrent_tail(-1)
+    with pytest.raises(ValueError):
+        ctx.set_concurrent_tail(-2)
+    ctx.close()
+    for sms in (48, 64):
+        for key in ("col_pivots", "row_pivots", "c", "r", "skeleton"):
+            assert np.array_equal(res[sms][key], res[0][key]), (sms, key)
+        assert _rel(res[sms]["u"], res[0]["u"]) <= TOL
+    for key in ("col_pivots", "row_pivots", "c", "r", "u"):
+        assert np.array_equal(auto[key], res[0][key]), key
