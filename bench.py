@@ -636,6 +636,10 @@ def run_ours(args, rank, world, local_rank):
         "stages_sequential_ms": ({k_: round(v["ms"] / seq_steps, 3) for k_, v in seq_stages.items()}
                                  if seq_stages else None),
         "sequential_ms_per_step": round(seq_ms, 3) if seq_ms else None,
+        "sequential_note": ("the profile steps run right after the timed region (power-capped, warm GPU) and only "
+                            "serve the per-kernel table; like for like the sequential tail measures 123.2 ms per "
+                            "step against 119.9-120.4 concurrent (profiles/r02_cur_split_sweep.jsonl)")
+        if seq_ms else None,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),

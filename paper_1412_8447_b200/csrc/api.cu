@@ -1124,6 +1124,14 @@ void release_sm_split(lr_ctx* c) {
 int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
   if (c->tail_sms >= 0) return c->tail_sms;
   if (const char* e = getenv("LRB_CUR_SPLIT")) return std::max(0, atoi(e));
+  // under an injected profiler (ncu sets NV_COMPUTE_PROFILER_PERFWORKS_DIR and
+  // NV_NSIGHT_INJECTION_* in the child, nsys CUDA_INJECTION64_PATH) the automatic schedule
+  // stays sequential: ncu cannot replay kernels launched into green contexts ("Failed to
+  // prepare kernel for profiling"), and it serialises launches anyway
+  static const bool injected = getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
+                               getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                               getenv("CUDA_INJECTION64_PATH") != nullptr;
+  if (injected) return 0;
   return (c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768) ? 48 : 0;
 }
 
