@@ -11,6 +11,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <optional>
 #include <vector>
 
 #include <cuda.h>
@@ -279,8 +280,8 @@ constexpr int64_t kOzakiMaxK = int64_t(1) << 17;
 // operands (A of the current CUR call) are split once and reused while an
 // OzakiScope is open; `tmp_slot` 0/1 picks the slots of the other operand.
 const OzakiOperand* ozaki_operand(lr_ctx* c, int64_t K, int64_t cols, const double* X, int64_t ldx, bool cacheable,
-                                  int tmp_slot, OzakiOperand& out) {
-  const int beta = ozaki_beta(K);
+                                  int tmp_slot, OzakiOperand& out, int beta_override = 0) {
+  const int beta = beta_override > 0 ? beta_override : ozaki_beta(K);
   if (cacheable) {  // the input matrix: kOzA slot, reused while an OzakiScope is open
     if (c->oz_cache_on && c->oz_src == X && c->oz_K == K && c->oz_cols == cols && c->oz_ld == ldx)
       return &c->oz_op;
@@ -855,12 +856,39 @@ int64_t orth_cols_core(lr_ctx* c, int64_t rows, int64_t k, const double* X, int6
 // Z^T = A Y^T (A^T materialised once so both products are K-contiguous),
 // Y = Z A (the input matrix's contraction: Ozaki or DMMA per the context).
 // Returns the new sample in Yb (ld work_ld(rows), zero padded); *rows updated.
+//
+// On the INT8 engine with A's residue planes cached (the sketch split them), Z^T = A Y^T contracts
+// over A's columns, the index A's planes are scaled along: with x_ij = rint(a_ij 2^s_j) the
+// integers behind the planes, A Y^T = X (diag(2^-s) Y^T) exactly, so the column scales are folded
+// into Y^T's rows, that product's right operand is split along its own columns as usual, and A's
+// planes enter the tcgen05 GEMM as the M-major operand (ozaki_gemm_a_cols).  No A^T is formed
+// (34 GB at C4) and the round's 2 l m n flops leave the DMMA pipe.  The rounding differs from the
+// TN products': A is rounded to beta bits relative to its COLUMN maxima (a columnwise backward
+// error of 2^-beta), Y^T's scaled rows relative to their column maxima.
+bool power_zt_int8(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int64_t rows, const double* Ym,
+                   int64_t ldym, double* Zt, int64_t ldz) {
+  static const bool off = getenv("LRB_POWER_INT8") && atoi(getenv("LRB_POWER_INT8")) == 0;
+  if (off || c->gemm_mode != LR_GEMM_OZAKI_INT8 || !c->oz_cache_on || c->oz_src != a || c->oz_K != m ||
+      c->oz_cols != n || c->oz_ld != lda || n > kOzakiMaxK || (c->oz_op.unsigned_res && n > kOzakiMaxKUnsigned))
+    return false;
+  const int bq = ozaki_partner_beta(n, c->oz_op.beta);
+  if (bq < 40) return false;  // too few bits left for the partner (n much larger than m)
+  DBuf<double> Ys((size_t)even(n) * rows, c->st);
+  ozaki_fold_scales(n, rows, Ym, ldym, c->oz_op.shift, Ys, even(n), c->st);
+  OzakiOperand oq;
+  const OzakiOperand* Qo = ozaki_operand(c, n, rows, Ys, even(n), false, 1, oq, bq);
+  if (!Qo) return false;
+  DBuf<int> zero((size_t)m, c->st);
+  LRB_CUDA(cudaMemsetAsync(zero.p, 0, sizeof(int) * (size_t)m, c->st));
+  mark(c, "ozaki_split");
+  ozaki_gemm_a_cols(c->ws, c->oz_op, *Qo, rows, Zt, ldz, zero, c->st);
+  return true;
+}
+
 void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t lda, int q, bool reorth,
                        DBuf<double>& Yb, int64_t& ldy, int64_t& rows) {
   const int64_t ldat = even(n);
-  DBuf<double> At((size_t)ldat * m, c->st);
-  transpose_matrix(m, n, a, lda, At, ldat, c->st);  // A^T: n x m
-  mark(c, "power_transpose_a");
+  DBuf<double> At;  // A^T (n x m), formed only when a round takes the DMMA path
   for (int round = 0; round < q; ++round) {
     DBuf<double> Yt((size_t)ldat * rows, c->st), Qy;
     transpose_matrix(rows, n, Yb, ldy, Yt, ldat, c->st);  // Y^T: n x rows
@@ -873,7 +901,14 @@ void power_rounds_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t
     if (rows < 1) fail(LR_ERUNTIME, "randomized_id: sample rank collapsed below target rank");
     mark(c, "power_orth");
     DBuf<double> Zt((size_t)even(m) * rows, c->st), Qz;
-    gemm(c, m, rows, n, At, ldat, Ym, ldat, Zt, even(m));  // Z^T = A Y^T (m x rows)
+    if (!power_zt_int8(c, m, n, a, lda, rows, Ym, ldat, Zt, even(m))) {
+      if (!At.p) {
+        At = DBuf<double>((size_t)ldat * m, c->st);
+        transpose_matrix(m, n, a, lda, At, ldat, c->st);
+        mark(c, "power_transpose_a");
+      }
+      gemm(c, m, rows, n, At, ldat, Ym, ldat, Zt, even(m));  // Z^T = A Y^T (m x rows)
+    }
     mark(c, "power_zt_gemm");
     const double* Zm = Zt;
     if (reorth) {
@@ -914,6 +949,10 @@ void randomized_id_core(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_
                         int64_t ldc, double* Ypre = nullptr) {
   int64_t ell = check_randomized_id(m, n, k, cfg);
   int64_t ldy = work_ld(ell);
+  // power rounds contract A 1 + 2q times: keep its residue planes for the whole call
+  // (a CUR caller has its own scope open already)
+  std::optional<OzakiScope> planes_scope;
+  if (cfg.power > 0 && !c->oz_cache_on) planes_scope.emplace(c);
   DBuf<double> Yb;
   double* Y = Ypre;
   if (!Y) {

@@ -196,6 +196,15 @@ OzakiOperand ozaki_cols(const OzakiOperand& op, int64_t off, int64_t cols);
 void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, int64_t M, int64_t N, double* out,
                    int64_t ldo, double alpha, double beta, cudaStream_t st);
 
+// out (A.K x N) = A_int Q: the contraction over the COLUMNS of the split operand A (its planes are the
+// M-major operand); A's column scales folded into Q's rows beforehand (ozaki_fold_scales), Q split
+// with ozaki_partner_beta(A.cols, A.beta) bits; zero_shift: A.K zero ints
+void ozaki_gemm_a_cols(Workspace& ws, const OzakiOperand& A, const OzakiOperand& Q, int64_t N, double* out,
+                       int64_t ldo, const int* zero_shift, cudaStream_t st);
+void ozaki_fold_scales(int64_t K, int64_t cols, const double* X, int64_t ldx, const int* shift, double* out,
+                       int64_t ldo, cudaStream_t st);
+int ozaki_partner_beta(int64_t K, int beta_a);
+
 // ---------------------------------------------------------------- sparse (config 5)
 // CSR (m x n, int64 indices) -> CSC with rows ascending within each column
 void csr_to_csc(int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr, const int64_t* col_idx, const double* val,

@@ -320,6 +320,14 @@ __device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t saddr) {
+  // MN-major, SWIZZLE_128B (canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units): 128 bytes
+  // (= 128 int8 rows of the tile) contiguous along M, K rows at a 128-byte pitch, 8-row groups
+  // SBO = 1024 B apart; one 128-byte group along M (n = 1), so LBO (the tile size) is never used
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(8192 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
   asm volatile(
@@ -354,7 +362,8 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 template <int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(ITHREADS, 1)
     imma_gemm_kernel(const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmq, int M, int N,
-                     int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride, uint32_t ab_fmt) {
+                     int K, int8_t* __restrict__ out, int64_t ldo, int64_t out_plane_stride, uint32_t ab_fmt,
+                     int p_mn) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ISTAGES * ISTAGE_BYTES);
@@ -397,7 +406,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(ITHREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);  // stage s free in all four CTAs
         uint8_t* sp = smem + s * ISTAGE_BYTES;
         mbar_arrive_expect_tx(&full[s], ISTAGE_BYTES);
-        tma_load_3d(sp, &tmp, &full[s], i * IBK, m0, plane);
+        // P stage: K-major planes [K][M] (box 64 K-bytes x 128 rows, 64B swizzle) or, p_mn, the
+        // planes of the transposed operand [M][K] (box 128 M-bytes x 64 K rows, 128B swizzle)
+        if (p_mn) tma_load_3d(sp, &tmp, &full[s], m0, i * IBK, plane);
+        else tma_load_3d(sp, &tmp, &full[s], i * IBK, m0, plane);
         // this CTA's 512 / CL columns of the Q stage, in TMA boxes of at most 256 columns
         constexpr int kBox = IBN / CL < 256 ? IBN / CL : 256;
 #pragma unroll
@@ -409,7 +421,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(ITHREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // kind::i8: D s32; A/B u8 (0) or s8 (1) per operand (ab_fmt bits 7, 10)
-      const uint32_t idesc = (2u << 4) | ab_fmt | ((uint32_t)(256 >> 3) << 17) |
+      // bit 15: A (our P) is MN-major in shared memory
+      const uint32_t idesc = (2u << 4) | ab_fmt | (p_mn ? (1u << 15) : 0u) | ((uint32_t)(256 >> 3) << 17) |
                              ((uint32_t)(IBM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ISTAGES;
@@ -420,7 +433,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(ITHREADS, 1)
         const uint32_t sb = sa + IA_BYTES;
 #pragma unroll
         for (int kk = 0; kk < IBK / 32; ++kk) {
-          const uint64_t da = smem_desc_sw64(sa + kk * 32);
+          // 32 K entries further: 32 bytes along a K-major row, 32 rows of 128 bytes MN-major
+          const uint64_t da = p_mn ? smem_desc_sw128_mn(sa + kk * 32 * IBM) : smem_desc_sw64(sa + kk * 32);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint64_t db = smem_desc_sw64(sb + h * 256 * IBK + kk * 32);
@@ -608,6 +622,31 @@ CUtensorMap make_tmap_i8_planes(const int8_t* base, int64_t K, int64_t cols, int
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8 planes) failed: " + std::to_string((int)r));
+  return map;
+}
+
+// The planes of an operand split along its columns ([plane][col][K], K contiguous), read as the
+// M-major operand of a product that contracts over its COLUMNS: box = 128 K-bytes (the product's M
+// rows) x IBK columns (the product's K), 128B swizzle.
+CUtensorMap make_tmap_i8_planes_mn(const int8_t* base, int64_t K, int64_t cols, int64_t ld, int64_t plane_stride) {
+  using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    LRB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)cols, (cuuint64_t)kOzakiModuli};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)plane_stride};
+  cuuint32_t box[3] = {(cuuint32_t)IBM, (cuuint32_t)IBK, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8 planes, M-major) failed: " + std::to_string((int)r));
   return map;
 }
 
@@ -833,11 +872,78 @@ void ozaki_gemm_tn(Workspace& ws, const OzakiOperand& P, const OzakiOperand& Q, 
     throw CudaError("ozaki_gemm_tn: K too large for an unsigned-residue operand");
   const uint32_t ab_fmt = (P.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
   auto kern = cl == 4 ? imma_gemm_kernel<4> : (cl == 2 ? imma_gemm_kernel<2> : imma_gemm_kernel<1>);
-  kern<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, ldr * N, ab_fmt);
+  kern<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)P.K, res, ldr, ldr * N, ab_fmt, 0);
   LRB_CHECK_LAUNCH();
   const int64_t items = (M + 3) / 4 * N;
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 8 * num_sms()));
   crt4_kernel<<<gx, 256, 0, st>>>(M, N, res, ldr, ldr * N, P.shift, Q.shift, out, ldo, alpha, beta);
+  LRB_CHECK_LAUNCH();
+}
+
+namespace {
+// out(j, r) = X(j, r) 2^-shift[j]: the column scales of the split operand folded into its partner
+__global__ void scale_rows_pow2_kernel(int64_t K, int64_t cols, const double* __restrict__ X, int64_t ldx,
+                                       const int* __restrict__ shift, double* __restrict__ out, int64_t ldo) {
+  for (int64_t r = blockIdx.y; r < cols; r += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
+      const int sft = shift[j];
+      out[j + r * ldo] = sft == kOzakiNonFinite ? CUDART_NAN : ldexp(X[j + r * ldx], -sft);
+    }
+}
+}  // namespace
+
+void ozaki_fold_scales(int64_t K, int64_t cols, const double* X, int64_t ldx, const int* shift, double* out,
+                       int64_t ldo, cudaStream_t st) {
+  if (K <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)std::min<int64_t>((K + 255) / 256, 1024), (unsigned)std::min<int64_t>(cols, 65535));
+  scale_rows_pow2_kernel<<<grid, 256, 0, st>>>(K, cols, X, ldx, shift, out, ldo);
+  LRB_CHECK_LAUNCH();
+}
+
+namespace {
+// bits the two operands of a length-K contraction may share: K 2^(ba + bq) < M_crt / 2
+int ozaki_room(int64_t K) {
+  return (int)std::floor(crt_host().log2M - 1.0 - std::log2((double)std::max<int64_t>(K, 1)));
+}
+}  // namespace
+
+int ozaki_partner_beta(int64_t K, int beta_a) { return std::min(ozaki_room(K) - beta_a, 60); }
+
+// out (A.K x N) = A_int Q with A_int the integer matrix behind A's planes (A.K x A.cols, entry (i, j) =
+// rint(a_ij 2^shift_j)) and Q (A.cols x N) split along ITS columns: the contraction runs over A's
+// columns, so A's planes are the M-major operand of the INT8 GEMM.  A's column scales are not
+// applied here (the caller folded 2^-shift_j into Q's rows: ozaki_fold_scales); zero_shift: A.K zeros.
+void ozaki_gemm_a_cols(Workspace& ws, const OzakiOperand& A, const OzakiOperand& Q, int64_t N, double* out,
+                       int64_t ldo, const int* zero_shift, cudaStream_t st) {
+  upload_constants();
+  const int64_t M = A.K, K = A.cols;
+  if (Q.K != K || N > Q.cols) throw CudaError("ozaki_gemm_a_cols: operand shape mismatch");
+  if (K > (int64_t(1) << 17)) throw CudaError("ozaki_gemm_a_cols: K > 2^17 would overflow the int32 accumulators");
+  if (A.unsigned_res && Q.unsigned_res) throw CudaError("ozaki_gemm_a_cols: at most one unsigned-residue operand");
+  if ((A.unsigned_res || Q.unsigned_res) && K > kOzakiMaxKUnsigned)
+    throw CudaError("ozaki_gemm_a_cols: K too large for an unsigned-residue operand");
+  if (A.beta + Q.beta > ozaki_room(K)) throw CudaError("ozaki_gemm_a_cols: operand bits exceed the CRT range");
+  static bool attr = false;
+  if (!attr) {
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    LRB_CUDA(cudaFuncSetAttribute(imma_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM));
+    attr = true;
+  }
+  const int tiles_m = (int)((M + IBM - 1) / IBM), tiles_n = (int)((N + IBN - 1) / IBN);
+  const int cl = tiles_m % 4 == 0 ? 4 : (tiles_m % 2 == 0 ? 2 : (tiles_m == 1 ? 1 : 4));
+  const CUtensorMap tp = make_tmap_i8_planes_mn(A.planes, A.K, A.cols, A.ld, A.plane_stride);
+  const CUtensorMap tq = make_tmap_i8_planes(Q.planes, Q.K, Q.cols, Q.ld, Q.plane_stride, std::min(256, IBN / cl));
+  const int64_t ldr = (M + 15) / 16 * 16;
+  int8_t* res = static_cast<int8_t*>(ws.get(WsSlot::kTmp7, (size_t)ldr * N * kOzakiModuli));
+  dim3 grid((tiles_m + cl - 1) / cl * cl, tiles_n, kOzakiModuli);
+  const uint32_t ab_fmt = (A.unsigned_res ? 0u : (1u << 7)) | (Q.unsigned_res ? 0u : (1u << 10));
+  auto kern = cl == 4 ? imma_gemm_kernel<4> : (cl == 2 ? imma_gemm_kernel<2> : imma_gemm_kernel<1>);
+  kern<<<grid, ITHREADS, ISMEM, st>>>(tp, tq, (int)M, (int)N, (int)K, res, ldr, ldr * N, ab_fmt, 1);
+  LRB_CHECK_LAUNCH();
+  const int64_t items = (M + 3) / 4 * N;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 8 * num_sms()));
+  crt4_kernel<<<gx, 256, 0, st>>>(M, N, res, ldr, ldr * N, zero_shift, Q.shift, out, ldo, 1.0, 0.0);
   LRB_CHECK_LAUNCH();
 }
 

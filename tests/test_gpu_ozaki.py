@@ -289,3 +289,63 @@ def test_ozaki_falls_back_to_dmma_when_planes_do_not_fit(lr, oracle):
         torch.cuda.empty_cache()
     assert np.array_equal(cur.col_pivots, ref.col_pivots) and np.array_equal(cur.row_pivots, ref.row_pivots)
     assert rel(cur.u, ref.u) <= TOL
+
+
+# ------------------------------------------------------------------ power rounds on the INT8 engine
+# Z^T = A Y^T contracts over A's columns: A's cached residue planes enter the tcgen05 GEMM as the
+# M-major operand with their column scales folded into Y^T (api.cu power_zt_int8, SURVEY 8f.1 /
+# sketch.hpp:148-164).
+def _stages(ctx, fn):
+    ctx.reset_stats()
+    ctx.enable_timing(True)
+    try:
+        res = fn()
+        ctx.synchronize()
+        return res, ctx.stage_report()
+    finally:
+        ctx.enable_timing(False)
+
+
+@pytest.mark.parametrize("m,n,width,k,q", [(1500, 1200, 400, 60, 1), (1200, 2500, 400, 60, 1),
+                                           (2600, 1100, 300, 50, 2), (1024, 4096, 512, 100, 1),
+                                           (4099, 3001, 600, 120, 1)])
+def test_power_rounds_on_int8_match_oracle(lr, oracle, ozaki, m, n, width, k, q):
+    """Identical pivots and T within 1e-10 of the oracle; the stage marks show
+    that no A^T was formed (the rounds ran on A's residue planes)."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], m, n, width=width, k=k)
+    a = inputs.synthetic_np(cfg)
+    sk = lr.SketchConfig(oversample=10, seed=5, power=q)
+    cid, st = _stages(ozaki, lambda: lr.randomized_id(a, k, sk, ctx=ozaki))
+    assert "power_zt_gemm" in st and "power_transpose_a" not in st, sorted(st)
+    piv, coeff = oracle.randomized_id_power(a, k, 10, q, True, 5)
+    assert np.array_equal(cid.pivots, piv)
+    assert rel(cid.coeff, coeff) <= TOL
+
+
+def test_power_round_int8_with_wild_column_scales(lr, ozaki):
+    """Columns of A spanning 60 orders of magnitude (the scales folded into
+    Y^T span the same range): the INT8 round against the FP64 DMMA round."""
+    rng = np.random.default_rng(3)
+    m, n, k = 1800, 1500, 40
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], m, n, width=300, k=k)
+    a = inputs.synthetic_np(cfg) * (10.0 ** rng.integers(-30, 31, size=n))[None, :]
+    a = np.asfortranarray(a)
+    sk = lr.SketchConfig(oversample=10, seed=9, power=1)
+    got, st = _stages(ozaki, lambda: lr.randomized_id(a, k, sk, ctx=ozaki))
+    assert "power_transpose_a" not in st
+    ozaki.set_gemm_mode(ozaki.GEMM_DMMA)
+    ref = lr.randomized_id(a, k, sk, ctx=ozaki)
+    assert np.array_equal(got.pivots, ref.pivots)
+    assert rel(got.coeff, ref.coeff) <= 1e-9
+
+
+def test_power_round_int8_randomized_cur_reuses_planes(lr, oracle, ozaki):
+    """randomized_cur with q = 1: sketch, both halves of the round and
+    A^T Q_c all run on one split of A."""
+    cfg = inputs.scaled(inputs.CONFIGS["c4"], 2000, 1600, width=512, k=80)
+    a = inputs.synthetic_np(cfg)
+    piv, _ = oracle.randomized_id_power(a, 80, 10, 1, True, 2)
+    cur, st = _stages(ozaki, lambda: lr.randomized_cur(a, 80, lr.SketchConfig(oversample=10, seed=2, power=1),
+                                                       u_mode=lr.U_CPINV_A_RPINV, ctx=ozaki))
+    assert "power_transpose_a" not in st
+    assert np.array_equal(cur.col_pivots, piv)
