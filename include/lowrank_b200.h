@@ -121,7 +121,7 @@ int lr_ctx_get_gemm_mode(lr_ctx* ctx);
    id.hpp:101-128) and Q_c -> A^T Q_c (lowrank_main.cpp:210-215).  sms > 0 runs
    them concurrently, the row ID on an SM partition of that size; 0 runs them
    one after the other; -1 (default) chooses: concurrent with 48 SMs when the
-   INT8 engine contracts A and m, n >= 32768.  Same kernels and index sets
+   INT8 engine contracts A, m, n >= 32768 and m n >= 2^31 (measured break-even).  Same kernels and index sets
    either way; the factors agree to roundoff (split-K depends on the SM count). */
 int lr_ctx_set_concurrent_tail(lr_ctx* ctx, int sms);
 /* back to the context's own (non-blocking) stream, the default after creation */

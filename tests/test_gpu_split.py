@@ -89,7 +89,7 @@ def test_concurrent_tail_setter_and_automatic_choice(lr):
     """lr_ctx_set_concurrent_tail: an explicit partition size gives the
     sequential results on one context (green contexts rebuilt when the size
     changes); the automatic choice keeps a 16384^2 problem sequential (it
-    switches on at m, n >= 32768 on the INT8 engine: tests/test_gpu_c4_full.py
+    switches on at m, n >= 32768 with m n >= 2^31 on the INT8 engine: tests/test_gpu_c4_full.py
     runs that against the full-size oracle result) and stays off on the DMMA
     engine."""
     import torch
