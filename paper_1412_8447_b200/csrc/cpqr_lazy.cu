@@ -59,6 +59,9 @@ __device__ __forceinline__ void lazy_tag_wait(const unsigned int* tag, unsigned 
 // update.  The pivot sequence is the one of evaluating every column every step.
 
 
+constexpr double kLazyGapInit = 0.1, kLazyGapMin = 0.02, kLazyGapMax = 0.5;
+constexpr double kLazyGapHit = 0.98, kLazyGapMiss = 1.9;  // 0.98^32 ~ 1 / 1.9: one retry per ~30 steps
+
 // Reflector of column b for step s1 from A_p - V F^T (c_used panel reflectors
 // applied) into the candidate buffer cd, plus w = V^T v when the next step
 // continues this panel (the eager kernel's `stage`, as a function).
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
   __shared__ double sM[NBL * NBL];  // F = M D' for the catch-ups (lower triangular, row c set at step c)
   __shared__ double fb[NB];
   __shared__ double sh_alpha;
-  __shared__ double sh_ratio[8];  // recent M_s / M_{s-1} (adaptive threshold)
+  __shared__ double sh_gap;  // 1 - beta of the adaptive threshold (carried across launches in lstats[2])
   __shared__ int sh_cnt[2 * PT];
   __shared__ int sh_nact, sh_nzero, sh_ecnt;
   __shared__ unsigned long long sh_zkey;
@@ -367,7 +370,10 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
   for (int64_t i = threadIdx.x; i < (NB + 2) * ld; i += PT) dyn[i] = 0.0;
   for (int i = threadIdx.x; i < NB * NB; i += PT) swall[i] = 0.0;
   for (int i = threadIdx.x; i < NBL * NBL; i += PT) sM[i] = 0.0;
-  if (threadIdx.x < 8) sh_ratio[threadIdx.x] = 0.9;
+  if (threadIdx.x == 0) {
+    const double g = __longlong_as_double((long long)__ldcg(a.lstats + 2));
+    sh_gap = (g >= kLazyGapMin && g <= kLazyGapMax) ? g : kLazyGapInit;  // zeroed at the start of a CPQR
+  }
   unsigned int ep = __ldcg(a.epoch);
   unsigned long long my_recomputes = 0, my_evals = 0, my_retries = 0;
   __syncthreads();
@@ -568,10 +574,11 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
       tprev = t;
     }
   };
-  double Lprev = -INFINITY, Mprev = -1.0;
+  double Lprev = -INFINITY;
   bool check = false;
   for (int64_t s = a.t0; s < a.t1; ++s) {
     const int c = (int)(s - a.t0);
+    bool retried = false;
     for (;;) {
       // (1) global argmax over the per-CTA partials of round ep
       if (warp == 0) {
@@ -623,6 +630,7 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
       lazy_grid_wait(a.bar, bar_target, s);
       ++ep;
       ++my_retries;
+      retried = true;
       Lprev = thr;
     }
     const int64_t p = sh_piv[0] >> 32;
@@ -632,16 +640,14 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
 
     const bool owner = (sp >= c0 && sp < c1);
     const bool last = c == C - 1;  // last step of the panel: relabel only (panel_finalize_kernel applies it)
-    // (2) threshold for the next pass: the step-(s+1) maximum is at least beta M_s
-    // with high probability (beta from the recent ratios; a miss costs one retry round)
+    // (2) threshold for the next pass, L = beta M_s.  A miss (the next maximum below L) costs a
+    // retry round over everything skipped, a low beta costs extra columns every step, and where
+    // the balance lies depends on the spectrum (C4: beta ~ 0.9, a Gaussian matrix: ~ 0.97).  beta
+    // follows the retries: the gap 1 - beta shrinks 2% after a step without one and grows by
+    // kLazyGapMiss after one, which settles near one retry in ~30 steps.
     if (threadIdx.x == 0) {
-      if (Mprev > 0.0 && Ms > 0.0) {
-        for (int i = 7; i > 0; --i) sh_ratio[i] = sh_ratio[i - 1];
-        sh_ratio[0] = Ms / Mprev;
-      }
-      double rmin = sh_ratio[0];
-      for (int i = 1; i < 8; ++i) rmin = fmin(rmin, sh_ratio[i]);
-      const double beta = a.beta > 0.0 ? a.beta : fmin(0.98, fmax(0.5, 0.95 * rmin));
+      if (check) sh_gap = fmin(kLazyGapMax, fmax(kLazyGapMin, retried ? sh_gap * (a.gap_miss > 1.0 ? a.gap_miss : kLazyGapMiss) : sh_gap * kLazyGapHit));
+      const double beta = a.beta > 0.0 ? a.beta : 1.0 - sh_gap;
       sh_thr = last ? INFINITY : beta * Ms;
       sh_ecnt = 0;
       if (owner) {  // the pivot's slot leaves the active set (the reference's swap is a relabelling)
@@ -726,7 +732,6 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
         for (int64_t i = threadIdx.x; i < ld; i += PT) a.Vg[i * NB + c] = Vs[c * ld + i];
       __syncthreads();
     }
-    Mprev = Ms;
   }
   for (int64_t j = c0 + threadIdx.x; j < c1; j += PT) {
     a.nrm[j] = snr[j - c0];
@@ -734,7 +739,10 @@ __global__ void __launch_bounds__(PT, 1) cpqr_lazy_kernel(PanelArgs a) {
     a.posof[j] = spos[j - c0];
     a.cjg[j] = scj[j - c0];
   }
-  if (cta == 0 && threadIdx.x == 0) *a.epoch = ep + 1u;  // every CTA read the old value before the first barrier
+  if (cta == 0 && threadIdx.x == 0) {  // every CTA read the old values before the first barrier
+    *a.epoch = ep + 1u;
+    a.lstats[2] = (unsigned long long)__double_as_longlong(sh_gap);
+  }
   if (tr) {
     a.trace[cta * 8 + 6] += clock64() - ck0;
     a.trace[cta * 8 + 7] += gtimer() - tk0;

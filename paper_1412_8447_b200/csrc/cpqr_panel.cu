@@ -896,6 +896,8 @@ void cpqr_panel(Workspace& ws, int64_t m, int64_t n, double* W, int64_t ld, int6
     a.epoch = reinterpret_cast<unsigned int*>(a.lstats + 3);
     a.cjg = reinterpret_cast<int*>(a.lstats + 4);
     a.beta = lazy_beta;
+    static const double gap_miss = getenv("LRB_CPQR_GAPMISS") ? atof(getenv("LRB_CPQR_GAPMISS")) : 0.0;  // diagnostic
+    a.gap_miss = gap_miss;
     if (lazy) LRB_CUDA(cudaMemsetAsync(a.lstats, 0, 4 * sizeof(unsigned long long), st));
   }
   LRB_CUDA(cudaMemsetAsync(a.nzero, 0, sizeof(int), st));

@@ -54,7 +54,8 @@ struct PanelArgs {
   unsigned int* epoch;        // rounds published so far (candidate tags / buffer parity across launches)
   double beta;                // > 0: fixed threshold factor; <= 0: adaptive
   int entry;                  // eager kernel after lazy panels: stage the step-t0 candidate first
-  unsigned long long* lstats; // [0] retry rounds, [1] columns evaluated by the step passes
+  double gap_miss;            // growth of 1 - beta after a retry round (0: default)
+  unsigned long long* lstats; // [0] retry rounds, [1] columns evaluated by the step passes, [2] 1 - beta (double bits)
 };
 
 // Grid barrier for the co-resident (cooperative) grid: one release atomic per
