@@ -1157,7 +1157,8 @@ void release_sm_split(lr_ctx* c) {
 // SMs for the row-ID chain of the concurrent tail, 0 = sequential tail.
 // Automatic choice (measured at C4 on the Ozaki engine with the bound-pruned
 // CPQR, profiles/r02_cur_split_sweep.jsonl: 123.2 ms sequential, 119.9-120.4 ms
-// with 32-48 SMs): 48 SMs when A^T Q_c runs on the INT8 engine, both
+// with 32-48 SMs; with the retry-driven CPQR threshold 40 SMs lead 48 by ~1 ms,
+// profiles/r02_cur_split_p_sweep.log): 40 SMs when A^T Q_c runs on the INT8 engine, both
 // dimensions are >= 32768 and A has at least 2^31 entries.  On the DMMA engine the A^T Q_c GEMM is 5x longer
 // than the row ID, and a static partition would slow it for its whole length.
 int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
@@ -1173,7 +1174,7 @@ int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
   if (injected) return 0;
   // other shapes (profiles/r02_cur_split_shapes.jsonl): 32768 x 65536 74.7 -> 70.6 ms, 65536 x 32768
   // 74.3 -> 72.9, 49152^2 (k = 300) 62.3 -> 61.4, but 32768^2 46.8 -> 47.3: on from 2^31 entries
-  return (c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768 && m * n >= (int64_t(1) << 31)) ? 48 : 0;
+  return (c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768 && m * n >= (int64_t(1) << 31)) ? 40 : 0;
 }
 
 bool sm_split(lr_ctx* c, int want) {
