@@ -1174,7 +1174,11 @@ int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
   if (injected) return 0;
   // other shapes (profiles/r02_cur_split_shapes.jsonl): 32768 x 65536 74.7 -> 70.6 ms, 65536 x 32768
   // 74.3 -> 72.9, 49152^2 (k = 300) 62.3 -> 61.4, but 32768^2 46.8 -> 47.3: on from 2^31 entries
-  return (c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768 && m * n >= (int64_t(1) << 31)) ? 40 : 0;
+  // the row ID works on m columns whatever n is, the GEMM chain scales with m n: a tall A
+  // (65536 x 32768: 72.9 ms sequential, P = 40: 74.8, 48: 71.6, 56: 69.3, 64: 69.2, 72: 71.6)
+  // wants the larger row-ID partition
+  if (!(c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768 && m * n >= (int64_t(1) << 31))) return 0;
+  return (m > n && n < 49152) ? 56 : 40;
 }
 
 bool sm_split(lr_ctx* c, int want) {
