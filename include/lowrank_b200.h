@@ -102,7 +102,10 @@ int lr_ctx_set_stream(lr_ctx* ctx, void* cuda_stream);
    LR_GEMM_DMMA (default): FP64 tensor-core GEMM (DMMA), FP64 rounding per FMA;
    LR_GEMM_OZAKI_INT8: FP64 emulated on the INT8 tensor cores (Ozaki scheme II,
    16 moduli): exact integer products of the inputs truncated to 54+ bits
-   relative to each column's largest entry (K <= 2^17; larger K uses DMMA) */
+   relative to each column's largest entry (K <= 2^17; larger K uses DMMA).
+   Power rounds (sketch.hpp:148-164) use it for both halves: A Y^T contracts
+   over A's columns, so the column scales of A's cached residue planes are
+   folded into Y^T and the planes enter the GEMM as the M-major operand. */
 #define LR_GEMM_DMMA 0
 #define LR_GEMM_OZAKI_INT8 1
 int lr_ctx_set_gemm_mode(lr_ctx* ctx, int mode);
