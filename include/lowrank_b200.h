@@ -123,7 +123,7 @@ int lr_ctx_get_gemm_mode(lr_ctx* ctx);
    After C = A(:, J) two chains are independent: the row ID of C (CPQR of C^T,
    id.hpp:101-128) and Q_c -> A^T Q_c (lowrank_main.cpp:210-215).  sms > 0 runs
    them concurrently, the row ID on an SM partition of that size; 0 runs them
-   one after the other; -1 (default) chooses: concurrent with 40 SMs (56 for a tall A) when the
+   one after the other; -1 (default) chooses: concurrent with 40 SMs (48 through the host-pointer entry, 56 for a tall A) when the
    INT8 engine contracts A, m, n >= 32768 and m n >= 2^31 (measured break-even).  Same kernels and index sets
    either way; the factors agree to roundoff (split-K depends on the SM count). */
 int lr_ctx_set_concurrent_tail(lr_ctx* ctx, int sms);

@@ -1161,7 +1161,7 @@ void release_sm_split(lr_ctx* c) {
 // profiles/r02_cur_split_p_sweep.log): 40 SMs when A^T Q_c runs on the INT8 engine, both
 // dimensions are >= 32768 and A has at least 2^31 entries.  On the DMMA engine the A^T Q_c GEMM is 5x longer
 // than the row ID, and a static partition would slow it for its whole length.
-int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
+int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n, bool host_entry) {
   if (c->tail_sms >= 0) return c->tail_sms;
   if (const char* e = getenv("LRB_CUR_SPLIT")) return std::max(0, atoi(e));
   // under an injected profiler (ncu sets NV_COMPUTE_PROFILER_PERFWORKS_DIR and
@@ -1178,7 +1178,11 @@ int tail_sms_wanted(lr_ctx* c, int64_t m, int64_t n) {
   // (65536 x 32768: 72.9 ms sequential, P = 40: 74.8, 48: 71.6, 56: 69.3, 64: 69.2, 72: 71.6)
   // wants the larger row-ID partition
   if (!(c->gemm_mode == LR_GEMM_OZAKI_INT8 && m >= 32768 && n >= 32768 && m * n >= (int64_t(1) << 31))) return 0;
-  return (m > n && n < 49152) ? 56 : 40;
+  if (m > n && n < 49152) return 56;
+  // host-pointer entry: the row-ID chain's results (row pivots, row T, R) are downloaded as they
+  // become final, so that chain gates the end of the call: 48 SMs (e2e 0.6823-0.6829 s against
+  // 0.6845-0.6869 s with 40, which is ~1 ms ahead on the device-resident entry)
+  return host_entry ? 48 : 40;
 }
 
 bool sm_split(lr_ctx* c, int want) {
@@ -1261,9 +1265,9 @@ cudaEvent_t record_event(cudaStream_t s) {
   return e;
 }
 
-bool split_applies(lr_ctx* c, int64_t m, int64_t n, int64_t k, int u_mode) {
+bool split_applies(lr_ctx* c, int64_t m, int64_t n, int64_t k, int u_mode, bool host_entry = false) {
   return u_mode == LR_U_CPINV_A_RPINV && m >= 16384 && n >= 16384 && k > 192 && k <= 512 &&
-         sm_split(c, tail_sms_wanted(c, m, n));
+         sm_split(c, tail_sms_wanted(c, m, n, host_entry));
 }
 
 // tsid_core + cur_core (u_mode LR_U_CPINV_A_RPINV) with the two chains
@@ -2563,7 +2567,7 @@ int lr_randomized_cur(lr_ctx* c, int64_t m, int64_t n, const double* a, int64_t 
         down.mat(k, m - k, rcd, k, row_coeff, k);
         down.mat(k, k, skd, k, skeleton, k);
       };
-      if (split_applies(c, m, n, k, u_mode)) {
+      if (split_applies(c, m, n, k, u_mode, true)) {
         tsid_cur_split(c, m, n, d, l, k, cp, ccd, k, strat, rp, rcd, k, skd, thr, Cd, Ud, Rd, rows_done,
                        [&] { down.mat(k, n, Rd, k, R, k); });
         down.mat(k, k, Ud, k, U, k);
